@@ -1,0 +1,125 @@
+/*
+ * lss.h — C ABI of the B200-native LSS sequence-distributed attention path.
+ *
+ * Drop-in boundary for the attention half of the reference's transformer layer
+ * (reference: /root/reference/pkg/src/seqpar).  Every entry point replaces one
+ * numpy function of the reference's hot path; the citation next to each entry
+ * names it.  All pointers are DEVICE pointers owned by the caller (no
+ * allocation inside the library except cached launch metadata); every call is
+ * stream-ordered on `stream` (a cudaStream_t) and never synchronises the host.
+ *
+ * Layouts (row-major, the reference's (batch, rows, features) convention,
+ * model.py:16-19; head h <-> feature columns [h*d, (h+1)*d), model.py:309):
+ *   activations  [batch][rows][embed]
+ *   packed K/V   [workers][batch][seg_len][2*embed]   K in columns [0,embed),
+ *                V in [embed, 2*embed); this is the rank-ordered all-gather of
+ *                every rank's [K_r | V_r] (sharded.py:144-154, collectives.py:340)
+ *   weights      reference layout [d_in][d_out] (nnops.py:172-177), y = x W + b
+ *   lse2         [batch][heads][rows_pad], rows_pad = lss_rows_pad(rows),
+ *                base-2 log-sum-exp of each softmax row
+ *
+ * Return value: LSS_OK (0) or an error code; lss_last_error() describes the
+ * last failure of the calling thread.  Error codes map onto the reference's
+ * exception taxonomy (errors.py:8-29).
+ */
+#ifndef LSS_H_
+#define LSS_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSS_ABI_VERSION 1
+
+enum lss_status {
+  LSS_OK = 0,
+  LSS_ERR_SHAPE = 1,        /* errors.ShapeError          (errors.py:8)  */
+  LSS_ERR_PARTITION = 2,    /* errors.PartitionError      (errors.py:12) */
+  LSS_ERR_DEGENERATE = 3,   /* errors.DegenerateRowError  (errors.py:16) */
+  LSS_ERR_NUMERICS = 4,     /* errors.NumericsError       (errors.py:20) */
+  LSS_ERR_CUDA = 5,         /* CUDA launch / driver failure              */
+  LSS_ERR_UNSUPPORTED = 6,  /* shape outside what the sm_100a kernels do */
+  LSS_ERR_ARG = 7           /* null pointer / bad enum                   */
+};
+
+enum lss_dtype {
+  LSS_BF16 = 0, /* bf16 operands, fp32 accumulation: tcgen05/TMEM/TMA kernels */
+  LSS_F32 = 1   /* fp32 check mode: FFMA kernels (<= 1e-4 vs the fp64 oracle) */
+};
+
+int lss_abi_version(void);
+const char* lss_last_error(void);
+/* rows rounded up to the 128-row query tile (size of the lse2 / delta rows) */
+long lss_rows_pad(long rows);
+
+/* nnops.layernorm_fwd (nnops.py:199-208) as called by model.norm3 (model.py:248-251).
+ * x [rows][embed] fp32 -> y (bf16 or fp32 per y_dtype), mean/rstd [rows] cache. */
+int lss_layernorm_fwd(const float* x, const float* gain, const float* bias, void* y, int y_dtype,
+                      float* mean, float* rstd, long rows, int embed, float eps, void* stream);
+
+/* nnops.layernorm_bwd (nnops.py:211-227) fused with the residual add of
+ * model.layer_bwd (model.py:485-486): grad_x = grad_res + LN'(grad_xh).
+ * grad_gain/grad_bias are ACCUMULATED (+= alpha * column sums). grad_res may be null. */
+int lss_layernorm_bwd(const float* grad_xh, const float* x, const float* mean, const float* rstd,
+                      const float* gain, const float* grad_res, float* grad_x, float* grad_gain,
+                      float* grad_bias, float alpha, long rows, int embed, void* stream);
+
+/* Products of nnops.linear_fwd / linear_bwd (nnops.py:180-193):
+ *   C[M][N] = alpha * A . B^T (+ bias[N]) (+ residual[M][N])
+ * A is [M][K] (a_mn_major=0, row stride lda) or stored [K][M] (a_mn_major=1);
+ * B is [N][K] (b_mn_major=0) or stored [K][N] (b_mn_major=1).
+ * dtype LSS_BF16: A/B bf16, tcgen05 GEMM; LSS_F32: A/B fp32, FFMA GEMM (fp32 out).
+ * Output columns are split into up to 3 segments of seg_width columns, segment
+ * s written to out[s] with leading dimension ldo[s] (e.g. Q and packed K|V). */
+typedef struct lss_gemm_epilogue {
+  void* out[3];
+  long ldo[3];
+  int seg_width;
+  int out_dtype; /* LSS_BF16 or LSS_F32 */
+  float alpha;
+  const float* bias;     /* [N] fp32 or null */
+  const float* residual; /* [M][ld_res] fp32 or null */
+  long ld_res;
+} lss_gemm_epilogue;
+
+int lss_gemm(int dtype, const void* A, long lda, int a_mn_major, const void* B, long ldb,
+             int b_mn_major, int M, int N, int K, const lss_gemm_epilogue* ep, void* stream);
+
+/* Stage the attention weights (model.LayerParams attn_q/k/v/out, model.py:83-94)
+ * in the GEMM operand layouts: wqkv_t [3E][E] = [Wq|Wk|Wv]^T, wqkv [E][3E],
+ * wo_t [E][E] = Wo^T, wo [E][E], bqkv [3E] = [bq|bk|bv]. */
+int lss_stage_weights(int dtype, const float* wq, const float* wk, const float* wv,
+                      const float* wo, const float* bq, const float* bk, const float* bv,
+                      void* wqkv_t, void* wqkv, void* wo_t, void* wo_n, float* bqkv, int embed,
+                      void* stream);
+
+/* Column-concatenate up to 3 fp32 blocks into dst (bf16/fp32, may be null) and
+ * ACCUMULATE alpha * column sums into colsum (may be null): bias gradients
+ * (nnops.py:192) fused with the operand casts of the backward GEMMs. */
+int lss_cat_cast_colsum(int out_dtype, const float* const* srcs, const long* lds, const int* cols,
+                        int nsrc, void* dst, long ld_dst, float* colsum, float alpha, long rows,
+                        void* stream);
+
+/* model.scores_fwd (model.py:280-326): this rank's query rows (global
+ * positions offset..offset+rows-1) against the whole sequence held in the
+ * packed K/V buffer of `workers` segments of seg_len rows.  Causal keep-mask
+ * key <= query position (model.py:301-304).  Writes ctx `o` and lse2. */
+int lss_attn_fwd(int dtype, const void* q, const void* kv, void* o, float* lse2, int batch,
+                 int rows, int workers, int seg_len, int heads, int head_dim, long offset,
+                 int causal, void* stream);
+
+/* model.scores_bwd (model.py:329-359).  grad_q [batch][rows][embed] fp32 is
+ * overwritten; grad_kv [workers][batch][seg_len][2*embed] fp32 is fully
+ * written (partial dK|dV over the whole sequence, reduce-scatter input).
+ * delta_ws: workspace of batch*heads*lss_rows_pad(rows) floats. */
+int lss_attn_bwd(int dtype, const void* q, const void* kv, const void* o, const void* grad_o,
+                 const float* lse2, float* delta_ws, float* grad_q, float* grad_kv, int batch,
+                 int rows, int workers, int seg_len, int heads, int head_dim, long offset,
+                 int causal, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSS_H_ */

@@ -1,0 +1,309 @@
+"""CPU oracle for the LSS sequence-distributed attention sublayer.
+
+TEST INFRASTRUCTURE ONLY.  Nothing in the product path (``paper_2311_02382_b200``)
+imports this module; only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may use it, and
+only as the checker / the reference CPU arm, never as the thing measured.
+
+This is a numpy restatement of the reference's algorithm for the hot path
+(``/root/reference/pkg/src/seqpar``), written independently from the
+definitions, vectorised over (batch, head) instead of the reference's Python
+loops.  Every function cites the reference lines it follows.
+
+Parity pinning: ``tests/golden/make_golden.py`` runs the real reference
+(``seqpar`` imported from ``/root/reference``) on seeded inputs and commits the
+outputs under ``tests/golden/``; ``tests/test_oracle.py`` checks this oracle
+against those fixtures and against the reference's own known-answer tests
+(``tests/test_model.py:17-163`` in the reference).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+LAYERNORM_EPS = 1e-5  # nnops.py:28
+
+
+class OracleShapeError(ValueError):
+    pass
+
+
+class OracleDegenerateRow(ValueError):
+    pass
+
+
+# --------------------------------------------------------------------------
+# L1 primitives (nnops.py)
+# --------------------------------------------------------------------------
+
+
+def layernorm_fwd(x, gain, bias, eps=LAYERNORM_EPS):
+    """nnops.py:199-208: y = (x-mu)*inv_std*g + b; cache (xhat, inv_std)."""
+    mu = x.mean(axis=-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+    inv_std = 1.0 / np.sqrt(var + eps)
+    xhat = (x - mu) * inv_std
+    return xhat * gain + bias, (xhat, inv_std)
+
+
+def layernorm_bwd(cache, gain, gy):
+    """nnops.py:211-227: gx = inv_std*(g - mean(g) - xhat*mean(g*xhat)), g = gy*gain."""
+    xhat, inv_std = cache
+    red = tuple(range(gy.ndim - 1))
+    g_gain = (gy * xhat).sum(axis=red)
+    g_bias = gy.sum(axis=red)
+    g = gy * gain
+    gx = inv_std * (g - g.mean(-1, keepdims=True) - xhat * (g * xhat).mean(-1, keepdims=True))
+    return gx, g_gain, g_bias
+
+
+def linear_fwd(x, w, b):
+    """nnops.py:180-183 via model.linear3 (model.py:237-239): y = x @ W + b, W is [in, out]."""
+    return x @ w + b
+
+
+def linear_bwd(x, w, gy):
+    """nnops.py:186-193 via model.linear3_bwd (model.py:242-245)."""
+    e_in = x.shape[-1]
+    x2 = x.reshape(-1, e_in)
+    g2 = gy.reshape(-1, gy.shape[-1])
+    gx = gy @ w.T
+    return gx, x2.T @ g2, g2.sum(axis=0)
+
+
+# --------------------------------------------------------------------------
+# Attention core (model.py:280-359, tensor.py:104-131)
+# --------------------------------------------------------------------------
+
+
+def _split_heads(a, n_heads):
+    # (B, rows, E) -> (B, H, rows, d); head h <-> columns [h*d, (h+1)*d) (model.py:309)
+    b, r, e = a.shape
+    d = e // n_heads
+    return a.reshape(b, r, n_heads, d).transpose(0, 2, 1, 3)
+
+
+def _merge_heads(a):
+    b, h, r, d = a.shape
+    return a.transpose(0, 2, 1, 3).reshape(b, r, h * d)
+
+
+def causal_keep(m, t, offset):
+    """model.py:301-304: keep[i, j] = j <= offset + i (global query position)."""
+    q_pos = np.arange(offset, offset + m)
+    return np.arange(t)[None, :] <= q_pos[:, None]
+
+
+def scores_fwd(q, k, v, offset, n_heads, causal=True):
+    """model.py:280-326.  q (B,m,E) local rows at global positions offset..offset+m,
+    k/v (B,t,E) whole sequence.  Returns (ctx, P) with P (B,H,m,t) the softmax
+    probabilities (the reference's cached ``aw``).  Masked entries are exact
+    zeros and a fully-masked row raises (tensor.py:123-130)."""
+    bsz, m, e = q.shape
+    t = k.shape[1]
+    d = e // n_heads
+    scale = 1.0 / math.sqrt(d)
+    qh, kh, vh = (_split_heads(a, n_heads) for a in (q, k, v))
+    s = np.einsum("bhid,bhjd->bhij", qh, kh) * scale
+    if causal:
+        keep = causal_keep(m, t, offset)
+        if np.any(keep.sum(axis=1) == 0):
+            raise OracleDegenerateRow("softmax row fully masked")
+        s = np.where(keep, s, -np.inf)
+    s = s - s.max(axis=-1, keepdims=True)
+    p = np.exp(s)
+    p = p / p.sum(axis=-1, keepdims=True)
+    ctx = _merge_heads(np.einsum("bhij,bhjd->bhid", p, vh))
+    return ctx, p
+
+
+def scores_bwd(p, q, k, v, grad_ctx, n_heads):
+    """model.py:329-359: dP = dO V^T; dV = P^T dO; dS = P*(dP - rowsum(dP*P))*scale;
+    dQ = dS K; dK = dS^T Q.  dK/dV span the full key length t (partials of this
+    block's query rows)."""
+    d = q.shape[2] // n_heads
+    scale = 1.0 / math.sqrt(d)
+    qh, kh, vh, gh = (_split_heads(a, n_heads) for a in (q, k, v, grad_ctx))
+    dp = np.einsum("bhid,bhjd->bhij", gh, vh)
+    dv = np.einsum("bhij,bhid->bhjd", p, gh)
+    ds = p * (dp - (dp * p).sum(axis=-1, keepdims=True)) * scale
+    dq = np.einsum("bhij,bhjd->bhid", ds, kh)
+    dk = np.einsum("bhij,bhid->bhjd", ds, qh)
+    return _merge_heads(dq), _merge_heads(dk), _merge_heads(dv)
+
+
+def attention_from_definition(q, k, v, offset, n_heads, causal=True):
+    """Scalar-loop oracle of the reference's own test (tests/test_model.py:17-37)."""
+    bsz, m, e = q.shape
+    t = k.shape[1]
+    d = e // n_heads
+    out = np.zeros_like(q, dtype=np.float64)
+    for b in range(bsz):
+        for h in range(n_heads):
+            lo, hi = h * d, (h + 1) * d
+            for i in range(m):
+                limit = offset + i + 1 if causal else t
+                sc = np.array([float(np.dot(q[b, i, lo:hi], k[b, j, lo:hi])) / math.sqrt(d)
+                               for j in range(limit)])
+                w = np.exp(sc - sc.max())
+                w = w / w.sum()
+                out[b, i, lo:hi] = w @ v[b, :limit, lo:hi]
+    return out
+
+
+# --------------------------------------------------------------------------
+# Attention half of one LSS layer (model.py:442-448 fwd, 479-486 bwd) with the
+# packed-K/V kv_fwd/kv_bwd of sharded.py:144-154 / 192-202.
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class AttnParams:
+    """The attention-half parameters of model.LayerParams (model.py:83-94)."""
+    ln1_gain: np.ndarray
+    ln1_bias: np.ndarray
+    wq: np.ndarray
+    bq: np.ndarray
+    wk: np.ndarray
+    bk: np.ndarray
+    wv: np.ndarray
+    bv: np.ndarray
+    wo: np.ndarray
+    bo: np.ndarray
+
+    GRAD_ORDER = ("ln1_gain", "ln1_bias", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo")
+
+    def astype(self, dt):
+        return AttnParams(*[getattr(self, n).astype(dt) for n in self.GRAD_ORDER])
+
+
+def init_attn_params(embed_dim, seed=0, dtype=np.float64):
+    """Same draw convention as model.init_params (model.py:179-224) restricted to
+    layer 0's attention half: U(+-1/sqrt(E)) weights in draw order q, k, v, out
+    AFTER the token and position tables.  Because the tables are drawn first the
+    exact stream only matches init_params when vocab/seq_len match, so the
+    golden fixtures store the weights they used."""
+    rng = np.random.default_rng(seed)
+    bound = 1.0 / math.sqrt(embed_dim)
+    e = embed_dim
+
+    def u():
+        return rng.uniform(-bound, bound, (e, e)).astype(dtype)
+
+    wq, wk, wv, wo = u(), u(), u(), u()
+    z = np.zeros(e, dtype=dtype)
+    return AttnParams(np.ones(e, dtype=dtype), z.copy(), wq, z.copy(), wk, z.copy(),
+                      wv, z.copy(), wo, z.copy())
+
+
+def attn_rank_fwd(x_seg, p: AttnParams, offset, kv_full, n_heads, causal=True):
+    """model.layer_fwd lines 442-448 for one rank: LN1 -> Q -> scores -> out -> residual.
+    ``kv_full`` = (k, v) for the whole sequence (the all-gather result)."""
+    xh, ln_cache = layernorm_fwd(x_seg, p.ln1_gain, p.ln1_bias)
+    q = linear_fwd(xh, p.wq, p.bq)
+    k, v = kv_full
+    ctx, prob = scores_fwd(q, k, v, offset, n_heads, causal)
+    y = x_seg + linear_fwd(ctx, p.wo, p.bo)
+    return y, dict(xh=xh, ln=ln_cache, q=q, ctx=ctx, p=prob)
+
+
+def lss_attention(x, grad_y, p: AttnParams, n_heads, workers, causal=True):
+    """Run the attention half of one LSS layer on ``workers`` simulated ranks,
+    forward and backward, with the packed-K/V exchange: each rank projects its
+    own [K_r|V_r] and all-gathers them in rank order (sharded.py:144-154); the
+    backward reduce-scatters [dK|dV] (sharded.py:192-202) and the replicated
+    parameter gradients are averaged over the group (sharded.py:219-244).
+
+    x, grad_y: (B, l, E).  Returns dict with y (B,l,E) (rank rows concatenated),
+    dx (B,l,E), and the averaged parameter gradients (AttnParams)."""
+    bsz, seq, e = x.shape
+    if seq % workers:
+        raise OracleShapeError(f"sequence length {seq} not divisible by {workers}")  # sharded.py:50-53
+    m = seq // workers
+    segs = [slice(r * m, (r + 1) * m) for r in range(workers)]  # ShardSpec.offset = rank*block
+    # forward: each rank LN1 + own K/V projection, then the rank-ordered gather
+    xh = [layernorm_fwd(x[:, s], p.ln1_gain, p.ln1_bias) for s in segs]
+    k_parts = [linear_fwd(xh[r][0], p.wk, p.bk) for r in range(workers)]
+    v_parts = [linear_fwd(xh[r][0], p.wv, p.bv) for r in range(workers)]
+    k_full = np.concatenate(k_parts, axis=1)  # collectives.py:340 (rank order, dim=1)
+    v_full = np.concatenate(v_parts, axis=1)
+    ys, caches = [], []
+    for r, s in enumerate(segs):
+        y, c = attn_rank_fwd(x[:, s], p, r * m, (k_full, v_full), n_heads, causal)
+        ys.append(y)
+        caches.append(c)
+    # backward (model.py:479-486 with the unfused kv_bwd of sharded.py:193-202)
+    dk_full = np.zeros_like(k_full)
+    dv_full = np.zeros_like(v_full)
+    per_rank = []
+    for r, s in enumerate(segs):
+        c = caches[r]
+        gy = grad_y[:, s]
+        g_ctx, g_wo, g_bo = linear_bwd(c["ctx"], p.wo, gy)
+        dq, dk, dv = scores_bwd(c["p"], c["q"], k_full, v_full, g_ctx, n_heads)
+        dk_full = dk_full + dk  # reduce_scatter sums contributions (collectives.py:365-367)
+        dv_full = dv_full + dv
+        per_rank.append((gy, dq, g_wo, g_bo))
+    grads_sum = None
+    dxs = []
+    for r, s in enumerate(segs):
+        c = caches[r]
+        gy, dq, g_wo, g_bo = per_rank[r]
+        gk, gv = dk_full[:, s], dv_full[:, s]  # block r of the sum (collectives.py:368-370)
+        gxq, g_wq, g_bq = linear_bwd(c["xh"], p.wq, dq)
+        gxk, g_wk, g_bk = linear_bwd(c["xh"], p.wk, gk)
+        gxv, g_wv, g_bv = linear_bwd(c["xh"], p.wv, gv)
+        gx_ln, g_g, g_b = layernorm_bwd(c["ln"], p.ln1_gain, gxq + gxk + gxv)
+        dxs.append(gy + gx_ln)  # grad_in = grad_mid + g_ln1 (model.py:486)
+        g = [g_g, g_b, g_wq, g_bq, g_wk, g_bk, g_wv, g_bv, g_wo, g_bo]
+        grads_sum = g if grads_sum is None else [a + b for a, b in zip(grads_sum, g)]
+    grads = AttnParams(*[a / workers for a in grads_sum])  # all_reduce mean (sharded.py:238)
+    return dict(y=np.concatenate(ys, axis=1), dx=np.concatenate(dxs, axis=1), grads=grads,
+                k_full=k_full, v_full=v_full)
+
+
+# --------------------------------------------------------------------------
+# Work accounting (costs.py:98 convention, extended to fwd+bwd)
+# --------------------------------------------------------------------------
+
+
+def attention_pairs(seq, causal):
+    return seq * (seq + 1) // 2 if causal else seq * seq
+
+
+def layer_flops(batch, seq, embed, causal):
+    """F = 24*l*E^2 + 12*E*P per sequence."""
+    return batch * (24 * seq * embed * embed + 12 * embed * attention_pairs(seq, causal))
+
+
+def sample_rows(x, grad_y, p, n_heads, offset, rows, causal=True):
+    """The bounded CPU sample used as the reference arm: one block of ``rows``
+    query rows at global ``offset`` through the attention half forward and
+    backward against full-length K/V (whose projection is done outside the
+    timed region, as if received from the all-gather).  Returns the time-relevant
+    outputs so the caller can keep them alive."""
+    s = slice(offset, offset + rows)
+    xh_all, _ = layernorm_fwd(x, p.ln1_gain, p.ln1_bias)
+    k_full = linear_fwd(xh_all, p.wk, p.bk)
+    v_full = linear_fwd(xh_all, p.wv, p.bv)
+
+    def run():
+        xh, ln = layernorm_fwd(x[:, s], p.ln1_gain, p.ln1_bias)
+        k_own = linear_fwd(xh, p.wk, p.bk)
+        v_own = linear_fwd(xh, p.wv, p.bv)
+        q = linear_fwd(xh, p.wq, p.bq)
+        ctx, prob = scores_fwd(q, k_full, v_full, offset, n_heads, causal)
+        y = x[:, s] + linear_fwd(ctx, p.wo, p.bo)
+        gy = grad_y[:, s]
+        g_ctx, g_wo, g_bo = linear_bwd(ctx, p.wo, gy)
+        dq, dk, dv = scores_bwd(prob, q, k_full, v_full, g_ctx, n_heads)
+        gxq, g_wq, _ = linear_bwd(xh, p.wq, dq)
+        gxk, g_wk, _ = linear_bwd(xh, p.wk, dk[:, s])
+        gxv, g_wv, _ = linear_bwd(xh, p.wv, dv[:, s])
+        gx, _, _ = layernorm_bwd(ln, p.ln1_gain, gxq + gxk + gxv)
+        return y, gy + gx, k_own, v_own
+
+    return run

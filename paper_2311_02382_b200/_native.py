@@ -1,0 +1,108 @@
+"""ctypes binding of liblss.so (the C ABI declared in include/lss.h).
+
+The library is built in-tree (``paper_2311_02382_b200/liblss.so``, see
+``build.py``).  There is no fallback: if the library is missing or fails to
+load, every entry point raises :class:`NativeError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import (DegenerateRowError, NativeError, NumericsError, PartitionError, ShapeError,
+                     UnsupportedError)
+
+LIB_PATH = Path(__file__).resolve().parent / "liblss.so"
+
+LSS_BF16 = 0
+LSS_F32 = 1
+
+_STATUS = {
+    1: ShapeError,
+    2: PartitionError,
+    3: DegenerateRowError,
+    4: NumericsError,
+    5: NativeError,
+    6: UnsupportedError,
+    7: ValueError,
+}
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_long
+_F = ctypes.c_float
+
+
+class GemmEpilogue(ctypes.Structure):
+    _fields_ = [
+        ("out", _P * 3),
+        ("ldo", _L * 3),
+        ("seg_width", _I),
+        ("out_dtype", _I),
+        ("alpha", _F),
+        ("bias", _P),
+        ("residual", _P),
+        ("ld_res", _L),
+    ]
+
+
+# name -> argtypes (all return int status, except noted)
+SIGNATURES = {
+    "lss_layernorm_fwd": [_P, _P, _P, _P, _I, _P, _P, _L, _I, _F, _P],
+    "lss_layernorm_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _L, _I, _P],
+    "lss_gemm": [_I, _P, _L, _I, _P, _L, _I, _I, _I, _I, ctypes.POINTER(GemmEpilogue), _P],
+    "lss_stage_weights": [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],
+    "lss_cat_cast_colsum": [_I, ctypes.POINTER(_P), ctypes.POINTER(_L), ctypes.POINTER(_I), _I, _P, _L,
+                            _P, _F, _L, _P],
+    "lss_attn_fwd": [_I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P],
+    "lss_attn_bwd": [_I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P],
+}
+EXTRA = {
+    "lss_abi_version": ([], _I),
+    "lss_last_error": ([], ctypes.c_char_p),
+    "lss_rows_pad": ([_L], _L),
+}
+ABI_VERSION = 1
+
+_lib = None
+
+
+def load():
+    """Load liblss.so once; raise NativeError if it is absent or incompatible."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("LSS_LIB", LIB_PATH))
+    if not path.exists():
+        raise NativeError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    try:
+        lib = ctypes.CDLL(str(path))
+    except OSError as exc:  # pragma: no cover - depends on the box
+        raise NativeError(f"failed to load {path}: {exc}") from exc
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = _I
+    for name, (argtypes, res) in EXTRA.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = res
+    if lib.lss_abi_version() != ABI_VERSION:
+        raise NativeError(f"liblss.so ABI {lib.lss_abi_version()} != {ABI_VERSION}")
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args):
+    """Invoke an entry point and map a non-zero status onto the reference's exceptions."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.lss_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, NativeError)(f"{name}: {msg}")
+
+
+def rows_pad(rows: int) -> int:
+    return int(load().lss_rows_pad(rows))

@@ -1,0 +1,291 @@
+// Segment attention backward for the LSS layer on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Semantics follow model.scores_bwd (reference model.py:329-359):
+//   dP = dO V^T, dV = P^T dO, dS = P (dP - rowsum(dP P)) / sqrt(d),
+//   dQ = dS K, dK = dS^T Q,
+// with P recomputed from the forward's base-2 log-sum-exp and
+// rowsum(dP P) = rowsum(dO O) = delta precomputed per query row.  dK/dV span
+// the FULL key length (this rank's partial contribution for every rank's key
+// rows) and are written in the packed [G][B][seg][2E] fp32 layout that the
+// reduce-scatter consumes directly (sharded.py:192-199 math, one collective).
+//
+// CTA = one 128-row key tile of one (batch, head); it walks the query tiles of
+// this rank that can see the keys (causal: q_pos >= k_pos).  Transposed
+// formulation so the key rows are TMEM lanes:
+//   S^T  = K Q_i^T        (TMEM, 128 cols)        dP^T = V dO_i^T (TMEM, 128 cols)
+//   P^T, dS^T computed by 256 threads (2 warpgroups, 64 query columns each)
+//   dV  += P^T dO_i       (A = P^T from TMEM)
+//   dK  += dS^T Q_i       (A = dS^T from SMEM, K-major)
+//   dQ_i = dS K           (A = dS^T from SMEM read MN-major; drained to global
+//                          fp32 with bulk async reduce-add)
+// TMEM: S^T[0,128) dP^T[128,256) dV[256,320) dK[320,384) dQ[384,448) P^T[448,512)
+// S/dP for tile i+1 are issued as soon as tile i's values are in registers.
+#pragma once
+#include "common.cuh"
+#include "attn_fwd.cuh"
+
+namespace lss {
+
+constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES + 2 * 512;  // Q, dO, lse2[128], delta[128]
+constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATT_TILE_BYTES /*dS*/ +
+                         2 * 128 * 128 /*dQ staging*/ + 1024 + 256;
+constexpr int ATB_THREADS = 384;
+
+struct AttnBwdParams {
+  int B, m, m_pad, G, seg_len, H;
+  long offset;
+  int causal;
+  float scale_log2;  // log2(e)/sqrt(d)
+  float scale;       // 1/sqrt(d)
+  const float* lse2;   // [B][H][m_pad] (+inf padded)
+  const float* delta;  // [B][H][m_pad] (0 padded)
+  float* dq;           // [B][m][E] fp32, accumulated (must be zeroed)
+  float* dkv;          // [G][B][seg_len][2E] fp32, fully written
+};
+
+LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(ATB_THREADS, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
+                       const __grid_constant__ CUtensorMap tmKV, const __grid_constant__ CUtensorMap tmdQ,
+                       AttnBwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + ATT_TILE_BYTES;
+  uint8_t* sQst = sV + ATT_TILE_BYTES;                      // 2 stages
+  uint8_t* sdS = sQst + 2 * ATB_QSTAGE_BYTES;               // 2 sub-tiles [128 kv][64 q] bf16
+  uint8_t* sStage = sdS + 2 * ATT_TILE_BYTES;               // dQ staging, 2 x [128][32] fp32 (SW128)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + 2 * 128 * 128);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;   // [2]
+  uint64_t* q_empty = bars + 3;  // [2]
+  uint64_t* sdp_full = bars + 5;
+  uint64_t* sdp_free = bars + 6;
+  uint64_t* pds_full = bars + 7;
+  uint64_t* dq_full = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int E = p.H * ATT_D;
+  const int h = blockIdx.y;
+  const int b = blockIdx.z;
+  const int tps = (p.seg_len + ATT_BN - 1) / ATT_BN;
+  const int g = blockIdx.x / tps;
+  const int kt = blockIdx.x % tps;
+  const int kv_row0 = kt * ATT_BN;                         // row within segment
+  const int kv_valid = min(ATT_BN, p.seg_len - kv_row0);
+  const long kpos0 = (long)g * p.seg_len + kv_row0;        // global key position of row 0
+  const int n_qt = (p.m + ATT_BM - 1) / ATT_BM;
+  int i_first = 0;
+  if (p.causal) {
+    const long d0 = kpos0 - p.offset;  // first local q row that can see key row 0
+    i_first = d0 <= 0 ? 0 : (int)min((long)n_qt, d0 / ATT_BM);
+  }
+  const int n_iter = n_qt - i_first;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmdO);
+    tma_prefetch_desc(&tmKV);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(sdp_free, 256);
+    mbar_init(pds_full, 256);
+    mbar_init(dq_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320,
+                 tdQ = tmem + 384, tP = tmem + 448;
+
+  if (warp == 0) {
+    if (lane == 0 && n_iter > 0) {
+      // ------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(kv_full, 2 * ATT_TILE_BYTES);
+      tma_load_4d(&tmKV, kv_full, sK, h * ATT_D, kv_row0, b, g);
+      tma_load_4d(&tmKV, kv_full, sV, E + h * ATT_D, kv_row0, b, g);
+      for (int it = 0; it < n_iter; ++it) {
+        const int s = it & 1;
+        mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
+        uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
+        const int q0 = (i_first + it) * ATT_BM;
+        mbar_arrive_expect_tx(&q_full[s], ATB_QSTAGE_BYTES);
+        tma_load_3d(&tmQ, &q_full[s], st, h * ATT_D, q0, b);
+        tma_load_3d(&tmdO, &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
+        const long lo = ((long)b * p.H + h) * p.m_pad + q0;
+        bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.lse2 + lo, 512, &q_full[s]);
+        bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.delta + lo, 512, &q_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_iter > 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idSS = idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
+      constexpr uint32_t idKN = idesc_bf16_f32(128, 64, 0, 1);   // dV, dK (B MN-major)
+      constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);    // dQ (A and B MN-major)
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sdS);
+      auto issue_sdp = [&](int it) {
+        const int s = it & 1;
+        mbar_wait(&q_full[s], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
+        const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
+#pragma unroll
+        for (int k = 0; k < ATT_D / 16; ++k)
+          mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
+                      smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
+#pragma unroll
+        for (int k = 0; k < ATT_D / 16; ++k)
+          mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
+                      smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
+        mma_commit(sdp_full);
+      };
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      issue_sdp(0);
+      for (int it = 0; it < n_iter; ++it) {
+        if (it + 1 < n_iter) {
+          mbar_wait(sdp_free, it & 1);
+          issue_sdp(it + 1);
+        }
+        const int s = it & 1;
+        const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
+        const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
+        mbar_wait(pds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < ATT_BM / 16; ++k)  // dV += P^T dO
+          mma_bf16_ts(tdV, tP + k * 8, smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
+                      (it > 0 || k > 0));
+#pragma unroll
+        for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q
+          mma_bf16_ss(tdK, smem_desc_sw128(ds_addr + (k >> 2) * ATT_TILE_BYTES + (k & 3) * 32, 16, 1024),
+                      smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN, (it > 0 || k > 0));
+        mma_commit(&q_empty[s]);
+#pragma unroll
+        for (int k = 0; k < ATT_BN / 16; ++k)  // dQ = dS K
+          mma_bf16_ss(tdQ, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
+                      smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
+        mma_commit(dq_full);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ elementwise + dQ drain + dK/dV epilogue
+    const int half = (warp - 4) / 4;  // query columns [64*half, 64*half+64) of each tile
+    const int quad = warp % 4;
+    const int t = quad * 32 + lane;   // key row within tile == TMEM lane (and q row for dQ)
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const long kpos = kpos0 + t;
+    const bool row_ok = t < kv_valid;
+    uint8_t* stg_half = sStage + half * 128 * 128;  // [128 q rows][32 fp32], 128B-swizzled
+    uint8_t* stg_row = stg_half + t * 128;
+    const bool issuer = (t == 0);                    // one thread per half issues the reduce
+    auto drain_dq = [&](int it) {
+      // dQ rows of query tile `it` (TMEM lane = query row), columns [32*half, +32):
+      // TMEM -> registers -> swizzled smem tile -> TMA tensor reduce-add into fp32 dQ
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(tdQ + lane_off + half * 32, v);
+      if (issuer) bulk_wait_read0();  // previous reduce has finished reading the staging tile
+      named_bar_sync(1 + half, 128);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(stg_row + ((c ^ (t & 7)) << 4)) =
+            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      fence_proxy_async_smem();
+      named_bar_sync(1 + half, 128);
+      if (issuer) {
+        tma_reduce_add_3d(&tmdQ, stg_half, h * ATT_D + half * 32, (i_first + it) * ATT_BM, b);
+        bulk_commit();
+      }
+    };
+    for (int it = 0; it < n_iter; ++it) {
+      const int s = it & 1;
+      const int q0 = (i_first + it) * ATT_BM;
+      const uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
+      const float* s_lse = reinterpret_cast<const float*>(st + 2 * ATT_TILE_BYTES) + half * 64;
+      const float* s_del = reinterpret_cast<const float*>(st + 2 * ATT_TILE_BYTES + 512) + half * 64;
+      mbar_wait(sdp_full, it & 1);
+      tc_fence_after();
+      uint32_t sv[64], dp[64];
+      tmem_ld64(tS + lane_off + half * 64, sv);
+      tmem_ld64(tdP + lane_off + half * 64, dp);
+      tc_fence_before();
+      mbar_arrive(sdp_free);
+      // q tile visible to key row t: q_pos = offset + q0 + col >= kpos
+      const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > p.offset + q0 + half * 64);
+      const long first_vis = kpos - p.offset - q0 - half * 64;  // col >= first_vis is visible
+      uint32_t pk[32], dk[32];
+#pragma unroll
+      for (int c = 0; c < 64; c += 2) {
+        float p0 = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -s_lse[c]));
+        float p1 = ex2(fmaf(__uint_as_float(sv[c + 1]), p.scale_log2, -s_lse[c + 1]));
+        if (need_mask) {
+          if (!row_ok || (p.causal && (long)c < first_vis)) p0 = 0.f;
+          if (!row_ok || (p.causal && (long)(c + 1) < first_vis)) p1 = 0.f;
+        }
+        const float d0 = p0 * (__uint_as_float(dp[c]) - s_del[c]) * p.scale;
+        const float d1 = p1 * (__uint_as_float(dp[c + 1]) - s_del[c + 1]) * p.scale;
+        pk[c / 2] = pack_bf16(p0, p1);
+        dk[c / 2] = pack_bf16(d0, d1);
+      }
+      if (it > 0) drain_dq(it - 1);  // also guarantees dV/dK/dQ of tile it-1 are done
+      tmem_st32(tP + lane_off + half * 32, pk);
+      // dS^T row t, query columns [64*half, +64) -> sub-tile `half`, SW128 K-major
+      {
+        uint8_t* row = sdS + half * ATT_TILE_BYTES + t * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(row + ((c ^ (t & 7)) << 4)) =
+              make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(pds_full);
+    }
+    if (n_iter > 0) drain_dq(n_iter - 1);
+    // dK (half 0) / dV (half 1) epilogue: all MMAs are complete after the last dq_full
+    float* dst = p.dkv + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * (2L * E) +
+                 (half ? E : 0) + h * ATT_D;
+    if (n_iter > 0) {
+      uint32_t v[64];
+      tmem_ld64((half ? tdV : tdK) + lane_off, v);
+      if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          reinterpret_cast<float4*>(dst)[i] =
+              make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                          __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+      }
+    } else if (row_ok) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) reinterpret_cast<float4*>(dst)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (issuer) bulk_wait0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace lss

@@ -1,0 +1,294 @@
+// Segment attention forward for the LSS layer on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Semantics follow model.scores_fwd (reference model.py:280-326): for this
+// rank's query rows (global positions offset..offset+m) against the keys and
+// values of the WHOLE sequence, S = Q_h K_h^T / sqrt(d), causal keep-mask
+// key <= global query position (model.py:301-304), row softmax
+// (tensor.py:104-131), ctx[:, h*d:(h+1)*d] = P V_h.  Instead of caching P the
+// kernel emits the row log-sum-exp (base 2) so the backward recomputes P.
+//
+// K/V come from the packed all-gather buffer [G][B][seg][2E] (K in columns
+// [0,E), V in [E,2E)), i.e. the rank-ordered concatenation of every rank's
+// [K_r|V_r] (sharded.py:144-154 math, one collective).  The kernel walks the
+// key tiles segment by segment, so a segment length that is not a multiple of
+// 128 costs one partial tile per segment (masked), never a straddling TMA box.
+//
+// CTA = 2 query tiles (256 rows) of one (batch, head); 12 warps:
+//   warp 0      TMA producer (Q once; K/V ring of KV_STAGES)
+//   warp 1      MMA issuer (single thread): S_w = Q_w K^T (SS), O_w += P_w V (TS)
+//   warp 2      TMEM allocator
+//   warps 4-7   softmax for query tile 0 (thread <-> row <-> TMEM lane)
+//   warps 8-11  softmax for query tile 1
+// TMEM (512 cols): S0 | S1 | O0 | O1 | P0 | P1  (128,128,64,64,64,64).
+// S is released as soon as the softmax warps have loaded it, so S_{j+1} runs
+// on the tensor core while the exponentials of tile j are computed; P lives in
+// its own TMEM columns and feeds the P.V MMA directly (A operand from TMEM).
+// O rescaling is lazy (only when a row max grows by > 2^8).
+#pragma once
+#include "common.cuh"
+
+namespace lss {
+
+constexpr int ATT_BM = 128;
+constexpr int ATT_BN = 128;
+constexpr int ATT_D = 64;
+constexpr int ATT_KV_STAGES = 3;
+constexpr int ATT_TILE_BYTES = ATT_BM * ATT_D * 2;  // 16 KB (Q, K or V tile)
+constexpr int ATT_FWD_THREADS = 384;
+constexpr int ATT_FWD_SMEM = (2 + 2 * ATT_KV_STAGES) * ATT_TILE_BYTES + 1024 + 256;
+
+struct AttnFwdParams {
+  int B, m, m_pad, G, seg_len, H;  // q: [B][m][H*64]; kv: [G][B][seg_len][2*H*64]
+  long offset;              // global position of q row 0
+  int causal;
+  float scale_log2;         // log2(e)/sqrt(d)
+  __nv_bfloat16* o;         // [B][m][H*64]
+  float* lse2;              // [B][H][m_pad], log2 domain: m + log2(l); pad rows = +inf
+};
+
+__global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
+                       const __grid_constant__ CUtensorMap tmKV, AttnFwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                   // 2 tiles
+  uint8_t* sK = smem + 2 * ATT_TILE_BYTES;              // KV_STAGES tiles
+  uint8_t* sV = sK + ATT_KV_STAGES * ATT_TILE_BYTES;    // KV_STAGES tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + ATT_KV_STAGES * ATT_TILE_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + ATT_KV_STAGES;
+  uint64_t* s_full = kv_empty + ATT_KV_STAGES;  // [2]
+  uint64_t* s_empty = s_full + 2;               // [2]
+  uint64_t* p_full = s_empty + 2;               // [2]
+  uint64_t* o_full = p_full + 2;                // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int E = p.H * ATT_D;
+  const int h = blockIdx.y;
+  const int b = blockIdx.z;
+  // heavy (late, causal) query tiles first
+  const int n_pairs = (p.m + 2 * ATT_BM - 1) / (2 * ATT_BM);
+  const int pair = p.causal ? (n_pairs - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int q0 = pair * 2 * ATT_BM;
+  const bool has1 = q0 + ATT_BM < p.m;
+  const int q_last = min(q0 + 2 * ATT_BM, p.m) - 1;  // last valid local row in this CTA
+  const int tps = (p.seg_len + ATT_BN - 1) / ATT_BN;  // key tiles per segment
+  int n_kv = p.G * tps;
+  if (p.causal) {
+    const long max_key = p.offset + q_last;  // keys > max_key are masked for every row
+    int n = 0;
+    for (int g = 0; g < p.G; ++g) {
+      const long seg0 = (long)g * p.seg_len;
+      if (seg0 > max_key) break;
+      const long last_in_seg = min((long)p.seg_len - 1, max_key - seg0);
+      n = g * tps + (int)(last_in_seg / ATT_BN) + 1;
+    }
+    n_kv = n;
+  }
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmKV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < ATT_KV_STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&s_empty[w], 128);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&o_full[w], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem + 0, tmem + 128};
+  const uint32_t tO[2] = {tmem + 256, tmem + 320};
+  const uint32_t tP[2] = {tmem + 384, tmem + 448};
+
+  if (warp == 0) {
+    if (lane == 0 && n_kv > 0) {
+      // ------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * ATT_TILE_BYTES);
+      tma_load_3d(&tmQ, q_full, sQ, h * ATT_D, q0, b);
+      if (has1) tma_load_3d(&tmQ, q_full, sQ + ATT_TILE_BYTES, h * ATT_D, q0 + ATT_BM, b);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % ATT_KV_STAGES;
+        const uint32_t ph = (j / ATT_KV_STAGES) & 1;
+        mbar_wait(&kv_empty[st], ph ^ 1);
+        const int g = j / tps, t = j % tps;
+        mbar_arrive_expect_tx(&kv_full[st], 2 * ATT_TILE_BYTES);
+        tma_load_4d(&tmKV, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
+        tma_load_4d(&tmKV, &kv_full[st], sV + st * ATT_TILE_BYTES, E + h * ATT_D, t * ATT_BN, b, g);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_kv > 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idS = idesc_bf16_f32(ATT_BM, ATT_BN, 0, 0);
+      constexpr uint32_t idO = idesc_bf16_f32(ATT_BM, ATT_D, 0, 1);
+      const int nw = has1 ? 2 : 1;
+      const uint32_t q_addr = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int jj) {
+        const int st = jj % ATT_KV_STAGES;
+        const uint32_t v_addr = smem_u32(sV + st * ATT_TILE_BYTES);
+        for (int w = 0; w < nw; ++w) {
+          mbar_wait(&p_full[w], jj & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < ATT_BN / 16; ++k) {
+            mma_bf16_ts(tO[w], tP[w] + k * 8, smem_desc_sw128(v_addr + k * 2048, 8192, 1024), idO,
+                        (jj > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&o_full[w]);
+        }
+        mma_commit(&kv_empty[st]);
+      };
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % ATT_KV_STAGES;
+        mbar_wait(&kv_full[st], (j / ATT_KV_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + st * ATT_TILE_BYTES);
+        for (int w = 0; w < nw; ++w) {
+          if (j > 0) mbar_wait(&s_empty[w], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < ATT_D / 16; ++k) {
+            mma_bf16_ss(tS[w], smem_desc_sw128(q_addr + w * ATT_TILE_BYTES + k * 32, 16, 1024),
+                        smem_desc_sw128(k_addr + k * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[w]);
+        }
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_kv - 1);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax (one row per thread)
+    const int w = (warp - 4) / 4;  // query tile of this warpgroup
+    const int quad = warp % 4;
+    const int r = quad * 32 + lane;                    // row within tile == TMEM lane
+    const int lrow = q0 + w * ATT_BM + r;              // local query row
+    const long qpos = p.offset + lrow;                 // global query position
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const bool active = (w == 0) || has1;
+    if (active && n_kv > 0) {
+      float m_run = -INFINITY, l_run = 0.f;
+      const int tile_first_row = q0 + w * ATT_BM;  // for the mask decision (warp-uniform)
+      for (int j = 0; j < n_kv; ++j) {
+        const int g = j / tps, t = j % tps;
+        const int valid_cols = min(ATT_BN, p.seg_len - t * ATT_BN);
+        const long key0 = (long)g * p.seg_len + (long)t * ATT_BN;
+        const bool need_mask = valid_cols < ATT_BN ||
+                               (p.causal && key0 + ATT_BN - 1 > p.offset + tile_first_row);
+        mbar_wait(&s_full[w], j & 1);
+        tc_fence_after();
+        float s[ATT_BN];
+        {
+          uint32_t rr[64];
+          tmem_ld64(tS[w] + lane_off, rr);
+#pragma unroll
+          for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(rr[i]);
+          tmem_ld64(tS[w] + lane_off + 64, rr);
+#pragma unroll
+          for (int i = 0; i < 64; ++i) s[64 + i] = __uint_as_float(rr[i]);
+        }
+        tc_fence_before();
+        mbar_arrive(&s_empty[w]);
+        if (need_mask) {
+          const long lim = p.causal ? (qpos - key0) : (long)(ATT_BN - 1);
+#pragma unroll
+          for (int c = 0; c < ATT_BN; ++c)
+            if (c >= valid_cols || (long)c > lim) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < ATT_BN; ++c) mx = fmaxf(mx, s[c]);
+        const float m_tile = mx * p.scale_log2;
+        float alpha = 1.f;
+        bool rescale = false;
+        if (m_tile > m_run + 8.f) {  // also true on the first tile (m_run = -inf)
+          alpha = ex2(m_run - m_tile);
+          rescale = (j > 0);
+          m_run = m_tile;
+        }
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        float sum = 0.f;
+        uint32_t pk[ATT_BN / 2];
+#pragma unroll
+        for (int c = 0; c < ATT_BN; c += 2) {
+          const float e0 = ex2(fmaf(s[c], p.scale_log2, -m_use));
+          const float e1 = ex2(fmaf(s[c + 1], p.scale_log2, -m_use));
+          sum += e0 + e1;
+          pk[c / 2] = pack_bf16(e0, e1);
+        }
+        l_run = l_run * alpha + sum;
+        if (j > 0) {
+          mbar_wait(&o_full[w], (j - 1) & 1);  // PV_{j-1} done: P buffer free, O stable
+          tc_fence_after();
+        }
+        // tcgen05.ld/st are warp-collective: rescale the whole warp's rows if any row needs it
+        if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+          for (int c = 0; c < ATT_D / 32; ++c) {
+            uint32_t oo[32];
+            tmem_ld32(tO[w] + lane_off + c * 32, oo);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) oo[i] = __float_as_uint(__uint_as_float(oo[i]) * alpha);
+            tmem_st32(tO[w] + lane_off + c * 32, oo);
+          }
+        }
+        {
+          uint32_t p0[32], p1[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            p0[i] = pk[i];
+            p1[i] = pk[32 + i];
+          }
+          tmem_st32(tP[w] + lane_off + 0, p0);
+          tmem_st32(tP[w] + lane_off + 32, p1);
+        }
+        tc_fence_before();
+        mbar_arrive(&p_full[w]);
+      }
+      // ---------------------------------------------- epilogue
+      mbar_wait(&o_full[w], (n_kv - 1) & 1);
+      tc_fence_after();
+      uint32_t oo[ATT_D];
+      tmem_ld64(tO[w] + lane_off, oo);
+      if (lrow < p.m) {
+        const float inv = 1.f / l_run;
+        uint4* dst = reinterpret_cast<uint4*>(p.o + ((long)b * p.m + lrow) * E + h * ATT_D);
+#pragma unroll
+        for (int i = 0; i < ATT_D / 8; ++i) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(oo[8 * i + 0]) * inv, __uint_as_float(oo[8 * i + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(oo[8 * i + 2]) * inv, __uint_as_float(oo[8 * i + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(oo[8 * i + 4]) * inv, __uint_as_float(oo[8 * i + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(oo[8 * i + 6]) * inv, __uint_as_float(oo[8 * i + 7]) * inv);
+          dst[i] = v;
+        }
+        p.lse2[((long)b * p.H + h) * p.m_pad + lrow] = m_run + __log2f(l_run);
+      } else if (lrow < p.m_pad) {
+        p.lse2[((long)b * p.H + h) * p.m_pad + lrow] = INFINITY;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace lss

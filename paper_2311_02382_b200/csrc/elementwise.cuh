@@ -1,0 +1,223 @@
+// HBM-bound kernels around the attention core: LayerNorm fwd/bwd (nnops.py:199-227),
+// weight staging, casts fused with bias-gradient column sums, the attention
+// backward's per-row delta = rowsum(dO * O), and rank-local helpers.
+#pragma once
+#include "common.cuh"
+
+namespace lss {
+
+template <typename T>
+LSS_DEV void store4(T* dst, float a, float b, float c, float d);
+template <>
+LSS_DEV void store4<float>(float* dst, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(dst) = make_float4(a, b, c, d);
+}
+template <>
+LSS_DEV void store4<__nv_bfloat16>(__nv_bfloat16* dst, float a, float b, float c, float d) {
+  uint2 v;
+  v.x = pack_bf16(a, b);
+  v.y = pack_bf16(c, d);
+  *reinterpret_cast<uint2*>(dst) = v;
+}
+
+LSS_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide sum for blockDim.x <= 1024; `red` has >= 32 floats
+LSS_DEV float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) / 32;
+  float t = (l < nw) ? red[l] : 0.f;
+  return warp_sum(t);
+}
+
+// One block per row; each thread owns 4 consecutive features (E % 4 == 0, E <= 4*blockDim).
+template <typename TOut>
+__global__ void layernorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                     const float* __restrict__ bias, TOut* __restrict__ y,
+                                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                     int E, float eps) {
+  __shared__ float red[32];
+  const long row = blockIdx.x;
+  const int c = threadIdx.x * 4;
+  const bool ok = c < E;
+  float4 v = ok ? *reinterpret_cast<const float4*>(x + row * E + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float mu = block_sum(v.x + v.y + v.z + v.w, red) / E;
+  const float a = v.x - mu, b_ = v.y - mu, cc = v.z - mu, d = v.w - mu;
+  const float var = block_sum(ok ? a * a + b_ * b_ + cc * cc + d * d : 0.f, red) / E;
+  const float rs = rsqrtf(var + eps);
+  if (ok) {
+    const float4 g = *reinterpret_cast<const float4*>(gain + c);
+    const float4 bb = *reinterpret_cast<const float4*>(bias + c);
+    store4<TOut>(y + row * E + c, a * rs * g.x + bb.x, b_ * rs * g.y + bb.y, cc * rs * g.z + bb.z,
+                 d * rs * g.w + bb.w);
+  }
+  if (threadIdx.x == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = rs;
+  }
+}
+
+// gx = grad_res + rstd*(g - mean(g) - xhat*mean(g*xhat)), g = gxh*gain (nnops.py:211-227).
+// Each block handles ROWS rows; column partial sums of gxh*xhat and gxh are
+// accumulated in registers and added (scaled by alpha) to g_gain / g_bias once.
+constexpr int LN_BWD_ROWS = 16;
+__global__ void layernorm_bwd_kernel(const float* __restrict__ gxh, const float* __restrict__ x,
+                                     const float* __restrict__ mean, const float* __restrict__ rstd,
+                                     const float* __restrict__ gain, const float* __restrict__ grad_res,
+                                     float* __restrict__ gx, float* __restrict__ g_gain,
+                                     float* __restrict__ g_bias, float alpha, long rows, int E) {
+  __shared__ float red[32];
+  const int c = threadIdx.x * 4;
+  const bool ok = c < E;
+  float4 gg = make_float4(0.f, 0.f, 0.f, 0.f), gb = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 w = ok ? *reinterpret_cast<const float4*>(gain + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const long r0 = (long)blockIdx.x * LN_BWD_ROWS;
+  for (int i = 0; i < LN_BWD_ROWS; ++i) {
+    const long row = r0 + i;
+    if (row >= rows) break;
+    const float mu = mean[row], rs = rstd[row];
+    float4 gy = make_float4(0.f, 0.f, 0.f, 0.f), xv = gy;
+    if (ok) {
+      gy = *reinterpret_cast<const float4*>(gxh + row * E + c);
+      xv = *reinterpret_cast<const float4*>(x + row * E + c);
+    }
+    const float xh0 = (xv.x - mu) * rs, xh1 = (xv.y - mu) * rs, xh2 = (xv.z - mu) * rs,
+                xh3 = (xv.w - mu) * rs;
+    gg.x += gy.x * xh0; gg.y += gy.y * xh1; gg.z += gy.z * xh2; gg.w += gy.w * xh3;
+    gb.x += gy.x; gb.y += gy.y; gb.z += gy.z; gb.w += gy.w;
+    const float g0 = gy.x * w.x, g1 = gy.y * w.y, g2 = gy.z * w.z, g3 = gy.w * w.w;
+    const float mg = block_sum(ok ? g0 + g1 + g2 + g3 : 0.f, red) / E;
+    const float mgx = block_sum(ok ? g0 * xh0 + g1 * xh1 + g2 * xh2 + g3 * xh3 : 0.f, red) / E;
+    if (ok) {
+      float4 res = grad_res ? *reinterpret_cast<const float4*>(grad_res + row * E + c)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(gx + row * E + c) =
+          make_float4(res.x + rs * (g0 - mg - xh0 * mgx), res.y + rs * (g1 - mg - xh1 * mgx),
+                      res.z + rs * (g2 - mg - xh2 * mgx), res.w + rs * (g3 - mg - xh3 * mgx));
+    }
+  }
+  if (ok) {
+    atomicAdd(g_gain + c + 0, alpha * gg.x); atomicAdd(g_gain + c + 1, alpha * gg.y);
+    atomicAdd(g_gain + c + 2, alpha * gg.z); atomicAdd(g_gain + c + 3, alpha * gg.w);
+    atomicAdd(g_bias + c + 0, alpha * gb.x); atomicAdd(g_bias + c + 1, alpha * gb.y);
+    atomicAdd(g_bias + c + 2, alpha * gb.z); atomicAdd(g_bias + c + 3, alpha * gb.w);
+  }
+}
+
+// Concatenate up to 3 fp32 column blocks of `rows` rows into one row-major
+// destination (bf16 or fp32), and add alpha * column sums into colsum (optional).
+// Used for: grad_y -> bf16 (+ d bias_out), [dQ | dK dV] -> bf16 dQKV (+ d b_qkv).
+struct CatSrc {
+  const float* ptr[3];
+  long ld[3];
+  int cols[3];
+  int n;
+};
+constexpr int CAT_ROWS = 32;
+template <typename TOut>
+__global__ void cat_cast_colsum_kernel(CatSrc src, TOut* __restrict__ dst, long ld_dst,
+                                       float* __restrict__ colsum, float alpha, long rows) {
+  // grid.x over 4-column groups (blockDim.x threads each), grid.y over row blocks
+  const int col4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  int s = 0, base = 0;
+  while (s < src.n && col4 >= base + src.cols[s]) base += src.cols[s++];
+  if (s >= src.n) return;
+  const int lc = col4 - base;
+  const float* sp = src.ptr[s];
+  const long ld = src.ld[s];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const long r0 = (long)blockIdx.y * CAT_ROWS;
+  for (int i = 0; i < CAT_ROWS; ++i) {
+    const long r = r0 + i;
+    if (r >= rows) break;
+    const float4 v = *reinterpret_cast<const float4*>(sp + r * ld + lc);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    if (dst) store4<TOut>(dst + r * ld_dst + col4, v.x, v.y, v.z, v.w);
+  }
+  if (colsum) {
+    atomicAdd(colsum + col4 + 0, alpha * acc.x);
+    atomicAdd(colsum + col4 + 1, alpha * acc.y);
+    atomicAdd(colsum + col4 + 2, alpha * acc.z);
+    atomicAdd(colsum + col4 + 3, alpha * acc.w);
+  }
+}
+
+// Weight staging for the GEMMs (reference weights are [d_in, d_out], y = x W + b):
+//   wqkv_t [3E][E] = [Wq | Wk | Wv]^T  (K-major B operand of the forward projection)
+//   wqkv   [E][3E] = [Wq | Wk | Wv]    (K-major B operand of the input-gradient GEMM)
+//   wo_t   [E][E]  = Wo^T, wo [E][E] = Wo
+//   bqkv   [3E]    = [bq | bk | bv]
+template <typename TW>
+__global__ void weight_stage_kernel(const float* __restrict__ wq, const float* __restrict__ wk,
+                                    const float* __restrict__ wv, const float* __restrict__ wo,
+                                    const float* __restrict__ bq, const float* __restrict__ bk,
+                                    const float* __restrict__ bv, TW* __restrict__ wqkv_t,
+                                    TW* __restrict__ wqkv, TW* __restrict__ wo_t, TW* __restrict__ wo_n,
+                                    float* __restrict__ bqkv, int E) {
+  __shared__ float tile[32][33];
+  const int which = blockIdx.z;  // 0..3 = q,k,v,o
+  const float* w = which == 0 ? wq : which == 1 ? wk : which == 2 ? wv : wo;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;  // rows (in), cols (out)
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r, j = j0 + threadIdx.x;
+    float v = 0.f;
+    if (i < E && j < E) {
+      v = w[(long)i * E + j];
+      if (which < 3) wqkv[(long)i * 3 * E + which * E + j] = TW(v);
+      else wo_n[(long)i * E + j] = TW(v);
+    }
+    tile[r][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int j = j0 + r, i = i0 + threadIdx.x;  // transposed: row j (out), col i (in)
+    if (i < E && j < E) {
+      const float v = tile[threadIdx.x][r];
+      if (which < 3) wqkv_t[((long)which * E + j) * E + i] = TW(v);
+      else wo_t[(long)j * E + i] = TW(v);
+    }
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && which < 3) {
+    const float* bsrc = which == 0 ? bq : which == 1 ? bk : bv;
+    for (int j = threadIdx.y * blockDim.x + threadIdx.x; j < E; j += blockDim.x * blockDim.y)
+      bqkv[which * E + j] = bsrc ? bsrc[j] : 0.f;
+  }
+}
+
+// delta[b][h][row] = sum_d dO[b,row,h*d+k] * O[b,row,h*d+k], padded rows set to 0.
+template <typename T>
+__global__ void attn_delta_kernel(const T* __restrict__ dO, const T* __restrict__ O,
+                                  float* __restrict__ delta, int B, int m, int m_pad, int H, int d) {
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;  // over B*m_pad*H
+  const long total = (long)B * m_pad * H;
+  if (idx >= total) return;
+  const int h = idx % H;
+  const long br = idx / H;
+  const int row = br % m_pad;
+  const int b = br / m_pad;
+  float acc = 0.f;
+  if (row < m) {
+    const T* a = dO + ((long)b * m + row) * (long)H * d + (long)h * d;
+    const T* o = O + ((long)b * m + row) * (long)H * d + (long)h * d;
+    for (int k = 0; k < d; ++k) acc += float(a[k]) * float(o[k]);
+  }
+  delta[((long)b * H + h) * m_pad + row] = acc;
+}
+
+// Write +inf into the padded tail of a [B*H][m_pad] log-sum-exp buffer.
+__global__ void pad_fill_kernel(float* __restrict__ buf, long nrows, int m, int m_pad, float v) {
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int pad = m_pad - m;
+  if (pad <= 0 || idx >= nrows * pad) return;
+  buf[(idx / pad) * m_pad + m + (idx % pad)] = v;
+}
+
+}  // namespace lss

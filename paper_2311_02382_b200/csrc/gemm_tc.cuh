@@ -1,0 +1,224 @@
+// tcgen05/TMEM/TMA GEMM for the LSS projections (sm_100a).
+//
+//   C[M, N] = alpha * (A[M, K] . B[N, K]^T) (+ bias[N]) (+ residual[M, N])
+//
+// A and B are bf16 and may each be K-major (row-major with K contiguous) or
+// MN-major (row-major with M resp. N contiguous), which covers every product
+// the attention half of model.layer_fwd / layer_bwd needs without transposing
+// activations:
+//   fwd  [Q|K|V] = xh . [Wq|Wk|Wv]          (A K-major, B = W^T cached K-major)
+//        y       = x + ctx . Wo + bo         (residual epilogue)
+//   bwd  dctx    = dy . Wo^T                 (B = Wo as stored, K-major)
+//        dW      = xh^T . dy                 (A M-major, B N-major; fp32 out, alpha = 1/(D*N))
+// (reference: nnops.linear_fwd/linear_bwd, nnops.py:180-193; model.linear3, model.py:237-245)
+//
+// Persistent warp-specialised kernel: warp 0 = TMA producer, warp 1 = MMA
+// issuer (one thread), warp 2 = TMEM allocator, warps 4..7 = epilogue
+// (TMEM -> registers -> global).  Tile 128 x 256 x 64, 4-stage smem ring,
+// double-buffered TMEM accumulator (2 x 256 columns) so the epilogue of tile i
+// overlaps the mainloop of tile i+1.
+#pragma once
+#include "common.cuh"
+
+namespace lss {
+
+struct GemmEpilogue {
+  void* out[3];          // up to three column segments (e.g. Q / K|V destinations)
+  long ldo[3];           // leading dimension (elements) of each segment
+  int seg_width;         // columns per segment (multiple of 32); segment s covers [s*w, (s+1)*w)
+  int out_bf16;          // 1: bf16 output, 0: fp32 output
+  float alpha;
+  const float* bias;     // [N] or null
+  const float* residual; // [M, ld_res] fp32 or null
+  long ld_res;
+};
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BN = 256;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;  // 16 KB
+constexpr int GEMM_B_BYTES = GEMM_BN * GEMM_BK * 2;  // 32 KB
+constexpr int GEMM_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES;
+constexpr int GEMM_SMEM_BYTES = GEMM_STAGES * GEMM_STAGE_BYTES + 1024 /*align*/ + 256 /*bars*/;
+constexpr int GEMM_THREADS = 256;
+
+template <int A_MN, int B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                        GemmEpilogue ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + GEMM_STAGES * GEMM_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + GEMM_STAGES;
+  uint64_t* tfull_bar = empty_bar + GEMM_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int m_tiles = (M + GEMM_BM - 1) / GEMM_BM;
+  const int n_tiles = (N + GEMM_BN - 1) / GEMM_BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < GEMM_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile / n_tiles) * GEMM_BM;
+        const int n0 = (tile % n_tiles) * GEMM_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * GEMM_STAGE_BYTES;
+          uint8_t* sb = sa + GEMM_A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], GEMM_STAGE_BYTES);
+          const int k0 = kb * GEMM_BK;
+          if (A_MN) {
+            tma_load_2d(&tmA, &full_bar[stage], sa, m0, k0);
+            tma_load_2d(&tmA, &full_bar[stage], sa + 8192, m0 + 64, k0);
+          } else {
+            tma_load_2d(&tmA, &full_bar[stage], sa, k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tma_load_2d(&tmB, &full_bar[stage], sb + i * 8192, n0 + 64 * i, k0);
+          } else {
+            tma_load_2d(&tmB, &full_bar[stage], sb, k0, n0);
+          }
+          if (++stage == GEMM_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, GEMM_BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const int buf = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty_bar[buf], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * GEMM_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * GEMM_STAGE_BYTES);
+          const uint32_t sb = sa + GEMM_A_BYTES;
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            const uint64_t ad = A_MN ? smem_desc_sw128(sa + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(sb + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(sb + k * 32, 16, 1024);
+            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == GEMM_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: thread <-> accumulator row
+    const int quad = warp - 4;
+    const int row_in_tile = quad * 32 + lane;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int buf = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const int m0 = (tile / n_tiles) * GEMM_BM;
+      const int n0 = (tile % n_tiles) * GEMM_BN;
+      mbar_wait(&tfull_bar[buf], acc_phase);
+      tc_fence_after();
+      const int row = m0 + row_in_tile;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < GEMM_BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + buf * GEMM_BN + c, r);
+        const int n = n0 + c;
+        if (!row_ok || n >= N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * ep.alpha;
+        if (ep.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += __ldg(ep.bias + n + i);
+        }
+        if (ep.residual) {
+          const float4* rp = reinterpret_cast<const float4*>(ep.residual + (long)row * ep.ld_res + n);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 t = rp[i];
+            v[4 * i] += t.x;
+            v[4 * i + 1] += t.y;
+            v[4 * i + 2] += t.z;
+            v[4 * i + 3] += t.w;
+          }
+        }
+        const int seg = n / ep.seg_width;
+        const long col = n - (long)seg * ep.seg_width;
+        if (ep.out_bf16) {
+          uint4* op = reinterpret_cast<uint4*>(
+              reinterpret_cast<__nv_bfloat16*>(ep.out[seg]) + (long)row * ep.ldo[seg] + col);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 t;
+            t.x = pack_bf16(v[8 * i + 0], v[8 * i + 1]);
+            t.y = pack_bf16(v[8 * i + 2], v[8 * i + 3]);
+            t.z = pack_bf16(v[8 * i + 4], v[8 * i + 5]);
+            t.w = pack_bf16(v[8 * i + 6], v[8 * i + 7]);
+            op[i] = t;
+          }
+        } else {
+          float4* op =
+              reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out[seg]) + (long)row * ep.ldo[seg] + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[buf]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+}  // namespace lss

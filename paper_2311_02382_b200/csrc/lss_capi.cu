@@ -1,0 +1,390 @@
+// extern "C" entry points of liblss.so (declared in include/lss.h).
+// Host-side validation (mirroring the reference's ShapeError / PartitionError
+// checks), TMA tensor-map construction and kernel launches.  No allocation,
+// no host synchronisation: every call is ordered on the caller's stream.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/lss.h"
+#include "attn_bwd.cuh"
+#include "attn_fwd.cuh"
+#include "check_f32.cuh"
+#include "elementwise.cuh"
+#include "gemm_tc.cuh"
+
+using namespace lss;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return LSS_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 tensor map with 128B swizzle; dims[0] is the contiguous dimension.
+int make_map(CUtensorMap* m, CUtensorMapDataType dt, int elem_bytes, int rank, const void* addr,
+             const uint64_t* dims, const uint64_t* strides_elems, const uint32_t* box,
+             CUtensorMapSwizzle sw) {
+  auto fn = encode_fn();
+  if (!fn) return fail(LSS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[5], gstr[4];
+  cuuint32_t bdim[5], estr[5];
+  for (int i = 0; i < rank; ++i) {
+    gdim[i] = dims[i];
+    bdim[i] = box[i];
+    estr[i] = 1;
+  }
+  for (int i = 0; i < rank - 1; ++i) gstr[i] = strides_elems[i] * elem_bytes;
+  CUresult r = fn(m, dt, rank, const_cast<void*>(addr), gdim, gstr, bdim, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LSS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return LSS_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename K>
+int set_smem(K kernel, int bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  return LSS_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int lss_abi_version(void) { return LSS_ABI_VERSION; }
+const char* lss_last_error(void) { return g_last_error.c_str(); }
+long lss_rows_pad(long rows) { return (rows + ATT_BM - 1) / ATT_BM * ATT_BM; }
+
+int lss_layernorm_fwd(const float* x, const float* gain, const float* bias, void* y, int y_dtype,
+                      float* mean, float* rstd, long rows, int embed, float eps, void* stream) {
+  if (!x || !gain || !bias || !y || !mean || !rstd) return fail(LSS_ERR_ARG, "layernorm_fwd: null pointer");
+  if (embed <= 0 || embed % 4 || embed > 4096) return fail(LSS_ERR_UNSUPPORTED, "layernorm_fwd: embed %d", embed);
+  if (rows <= 0) return LSS_OK;
+  const int threads = ((embed / 4 + 31) / 32) * 32;
+  if (y_dtype == LSS_BF16)
+    layernorm_fwd_kernel<__nv_bfloat16><<<rows, threads, 0, S(stream)>>>(
+        x, gain, bias, reinterpret_cast<__nv_bfloat16*>(y), mean, rstd, embed, eps);
+  else if (y_dtype == LSS_F32)
+    layernorm_fwd_kernel<float><<<rows, threads, 0, S(stream)>>>(x, gain, bias, reinterpret_cast<float*>(y),
+                                                                 mean, rstd, embed, eps);
+  else
+    return fail(LSS_ERR_ARG, "layernorm_fwd: dtype %d", y_dtype);
+  return check_launch("layernorm_fwd");
+}
+
+int lss_layernorm_bwd(const float* grad_xh, const float* x, const float* mean, const float* rstd,
+                      const float* gain, const float* grad_res, float* grad_x, float* grad_gain,
+                      float* grad_bias, float alpha, long rows, int embed, void* stream) {
+  if (!grad_xh || !x || !mean || !rstd || !gain || !grad_x || !grad_gain || !grad_bias)
+    return fail(LSS_ERR_ARG, "layernorm_bwd: null pointer");
+  if (embed <= 0 || embed % 4 || embed > 4096) return fail(LSS_ERR_UNSUPPORTED, "layernorm_bwd: embed %d", embed);
+  if (rows <= 0) return LSS_OK;
+  const int threads = ((embed / 4 + 31) / 32) * 32;
+  const long blocks = (rows + LN_BWD_ROWS - 1) / LN_BWD_ROWS;
+  layernorm_bwd_kernel<<<blocks, threads, 0, S(stream)>>>(grad_xh, x, mean, rstd, gain, grad_res, grad_x,
+                                                          grad_gain, grad_bias, alpha, rows, embed);
+  return check_launch("layernorm_bwd");
+}
+
+int lss_gemm(int dtype, const void* A, long lda, int a_mn_major, const void* B, long ldb, int b_mn_major,
+             int M, int N, int K, const lss_gemm_epilogue* ep_in, void* stream) {
+  if (!A || !B || !ep_in) return fail(LSS_ERR_ARG, "gemm: null pointer");
+  if (M < 0 || N < 0 || K < 0) return fail(LSS_ERR_SHAPE, "gemm: negative extent");
+  if (M == 0 || N == 0) return LSS_OK;
+  GemmEpilogue ep;
+  for (int i = 0; i < 3; ++i) {
+    ep.out[i] = ep_in->out[i];
+    ep.ldo[i] = ep_in->ldo[i];
+  }
+  ep.seg_width = ep_in->seg_width > 0 ? ep_in->seg_width : N;
+  ep.out_bf16 = ep_in->out_dtype == LSS_BF16;
+  ep.alpha = ep_in->alpha;
+  ep.bias = ep_in->bias;
+  ep.residual = ep_in->residual;
+  ep.ld_res = ep_in->ld_res;
+  const int nseg = (N + ep.seg_width - 1) / ep.seg_width;
+  if (nseg > 3) return fail(LSS_ERR_SHAPE, "gemm: %d output segments (max 3)", nseg);
+  for (int s = 0; s < nseg; ++s)
+    if (!ep.out[s]) return fail(LSS_ERR_ARG, "gemm: output segment %d is null", s);
+
+  if (dtype == LSS_F32) {
+    if (ep.out_bf16) return fail(LSS_ERR_UNSUPPORTED, "gemm f32: bf16 output");
+    const float* a = reinterpret_cast<const float*>(A);
+    const float* b = reinterpret_cast<const float*>(B);
+    const long sam = a_mn_major ? 1 : lda, sak = a_mn_major ? lda : 1;
+    const long sbn = b_mn_major ? 1 : ldb, sbk = b_mn_major ? ldb : 1;
+    dim3 grid((N + SG_T - 1) / SG_T, (M + SG_T - 1) / SG_T);
+    gemm_f32_simt_kernel<<<grid, 256, 0, S(stream)>>>(a, sam, sak, b, sbn, sbk, M, N, K, ep);
+    return check_launch("gemm_f32");
+  }
+  if (dtype != LSS_BF16) return fail(LSS_ERR_ARG, "gemm: dtype %d", dtype);
+  if (N % 32 || ep.seg_width % 32) return fail(LSS_ERR_UNSUPPORTED, "gemm bf16: N=%d seg=%d not multiples of 32", N, ep.seg_width);
+  if (K % 8 || lda % 8 || ldb % 8 || (a_mn_major && M % 8) || (b_mn_major && N % 8))
+    return fail(LSS_ERR_UNSUPPORTED, "gemm bf16: 16-byte row alignment required");
+  if (!aligned16(A) || !aligned16(B)) return fail(LSS_ERR_UNSUPPORTED, "gemm bf16: operands not 16B aligned");
+  CUtensorMap ma, mb;
+  int rc;
+  {
+    uint64_t dims[2], str[1] = {(uint64_t)lda};
+    uint32_t box[2];
+    if (a_mn_major) { dims[0] = M; dims[1] = K; box[0] = 64; box[1] = 64; }
+    else            { dims[0] = K; dims[1] = M; box[0] = 64; box[1] = GEMM_BM; }
+    if ((rc = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, A, dims, str, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  {
+    uint64_t dims[2], str[1] = {(uint64_t)ldb};
+    uint32_t box[2];
+    if (b_mn_major) { dims[0] = N; dims[1] = K; box[0] = 64; box[1] = 64; }
+    else            { dims[0] = K; dims[1] = N; box[0] = 64; box[1] = GEMM_BN; }
+    if ((rc = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, B, dims, str, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + GEMM_BN - 1) / GEMM_BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+#define LSS_GEMM_LAUNCH(AM, BM_)                                                                  \
+  do {                                                                                             \
+    if ((rc = set_smem(gemm_bf16_tc_kernel<AM, BM_>, GEMM_SMEM_BYTES))) return rc;                \
+    gemm_bf16_tc_kernel<AM, BM_><<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, S(stream)>>>(ma, mb, M, N, K, ep); \
+  } while (0)
+  if (!a_mn_major && !b_mn_major) LSS_GEMM_LAUNCH(0, 0);
+  else if (!a_mn_major && b_mn_major) LSS_GEMM_LAUNCH(0, 1);
+  else if (a_mn_major && !b_mn_major) LSS_GEMM_LAUNCH(1, 0);
+  else LSS_GEMM_LAUNCH(1, 1);
+#undef LSS_GEMM_LAUNCH
+  return check_launch("gemm_bf16_tc");
+}
+
+int lss_stage_weights(int dtype, const float* wq, const float* wk, const float* wv, const float* wo,
+                      const float* bq, const float* bk, const float* bv, void* wqkv_t, void* wqkv,
+                      void* wo_t, void* wo_n, float* bqkv, int embed, void* stream) {
+  if (!wq || !wk || !wv || !wo || !wqkv_t || !wqkv || !wo_t || !wo_n || !bqkv)
+    return fail(LSS_ERR_ARG, "stage_weights: null pointer");
+  dim3 grid((embed + 31) / 32, (embed + 31) / 32, 4), block(32, 8);
+  if (dtype == LSS_BF16)
+    weight_stage_kernel<__nv_bfloat16><<<grid, block, 0, S(stream)>>>(
+        wq, wk, wv, wo, bq, bk, bv, reinterpret_cast<__nv_bfloat16*>(wqkv_t),
+        reinterpret_cast<__nv_bfloat16*>(wqkv), reinterpret_cast<__nv_bfloat16*>(wo_t),
+        reinterpret_cast<__nv_bfloat16*>(wo_n), bqkv, embed);
+  else if (dtype == LSS_F32)
+    weight_stage_kernel<float><<<grid, block, 0, S(stream)>>>(
+        wq, wk, wv, wo, bq, bk, bv, reinterpret_cast<float*>(wqkv_t), reinterpret_cast<float*>(wqkv),
+        reinterpret_cast<float*>(wo_t), reinterpret_cast<float*>(wo_n), bqkv, embed);
+  else
+    return fail(LSS_ERR_ARG, "stage_weights: dtype %d", dtype);
+  return check_launch("stage_weights");
+}
+
+int lss_cat_cast_colsum(int out_dtype, const float* const* srcs, const long* lds, const int* cols,
+                        int nsrc, void* dst, long ld_dst, float* colsum, float alpha, long rows,
+                        void* stream) {
+  if (nsrc < 1 || nsrc > 3 || !srcs || !lds || !cols) return fail(LSS_ERR_ARG, "cat_cast_colsum: bad sources");
+  CatSrc cs;
+  int total = 0;
+  for (int i = 0; i < 3; ++i) {
+    cs.ptr[i] = i < nsrc ? srcs[i] : nullptr;
+    cs.ld[i] = i < nsrc ? lds[i] : 0;
+    cs.cols[i] = i < nsrc ? cols[i] : 0;
+    if (i < nsrc) {
+      if (!srcs[i] || cols[i] % 4 || lds[i] % 4) return fail(LSS_ERR_UNSUPPORTED, "cat_cast_colsum: source %d", i);
+      total += cols[i];
+    }
+  }
+  cs.n = nsrc;
+  if (rows <= 0) return LSS_OK;
+  const int threads = 128;
+  dim3 grid((total / 4 + threads - 1) / threads, (rows + CAT_ROWS - 1) / CAT_ROWS);
+  if (out_dtype == LSS_BF16)
+    cat_cast_colsum_kernel<__nv_bfloat16><<<grid, threads, 0, S(stream)>>>(
+        cs, reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, colsum, alpha, rows);
+  else
+    cat_cast_colsum_kernel<float><<<grid, threads, 0, S(stream)>>>(cs, reinterpret_cast<float*>(dst), ld_dst,
+                                                                   colsum, alpha, rows);
+  return check_launch("cat_cast_colsum");
+}
+
+static int attn_check(int dtype, int batch, int rows, int workers, int seg_len, int heads, int head_dim) {
+  if (batch <= 0 || rows <= 0 || workers <= 0 || seg_len <= 0 || heads <= 0 || head_dim <= 0)
+    return fail(LSS_ERR_SHAPE, "attention: non-positive extent");
+  if (dtype == LSS_BF16 && head_dim != ATT_D)
+    return fail(LSS_ERR_UNSUPPORTED, "attention bf16: head_dim %d (tcgen05 path supports 64)", head_dim);
+  if (dtype == LSS_F32 && head_dim > 128)
+    return fail(LSS_ERR_UNSUPPORTED, "attention f32: head_dim %d > 128", head_dim);
+  if (dtype != LSS_BF16 && dtype != LSS_F32) return fail(LSS_ERR_ARG, "attention: dtype %d", dtype);
+  return LSS_OK;
+}
+
+int lss_attn_fwd(int dtype, const void* q, const void* kv, void* o, float* lse2, int batch, int rows,
+                 int workers, int seg_len, int heads, int head_dim, long offset, int causal, void* stream) {
+  int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
+  if (rc) return rc;
+  if (!q || !kv || !o || !lse2) return fail(LSS_ERR_ARG, "attn_fwd: null pointer");
+  if (causal && offset < 0) return fail(LSS_ERR_DEGENERATE, "attn_fwd: negative offset leaves rows fully masked");
+  const int E = heads * head_dim;
+  const int m_pad = (int)lss_rows_pad(rows);
+  const float scale = 1.0f / sqrtf((float)head_dim);
+  if (dtype == LSS_F32) {
+    dim3 grid((rows + 3) / 4, heads, batch);
+    attn_fwd_f32_kernel<<<grid, 128, 0, S(stream)>>>(
+        reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(kv), reinterpret_cast<float*>(o), lse2,
+        batch, rows, m_pad, workers, seg_len, heads, head_dim, offset, causal, scale);
+    return check_launch("attn_fwd_f32");
+  }
+  if (!aligned16(q) || !aligned16(kv) || !aligned16(o)) return fail(LSS_ERR_UNSUPPORTED, "attn_fwd: 16B alignment");
+  CUtensorMap mq, mkv;
+  {
+    uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
+    uint64_t str[2] = {(uint64_t)E, (uint64_t)rows * E};
+    uint32_t box[3] = {64, 128, 1};
+    if ((rc = make_map(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, q, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  {
+    uint64_t dims[4] = {(uint64_t)2 * E, (uint64_t)seg_len, (uint64_t)batch, (uint64_t)workers};
+    uint64_t str[3] = {(uint64_t)2 * E, (uint64_t)seg_len * 2 * E, (uint64_t)batch * seg_len * 2 * E};
+    uint32_t box[4] = {64, 128, 1, 1};
+    if ((rc = make_map(&mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, kv, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  AttnFwdParams p;
+  p.B = batch; p.m = rows; p.m_pad = m_pad; p.G = workers; p.seg_len = seg_len; p.H = heads;
+  p.offset = offset; p.causal = causal;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.o = reinterpret_cast<__nv_bfloat16*>(o);
+  p.lse2 = lse2;
+  if ((rc = set_smem(attn_fwd_tc_kernel, ATT_FWD_SMEM))) return rc;
+  dim3 grid((rows + 2 * ATT_BM - 1) / (2 * ATT_BM), heads, batch);
+  attn_fwd_tc_kernel<<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mkv, p);
+  return check_launch("attn_fwd_tc");
+}
+
+int lss_attn_bwd(int dtype, const void* q, const void* kv, const void* o, const void* grad_o, const float* lse2,
+                 float* delta_ws, float* grad_q, float* grad_kv, int batch, int rows, int workers, int seg_len,
+                 int heads, int head_dim, long offset, int causal, void* stream) {
+  int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
+  if (rc) return rc;
+  if (!q || !kv || !o || !grad_o || !lse2 || !delta_ws || !grad_q || !grad_kv)
+    return fail(LSS_ERR_ARG, "attn_bwd: null pointer");
+  const int E = heads * head_dim;
+  const int m_pad = (int)lss_rows_pad(rows);
+  const float scale = 1.0f / sqrtf((float)head_dim);
+  {
+    const long total = (long)batch * m_pad * heads;
+    const int threads = 256;
+    if (dtype == LSS_BF16)
+      attn_delta_kernel<__nv_bfloat16><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
+          reinterpret_cast<const __nv_bfloat16*>(grad_o), reinterpret_cast<const __nv_bfloat16*>(o), delta_ws,
+          batch, rows, m_pad, heads, head_dim);
+    else
+      attn_delta_kernel<float><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
+          reinterpret_cast<const float*>(grad_o), reinterpret_cast<const float*>(o), delta_ws, batch, rows, m_pad,
+          heads, head_dim);
+    if ((rc = check_launch("attn_delta"))) return rc;
+  }
+  if (dtype == LSS_F32) {
+    const float* qf = reinterpret_cast<const float*>(q);
+    const float* kvf = reinterpret_cast<const float*>(kv);
+    const float* gof = reinterpret_cast<const float*>(grad_o);
+    dim3 g1((rows + 3) / 4, heads, batch);
+    attn_bwd_dq_f32_kernel<<<g1, 128, 0, S(stream)>>>(qf, kvf, gof, lse2, delta_ws, grad_q, batch, rows, m_pad,
+                                                     workers, seg_len, heads, head_dim, offset, causal, scale);
+    if ((rc = check_launch("attn_bwd_dq_f32"))) return rc;
+    const long t = (long)workers * seg_len;
+    dim3 g2((t + 3) / 4, heads, batch);
+    attn_bwd_dkv_f32_kernel<<<g2, 128, 0, S(stream)>>>(qf, kvf, gof, lse2, delta_ws, grad_kv, batch, rows, m_pad,
+                                                      workers, seg_len, heads, head_dim, offset, causal, scale);
+    return check_launch("attn_bwd_dkv_f32");
+  }
+  if (!aligned16(q) || !aligned16(kv) || !aligned16(grad_o) || !aligned16(grad_q) || !aligned16(grad_kv))
+    return fail(LSS_ERR_UNSUPPORTED, "attn_bwd: 16B alignment");
+  cudaError_t e = cudaMemsetAsync(grad_q, 0, sizeof(float) * (size_t)batch * rows * E, S(stream));
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "attn_bwd memset: %s", cudaGetErrorString(e));
+  CUtensorMap mq, mdo, mkv;
+  {
+    uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
+    uint64_t str[2] = {(uint64_t)E, (uint64_t)rows * E};
+    uint32_t box[3] = {64, 128, 1};
+    if ((rc = make_map(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, q, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+    if ((rc = make_map(&mdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, grad_o, dims, str, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  {
+    uint64_t dims[4] = {(uint64_t)2 * E, (uint64_t)seg_len, (uint64_t)batch, (uint64_t)workers};
+    uint64_t str[3] = {(uint64_t)2 * E, (uint64_t)seg_len * 2 * E, (uint64_t)batch * seg_len * 2 * E};
+    uint32_t box[4] = {64, 128, 1, 1};
+    if ((rc = make_map(&mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, kv, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  AttnBwdParams p;
+  p.B = batch; p.m = rows; p.m_pad = m_pad; p.G = workers; p.seg_len = seg_len; p.H = heads;
+  p.offset = offset; p.causal = causal;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.scale = scale;
+  p.lse2 = lse2; p.delta = delta_ws; p.dq = grad_q; p.dkv = grad_kv;
+  CUtensorMap mdq;
+  {
+    uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
+    uint64_t str[2] = {(uint64_t)E, (uint64_t)rows * E};
+    uint32_t box[3] = {32, 128, 1};
+    if ((rc = make_map(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, grad_q, dims, str, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  if ((rc = set_smem(attn_bwd_tc_kernel, ATB_SMEM))) return rc;
+  const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
+  dim3 grid(workers * tps, heads, batch);
+  attn_bwd_tc_kernel<<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mq, mdo, mkv, mdq, p);
+  return check_launch("attn_bwd_tc");
+}
+
+}  // extern "C"

@@ -1,0 +1,202 @@
+"""Tensor-level wrappers over the C ABI (torch is used for device memory and
+streams only; every op here runs a liblss.so kernel on the current stream).
+
+Precision names follow the reference's ``ModelConfig.precision``
+(model.py:50, tensor.py:24-32): ``"bf16"`` runs the tcgen05 path (bf16
+operands, fp32 accumulation); ``"single"`` is the fp32 check mode (FFMA
+kernels).  ``"double"`` has no GPU path (fp64 tensor throughput is not a
+B200 target) and raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+from ._native import LSS_BF16, LSS_F32, GemmEpilogue, call
+from .errors import ShapeError, UnsupportedError
+
+LAYERNORM_EPS = 1e-5  # nnops.py:28
+
+_DT = {"bf16": LSS_BF16, "single": LSS_F32}
+_TORCH = {LSS_BF16: torch.bfloat16, LSS_F32: torch.float32}
+
+
+def code(precision: str) -> int:
+    try:
+        return _DT[precision]
+    except KeyError:
+        raise UnsupportedError(f"precision {precision!r} has no B200 path (use 'bf16' or 'single')")
+
+
+def act_dtype(precision: str) -> torch.dtype:
+    return _TORCH[code(precision)]
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise ShapeError(f"{name} must be a CUDA tensor (no CPU path)")
+    if not t.is_contiguous():
+        raise ShapeError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ShapeError(f"{name} has dtype {t.dtype}, expected {dtype}")
+
+
+# ----------------------------------------------------------------- LayerNorm
+
+
+def layernorm_fwd(x, gain, bias, out=None, out_dtype=torch.bfloat16, eps=LAYERNORM_EPS):
+    """nnops.layernorm_fwd (nnops.py:199-208) over the last dim.  Returns (y, mean, rstd)."""
+    _need(x, "x", torch.float32)
+    e = x.shape[-1]
+    rows = x.numel() // e
+    if gain.shape != (e,) or bias.shape != (e,):
+        raise ShapeError(f"layernorm gain/bias {tuple(gain.shape)} do not match embed {e}")
+    y = out if out is not None else torch.empty(x.shape, dtype=out_dtype, device=x.device)
+    mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+    rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    dt = LSS_BF16 if y.dtype == torch.bfloat16 else LSS_F32
+    call("lss_layernorm_fwd", _ptr(x), _ptr(gain), _ptr(bias), _ptr(y), dt, _ptr(mean), _ptr(rstd),
+         rows, e, eps, _stream())
+    return y, mean, rstd
+
+
+def layernorm_bwd(grad_xh, x, mean, rstd, gain, grad_res=None, grad_x=None, grad_gain=None,
+                  grad_bias=None, alpha=1.0):
+    """nnops.layernorm_bwd (nnops.py:211-227) + residual (model.py:486).  grad_gain /
+    grad_bias are accumulated (+= alpha * sums); pass zeroed buffers for a plain result."""
+    _need(grad_xh, "grad_xh", torch.float32)
+    _need(x, "x", torch.float32)
+    e = x.shape[-1]
+    rows = x.numel() // e
+    gx = grad_x if grad_x is not None else torch.empty_like(x)
+    gg = grad_gain if grad_gain is not None else torch.zeros(e, dtype=torch.float32, device=x.device)
+    gb = grad_bias if grad_bias is not None else torch.zeros(e, dtype=torch.float32, device=x.device)
+    call("lss_layernorm_bwd", _ptr(grad_xh), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gain),
+         _ptr(grad_res), _ptr(gx), _ptr(gg), _ptr(gb), alpha, rows, e, _stream())
+    return gx, gg, gb
+
+
+# ----------------------------------------------------------------- GEMM
+
+
+def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_dtype=torch.float32, alpha=1.0,
+         bias=None, residual=None, seg_width=0, M=None, N=None, K=None, lda=None, ldb=None):
+    """C = alpha * A.B^T (+bias) (+residual) with A [M,K] or (a_mn_major) [K,M],
+    B [N,K] or (b_mn_major) [K,N].  ``out`` may be a tensor or a list of up to 3
+    (tensor, ld) column segments of ``seg_width`` columns."""
+    dt = LSS_BF16 if a.dtype == torch.bfloat16 else LSS_F32
+    if b.dtype != a.dtype:
+        raise ShapeError("gemm operands must share a dtype")
+    if M is None:
+        M = a.shape[-1] if a_mn_major else a.numel() // a.shape[-1]
+        K = a.numel() // a.shape[-1] if a_mn_major else a.shape[-1]
+    if N is None:
+        N = b.shape[-1] if b_mn_major else b.numel() // b.shape[-1]
+    lda = lda if lda is not None else a.shape[-1]
+    ldb = ldb if ldb is not None else b.shape[-1]
+    ep = GemmEpilogue()
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=a.device)
+    segs = out if isinstance(out, (list, tuple)) else [(out, out.shape[-1])]
+    for i, (t, ld) in enumerate(segs):
+        ep.out[i] = t.data_ptr()
+        ep.ldo[i] = ld
+    ep.seg_width = seg_width if seg_width else N
+    ep.out_dtype = LSS_BF16 if segs[0][0].dtype == torch.bfloat16 else LSS_F32
+    ep.alpha = alpha
+    ep.bias = bias.data_ptr() if bias is not None else None
+    ep.residual = residual.data_ptr() if residual is not None else None
+    ep.ld_res = residual.shape[-1] if residual is not None else 0
+    call("lss_gemm", dt, _ptr(a), lda, int(a_mn_major), _ptr(b), ldb, int(b_mn_major), M, N, K,
+         ctypes.byref(ep), _stream())
+    return out
+
+
+# ----------------------------------------------------------------- weights / casts
+
+
+def stage_weights(wq, wk, wv, wo, bq, bk, bv, precision="bf16", bufs=None):
+    """Stage reference-layout weights ([d_in, d_out]) into the GEMM operand layouts."""
+    e = wq.shape[0]
+    dt = code(precision)
+    tdt = _TORCH[dt]
+    dev = wq.device
+    if bufs is None:
+        bufs = dict(wqkv_t=torch.empty(3 * e, e, dtype=tdt, device=dev),
+                    wqkv=torch.empty(e, 3 * e, dtype=tdt, device=dev),
+                    wo_t=torch.empty(e, e, dtype=tdt, device=dev),
+                    wo=torch.empty(e, e, dtype=tdt, device=dev),
+                    bqkv=torch.empty(3 * e, dtype=torch.float32, device=dev))
+    call("lss_stage_weights", dt, _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(bq), _ptr(bk), _ptr(bv),
+         _ptr(bufs["wqkv_t"]), _ptr(bufs["wqkv"]), _ptr(bufs["wo_t"]), _ptr(bufs["wo"]),
+         _ptr(bufs["bqkv"]), e, _stream())
+    return bufs
+
+
+def cat_cast_colsum(srcs, rows, dst=None, colsum=None, alpha=1.0, out_dtype=torch.bfloat16):
+    """srcs: list of (fp32 tensor, ld, cols).  Writes the column concatenation into
+    ``dst`` (ld = total cols) and accumulates alpha * column sums into ``colsum``."""
+    n = len(srcs)
+    ptrs = (ctypes.c_void_p * n)(*[s[0].data_ptr() for s in srcs])
+    lds = (ctypes.c_long * n)(*[s[1] for s in srcs])
+    cols = (ctypes.c_int * n)(*[s[2] for s in srcs])
+    total = sum(s[2] for s in srcs)
+    dt = LSS_BF16 if (dst is not None and dst.dtype == torch.bfloat16) or (
+        dst is None and out_dtype == torch.bfloat16) else LSS_F32
+    call("lss_cat_cast_colsum", dt, ptrs, lds, cols, n, _ptr(dst), total, _ptr(colsum), alpha, rows,
+         _stream())
+    return dst, colsum
+
+
+# ----------------------------------------------------------------- attention
+
+
+def rows_pad(rows: int) -> int:
+    return _native.rows_pad(rows)
+
+
+def attn_fwd(q, kv, *, workers, seg_len, heads, offset, causal, out=None, lse2=None):
+    """model.scores_fwd core.  q [B,m,E]; kv packed [G,B,seg,2E].  Returns (ctx, lse2)."""
+    _need(q, "q")
+    _need(kv, "kv", q.dtype)
+    bsz, m, e = q.shape
+    if e % heads:
+        raise ShapeError(f"embed {e} not divisible by heads {heads}")
+    if kv.shape != (workers, bsz, seg_len, 2 * e):
+        raise ShapeError(f"kv shape {tuple(kv.shape)} != {(workers, bsz, seg_len, 2 * e)}")
+    dt = LSS_BF16 if q.dtype == torch.bfloat16 else LSS_F32
+    o = out if out is not None else torch.empty_like(q)
+    lse = lse2 if lse2 is not None else torch.empty(bsz, heads, rows_pad(m), dtype=torch.float32,
+                                                   device=q.device)
+    call("lss_attn_fwd", dt, _ptr(q), _ptr(kv), _ptr(o), _ptr(lse), bsz, m, workers, seg_len, heads,
+         e // heads, offset, int(causal), _stream())
+    return o, lse
+
+
+def attn_bwd(q, kv, o, grad_o, lse2, *, workers, seg_len, heads, offset, causal, grad_q=None,
+             grad_kv=None, delta=None):
+    """model.scores_bwd core.  Returns (grad_q fp32 [B,m,E], grad_kv fp32 [G,B,seg,2E])."""
+    for t, n in ((q, "q"), (kv, "kv"), (o, "o"), (grad_o, "grad_o")):
+        _need(t, n, q.dtype)
+    bsz, m, e = q.shape
+    dt = LSS_BF16 if q.dtype == torch.bfloat16 else LSS_F32
+    dev = q.device
+    gq = grad_q if grad_q is not None else torch.empty(bsz, m, e, dtype=torch.float32, device=dev)
+    gkv = grad_kv if grad_kv is not None else torch.empty(workers, bsz, seg_len, 2 * e,
+                                                          dtype=torch.float32, device=dev)
+    dl = delta if delta is not None else torch.empty(bsz, heads, rows_pad(m), dtype=torch.float32,
+                                                     device=dev)
+    call("lss_attn_bwd", dt, _ptr(q), _ptr(kv), _ptr(o), _ptr(grad_o), _ptr(lse2), _ptr(dl), _ptr(gq),
+         _ptr(gkv), bsz, m, workers, seg_len, heads, e // heads, offset, int(causal), _stream())
+    return gq, gkv

@@ -1,0 +1,118 @@
+"""Generate golden fixtures by running the REAL reference (seqpar) on seeded inputs.
+
+Run in the dev container (needs /root/reference):  python tests/golden/make_golden.py
+
+For each case the reference's own layer code runs on G simulated workers
+(threads + its Communicator), exactly as sharded.forward/backward wire it
+(sharded.py:138-143 fused kv_fwd, 186-190 fused kv_bwd, 219-244 sync):
+model.layer_fwd / model.layer_bwd (model.py:424-499) with the FFN half's
+weights set to zero so the layer reduces to its attention half (the FFN then
+adds exactly 0 and its backward passes grad_out through unchanged).
+
+Inputs are rounded to float32 and then computed in float64 ("double"
+precision, the reference's default).  Stored: inputs, per-rank outputs
+concatenated (y, dx), and the group-averaged attention-parameter grads.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from seqpar import model  # noqa: E402
+from seqpar.collectives import Communicator, run_workers  # noqa: E402
+from seqpar.model import ModelConfig  # noqa: E402
+from seqpar.nnops import DropoutPolicy, LinearParams  # noqa: E402
+from seqpar.sharded import ShardSpec  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+CASES = {
+    # name: (seq_len, embed, heads, workers, batch, causal, out dtype)
+    "small_causal": (256, 128, 2, 2, 1, True, np.float64),
+    "small_noncausal": (256, 128, 2, 2, 1, False, np.float64),
+    "batch2_g3": (192, 128, 2, 3, 2, True, np.float64),
+    "configA": (1024, 256, 4, 2, 1, True, np.float32),
+}
+
+GRAD_NAMES = ("ln1_gain", "ln1_bias", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo")
+
+
+def run_case(seq, e, h, g, b, causal, seed=0):
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=8, vocab=16, seq_len=seq,
+                      batch=b, causal=causal, precision="double")
+    rng = np.random.default_rng(seed)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    lp = model.init_params(cfg, seed).layers[0]
+    # non-trivial LN affine and biases so every gradient is exercised
+    lp.ln1_gain = f32(1.0 + 0.1 * rng.standard_normal(e))
+    lp.ln1_bias = f32(0.1 * rng.standard_normal(e))
+    lin = lambda p: LinearParams(f32(p.weight), f32(0.05 * rng.standard_normal(e)))  # noqa: E731
+    lp.attn_q, lp.attn_k, lp.attn_v, lp.attn_out = (lin(lp.attn_q), lin(lp.attn_k),
+                                                    lin(lp.attn_v), lin(lp.attn_out))
+    lp.ff_in = LinearParams(np.zeros_like(lp.ff_in.weight), np.zeros_like(lp.ff_in.bias))
+    lp.ff_out = LinearParams(np.zeros_like(lp.ff_out.weight), np.zeros_like(lp.ff_out.bias))
+    x = f32(rng.standard_normal((b, seq, e)))
+    gy = f32(rng.standard_normal((b, seq, e)))
+    off = DropoutPolicy.off()
+    comm = Communicator(g, timeout=120.0)
+    group = comm.group("sequence", tuple(range(g)))
+
+    def worker(rank):
+        spec = ShardSpec(rank, g, seq)
+        xs = np.ascontiguousarray(x[:, spec.offset:spec.offset + spec.block])
+        gys = np.ascontiguousarray(gy[:, spec.offset:spec.offset + spec.block])
+
+        def kv_fwd(xh, lp_):  # sharded.py:139-143
+            xh_full = comm.all_gather(group, rank, xh, dim=1, step=0, phase="forward", layer=0)
+            return model.linear3(xh_full, lp_.attn_k), model.linear3(xh_full, lp_.attn_v), xh_full
+
+        def kv_bwd(kv_ctx, lp_, gk, gv):  # sharded.py:186-191
+            grad_full, k_wg, k_bg, v_wg, v_bg = model.local_kv_bwd(kv_ctx, lp_, gk, gv)
+            seg = comm.reduce_scatter(group, rank, grad_full, dim=1, step=0, phase="backward",
+                                      layer=0)
+            return seg, k_wg, k_bg, v_wg, v_bg
+
+        y, cache = model.layer_fwd(lp, cfg, off, 0, xs, spec.offset, kv_fwd)
+        dx, grads = model.layer_bwd(lp, cfg, off, 0, cache, gys, kv_bwd)
+        flat = [grads.ln1_gain, grads.ln1_bias, grads.attn_q.weight, grads.attn_q.bias,
+                grads.attn_k.weight, grads.attn_k.bias, grads.attn_v.weight, grads.attn_v.bias,
+                grads.attn_out.weight, grads.attn_out.bias]
+        vec = np.concatenate([a.ravel() for a in flat])
+        vec = comm.all_reduce_mean(group, rank, vec, step=0, phase="sync")  # sharded.py:238
+        return y, dx, vec, [a.shape for a in flat]
+
+    res = run_workers(g, worker, comm=comm)
+    y = np.concatenate([r[0] for r in res], axis=1)
+    dx = np.concatenate([r[1] for r in res], axis=1)
+    vec, shapes = res[0][2], res[0][3]
+    grads, pos = {}, 0
+    for name, shp in zip(GRAD_NAMES, shapes):
+        n = int(np.prod(shp))
+        grads["g_" + name] = vec[pos:pos + n].reshape(shp)
+        pos += n
+    params = dict(ln1_gain=lp.ln1_gain, ln1_bias=lp.ln1_bias, wq=lp.attn_q.weight,
+                  bq=lp.attn_q.bias, wk=lp.attn_k.weight, bk=lp.attn_k.bias,
+                  wv=lp.attn_v.weight, bv=lp.attn_v.bias, wo=lp.attn_out.weight,
+                  bo=lp.attn_out.bias)
+    return x, gy, params, y, dx, grads
+
+
+def main():
+    for name, (seq, e, h, g, b, causal, odt) in CASES.items():
+        x, gy, params, y, dx, grads = run_case(seq, e, h, g, b, causal)
+        arrays = dict(x=x.astype(np.float32), grad_y=gy.astype(np.float32),
+                      meta=np.array([seq, e, h, g, b, int(causal)], dtype=np.int64),
+                      y=y.astype(odt), dx=dx.astype(odt))
+        arrays.update({k: v.astype(np.float32) for k, v in params.items()})
+        arrays.update({k: v.astype(odt) for k, v in grads.items()})
+        np.savez_compressed(OUT / f"{name}.npz", **arrays)
+        print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("x", "y")})
+
+
+if __name__ == "__main__":
+    main()

@@ -103,21 +103,26 @@ int lss_cat_cast_colsum(int out_dtype, const float* const* srcs, const long* lds
                         void* stream);
 
 /* model.scores_fwd (model.py:280-326): this rank's query rows (global
- * positions offset..offset+rows-1) against the whole sequence held in the
- * packed K/V buffer of `workers` segments of seg_len rows.  Causal keep-mask
- * key <= query position (model.py:301-304).  Writes ctx `o` and lse2. */
-int lss_attn_fwd(int dtype, const void* q, const void* kv, void* o, float* lse2, int batch,
-                 int rows, int workers, int seg_len, int heads, int head_dim, long offset,
-                 int causal, void* stream);
+ * positions offset..offset+rows-1) against the whole sequence, whose keys and
+ * values are given as `workers` segments of seg_len rows, row layout
+ * [workers][batch][seg_len][ld_kv] (elements).  The packed all-gather buffer
+ * [workers][batch][seg_len][2*embed] is k = kv, v = kv + embed, ld_kv = 2*embed;
+ * a single (batch, t, embed) tensor is workers = 1, seg_len = t, ld_kv = embed.
+ * Causal keep-mask key <= query position (model.py:301-304).  Writes ctx `o`
+ * [batch][rows][embed] and lse2. */
+int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, void* o,
+                 float* lse2, int batch, int rows, int workers, int seg_len, int heads,
+                 int head_dim, long offset, int causal, void* stream);
 
 /* model.scores_bwd (model.py:329-359).  grad_q [batch][rows][embed] fp32 is
- * overwritten; grad_kv [workers][batch][seg_len][2*embed] fp32 is fully
- * written (partial dK|dV over the whole sequence, reduce-scatter input).
+ * overwritten; grad_k / grad_v (fp32, layout [workers][batch][seg_len][ld_dkv])
+ * are fully written: this rank's partial dK, dV over the WHOLE sequence (the
+ * reduce-scatter input; packed [dK|dV] when grad_v = grad_k + embed, ld = 2E).
  * delta_ws: workspace of batch*heads*lss_rows_pad(rows) floats. */
-int lss_attn_bwd(int dtype, const void* q, const void* kv, const void* o, const void* grad_o,
-                 const float* lse2, float* delta_ws, float* grad_q, float* grad_kv, int batch,
-                 int rows, int workers, int seg_len, int heads, int head_dim, long offset,
-                 int causal, void* stream);
+int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, const void* o,
+                 const void* grad_o, const float* lse2, float* delta_ws, float* grad_q,
+                 float* grad_k, float* grad_v, long ld_dkv, int batch, int rows, int workers,
+                 int seg_len, int heads, int head_dim, long offset, int causal, void* stream);
 
 #ifdef __cplusplus
 }

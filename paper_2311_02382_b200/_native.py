@@ -56,8 +56,9 @@ SIGNATURES = {
     "lss_stage_weights": [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],
     "lss_cat_cast_colsum": [_I, ctypes.POINTER(_P), ctypes.POINTER(_L), ctypes.POINTER(_I), _I, _P, _L,
                             _P, _F, _L, _P],
-    "lss_attn_fwd": [_I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P],
-    "lss_attn_bwd": [_I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P],
+    "lss_attn_fwd": [_I, _P, _P, _P, _L, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P],
+    "lss_attn_bwd": [_I, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _I, _L, _I,
+                     _P],
 }
 EXTRA = {
     "lss_abi_version": ([], _I),

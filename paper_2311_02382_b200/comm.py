@@ -1,0 +1,131 @@
+"""Collectives of the LSS hot path, with the reference's ledger semantics.
+
+Reference: collectives.py (Communicator.all_gather / reduce_scatter /
+all_reduce, 325-406; CommLedger, 52-143).  On B200 the fabric is NCCL over
+NVLink 5 / NVSwitch via torch.distributed (one process per GPU).  Per LSS
+layer and step the path issues exactly:
+
+  forward   1 all-gather of the packed [K_r | V_r] segments      (phase "forward")
+  backward  1 reduce-scatter of the packed partial [dK | dV]      (phase "backward")
+  sync      1 all-reduce (sum) of the pre-scaled gradients        (phase "sync")
+
+The packed exchange is the arithmetic of the reference's ``fused=False``
+ablation (sharded.py:144-154, 192-202) done as ONE collective per direction;
+the ledger records it as one call whose element count is the full logical
+payload (2*B*l*E), like collectives.py:341/369.
+
+``SimComm`` is the single-process fabric used by the GPU tests to run G
+virtual ranks on one device (the role the reference's in-process
+Communicator plays): rank-ordered concatenation / ascending-rank sums.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+
+@dataclass
+class LedgerRecord:
+    kind: str
+    group: str
+    elements: int
+    step: int
+    phase: str
+    layer: int | None
+
+
+@dataclass
+class Ledger:
+    """collectives.CommLedger (collectives.py:52-143), Python-side log of NCCL calls."""
+
+    records: list = field(default_factory=list)
+
+    def record(self, kind, group, elements, step, phase, layer=None):
+        self.records.append(LedgerRecord(kind, group, int(elements), step, phase, layer))
+
+    def count(self, kind=None, phase=None):
+        return sum(1 for r in self.records
+                   if (kind is None or r.kind == kind) and (phase is None or r.phase == phase))
+
+    def clear(self):
+        self.records.clear()
+
+
+class TorchDistComm:
+    """NCCL (or gloo on CPU tests) through torch.distributed.
+
+    ``seq_group``: the sequence-parallel group of this rank (ranks ordered by
+    sequence segment); ``world_group``: every rank that shares the parameters
+    (seq x data), used for the single folded gradient all-reduce."""
+
+    def __init__(self, seq_group=None, world_group=None, ledger: Ledger | None = None,
+                 seq_name="sequence", world_name="world"):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.seq_group = seq_group
+        self.world_group = world_group
+        self.ledger = ledger if ledger is not None else Ledger()
+        self.seq_name, self.world_name = seq_name, world_name
+        self.seq_size = dist.get_world_size(seq_group)
+        self.seq_rank = dist.get_rank(seq_group)
+
+    def all_gather_rows(self, full: torch.Tensor, step=0, layer=0, async_op=False):
+        """In-place all-gather: ``full`` is [G, ...]; this rank's slot full[seq_rank]
+        is already written; afterwards full holds every rank's slot in rank order."""
+        self.ledger.record("all-gather", self.seq_name, full.numel(), step, "forward", layer)
+        if self.seq_size == 1:
+            return None
+        return self.dist.all_gather_into_tensor(full, full[self.seq_rank], group=self.seq_group,
+                                                async_op=async_op)
+
+    def reduce_scatter_rows(self, out: torch.Tensor, full: torch.Tensor, step=0, layer=0, async_op=False):
+        """out = sum over ranks of full[seq_rank] (rank-ordered blocks, collectives.py:346-372)."""
+        self.ledger.record("reduce-scatter", self.seq_name, full.numel(), step, "backward", layer)
+        if self.seq_size == 1:
+            out.copy_(full[0])
+            return None
+        return self.dist.reduce_scatter_tensor(out, full, group=self.seq_group, async_op=async_op)
+
+    def all_reduce_sum(self, buf: torch.Tensor, step=0, async_op=False):
+        """Folded double gradient averaging: one world all-reduce of gradients that
+        were pre-scaled by 1/(D*N) in the kernels that produced them."""
+        self.ledger.record("all-reduce", self.world_name, buf.numel(), step, "sync", None)
+        world = self.dist.get_world_size(self.world_group)
+        if world == 1:
+            return None
+        return self.dist.all_reduce(buf, group=self.world_group, async_op=async_op)
+
+
+class SimComm:
+    """G virtual ranks in one process (tests): deterministic, ascending-rank folds."""
+
+    def __init__(self, ledger: Ledger | None = None):
+        self.ledger = ledger if ledger is not None else Ledger()
+
+    def all_gather_rows(self, fulls, step=0, layer=0):
+        g = len(fulls)
+        self.ledger.record("all-gather", "sequence", fulls[0].numel(), step, "forward", layer)
+        for dst in range(g):
+            for src in range(g):
+                if src != dst:
+                    fulls[dst][src].copy_(fulls[src][src])
+
+    def reduce_scatter_rows(self, outs, fulls, step=0, layer=0):
+        g = len(fulls)
+        self.ledger.record("reduce-scatter", "sequence", fulls[0].numel(), step, "backward", layer)
+        for r in range(g):
+            acc = fulls[0][r].clone()
+            for j in range(1, g):
+                acc += fulls[j][r]
+            outs[r].copy_(acc)
+
+    def all_reduce_sum(self, bufs, step=0):
+        self.ledger.record("all-reduce", "world", bufs[0].numel(), step, "sync", None)
+        acc = bufs[0].clone()
+        for b in bufs[1:]:
+            acc += b
+        for b in bufs:
+            b.copy_(acc)

@@ -6,8 +6,9 @@
 // with P recomputed from the forward's base-2 log-sum-exp and
 // rowsum(dP P) = rowsum(dO O) = delta precomputed per query row.  dK/dV span
 // the FULL key length (this rank's partial contribution for every rank's key
-// rows) and are written in the packed [G][B][seg][2E] fp32 layout that the
-// reduce-scatter consumes directly (sharded.py:192-199 math, one collective).
+// rows) and are written in the [G][B][seg][ld] fp32 layout; with dv = dk + E and
+// ld = 2E that is the packed [dK|dV] buffer the reduce-scatter consumes
+// directly (sharded.py:192-199 math, one collective).
 //
 // CTA = one 128-row key tile of one (batch, head); it walks the query tiles of
 // this rank that can see the keys (causal: q_pos >= k_pos).  Transposed
@@ -40,7 +41,9 @@ struct AttnBwdParams {
   const float* lse2;   // [B][H][m_pad] (+inf padded)
   const float* delta;  // [B][H][m_pad] (0 padded)
   float* dq;           // [B][m][E] fp32, accumulated (must be zeroed)
-  float* dkv;          // [G][B][seg_len][2E] fp32, fully written
+  float* dk;           // [G][B][seg_len][ld_dkv] fp32, fully written
+  float* dv;           // same layout
+  long ld_dkv;
 };
 
 LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -53,7 +56,8 @@ LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t
 
 __global__ void __launch_bounds__(ATB_THREADS, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
-                       const __grid_constant__ CUtensorMap tmKV, const __grid_constant__ CUtensorMap tmdQ,
+                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                       const __grid_constant__ CUtensorMap tmdQ,
                        AttnBwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -95,7 +99,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmdO);
-    tma_prefetch_desc(&tmKV);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmdQ);
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
@@ -119,8 +125,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     if (lane == 0 && n_iter > 0) {
       // ------------------------------------------------ TMA producer
       mbar_arrive_expect_tx(kv_full, 2 * ATT_TILE_BYTES);
-      tma_load_4d(&tmKV, kv_full, sK, h * ATT_D, kv_row0, b, g);
-      tma_load_4d(&tmKV, kv_full, sV, E + h * ATT_D, kv_row0, b, g);
+      tma_load_4d(&tmK, kv_full, sK, h * ATT_D, kv_row0, b, g);
+      tma_load_4d(&tmV, kv_full, sV, h * ATT_D, kv_row0, b, g);
       for (int it = 0; it < n_iter; ++it) {
         const int s = it & 1;
         mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
@@ -263,8 +269,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     }
     if (n_iter > 0) drain_dq(n_iter - 1);
     // dK (half 0) / dV (half 1) epilogue: all MMAs are complete after the last dq_full
-    float* dst = p.dkv + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * (2L * E) +
-                 (half ? E : 0) + h * ATT_D;
+    float* dst = (half ? p.dv : p.dk) + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * p.ld_dkv +
+                 h * ATT_D;
     if (n_iter > 0) {
       uint32_t v[64];
       tmem_ld64((half ? tdV : tdK) + lane_off, v);

@@ -7,9 +7,10 @@
 // (tensor.py:104-131), ctx[:, h*d:(h+1)*d] = P V_h.  Instead of caching P the
 // kernel emits the row log-sum-exp (base 2) so the backward recomputes P.
 //
-// K/V come from the packed all-gather buffer [G][B][seg][2E] (K in columns
-// [0,E), V in [E,2E)), i.e. the rank-ordered concatenation of every rank's
-// [K_r|V_r] (sharded.py:144-154 math, one collective).  The kernel walks the
+// K/V rows are laid out [G][B][seg][ld] (two TMA maps, one per operand); for the
+// packed all-gather buffer [G][B][seg][2E] K is columns [0,E) and V [E,2E),
+// i.e. the rank-ordered concatenation of every rank's [K_r|V_r]
+// (sharded.py:144-154 math, one collective).  The kernel walks the
 // key tiles segment by segment, so a segment length that is not a multiple of
 // 128 costs one partial tile per segment (masked), never a straddling TMA box.
 //
@@ -47,8 +48,8 @@ struct AttnFwdParams {
 };
 
 __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
-                       const __grid_constant__ CUtensorMap tmKV, AttnFwdParams p) {
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, AttnFwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -92,7 +93,8 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmKV);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
     for (int s = 0; s < ATT_KV_STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
@@ -127,8 +129,8 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         mbar_wait(&kv_empty[st], ph ^ 1);
         const int g = j / tps, t = j % tps;
         mbar_arrive_expect_tx(&kv_full[st], 2 * ATT_TILE_BYTES);
-        tma_load_4d(&tmKV, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
-        tma_load_4d(&tmKV, &kv_full[st], sV + st * ATT_TILE_BYTES, E + h * ATT_D, t * ATT_BN, b, g);
+        tma_load_4d(&tmK, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
+        tma_load_4d(&tmV, &kv_full[st], sV + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
       }
     }
   } else if (warp == 1) {

@@ -63,8 +63,8 @@ __global__ void gemm_f32_simt_kernel(const float* __restrict__ A, long sam, long
 // Attention forward, fp32: one warp per (query row, head, batch); lanes own
 // head dimensions (d <= 128), keys walked in order with an online softmax.
 // q [B][m][E], kv [G][B][seg][2E]; o [B][m][E]; lse2 [B][H][m_pad] (base 2).
-__global__ void attn_fwd_f32_kernel(const float* __restrict__ q, const float* __restrict__ kv,
-                                    float* __restrict__ o, float* __restrict__ lse2, int B, int m,
+__global__ void attn_fwd_f32_kernel(const float* __restrict__ q, const float* __restrict__ kb,
+                                    const float* __restrict__ vb, long ldkv, float* __restrict__ o, float* __restrict__ lse2, int B, int m,
                                     int m_pad, int G, int seg, int H, int d, long offset, int causal,
                                     float scale) {
   const int warps = blockDim.x / 32;
@@ -85,8 +85,8 @@ __global__ void attn_fwd_f32_kernel(const float* __restrict__ q, const float* __
   for (long j = 0; j < kend; ++j) {
     const int g = j / seg;
     const long r = j % seg;
-    const float* kr = kv + (((long)g * B + b) * seg + r) * 2L * E + h * d;
-    const float* vr = kr + E;
+    const float* kr = kb + (((long)g * B + b) * seg + r) * ldkv + h * d;
+    const float* vr = vb + (((long)g * B + b) * seg + r) * ldkv + h * d;
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -115,8 +115,8 @@ __global__ void attn_fwd_f32_kernel(const float* __restrict__ q, const float* __
 }
 
 // dQ rows: one warp per (query row, head, batch).
-__global__ void attn_bwd_dq_f32_kernel(const float* __restrict__ q, const float* __restrict__ kv,
-                                       const float* __restrict__ dO, const float* __restrict__ lse2,
+__global__ void attn_bwd_dq_f32_kernel(const float* __restrict__ q, const float* __restrict__ kb,
+                                       const float* __restrict__ vb, long ldkv, const float* __restrict__ dO, const float* __restrict__ lse2,
                                        const float* __restrict__ delta, float* __restrict__ dq, int B,
                                        int m, int m_pad, int G, int seg, int H, int d, long offset,
                                        int causal, float scale) {
@@ -140,8 +140,8 @@ __global__ void attn_bwd_dq_f32_kernel(const float* __restrict__ q, const float*
   for (long j = 0; j < kend; ++j) {
     const int g = j / seg;
     const long r = j % seg;
-    const float* kr = kv + (((long)g * B + b) * seg + r) * 2L * E + h * d;
-    const float* vr = kr + E;
+    const float* kr = kb + (((long)g * B + b) * seg + r) * ldkv + h * d;
+    const float* vr = vb + (((long)g * B + b) * seg + r) * ldkv + h * d;
     float s = 0.f, dp = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -172,9 +172,11 @@ __global__ void attn_bwd_dq_f32_kernel(const float* __restrict__ q, const float*
 }
 
 // dK/dV rows over the full key length: one warp per (key row, head, batch).
-__global__ void attn_bwd_dkv_f32_kernel(const float* __restrict__ q, const float* __restrict__ kv,
+__global__ void attn_bwd_dkv_f32_kernel(const float* __restrict__ q, const float* __restrict__ kb,
+                                        const float* __restrict__ vb, long ldkv,
                                         const float* __restrict__ dO, const float* __restrict__ lse2,
-                                        const float* __restrict__ delta, float* __restrict__ dkv,
+                                        const float* __restrict__ delta, float* __restrict__ dkb,
+                                        float* __restrict__ dvb, long lddkv,
                                         int B, int m, int m_pad, int G, int seg, int H, int d,
                                         long offset, int causal, float scale) {
   const int warps = blockDim.x / 32;
@@ -185,8 +187,8 @@ __global__ void attn_bwd_dkv_f32_kernel(const float* __restrict__ q, const float
   const int E = H * d;
   const int g = j / seg;
   const long r = j % seg;
-  const float* kr = kv + (((long)g * B + b) * seg + r) * 2L * E + h * d;
-  const float* vr = kr + E;
+  const float* kr = kb + (((long)g * B + b) * seg + r) * ldkv + h * d;
+  const float* vr = vb + (((long)g * B + b) * seg + r) * ldkv + h * d;
   float kvv[4], vv[4], dk[4] = {0.f, 0.f, 0.f, 0.f}, dv[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -225,13 +227,14 @@ __global__ void attn_bwd_dkv_f32_kernel(const float* __restrict__ q, const float
       }
     }
   }
-  float* dst = dkv + (((long)g * B + b) * seg + r) * 2L * E + h * d;
+  float* dstk = dkb + (((long)g * B + b) * seg + r) * lddkv + h * d;
+  float* dstv = dvb + (((long)g * B + b) * seg + r) * lddkv + h * d;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const int k = lane + 32 * c;
     if (k < d) {
-      dst[k] = dk[c];
-      dst[E + k] = dv[c];
+      dstk[k] = dk[c];
+      dstv[k] = dv[c];
     }
   }
 }

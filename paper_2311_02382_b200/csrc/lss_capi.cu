@@ -72,6 +72,16 @@ int make_map(CUtensorMap* m, CUtensorMapDataType dt, int elem_bytes, int rank, c
   return LSS_OK;
 }
 
+// bf16 rows [outer][mid][rows][ld] viewed as a 4-D (or 3-D when outer == 1) map of
+// `cols` visible columns; box 64 columns x 128 rows, 128B swizzle.
+int map_rows(CUtensorMap* m, const void* base, int cols, long ld, long rows, long mid, long outer, int rank) {
+  uint64_t dims[4] = {(uint64_t)cols, (uint64_t)rows, (uint64_t)mid, (uint64_t)outer};
+  uint64_t str[3] = {(uint64_t)ld, (uint64_t)(rows * ld), (uint64_t)(mid * rows * ld)};
+  uint32_t box[4] = {64, 128, 1, 1};
+  return make_map(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rank, base, dims, str, box,
+                  CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -262,38 +272,31 @@ static int attn_check(int dtype, int batch, int rows, int workers, int seg_len, 
   return LSS_OK;
 }
 
-int lss_attn_fwd(int dtype, const void* q, const void* kv, void* o, float* lse2, int batch, int rows,
-                 int workers, int seg_len, int heads, int head_dim, long offset, int causal, void* stream) {
+int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, void* o, float* lse2,
+                 int batch, int rows, int workers, int seg_len, int heads, int head_dim, long offset, int causal,
+                 void* stream) {
   int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
   if (rc) return rc;
-  if (!q || !kv || !o || !lse2) return fail(LSS_ERR_ARG, "attn_fwd: null pointer");
-  if (causal && offset < 0) return fail(LSS_ERR_DEGENERATE, "attn_fwd: negative offset leaves rows fully masked");
+  if (!q || !k || !v || !o || !lse2) return fail(LSS_ERR_ARG, "attn_fwd: null pointer");
   const int E = heads * head_dim;
+  if (ld_kv < E) return fail(LSS_ERR_SHAPE, "attn_fwd: ld_kv %ld < embed %d", ld_kv, E);
+  if (causal && offset < 0) return fail(LSS_ERR_DEGENERATE, "attn_fwd: negative offset leaves rows fully masked");
   const int m_pad = (int)lss_rows_pad(rows);
   const float scale = 1.0f / sqrtf((float)head_dim);
   if (dtype == LSS_F32) {
     dim3 grid((rows + 3) / 4, heads, batch);
     attn_fwd_f32_kernel<<<grid, 128, 0, S(stream)>>>(
-        reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(kv), reinterpret_cast<float*>(o), lse2,
-        batch, rows, m_pad, workers, seg_len, heads, head_dim, offset, causal, scale);
+        reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(k), reinterpret_cast<const float*>(v),
+        ld_kv, reinterpret_cast<float*>(o), lse2, batch, rows, m_pad, workers, seg_len, heads, head_dim, offset,
+        causal, scale);
     return check_launch("attn_fwd_f32");
   }
-  if (!aligned16(q) || !aligned16(kv) || !aligned16(o)) return fail(LSS_ERR_UNSUPPORTED, "attn_fwd: 16B alignment");
-  CUtensorMap mq, mkv;
-  {
-    uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
-    uint64_t str[2] = {(uint64_t)E, (uint64_t)rows * E};
-    uint32_t box[3] = {64, 128, 1};
-    if ((rc = make_map(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, q, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
-      return rc;
-  }
-  {
-    uint64_t dims[4] = {(uint64_t)2 * E, (uint64_t)seg_len, (uint64_t)batch, (uint64_t)workers};
-    uint64_t str[3] = {(uint64_t)2 * E, (uint64_t)seg_len * 2 * E, (uint64_t)batch * seg_len * 2 * E};
-    uint32_t box[4] = {64, 128, 1, 1};
-    if ((rc = make_map(&mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, kv, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
-      return rc;
-  }
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || ld_kv % 8)
+    return fail(LSS_ERR_UNSUPPORTED, "attn_fwd: 16B alignment");
+  CUtensorMap mq, mk, mv;
+  if ((rc = map_rows(&mq, q, E, E, rows, batch, 1, 3))) return rc;
+  if ((rc = map_rows(&mk, k, E, ld_kv, seg_len, batch, workers, 4))) return rc;
+  if ((rc = map_rows(&mv, v, E, ld_kv, seg_len, batch, workers, 4))) return rc;
   AttnFwdParams p;
   p.B = batch; p.m = rows; p.m_pad = m_pad; p.G = workers; p.seg_len = seg_len; p.H = heads;
   p.offset = offset; p.causal = causal;
@@ -302,18 +305,20 @@ int lss_attn_fwd(int dtype, const void* q, const void* kv, void* o, float* lse2,
   p.lse2 = lse2;
   if ((rc = set_smem(attn_fwd_tc_kernel, ATT_FWD_SMEM))) return rc;
   dim3 grid((rows + 2 * ATT_BM - 1) / (2 * ATT_BM), heads, batch);
-  attn_fwd_tc_kernel<<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mkv, p);
+  attn_fwd_tc_kernel<<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
   return check_launch("attn_fwd_tc");
 }
 
-int lss_attn_bwd(int dtype, const void* q, const void* kv, const void* o, const void* grad_o, const float* lse2,
-                 float* delta_ws, float* grad_q, float* grad_kv, int batch, int rows, int workers, int seg_len,
-                 int heads, int head_dim, long offset, int causal, void* stream) {
+int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, const void* o,
+                 const void* grad_o, const float* lse2, float* delta_ws, float* grad_q, float* grad_k,
+                 float* grad_v, long ld_dkv, int batch, int rows, int workers, int seg_len, int heads,
+                 int head_dim, long offset, int causal, void* stream) {
   int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
   if (rc) return rc;
-  if (!q || !kv || !o || !grad_o || !lse2 || !delta_ws || !grad_q || !grad_kv)
+  if (!q || !k || !v || !o || !grad_o || !lse2 || !delta_ws || !grad_q || !grad_k || !grad_v)
     return fail(LSS_ERR_ARG, "attn_bwd: null pointer");
   const int E = heads * head_dim;
+  if (ld_kv < E || ld_dkv < E) return fail(LSS_ERR_SHAPE, "attn_bwd: row strides smaller than embed");
   const int m_pad = (int)lss_rows_pad(rows);
   const float scale = 1.0f / sqrtf((float)head_dim);
   {
@@ -331,47 +336,30 @@ int lss_attn_bwd(int dtype, const void* q, const void* kv, const void* o, const 
   }
   if (dtype == LSS_F32) {
     const float* qf = reinterpret_cast<const float*>(q);
-    const float* kvf = reinterpret_cast<const float*>(kv);
+    const float* kf = reinterpret_cast<const float*>(k);
+    const float* vf = reinterpret_cast<const float*>(v);
     const float* gof = reinterpret_cast<const float*>(grad_o);
     dim3 g1((rows + 3) / 4, heads, batch);
-    attn_bwd_dq_f32_kernel<<<g1, 128, 0, S(stream)>>>(qf, kvf, gof, lse2, delta_ws, grad_q, batch, rows, m_pad,
-                                                     workers, seg_len, heads, head_dim, offset, causal, scale);
+    attn_bwd_dq_f32_kernel<<<g1, 128, 0, S(stream)>>>(qf, kf, vf, ld_kv, gof, lse2, delta_ws, grad_q, batch, rows,
+                                                     m_pad, workers, seg_len, heads, head_dim, offset, causal, scale);
     if ((rc = check_launch("attn_bwd_dq_f32"))) return rc;
     const long t = (long)workers * seg_len;
     dim3 g2((t + 3) / 4, heads, batch);
-    attn_bwd_dkv_f32_kernel<<<g2, 128, 0, S(stream)>>>(qf, kvf, gof, lse2, delta_ws, grad_kv, batch, rows, m_pad,
-                                                      workers, seg_len, heads, head_dim, offset, causal, scale);
+    attn_bwd_dkv_f32_kernel<<<g2, 128, 0, S(stream)>>>(qf, kf, vf, ld_kv, gof, lse2, delta_ws, grad_k, grad_v,
+                                                      ld_dkv, batch, rows, m_pad, workers, seg_len, heads, head_dim,
+                                                      offset, causal, scale);
     return check_launch("attn_bwd_dkv_f32");
   }
-  if (!aligned16(q) || !aligned16(kv) || !aligned16(grad_o) || !aligned16(grad_q) || !aligned16(grad_kv))
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(grad_o) || !aligned16(grad_q) ||
+      !aligned16(grad_k) || !aligned16(grad_v) || ld_kv % 8 || ld_dkv % 4)
     return fail(LSS_ERR_UNSUPPORTED, "attn_bwd: 16B alignment");
   cudaError_t e = cudaMemsetAsync(grad_q, 0, sizeof(float) * (size_t)batch * rows * E, S(stream));
   if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "attn_bwd memset: %s", cudaGetErrorString(e));
-  CUtensorMap mq, mdo, mkv;
-  {
-    uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
-    uint64_t str[2] = {(uint64_t)E, (uint64_t)rows * E};
-    uint32_t box[3] = {64, 128, 1};
-    if ((rc = make_map(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, q, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
-      return rc;
-    if ((rc = make_map(&mdo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, grad_o, dims, str, box,
-                       CU_TENSOR_MAP_SWIZZLE_128B)))
-      return rc;
-  }
-  {
-    uint64_t dims[4] = {(uint64_t)2 * E, (uint64_t)seg_len, (uint64_t)batch, (uint64_t)workers};
-    uint64_t str[3] = {(uint64_t)2 * E, (uint64_t)seg_len * 2 * E, (uint64_t)batch * seg_len * 2 * E};
-    uint32_t box[4] = {64, 128, 1, 1};
-    if ((rc = make_map(&mkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 4, kv, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
-      return rc;
-  }
-  AttnBwdParams p;
-  p.B = batch; p.m = rows; p.m_pad = m_pad; p.G = workers; p.seg_len = seg_len; p.H = heads;
-  p.offset = offset; p.causal = causal;
-  p.scale_log2 = scale * 1.4426950408889634f;
-  p.scale = scale;
-  p.lse2 = lse2; p.delta = delta_ws; p.dq = grad_q; p.dkv = grad_kv;
-  CUtensorMap mdq;
+  CUtensorMap mq, mdo, mk, mv, mdq;
+  if ((rc = map_rows(&mq, q, E, E, rows, batch, 1, 3))) return rc;
+  if ((rc = map_rows(&mdo, grad_o, E, E, rows, batch, 1, 3))) return rc;
+  if ((rc = map_rows(&mk, k, E, ld_kv, seg_len, batch, workers, 4))) return rc;
+  if ((rc = map_rows(&mv, v, E, ld_kv, seg_len, batch, workers, 4))) return rc;
   {
     uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
     uint64_t str[2] = {(uint64_t)E, (uint64_t)rows * E};
@@ -380,10 +368,16 @@ int lss_attn_bwd(int dtype, const void* q, const void* kv, const void* o, const 
                        CU_TENSOR_MAP_SWIZZLE_128B)))
       return rc;
   }
+  AttnBwdParams p;
+  p.B = batch; p.m = rows; p.m_pad = m_pad; p.G = workers; p.seg_len = seg_len; p.H = heads;
+  p.offset = offset; p.causal = causal;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.scale = scale;
+  p.lse2 = lse2; p.delta = delta_ws; p.dq = grad_q; p.dk = grad_k; p.dv = grad_v; p.ld_dkv = ld_dkv;
   if ((rc = set_smem(attn_bwd_tc_kernel, ATB_SMEM))) return rc;
   const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
   dim3 grid(workers * tps, heads, batch);
-  attn_bwd_tc_kernel<<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mq, mdo, mkv, mdq, p);
+  attn_bwd_tc_kernel<<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mq, mdo, mk, mv, mdq, p);
   return check_launch("attn_bwd_tc");
 }
 

@@ -55,7 +55,8 @@ def _need(t: torch.Tensor, name: str, dtype=None):
 # ----------------------------------------------------------------- LayerNorm
 
 
-def layernorm_fwd(x, gain, bias, out=None, out_dtype=torch.bfloat16, eps=LAYERNORM_EPS):
+def layernorm_fwd(x, gain, bias, out=None, out_dtype=torch.bfloat16, eps=LAYERNORM_EPS, mean=None,
+                  rstd=None):
     """nnops.layernorm_fwd (nnops.py:199-208) over the last dim.  Returns (y, mean, rstd)."""
     _need(x, "x", torch.float32)
     e = x.shape[-1]
@@ -63,8 +64,8 @@ def layernorm_fwd(x, gain, bias, out=None, out_dtype=torch.bfloat16, eps=LAYERNO
     if gain.shape != (e,) or bias.shape != (e,):
         raise ShapeError(f"layernorm gain/bias {tuple(gain.shape)} do not match embed {e}")
     y = out if out is not None else torch.empty(x.shape, dtype=out_dtype, device=x.device)
-    mean = torch.empty(rows, dtype=torch.float32, device=x.device)
-    rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    mean = mean if mean is not None else torch.empty(rows, dtype=torch.float32, device=x.device)
+    rstd = rstd if rstd is not None else torch.empty(rows, dtype=torch.float32, device=x.device)
     dt = LSS_BF16 if y.dtype == torch.bfloat16 else LSS_F32
     call("lss_layernorm_fwd", _ptr(x), _ptr(gain), _ptr(bias), _ptr(y), dt, _ptr(mean), _ptr(rstd),
          rows, e, eps, _stream())
@@ -166,37 +167,74 @@ def rows_pad(rows: int) -> int:
     return _native.rows_pad(rows)
 
 
-def attn_fwd(q, kv, *, workers, seg_len, heads, offset, causal, out=None, lse2=None):
-    """model.scores_fwd core.  q [B,m,E]; kv packed [G,B,seg,2E].  Returns (ctx, lse2)."""
+def _rows_view(t: torch.Tensor, name: str, workers: int, bsz: int, seg_len: int, e: int) -> int:
+    """Validate a [G][B][seg][ld] (or [B][t][ld] when G == 1) row layout with `e`
+    visible columns; return the row stride ld in elements."""
+    if not t.is_cuda:
+        raise ShapeError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dim() == 4:
+        if tuple(t.shape) != (workers, bsz, seg_len, e):
+            raise ShapeError(f"{name} shape {tuple(t.shape)} != {(workers, bsz, seg_len, e)}")
+    elif t.dim() == 3 and workers == 1:
+        if tuple(t.shape) != (bsz, seg_len, e):
+            raise ShapeError(f"{name} shape {tuple(t.shape)} != {(bsz, seg_len, e)}")
+    else:
+        raise ShapeError(f"{name} must be [workers, batch, seg, E] (or [batch, t, E] for one segment)")
+    ld = t.stride(-2)
+    if t.stride(-1) != 1 or ld < e:
+        raise ShapeError(f"{name} rows must be contiguous")
+    st = t.stride()
+    bad_b = bsz > 1 and st[-3] != seg_len * ld
+    bad_g = t.dim() == 4 and workers > 1 and st[0] != bsz * seg_len * ld
+    if bad_b or bad_g:
+        raise ShapeError(f"{name} must be a row-strided view of a [G][B][seg][ld] buffer")
+    return ld
+
+
+def attn_fwd(q, k, v, *, workers, seg_len, heads, offset, causal, out=None, lse2=None):
+    """model.scores_fwd core.  q [B,m,E]; k, v [G,B,seg,E] views (same row stride,
+    e.g. the two halves of the packed all-gather buffer) or [B,t,E] when G == 1.
+    Returns (ctx [B,m,E], lse2 [B,H,m_pad] base-2 log-sum-exp)."""
     _need(q, "q")
-    _need(kv, "kv", q.dtype)
     bsz, m, e = q.shape
     if e % heads:
         raise ShapeError(f"embed {e} not divisible by heads {heads}")
-    if kv.shape != (workers, bsz, seg_len, 2 * e):
-        raise ShapeError(f"kv shape {tuple(kv.shape)} != {(workers, bsz, seg_len, 2 * e)}")
+    ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
+    ldv = _rows_view(v, "v", workers, bsz, seg_len, e)
+    if ldk != ldv or k.dtype != q.dtype or v.dtype != q.dtype:
+        raise ShapeError("k and v must share dtype and row stride with q's dtype")
     dt = LSS_BF16 if q.dtype == torch.bfloat16 else LSS_F32
     o = out if out is not None else torch.empty_like(q)
     lse = lse2 if lse2 is not None else torch.empty(bsz, heads, rows_pad(m), dtype=torch.float32,
                                                    device=q.device)
-    call("lss_attn_fwd", dt, _ptr(q), _ptr(kv), _ptr(o), _ptr(lse), bsz, m, workers, seg_len, heads,
-         e // heads, offset, int(causal), _stream())
+    call("lss_attn_fwd", dt, _ptr(q), _ptr(k), _ptr(v), ldk, _ptr(o), _ptr(lse), bsz, m, workers,
+         seg_len, heads, e // heads, offset, int(causal), _stream())
     return o, lse
 
 
-def attn_bwd(q, kv, o, grad_o, lse2, *, workers, seg_len, heads, offset, causal, grad_q=None,
-             grad_kv=None, delta=None):
-    """model.scores_bwd core.  Returns (grad_q fp32 [B,m,E], grad_kv fp32 [G,B,seg,2E])."""
-    for t, n in ((q, "q"), (kv, "kv"), (o, "o"), (grad_o, "grad_o")):
+def attn_bwd(q, k, v, o, grad_o, lse2, *, workers, seg_len, heads, offset, causal, grad_q=None,
+             grad_k=None, grad_v=None, delta=None):
+    """model.scores_bwd core.  Returns (grad_q fp32 [B,m,E], grad_k, grad_v fp32 in the
+    [G,B,seg,E] row layout of the given buffers -- allocated packed [G,B,seg,2E]
+    (dK | dV halves) when not supplied)."""
+    for t, n in ((q, "q"), (o, "o"), (grad_o, "grad_o")):
         _need(t, n, q.dtype)
     bsz, m, e = q.shape
+    ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
+    if _rows_view(v, "v", workers, bsz, seg_len, e) != ldk:
+        raise ShapeError("k and v must share a row stride")
     dt = LSS_BF16 if q.dtype == torch.bfloat16 else LSS_F32
     dev = q.device
     gq = grad_q if grad_q is not None else torch.empty(bsz, m, e, dtype=torch.float32, device=dev)
-    gkv = grad_kv if grad_kv is not None else torch.empty(workers, bsz, seg_len, 2 * e,
-                                                          dtype=torch.float32, device=dev)
+    if grad_k is None:
+        packed = torch.empty(workers, bsz, seg_len, 2 * e, dtype=torch.float32, device=dev)
+        grad_k, grad_v = packed[..., :e], packed[..., e:]
+    lddkv = grad_k.stride(-2)
+    if grad_v.stride(-2) != lddkv or grad_k.dtype != torch.float32:
+        raise ShapeError("grad_k / grad_v must be fp32 with a shared row stride")
     dl = delta if delta is not None else torch.empty(bsz, heads, rows_pad(m), dtype=torch.float32,
                                                      device=dev)
-    call("lss_attn_bwd", dt, _ptr(q), _ptr(kv), _ptr(o), _ptr(grad_o), _ptr(lse2), _ptr(dl), _ptr(gq),
-         _ptr(gkv), bsz, m, workers, seg_len, heads, e // heads, offset, int(causal), _stream())
-    return gq, gkv
+    call("lss_attn_bwd", dt, _ptr(q), _ptr(k), _ptr(v), ldk, _ptr(o), _ptr(grad_o), _ptr(lse2),
+         _ptr(dl), _ptr(gq), _ptr(grad_k), _ptr(grad_v), lddkv, bsz, m, workers, seg_len, heads,
+         e // heads, offset, int(causal), _stream())
+    return gq, grad_k, grad_v

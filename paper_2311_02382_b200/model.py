@@ -1,0 +1,326 @@
+"""Attention half of the reference's layer API (seqpar.model), on B200 kernels.
+
+Same names, argument meaning and error behaviour as the reference
+(/root/reference/pkg/src/seqpar/model.py) for the hot path:
+
+  ModelConfig (model.py:39-80), LinearParams (nnops.py:172-177),
+  linear3 / linear3_bwd (model.py:237-245), norm3 / norm3_bwd (248-257),
+  scores_fwd / scores_bwd (280-359), local_kv_fwd / local_kv_bwd (413-421),
+  layer_fwd / layer_bwd restricted to the attention half (442-448, 479-486).
+
+Arrays are torch CUDA tensors.  ``precision`` selects the kernel family:
+"bf16" (tcgen05 path, bf16 operands / fp32 accumulation, the default) or
+"single" (fp32 FFMA check mode).  The residual stream and all gradients are
+fp32 in both.  The reference caches the full probability matrix P per
+(sample, head); the B200 ScoreCache keeps (ctx, lse) and the backward
+recomputes P (flash-attention), so ``cache.attn`` does not exist -- use
+``probabilities()`` to materialise P for a check.
+
+Out of scope here: dropout > 0 (raises), the FFN half of the
+layer, embeddings/head -- every BASELINE config runs dropout 0 and the hot
+path is the attention sublayer.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import torch
+
+from . import kernels as K
+from .errors import ShapeError, UnsupportedError
+
+LAYERNORM_EPS = 1e-5
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """model.py:39-80.  ``precision`` is "bf16" or "single" on the B200 path."""
+
+    embed_dim: int
+    n_layers: int
+    n_heads: int
+    ff_dim: int
+    vocab: int
+    seq_len: int
+    batch: int = 1
+    dropout: float = 0.0
+    causal: bool = True
+    precision: str = "bf16"
+
+    def __post_init__(self) -> None:
+        if self.embed_dim < 1 or self.n_heads < 1 or self.ff_dim < 1:
+            raise ValueError("model dimensions must be positive")
+        if self.embed_dim % self.n_heads != 0:
+            raise ShapeError(f"embed_dim {self.embed_dim} is not divisible by n_heads {self.n_heads}")
+        if self.n_layers < 0:
+            raise ValueError("n_layers must be non-negative")
+        if self.vocab < 1 or self.seq_len < 1 or self.batch < 1:
+            raise ValueError("vocab, seq_len and batch must be positive")
+        if not 0.0 <= self.dropout < 1.0:
+            raise ValueError(f"dropout must be in [0, 1), got {self.dropout}")
+        K.code(self.precision)  # UnsupportedError for "double"
+
+    @property
+    def head_dim(self) -> int:
+        return self.embed_dim // self.n_heads
+
+    @property
+    def act_dtype(self) -> torch.dtype:
+        return K.act_dtype(self.precision)
+
+
+@dataclass(frozen=True)
+class LinearParams:
+    """nnops.py:172-177: weight [d_in, d_out], bias [d_out], y = x W + b (fp32)."""
+
+    weight: torch.Tensor
+    bias: torch.Tensor
+
+
+@dataclass
+class LayerParams:
+    """Attention half of model.LayerParams (model.py:83-94)."""
+
+    ln1_gain: torch.Tensor
+    ln1_bias: torch.Tensor
+    attn_q: LinearParams
+    attn_k: LinearParams
+    attn_v: LinearParams
+    attn_out: LinearParams
+
+    def named_arrays(self):
+        """Same relative order as Parameters.named_arrays (model.py:118-127)."""
+        yield "ln1_gain", self.ln1_gain
+        yield "ln1_bias", self.ln1_bias
+        for n in ("attn_q", "attn_k", "attn_v", "attn_out"):
+            p = getattr(self, n)
+            yield f"{n}.weight", p.weight
+            yield f"{n}.bias", p.bias
+
+
+def layer_params_from_arrays(ln1_gain, ln1_bias, wq, bq, wk, bk, wv, bv, wo, bo, device="cuda"):
+    t = lambda a: torch.as_tensor(a, dtype=torch.float32, device=device).contiguous()  # noqa: E731
+    return LayerParams(t(ln1_gain), t(ln1_bias), LinearParams(t(wq), t(bq)), LinearParams(t(wk), t(bk)),
+                       LinearParams(t(wv), t(bv)), LinearParams(t(wo), t(bo)))
+
+
+def _check_dropout(cfg: ModelConfig, policy) -> None:
+    active = getattr(policy, "active", False) or cfg.dropout > 0
+    if active:
+        raise UnsupportedError("dropout > 0 is outside the B200 hot path (every BASELINE config runs 0)")
+
+
+def _as_act(x: torch.Tensor, cfg: ModelConfig) -> torch.Tensor:
+    return x if x.dtype == cfg.act_dtype else x.to(cfg.act_dtype)
+
+
+# ------------------------------------------------------------------ linear / norm
+
+
+def linear3(x: torch.Tensor, p: LinearParams, cfg: ModelConfig, out_dtype=torch.float32) -> torch.Tensor:
+    """model.linear3 (model.py:237-239): x (B, m, E_in) @ W + b -> (B, m, E_out)."""
+    b, m, e = x.shape
+    if p.weight.shape[0] != e:
+        raise ShapeError(f"matmul inner dims disagree: {tuple(x.shape)} x {tuple(p.weight.shape)}")
+    a = _as_act(x, cfg).contiguous()
+    w = _as_act(p.weight, cfg).contiguous()
+    n = w.shape[1]
+    out = torch.empty(b, m, n, dtype=out_dtype, device=x.device)
+    # B operand = W stored [d_in][d_out] = [K][N] -> N-major
+    K.gemm(a.view(b * m, e), w, b_mn_major=True, bias=p.bias, out=out.view(b * m, n), M=b * m, N=n, K=e)
+    return out
+
+
+def linear3_bwd(x: torch.Tensor, p: LinearParams, grad_y: torch.Tensor, cfg: ModelConfig):
+    """model.linear3_bwd (model.py:242-245) -> (grad_x, grad_W, grad_b), fp32."""
+    b, m, e = x.shape
+    n = p.weight.shape[1]
+    gy32 = grad_y.to(torch.float32).contiguous().view(b * m, n)
+    gy = _as_act(gy32, cfg).contiguous()
+    xa = _as_act(x, cfg).contiguous().view(b * m, e)
+    w = _as_act(p.weight, cfg).contiguous()
+    gx = torch.empty(b * m, e, dtype=torch.float32, device=x.device)
+    K.gemm(gy, w, out=gx, M=b * m, N=e, K=n)  # gy . W^T  (W [e][n] is K-major for N=e)
+    gw = torch.empty(e, n, dtype=torch.float32, device=x.device)
+    K.gemm(xa, gy, a_mn_major=True, b_mn_major=True, out=gw, M=e, N=n, K=b * m)  # x^T . gy
+    gb = torch.zeros(n, dtype=torch.float32, device=x.device)
+    K.cat_cast_colsum([(gy32, n, n)], b * m, dst=None, colsum=gb)
+    return gx.view(b, m, e), gw, gb
+
+
+@dataclass
+class NormCache:
+    x: torch.Tensor
+    mean: torch.Tensor
+    rstd: torch.Tensor
+
+
+def norm3(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, cfg: Optional[ModelConfig] = None,
+          out_dtype=torch.float32):
+    """model.norm3 (model.py:248-251) -> (y, cache)."""
+    x = x.to(torch.float32).contiguous()
+    y, mean, rstd = K.layernorm_fwd(x, gain, bias, out_dtype=out_dtype)
+    return y, NormCache(x, mean, rstd)
+
+
+def norm3_bwd(cache: NormCache, gain: torch.Tensor, grad_y: torch.Tensor, grad_res=None):
+    """model.norm3_bwd (model.py:254-257) -> (grad_x, grad_gain, grad_bias).
+    ``grad_res`` (optional) is added to grad_x (the residual of model.py:486)."""
+    gy = grad_y.to(torch.float32).contiguous()
+    return K.layernorm_bwd(gy, cache.x, cache.mean, cache.rstd, gain, grad_res=grad_res)
+
+
+# ------------------------------------------------------------------ attention core
+
+
+@dataclass
+class ScoreCache:
+    """B200 replacement of model.ScoreCache: (ctx, lse) instead of full P."""
+
+    offset: int
+    ctx: torch.Tensor
+    lse2: torch.Tensor
+    k: torch.Tensor = field(repr=False)
+    v: torch.Tensor = field(repr=False)
+    workers: int = 1
+    seg_len: int = 0
+
+
+def _kv_rows(k: torch.Tensor):
+    """Accept (B, t, E) or the packed segment layout (G, B, seg, E)."""
+    if k.dim() == 3:
+        return 1, k.shape[1]
+    if k.dim() == 4:
+        return k.shape[0], k.shape[2]
+    raise ShapeError(f"keys must be (B, t, E) or (G, B, seg, E), got {tuple(k.shape)}")
+
+
+def scores_fwd(q, k, v, offset: int, cfg: ModelConfig, policy=None, layer: int = 0, counters=None):
+    """model.scores_fwd (model.py:280-326) -> (ctx, ScoreCache).
+
+    q (B, m, E) holds this block's rows at global positions offset..offset+m;
+    k/v hold the whole sequence, (B, t, E), or as G row-segments (G, B, seg, E)
+    (e.g. views into the packed all-gather buffer).  Causal rows attend to
+    keys at or before their global position."""
+    _check_dropout(cfg, policy)
+    bsz, m, e = q.shape
+    if e != cfg.embed_dim:
+        raise ShapeError(f"q has {e} features, config says {cfg.embed_dim}")
+    workers, seg = _kv_rows(k)
+    t = workers * seg
+    if cfg.causal and offset < 0:
+        from .errors import DegenerateRowError
+
+        raise DegenerateRowError("negative offset leaves causal rows fully masked")
+    qa = _as_act(q, cfg).contiguous()
+    ka = k if k.dtype == cfg.act_dtype else k.to(cfg.act_dtype)
+    va = v if v.dtype == cfg.act_dtype else v.to(cfg.act_dtype)
+    if ka.dim() == 3:
+        ka, va = ka.contiguous(), va.contiguous()
+    ctx, lse = K.attn_fwd(qa, ka, va, workers=workers, seg_len=seg, heads=cfg.n_heads, offset=offset,
+                          causal=cfg.causal)
+    if counters is not None:  # model.py:312-313, 321-325: 2*m*d*t twice per (b, h)
+        bh = bsz * cfg.n_heads
+        counters.add_score_flops(m, cfg.head_dim * bh, t)
+        counters.add_score_flops(m, t, cfg.head_dim * bh)
+        counters.record_score_footprint(bh * m * t)
+    return ctx, ScoreCache(offset, ctx, lse, ka, va, workers, seg)
+
+
+def scores_bwd(cache: ScoreCache, q, k, v, grad_ctx, cfg: ModelConfig, policy=None):
+    """model.scores_bwd (model.py:329-359) -> (grad_q, grad_k, grad_v), fp32.
+    grad_k / grad_v cover the whole key length (this block's partials) in the
+    layout k/v were given in."""
+    _check_dropout(cfg, policy)
+    qa = _as_act(q, cfg).contiguous()
+    go = _as_act(grad_ctx, cfg).contiguous()
+    workers, seg = cache.workers, cache.seg_len
+    bsz, m, e = qa.shape
+    ka, va = cache.k, cache.v
+    if ka.dim() == 3:
+        packed = torch.empty(bsz, seg, 2 * e, dtype=torch.float32, device=qa.device)
+    else:
+        packed = torch.empty(workers, bsz, seg, 2 * e, dtype=torch.float32, device=qa.device)
+    gk, gv = packed[..., :e], packed[..., e:]
+    gq, gk, gv = K.attn_bwd(qa, ka, va, cache.ctx, go, cache.lse2, workers=workers, seg_len=seg,
+                            heads=cfg.n_heads, offset=cache.offset, causal=cfg.causal, grad_k=gk,
+                            grad_v=gv)
+    return gq, gk, gv
+
+
+def probabilities(cache: ScoreCache, q, cfg: ModelConfig) -> torch.Tensor:
+    """Materialise P (B, H, m, t) from (q, k, lse) for checks (the reference's cache.attn)."""
+    bsz, m, e = q.shape
+    d = cfg.head_dim
+    k = cache.k if cache.k.dim() == 3 else cache.k.permute(1, 0, 2, 3).reshape(bsz, -1, e)
+    qh = q.float().view(bsz, m, cfg.n_heads, d).transpose(1, 2)
+    kh = k.float().reshape(bsz, -1, cfg.n_heads, d).transpose(1, 2)
+    s = qh @ kh.transpose(-1, -2) / math.sqrt(d) * (1.0 / math.log(2))
+    p = torch.exp2(s - cache.lse2[:, :, :m, None])
+    if cfg.causal:
+        t = k.shape[1]
+        keep = torch.arange(t, device=q.device)[None, :] <= (cache.offset + torch.arange(m, device=q.device))[:, None]
+        p = torch.where(keep, p, torch.zeros((), device=q.device))
+    return p
+
+
+# ------------------------------------------------------------------ layer (attention half)
+
+
+def local_kv_fwd(xh: torch.Tensor, lp: LayerParams, cfg: ModelConfig):
+    """model.local_kv_fwd (model.py:413-415): project the block itself."""
+    return linear3(xh, lp.attn_k, cfg, cfg.act_dtype), linear3(xh, lp.attn_v, cfg, cfg.act_dtype), xh
+
+
+def local_kv_bwd(kv_ctx, lp: LayerParams, grad_k, grad_v, cfg: ModelConfig):
+    """model.local_kv_bwd (model.py:418-421)."""
+    gkx, k_wg, k_bg = linear3_bwd(kv_ctx, lp.attn_k, grad_k, cfg)
+    gvx, v_wg, v_bg = linear3_bwd(kv_ctx, lp.attn_v, grad_v, cfg)
+    return gkx + gvx, k_wg, k_bg, v_wg, v_bg
+
+
+@dataclass
+class LayerCache:
+    offset: int
+    ln1: NormCache
+    xh: torch.Tensor
+    kv_ctx: object
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    scores: ScoreCache
+    ctx: torch.Tensor
+
+
+def layer_fwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, x: torch.Tensor, offset: int,
+              kv_fwd: Optional[Callable] = None, counters=None):
+    """Attention half of model.layer_fwd (model.py:442-448):
+    norm -> kv_fwd -> q -> scores -> out-projection -> residual."""
+    _check_dropout(cfg, policy)
+    kv_fwd = kv_fwd or (lambda xh, lp_: local_kv_fwd(xh, lp_, cfg))
+    xh, ln1 = norm3(x, lp.ln1_gain, lp.ln1_bias, cfg, out_dtype=cfg.act_dtype)
+    k, v, kv_ctx = kv_fwd(xh, lp)
+    q = linear3(xh, lp.attn_q, cfg, cfg.act_dtype)
+    ctx, sc = scores_fwd(q, k, v, offset, cfg, policy, layer, counters)
+    x_out = linear3(ctx, lp.attn_out, cfg) + x
+    return x_out, LayerCache(offset, ln1, xh, kv_ctx, q, k, v, sc, ctx)
+
+
+def layer_bwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, cache: LayerCache,
+              grad_out: torch.Tensor, kv_bwd: Optional[Callable] = None):
+    """Attention half of model.layer_bwd (model.py:479-486) -> (grad_in, grads LayerParams)."""
+    _check_dropout(cfg, policy)
+    kv_bwd = kv_bwd or (lambda kv_ctx, lp_, gk, gv: local_kv_bwd(kv_ctx, lp_, gk, gv, cfg))
+    grad_mid = grad_out.to(torch.float32).contiguous()
+    grad_ctx, out_wg, out_bg = linear3_bwd(cache.ctx, lp.attn_out, grad_mid, cfg)
+    gq, gk, gv = scores_bwd(cache.scores, cache.q, cache.k, cache.v, grad_ctx, cfg, policy)
+    gxq, q_wg, q_bg = linear3_bwd(cache.xh, lp.attn_q, gq, cfg)
+    gxkv, k_wg, k_bg, v_wg, v_bg = kv_bwd(cache.kv_ctx, lp, gk, gv)
+    grad_xh = gxq + gxkv
+    g_in, g_gain, g_bias = norm3_bwd(cache.ln1, lp.ln1_gain, grad_xh, grad_res=grad_mid)
+    grads = LayerParams(g_gain, g_bias, LinearParams(q_wg, q_bg), LinearParams(k_wg, k_bg),
+                        LinearParams(v_wg, v_bg), LinearParams(out_wg, out_bg))
+    return g_in, grads

@@ -1,0 +1,265 @@
+"""LSS sequence-parallel attention layer on B200 (reference: seqpar/sharded.py).
+
+Each rank owns a contiguous block of the sequence (ShardSpec, sharded.py:37-61)
+and computes attention for its own query rows against the whole sequence.
+Per layer and step:
+
+  forward   LN1 -> one tcgen05 GEMM writes Q locally and [K_r|V_r] straight into
+            this rank's slot of the packed gather buffer -> ONE all-gather ->
+            segment attention (tcgen05 flash kernel) -> out-projection with the
+            residual fused in the epilogue.
+  backward  out-projection dgrad/wgrad -> attention backward writes this rank's
+            partial [dK|dV] for the whole sequence -> ONE reduce-scatter ->
+            fused cast/bias-sum -> dgrad/wgrad of [Wq|Wk|Wv] -> LN1 backward
+            fused with the residual.
+  sync      every gradient is produced pre-scaled by 1/(D*N) in the kernel that
+            writes it, so ONE world all-reduce (sum) equals the reference's
+            sequence-group mean followed by the data-group mean
+            (sharded.sync 219-244 + hybrid.vertical_sync 76-92).
+
+The engine keeps every buffer resident in HBM (allocated once) and issues no
+host synchronisation; all compute is liblss.so kernels on the current stream.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import kernels as K
+from .comm import Ledger, SimComm, TorchDistComm
+from .errors import PartitionError, ShapeError
+from .model import LayerParams, LinearParams, ModelConfig
+
+
+@dataclass(frozen=True)
+class ShardSpec:
+    """sharded.py:37-61: which contiguous block of the sequence a worker owns."""
+
+    rank: int
+    workers: int
+    seq_len: int
+
+    def __post_init__(self) -> None:
+        if self.workers < 1:
+            raise ValueError("worker count must be positive")
+        if not 0 <= self.rank < self.workers:
+            raise ValueError(f"rank {self.rank} outside worker range [0, {self.workers})")
+        if self.seq_len % self.workers != 0:
+            raise PartitionError(f"sequence length {self.seq_len} not divisible by {self.workers} workers")
+
+    @property
+    def block(self) -> int:
+        return self.seq_len // self.workers
+
+    @property
+    def offset(self) -> int:
+        return self.rank * self.block
+
+
+def slice_batch(x: torch.Tensor, spec: ShardSpec) -> torch.Tensor:
+    """sharded.py:84-88: this worker's rows [offset, offset+block) along dim 1."""
+    if x.shape[1] != spec.seq_len:
+        raise ShapeError(f"expected {spec.seq_len} columns, got {x.shape[1]}")
+    return x[:, spec.offset:spec.offset + spec.block].contiguous()
+
+
+GRAD_NAMES = ("ln1_gain", "ln1_bias", "attn_q.weight", "attn_q.bias", "attn_k.weight", "attn_k.bias",
+              "attn_v.weight", "attn_v.bias", "attn_out.weight", "attn_out.bias")
+
+
+class LSSAttention:
+    """One rank's attention sublayer with resident HBM buffers.
+
+    cfg.seq_len is the FULL sequence length l; spec gives this rank's block.
+    ``grad_scale`` = 1/(D*N) folds the two averaging steps into the kernels.
+    """
+
+    def __init__(self, cfg: ModelConfig, spec: ShardSpec, *, grad_scale: float | None = None,
+                 device=None):
+        if spec.seq_len != cfg.seq_len:
+            raise ShapeError(f"shard spec length {spec.seq_len} != config seq_len {cfg.seq_len}")
+        self.cfg, self.spec = cfg, spec
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.grad_scale = 1.0 / spec.workers if grad_scale is None else grad_scale
+        B, m, G, E, H = cfg.batch, spec.block, spec.workers, cfg.embed_dim, cfg.n_heads
+        self.B, self.m, self.G, self.E, self.H = B, m, G, E, H
+        ad = cfg.act_dtype
+        f32 = torch.float32
+        dev = self.device
+        mp = K.rows_pad(m)
+        z = lambda *s, dt=f32: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
+        # forward
+        self.xh = z(B, m, E, dt=ad)
+        self.mean, self.rstd = z(B * m), z(B * m)
+        self.q = z(B, m, E, dt=ad)
+        self.kv_full = z(G, B, m, 2 * E, dt=ad)          # packed gather buffer (slot r = rank r)
+        self.ctx = z(B, m, E, dt=ad)
+        self.lse2 = z(B, H, mp)
+        self.y = z(B, m, E)
+        # backward
+        self.gy = z(B, m, E, dt=ad)
+        self.dctx = z(B, m, E, dt=ad)
+        self.delta = z(B, H, mp)
+        self.dq = z(B, m, E)
+        self.dkv_full = z(G, B, m, 2 * E)                 # partial [dK|dV] over the whole sequence
+        self.dkv_own = z(B, m, 2 * E)                     # reduce-scatter output (own block)
+        self.dqkv = z(B, m, 3 * E, dt=ad)
+        self.dxh = z(B, m, E)
+        self.dx = z(B, m, E)
+        # gradients, one flat buffer: [Wq Wk Wv | Wo | bq bk bv | bo | ln_g | ln_b | extra]
+        n = 4 * E * E + 6 * E + 1
+        self.grads = torch.zeros(n, dtype=f32, device=dev)
+        o = 0
+        self.g_wqkv = self.grads[o:o + 3 * E * E]; o += 3 * E * E
+        self.g_wo = self.grads[o:o + E * E].view(E, E); o += E * E
+        self.g_bqkv = self.grads[o:o + 3 * E]; o += 3 * E
+        self.g_bo = self.grads[o:o + E]; o += E
+        self.g_ln_g = self.grads[o:o + E]; o += E
+        self.g_ln_b = self.grads[o:o + E]; o += E
+        self.g_extra = self.grads[o:o + 1]
+        self.staged = None
+        self.x = None
+
+    # ------------------------------------------------------------ parameters
+    def load_params(self, lp: LayerParams) -> None:
+        """Stage the reference-layout fp32 weights into the GEMM operand layouts."""
+        self.lp = lp
+        self.staged = K.stage_weights(lp.attn_q.weight, lp.attn_k.weight, lp.attn_v.weight,
+                                      lp.attn_out.weight, lp.attn_q.bias, lp.attn_k.bias,
+                                      lp.attn_v.bias, self.cfg.precision, bufs=self.staged)
+
+    def grad_views(self) -> dict:
+        """Gradients by reference name (model.LayerParams field order)."""
+        E = self.E
+        w = self.g_wqkv.view(3, E, E)
+        b = self.g_bqkv.view(3, E)
+        return {
+            "ln1_gain": self.g_ln_g, "ln1_bias": self.g_ln_b,
+            "attn_q.weight": w[0], "attn_q.bias": b[0],
+            "attn_k.weight": w[1], "attn_k.bias": b[1],
+            "attn_v.weight": w[2], "attn_v.bias": b[2],
+            "attn_out.weight": self.g_wo, "attn_out.bias": self.g_bo,
+        }
+
+    def grad_params(self) -> LayerParams:
+        g = self.grad_views()
+        return LayerParams(g["ln1_gain"], g["ln1_bias"],
+                           LinearParams(g["attn_q.weight"], g["attn_q.bias"]),
+                           LinearParams(g["attn_k.weight"], g["attn_k.bias"]),
+                           LinearParams(g["attn_v.weight"], g["attn_v.bias"]),
+                           LinearParams(g["attn_out.weight"], g["attn_out.bias"]))
+
+    # ------------------------------------------------------------ forward
+    @property
+    def kv_slot(self) -> torch.Tensor:
+        return self.kv_full[self.spec.rank]
+
+    def fwd_project(self, x: torch.Tensor) -> None:
+        """LN1 + [Q | K_r | V_r] projection; K_r|V_r land in this rank's gather slot."""
+        B, m, E = self.B, self.m, self.E
+        if x.shape != (B, m, E) or x.dtype != torch.float32 or not x.is_contiguous():
+            raise ShapeError(f"x must be contiguous fp32 {(B, m, E)}, got {tuple(x.shape)} {x.dtype}")
+        self.x = x
+        lp, st = self.lp, self.staged
+        K.layernorm_fwd(x, lp.ln1_gain, lp.ln1_bias, out=self.xh, mean=self.mean, rstd=self.rstd)
+        slot = self.kv_slot.view(B * m, 2 * E)
+        K.gemm(self.xh.view(B * m, E), st["wqkv_t"], bias=st["bqkv"], seg_width=E,
+               out=[(self.q.view(B * m, E), E), (slot[:, :E], 2 * E), (slot[:, E:], 2 * E)],
+               M=B * m, N=3 * E, K=E)
+
+    def fwd_attend(self) -> torch.Tensor:
+        """Segment attention over the gathered K/V, out-projection + residual."""
+        B, m, E = self.B, self.m, self.E
+        K.attn_fwd(self.q, self.kv_full[..., :E], self.kv_full[..., E:], workers=self.G, seg_len=m,
+                   heads=self.H, offset=self.spec.offset, causal=self.cfg.causal, out=self.ctx,
+                   lse2=self.lse2)
+        K.gemm(self.ctx.view(B * m, E), self.staged["wo_t"], bias=self.lp.attn_out.bias,
+               residual=self.x.view(B * m, E), out=self.y.view(B * m, E), M=B * m, N=E, K=E)
+        return self.y
+
+    # ------------------------------------------------------------ backward
+    def bwd_attend(self, grad_y: torch.Tensor) -> None:
+        """Out-projection backward and attention backward (partial dK|dV for all ranks)."""
+        B, m, E = self.B, self.m, self.E
+        if grad_y.shape != (B, m, E) or grad_y.dtype != torch.float32 or not grad_y.is_contiguous():
+            raise ShapeError(f"grad_y must be contiguous fp32 {(B, m, E)}")
+        self.grad_y = grad_y
+        a = self.grad_scale
+        self.grads.zero_()
+        # gy -> operand dtype, d b_out = alpha * column sums (nnops.py:192)
+        K.cat_cast_colsum([(grad_y.view(B * m, E), E, E)], B * m, dst=self.gy.view(B * m, E),
+                          colsum=self.g_bo, alpha=a)
+        # dctx = gy . Wo^T  (Wo [in][out] is the K-major B operand)
+        K.gemm(self.gy.view(B * m, E), self.staged["wo"], out=self.dctx.view(B * m, E), M=B * m, N=E, K=E)
+        # dWo = ctx^T . gy  (both operands MN-major), pre-scaled
+        K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True, alpha=a,
+               out=self.g_wo, M=E, N=E, K=B * m)
+        K.attn_bwd(self.q, self.kv_full[..., :E], self.kv_full[..., E:], self.ctx, self.dctx, self.lse2,
+                   workers=self.G, seg_len=m, heads=self.H, offset=self.spec.offset,
+                   causal=self.cfg.causal, grad_q=self.dq, grad_k=self.dkv_full[..., :E],
+                   grad_v=self.dkv_full[..., E:], delta=self.delta)
+
+    def bwd_project(self) -> torch.Tensor:
+        """After the reduce-scatter: [dQ|dK|dV] -> dx̂ and dW_qkv, LN1 backward + residual."""
+        B, m, E = self.B, self.m, self.E
+        a = self.grad_scale
+        M = B * m
+        K.cat_cast_colsum([(self.dq.view(M, E), E, E), (self.dkv_own.view(M, 2 * E), 2 * E, 2 * E)], M,
+                          dst=self.dqkv.view(M, 3 * E), colsum=self.g_bqkv, alpha=a)
+        K.gemm(self.dqkv.view(M, 3 * E), self.staged["wqkv"], out=self.dxh.view(M, E), M=M, N=E, K=3 * E)
+        gw = self.g_wqkv.view(3, E, E)
+        K.gemm(self.xh.view(M, E), self.dqkv.view(M, 3 * E), a_mn_major=True, b_mn_major=True, alpha=a,
+               seg_width=E, out=[(gw[0], E), (gw[1], E), (gw[2], E)], M=E, N=3 * E, K=M)
+        K.layernorm_bwd(self.dxh.view(M, E), self.x.view(M, E), self.mean, self.rstd, self.lp.ln1_gain,
+                        grad_res=self.grad_y.view(M, E), grad_x=self.dx.view(M, E),
+                        grad_gain=self.g_ln_g, grad_bias=self.g_ln_b, alpha=a)
+        return self.dx
+
+
+# ---------------------------------------------------------------- drivers
+
+
+def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True):
+    """One fwd+bwd(+sync) of the attention sublayer.
+
+    Real multi-GPU: ``engines`` = [this rank's LSSAttention], ``comm`` a
+    TorchDistComm.  Single-process simulation: G engines and a SimComm.
+    Returns the list of (y, dx) per engine (device tensors, not synchronised)."""
+    sim = isinstance(comm, SimComm)
+    for e, x in zip(engines, xs):
+        e.fwd_project(x)
+    if sim:
+        comm.all_gather_rows([e.kv_full for e in engines], step, layer)
+    else:
+        comm.all_gather_rows(engines[0].kv_full, step, layer)
+    ys = [e.fwd_attend() for e in engines]
+    for e, gy in zip(engines, grad_ys):
+        e.bwd_attend(gy)
+    if sim:
+        comm.reduce_scatter_rows([e.dkv_own for e in engines], [e.dkv_full for e in engines], step, layer)
+    else:
+        comm.reduce_scatter_rows(engines[0].dkv_own, engines[0].dkv_full, step, layer)
+    dxs = [e.bwd_project() for e in engines]
+    if sync:
+        if sim:
+            comm.all_reduce_sum([e.grads for e in engines], step)
+        else:
+            comm.all_reduce_sum(engines[0].grads, step)
+    return list(zip(ys, dxs))
+
+
+def make_sim_group(cfg: ModelConfig, lp: LayerParams, workers: int, *, replicas: int = 1, device=None):
+    """G engines of one sequence group on one device (tests / smoke), SimComm fabric."""
+    engines = []
+    for r in range(workers):
+        e = LSSAttention(cfg, ShardSpec(r, workers, cfg.seq_len), grad_scale=1.0 / (workers * replicas),
+                         device=device)
+        e.load_params(lp)
+        engines.append(e)
+    return engines, SimComm(Ledger())
+
+
+__all__ = ["ShardSpec", "slice_batch", "LSSAttention", "lss_step", "make_sim_group", "TorchDistComm",
+           "SimComm", "Ledger", "GRAD_NAMES"]

@@ -134,7 +134,8 @@ def test_attention_fwd_bwd_vs_oracle(cuda, rng, case, prec):
     E = 64 * H
     tq, tkv, qn, kn, vn = _attn_inputs(rng, bsz, m, G, H, rank, cuda, dt)
     offset = rank * m
-    o, lse = K.attn_fwd(tq, tkv, workers=G, seg_len=m, heads=H, offset=offset, causal=causal)
+    o, lse = K.attn_fwd(tq, tkv[..., :E], tkv[..., E:], workers=G, seg_len=m, heads=H, offset=offset,
+                        causal=causal)
     torch.cuda.synchronize()
     ctx_ref, p_ref = O.scores_fwd(qn, kn, vn, offset, H, causal)
     assert nerr(_np(o), ctx_ref) < tol
@@ -149,13 +150,12 @@ def test_attention_fwd_bwd_vs_oracle(cuda, rng, case, prec):
     # backward
     go = rng.standard_normal((bsz, m, E))
     tgo = _t(go, cuda, dt)
-    gq, gkv = K.attn_bwd(tq, tkv, o, tgo, lse, workers=G, seg_len=m, heads=H, offset=offset,
-                         causal=causal)
+    gq, gk, gv = K.attn_bwd(tq, tkv[..., :E], tkv[..., E:], o, tgo, lse, workers=G, seg_len=m, heads=H,
+                            offset=offset, causal=causal)
     torch.cuda.synchronize()
     dq_ref, dk_ref, dv_ref = O.scores_bwd(p_ref, qn, kn, vn, _np(tgo), H)
-    gkvn = _np(gkv)
-    dk = gkvn[..., :E].transpose(1, 0, 2, 3).reshape(bsz, -1, E)
-    dv = gkvn[..., E:].transpose(1, 0, 2, 3).reshape(bsz, -1, E)
+    dk = _np(gk).transpose(1, 0, 2, 3).reshape(bsz, -1, E)
+    dv = _np(gv).transpose(1, 0, 2, 3).reshape(bsz, -1, E)
     btol = 2 * tol
     assert nerr(_np(gq), dq_ref) < btol
     assert nerr(dk, dk_ref) < btol
@@ -169,7 +169,8 @@ def test_attention_peaked_softmax_bf16(cuda, rng):
 
     bsz, m, G, H = 1, 384, 2, 1
     tq, tkv, qn, kn, vn = _attn_inputs(rng, bsz, m, G, H, 1, cuda, torch.bfloat16, scale=3.0)
-    o, lse = K.attn_fwd(tq, tkv, workers=G, seg_len=m, heads=H, offset=m, causal=True)
+    o, lse = K.attn_fwd(tq, tkv[..., :64], tkv[..., 64:], workers=G, seg_len=m, heads=H, offset=m,
+                        causal=True)
     torch.cuda.synchronize()
     ctx_ref, _ = O.scores_fwd(qn, kn, vn, m, H, True)
     assert nerr(_np(o), ctx_ref) < BF16_TOL
@@ -183,4 +184,4 @@ def test_attention_rejects_unsupported_head_dim(cuda):
     q = torch.zeros(1, 16, 96, dtype=torch.bfloat16, device=cuda)  # d = 32 with 3 heads
     kv = torch.zeros(1, 1, 16, 192, dtype=torch.bfloat16, device=cuda)
     with pytest.raises(UnsupportedError):
-        K.attn_fwd(q, kv, workers=1, seg_len=16, heads=3, offset=0, causal=True)
+        K.attn_fwd(q, kv[..., :96], kv[..., 96:], workers=1, seg_len=16, heads=3, offset=0, causal=True)

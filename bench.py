@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: tokens/s for forward+backward of ONE LSS attention layer
+(l_x = 50112, E_m = 1024, 16 heads, causal, bf16 operands / fp32 accumulation)
+on N B200s of one node, N = 1, 2, 4, 8 (BASELINE.json `metric`).
+
+    python bench.py [--gpus N --steps K --warmup W]               # our B200 path
+    python bench.py --impl reference [...]                          # reference CPU arm
+    torchrun --nproc-per-node N bench.py --gpus N ...               # N > 1 (NCCL)
+
+A step = the attention sublayer of one layer: LN1, [Q|K|V] projection,
+packed-K/V all-gather, segment attention, out-projection + residual, and the
+whole backward incl. the dK/dV reduce-scatter and the folded gradient
+all-reduce, plus the per-step weight staging.  The sequence is split across the
+N ranks (ShardSpec), so total work is fixed: scaling = "strong".  Synthetic
+inputs (x, upstream gradient ~ N(0,1)) and random-init weights of the named
+shape (U(+-1/sqrt(E)), zero biases, unit LN gain -- model.init_params's
+convention).  The per-step working set (>= 0.6 GB of K/V and dK/dV buffers)
+is larger than the 126 MB L2, so no explicit flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tokens/sec fwd+bwd per LSS attention layer at l_x=50112, 1/2/4/8 B200; % bf16 peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seq", type=int, default=50112)
+    ap.add_argument("--embed", type=int, default=1024)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--noncausal", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=128, help="query rows in the CPU sample")
+    return ap.parse_args()
+
+
+def workload(args):
+    return (f"LSS attention sublayer fwd+bwd, l_x={args.seq}, E_m={args.embed}, {args.heads} heads, "
+            f"{'non-causal' if args.noncausal else 'causal'}, batch {args.batch}")
+
+
+def layer_flops(batch, seq, embed, causal):
+    """F = 24 l E^2 + 12 E P per sequence, P = l(l+1)/2 causal or l^2."""
+    pairs = seq * (seq + 1) // 2 if causal else seq * seq
+    return batch * (24 * seq * embed * embed + 12 * embed * pairs)
+
+
+def rank_pairs(offset, rows, seq, causal):
+    """Unmasked (q, k) pairs of query rows [offset, offset+rows) against seq keys."""
+    if not causal:
+        return rows * seq
+    full = max(0, min(rows, seq - offset))  # rows whose key range ends inside the sequence
+    return full * offset + full * (full + 1) // 2 + (rows - full) * seq
+
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["bf16_tflops"]), float(d["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, "fallback"
+
+
+def traffic_from_profile(name):
+    """dram bytes per launch of `name` from the committed ncu --set full summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        return d["kernels"][name]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.proc = None
+        self.t0 = self.t1 = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(device_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        self.lines = []
+
+    def start(self):
+        self.t0 = time.time()
+
+    def stop(self):
+        self.t1 = time.time()
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=5)
+        rows = [ln.split(", ") for ln in out.strip().splitlines() if ln.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for nm, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(nm)
+        # the sampler runs a little before/after the timed region: keep the loaded samples
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference / CPU arm
+
+
+def cpu_sample(args, rows, threads):
+    """Time the oracle port of the reference's attention sublayer on a bounded
+    sample: `rows` query rows centred on l/2 (the mean causal row) against the
+    full-length K/V.  Returns (seconds, description)."""
+    import numpy as np
+
+    from oracle import lss_oracle as O
+
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((args.batch, args.seq, args.embed), dtype=np.float32)
+    gy = rng.standard_normal((args.batch, args.seq, args.embed), dtype=np.float32)
+    p = O.init_attn_params(args.embed, seed=0, dtype=np.float32)
+    offset = max(0, args.seq // 2 - rows // 2)
+    run = O.sample_rows(x, gy, p, args.heads, offset, rows, causal=not args.noncausal)
+    return run, (f"{rows} query rows at offset {offset} of l_x={args.seq} (fp32 numpy oracle port of the "
+                 f"reference's scores_fwd/scores_bwd + projections + LN; K/V of the whole sequence "
+                 f"precomputed), {threads} host threads")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    rows = max(8, min(args.cpu_rows, 64))
+    run, desc = cpu_sample(args, rows, threads)
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    value = args.batch * rows / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload(args), "global_batch": args.batch, "seq_len": args.seq,
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_02382_b200 import _native
+    from paper_2311_02382_b200.comm import Ledger, SoloComm, TorchDistComm
+    from paper_2311_02382_b200.model import LayerParams, LinearParams, ModelConfig
+    from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = TorchDistComm(None, None, Ledger())
+    else:
+        comm = SoloComm(Ledger())
+    causal = not args.noncausal
+    B, l, E, H = args.batch, args.seq, args.embed, args.heads
+    cfg = ModelConfig(embed_dim=E, n_layers=1, n_heads=H, ff_dim=4 * E, vocab=256, seq_len=l, batch=B,
+                      causal=causal, precision="bf16")
+    spec = ShardSpec(rank, world, l)
+    m = spec.block
+    g = torch.Generator(device=dev).manual_seed(1234)
+    bound = 1.0 / math.sqrt(E)
+    u = lambda: (torch.rand(E, E, generator=g, device=dev) * 2 - 1) * bound  # noqa: E731
+    z = lambda: torch.zeros(E, device=dev)  # noqa: E731
+    lp = LayerParams(torch.ones(E, device=dev), z(), LinearParams(u(), z()), LinearParams(u(), z()),
+                     LinearParams(u(), z()), LinearParams(u(), z()))
+    gx = torch.Generator(device=dev).manual_seed(100 + rank)
+    x = torch.randn(B, m, E, generator=gx, device=dev)
+    gy = torch.randn(B, m, E, generator=gx, device=dev)
+    eng = LSSAttention(cfg, spec, grad_scale=1.0 / world, device=dev)
+
+    # per-kernel CUDA-event timing of the two attention kernels inside the timed region
+    stream = torch.cuda.current_stream()
+    marks = {"fwd": [], "bwd": []}
+    from paper_2311_02382_b200 import kernels as Kmod
+
+    orig_fwd, orig_bwd = Kmod.attn_fwd, Kmod.attn_bwd
+
+    def timed(kind, fn):
+        def wrapper(*a, **kw):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn(*a, **kw)
+            e1.record(stream)
+            marks[kind].append((e0, e1))
+            return out
+        return wrapper
+
+    def one_step():
+        eng.load_params(lp)  # weights change every training step: restage (1 kernel)
+        eng.step(x, gy, comm)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    Kmod.attn_fwd, Kmod.attn_bwd = timed("fwd", orig_fwd), timed("bwd", orig_bwd)
+    sampler = ClockSampler(local)
+    time.sleep(0.3)  # let the sampler come up
+    comm.ledger.clear()
+    launches0 = _native.launch_count
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    Kmod.attn_fwd, Kmod.attn_bwd = orig_fwd, orig_bwd
+    launches = (_native.launch_count - launches0) // args.steps
+    coll = {k: comm.ledger.count(k) // args.steps for k in ("all-gather", "reduce-scatter", "all-reduce")}
+    ms = t_start.elapsed_time(t_end) / args.steps
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in marks["fwd"])
+    bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in marks["bwd"])
+    my_pairs = rank_pairs(spec.offset, m, l, causal) * B
+    stats = torch.tensor([ms, fwd_ms, bwd_ms, float(my_pairs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        allst = [torch.zeros_like(stats) for _ in range(world)]
+        dist.all_gather(allst, stats)
+        allst = torch.stack(allst).cpu().tolist()
+    else:
+        allst = [stats.cpu().tolist()]
+    ms_max = max(r[0] for r in allst)
+    crit = max(allst, key=lambda r: r[2])  # rank with the slowest attention backward
+    tokens = B * l
+    value = tokens / (ms_max / 1e3)
+    burst, sustained, src = peaks()
+    total_flops = layer_flops(B, l, E, causal)
+    pct = {"burst": total_flops / (ms_max / 1e3) / (world * burst * 1e12),
+           "sustained": total_flops / (ms_max / 1e3) / (world * sustained * 1e12)}
+    bwd_flops = 8 * E * crit[3]
+    fwd_flops = 4 * E * crit[3]
+    ach_bwd = bwd_flops / (crit[2] / 1e3) / 1e12
+    ach_fwd = fwd_flops / (crit[1] / 1e3) / 1e12
+    roofline = {"kernel": "attn_bwd_tc_kernel (+ delta pre-pass)", "bound": "tensor",
+                "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s", "frac": ach_bwd / sustained,
+                "frac_of_burst": ach_bwd / burst, "peak_source": f"{src} bf16_tflops_sustained",
+                "traffic": traffic_from_profile("attn_bwd_tc_kernel"),
+                "algorithmic": f"8*E per unmasked (q,k) pair; {crit[3]:.4g} pairs on the critical rank",
+                "ms_per_launch": crit[2],
+                "fwd": {"kernel": "attn_fwd_tc_kernel", "achieved": ach_fwd, "frac": ach_fwd / sustained,
+                        "ms_per_launch": crit[1], "traffic": traffic_from_profile("attn_fwd_tc_kernel")}}
+
+    # ---------------- end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        gyh = gy.cpu().pin_memory()
+        grads_h = torch.empty(eng.grads.numel(), dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            eng.load_params(lp)
+            eng.step_from_host(xh, gyh, comm, grads_h)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.load_params(lp)
+            eng.step_from_host(xh, gyh, comm, grads_h)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_e2e = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": tokens / (t_e2e.item() / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * B * m * E * 4, "d2h_bytes_per_step": eng.grads.numel() * 4,
+               "ms_per_step": t_e2e.item(),
+               "api": "LSSAttention.step_from_host (pinned x, grad_y in; averaged grads out)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        run, desc = cpu_sample(args, args.cpu_rows, threads)
+        run()  # warm
+        reps, t0 = 0, time.perf_counter()
+        while True:  # >= 10 s of CPU work (bounded sample, repeated)
+            run()
+            reps += 1
+            dt = time.perf_counter() - t0
+            if dt >= 10.0 or reps >= 50:
+                break
+        cpu = {"value": B * args.cpu_rows * reps / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
+               "sample": f"{reps} x " + desc, "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": workload(args), "global_batch": B, "seq_len": l, "embed": E,
+                       "heads": H, "parallelism": f"sp{world}", "tokens_per_gpu": m,
+                       "l2": "inputs larger than L2 (no flush)"},
+            "pct_bf16_peak": pct,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "per_rank_ms": [r[0] for r in allst],
+            "collectives_per_step": coll,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return main_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -107,7 +107,7 @@ def scores_fwd(q, k, v, offset, n_heads, causal=True):
     d = e // n_heads
     scale = 1.0 / math.sqrt(d)
     qh, kh, vh = (_split_heads(a, n_heads) for a in (q, k, v))
-    s = np.einsum("bhid,bhjd->bhij", qh, kh) * scale
+    s = (qh @ kh.transpose(0, 1, 3, 2)) * scale  # BLAS, as tensor.matmul (tensor.py:91)
     if causal:
         keep = causal_keep(m, t, offset)
         if np.any(keep.sum(axis=1) == 0):
@@ -116,7 +116,7 @@ def scores_fwd(q, k, v, offset, n_heads, causal=True):
     s = s - s.max(axis=-1, keepdims=True)
     p = np.exp(s)
     p = p / p.sum(axis=-1, keepdims=True)
-    ctx = _merge_heads(np.einsum("bhij,bhjd->bhid", p, vh))
+    ctx = _merge_heads(p @ vh)
     return ctx, p
 
 
@@ -127,11 +127,11 @@ def scores_bwd(p, q, k, v, grad_ctx, n_heads):
     d = q.shape[2] // n_heads
     scale = 1.0 / math.sqrt(d)
     qh, kh, vh, gh = (_split_heads(a, n_heads) for a in (q, k, v, grad_ctx))
-    dp = np.einsum("bhid,bhjd->bhij", gh, vh)
-    dv = np.einsum("bhij,bhid->bhjd", p, gh)
+    dp = gh @ vh.transpose(0, 1, 3, 2)
+    dv = p.transpose(0, 1, 3, 2) @ gh
     ds = p * (dp - (dp * p).sum(axis=-1, keepdims=True)) * scale
-    dq = np.einsum("bhij,bhjd->bhid", ds, kh)
-    dk = np.einsum("bhij,bhid->bhjd", ds, qh)
+    dq = ds @ kh
+    dk = ds.transpose(0, 1, 3, 2) @ qh
     return _merge_heads(dq), _merge_heads(dk), _merge_heads(dv)
 
 

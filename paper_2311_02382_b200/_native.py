@@ -96,10 +96,18 @@ def load():
     return lib
 
 
+# kernels each entry point launches (bf16 path; attn_bwd = delta + main kernel)
+KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 1, "lss_stage_weights": 1,
+                    "lss_cat_cast_colsum": 1, "lss_attn_fwd": 1, "lss_attn_bwd": 2}
+launch_count = 0
+
+
 def call(name: str, *args):
     """Invoke an entry point and map a non-zero status onto the reference's exceptions."""
+    global launch_count
     lib = load()
     rc = getattr(lib, name)(*args)
+    launch_count += KERNELS_PER_CALL.get(name, 0)
     if rc != 0:
         msg = lib.lss_last_error().decode(errors="replace")
         raise _STATUS.get(rc, NativeError)(f"{name}: {msg}")

@@ -78,8 +78,8 @@ class TorchDistComm:
         self.ledger.record("all-gather", self.seq_name, full.numel(), step, "forward", layer)
         if self.seq_size == 1:
             return None
-        return self.dist.all_gather_into_tensor(full, full[self.seq_rank], group=self.seq_group,
-                                                async_op=async_op)
+        return self.dist.all_gather_into_tensor(full.view(-1), full[self.seq_rank].view(-1),
+                                                group=self.seq_group, async_op=async_op)
 
     def reduce_scatter_rows(self, out: torch.Tensor, full: torch.Tensor, step=0, layer=0, async_op=False):
         """out = sum over ranks of full[seq_rank] (rank-ordered blocks, collectives.py:346-372)."""
@@ -87,7 +87,8 @@ class TorchDistComm:
         if self.seq_size == 1:
             out.copy_(full[0])
             return None
-        return self.dist.reduce_scatter_tensor(out, full, group=self.seq_group, async_op=async_op)
+        return self.dist.reduce_scatter_tensor(out.view(-1), full.view(-1), group=self.seq_group,
+                                               async_op=async_op)
 
     def all_reduce_sum(self, buf: torch.Tensor, step=0, async_op=False):
         """Folded double gradient averaging: one world all-reduce of gradients that
@@ -97,6 +98,27 @@ class TorchDistComm:
         if world == 1:
             return None
         return self.dist.all_reduce(buf, group=self.world_group, async_op=async_op)
+
+
+class SoloComm:
+    """One rank, no process group (G = D = 1): collectives are identities."""
+
+    seq_size = 1
+    seq_rank = 0
+
+    def __init__(self, ledger: Ledger | None = None):
+        self.ledger = ledger if ledger is not None else Ledger()
+
+    def all_gather_rows(self, full, step=0, layer=0, async_op=False):
+        self.ledger.record("all-gather", "sequence", full.numel(), step, "forward", layer)
+
+    def reduce_scatter_rows(self, out, full, step=0, layer=0, async_op=False):
+        self.ledger.record("reduce-scatter", "sequence", full.numel(), step, "backward", layer)
+        if out.data_ptr() != full.data_ptr():
+            out.copy_(full[0])
+
+    def all_reduce_sum(self, buf, step=0, async_op=False):
+        self.ledger.record("all-reduce", "world", buf.numel(), step, "sync", None)
 
 
 class SimComm:

@@ -104,7 +104,8 @@ class LSSAttention:
         self.delta = z(B, H, mp)
         self.dq = z(B, m, E)
         self.dkv_full = z(G, B, m, 2 * E)                 # partial [dK|dV] over the whole sequence
-        self.dkv_own = z(B, m, 2 * E)                     # reduce-scatter output (own block)
+        # reduce-scatter output (own block); with one worker it IS the full buffer
+        self.dkv_own = self.dkv_full[0] if G == 1 else z(B, m, 2 * E)
         self.dqkv = z(B, m, 3 * E, dt=ad)
         self.dxh = z(B, m, E)
         self.dx = z(B, m, E)
@@ -216,6 +217,51 @@ class LSSAttention:
                         grad_res=self.grad_y.view(M, E), grad_x=self.dx.view(M, E),
                         grad_gain=self.g_ln_g, grad_bias=self.g_ln_b, alpha=a)
         return self.dx
+
+    # ------------------------------------------------------------ public step API
+    def step(self, x: torch.Tensor, grad_y: torch.Tensor, comm, *, step: int = 0, layer: int = 0,
+             sync: bool = True):
+        """Forward + backward (+ folded gradient sync) of this rank's block, device
+        tensors in and out.  Returns (y, dx); gradients are in ``grads`` /
+        ``grad_views()`` (already averaged over the group(s) when sync=True)."""
+        self.fwd_project(x)
+        comm.all_gather_rows(self.kv_full, step, layer)
+        y = self.fwd_attend()
+        self.bwd_attend(grad_y)
+        comm.reduce_scatter_rows(self.dkv_own, self.dkv_full, step, layer)
+        dx = self.bwd_project()
+        if sync:
+            comm.all_reduce_sum(self.grads, step)
+        return y, dx
+
+    def step_from_host(self, x_host: torch.Tensor, grad_y_host: torch.Tensor, comm, grads_host=None,
+                       *, step: int = 0, layer: int = 0):
+        """End-to-end call with HOST buffers: pinned x / grad_y are copied in (grad_y
+        on a side stream, overlapped with the forward), the averaged gradients are
+        copied back to ``grads_host`` (pinned).  Stream-ordered; the caller
+        synchronises when it needs the host result."""
+        cur = torch.cuda.current_stream()
+        if not hasattr(self, "_x_dev"):
+            self._x_dev = torch.empty(self.B, self.m, self.E, dtype=torch.float32, device=self.device)
+            self._gy_dev = torch.empty_like(self._x_dev)
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+            self._gy_ready = torch.cuda.Event()
+        self._copy_stream.wait_stream(cur)
+        with torch.cuda.stream(self._copy_stream):
+            self._gy_dev.copy_(grad_y_host, non_blocking=True)
+            self._gy_ready.record()
+        self._x_dev.copy_(x_host, non_blocking=True)
+        self.fwd_project(self._x_dev)
+        comm.all_gather_rows(self.kv_full, step, layer)
+        y = self.fwd_attend()
+        cur.wait_event(self._gy_ready)
+        self.bwd_attend(self._gy_dev)
+        comm.reduce_scatter_rows(self.dkv_own, self.dkv_full, step, layer)
+        dx = self.bwd_project()
+        comm.all_reduce_sum(self.grads, step)
+        if grads_host is not None:
+            grads_host.copy_(self.grads, non_blocking=True)
+        return y, dx
 
 
 # ---------------------------------------------------------------- drivers

@@ -39,7 +39,7 @@ struct AttnBwdParams {
   float scale_log2;  // log2(e)/sqrt(d)
   float scale;       // 1/sqrt(d)
   const float* lse2;   // [B][H][m_pad] (+inf padded)
-  const float* delta;  // [B][H][m_pad] (0 padded)
+  const float* delta;  // [B][H][m_pad] rowsum(dO*O)/sqrt(d) (0 padded)
   float* dq;           // [B][m][E] fp32, accumulated (must be zeroed)
   float* dk;           // [G][B][seg_len][ld_dkv] fp32, fully written
   float* dv;           // same layout
@@ -52,6 +52,36 @@ LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t
           smem_u32(sdst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// P^T and dS^T for one key row and 64 query columns:
+//   p = 2^(s*log2e/sqrt(d) - lse2[q]),  ds = p * (dp/sqrt(d) - delta[q]/sqrt(d))
+// lse2 / scaled delta come from shared memory as 128-bit broadcast loads; the
+// causal / tail mask (column c visible iff c >= fv) is compiled only into the
+// MASK instance so full tiles carry no per-element predicate work.
+template <bool MASK>
+LSS_DEV void bwd_pds(const uint32_t (&sv)[64], const uint32_t (&dp)[64], uint32_t s_lse, uint32_t s_dsc,
+                     float sl2, float scale, int fv, uint32_t (&pk)[32], uint32_t (&dk)[32]) {
+#pragma unroll
+  for (int c4 = 0; c4 < 16; ++c4) {
+    const float4 l = ld_shared_f4(s_lse + c4 * 16);
+    const float4 d = ld_shared_f4(s_dsc + c4 * 16);
+    const float lv[4] = {l.x, l.y, l.z, l.w};
+    const float dv[4] = {d.x, d.y, d.z, d.w};
+    float pr[4], dr[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = 4 * c4 + j;
+      float pj = ex2(fmaf(__uint_as_float(sv[c]), sl2, -lv[j]));
+      if (MASK) pj = (c >= fv) ? pj : 0.f;
+      pr[j] = pj;
+      dr[j] = pj * fmaf(__uint_as_float(dp[c]), scale, -dv[j]);
+    }
+    pk[2 * c4] = pack_bf16(pr[0], pr[1]);
+    pk[2 * c4 + 1] = pack_bf16(pr[2], pr[3]);
+    dk[2 * c4] = pack_bf16(dr[0], dr[1]);
+    dk[2 * c4 + 1] = pack_bf16(dr[2], dr[3]);
+  }
 }
 
 __global__ void __launch_bounds__(ATB_THREADS, 1)
@@ -201,7 +231,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     const long kpos = kpos0 + t;
     const bool row_ok = t < kv_valid;
     uint8_t* stg_half = sStage + half * 128 * 128;  // [128 q rows][32 fp32], 128B-swizzled
-    uint8_t* stg_row = stg_half + t * 128;
+    const uint32_t stg_row = smem_u32(stg_half + t * 128);
     const bool issuer = (t == 0);                    // one thread per half issues the reduce
     auto drain_dq = [&](int it) {
       // dQ rows of query tile `it` (TMEM lane = query row), columns [32*half, +32):
@@ -214,8 +244,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       named_bar_sync(1 + half, 128);
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(stg_row + ((c ^ (t & 7)) << 4)) =
-            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        st_shared_v4(stg_row + ((c ^ (t & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
       fence_proxy_async_smem();
       named_bar_sync(1 + half, 128);
       if (issuer) {
@@ -226,9 +255,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     for (int it = 0; it < n_iter; ++it) {
       const int s = it & 1;
       const int q0 = (i_first + it) * ATT_BM;
-      const uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
-      const float* s_lse = reinterpret_cast<const float*>(st + 2 * ATT_TILE_BYTES) + half * 64;
-      const float* s_del = reinterpret_cast<const float*>(st + 2 * ATT_TILE_BYTES + 512) + half * 64;
+      const uint32_t st = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
+      const uint32_t s_lse = st + 2 * ATT_TILE_BYTES + half * 256;        // lse2[q], 64 floats
+      const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + half * 256;  // delta[q]/sqrt(d)
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
       uint32_t sv[64], dp[64];
@@ -236,32 +265,24 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       tmem_ld64(tdP + lane_off + half * 64, dp);
       tc_fence_before();
       mbar_arrive(sdp_free);
-      // q tile visible to key row t: q_pos = offset + q0 + col >= kpos
+      // query column c of this half is visible to key row t iff c >= fv
       const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > p.offset + q0 + half * 64);
-      const long first_vis = kpos - p.offset - q0 - half * 64;  // col >= first_vis is visible
       uint32_t pk[32], dk[32];
-#pragma unroll
-      for (int c = 0; c < 64; c += 2) {
-        float p0 = ex2(fmaf(__uint_as_float(sv[c]), p.scale_log2, -s_lse[c]));
-        float p1 = ex2(fmaf(__uint_as_float(sv[c + 1]), p.scale_log2, -s_lse[c + 1]));
-        if (need_mask) {
-          if (!row_ok || (p.causal && (long)c < first_vis)) p0 = 0.f;
-          if (!row_ok || (p.causal && (long)(c + 1) < first_vis)) p1 = 0.f;
-        }
-        const float d0 = p0 * (__uint_as_float(dp[c]) - s_del[c]) * p.scale;
-        const float d1 = p1 * (__uint_as_float(dp[c + 1]) - s_del[c + 1]) * p.scale;
-        pk[c / 2] = pack_bf16(p0, p1);
-        dk[c / 2] = pack_bf16(d0, d1);
+      if (need_mask) {
+        const long first_vis = kpos - p.offset - q0 - half * 64;
+        const int fv = !row_ok ? 64 : (p.causal ? (int)max(0L, min(64L, first_vis)) : 0);
+        bwd_pds<true>(sv, dp, s_lse, s_dsc, p.scale_log2, p.scale, fv, pk, dk);
+      } else {
+        bwd_pds<false>(sv, dp, s_lse, s_dsc, p.scale_log2, p.scale, 0, pk, dk);
       }
       if (it > 0) drain_dq(it - 1);  // also guarantees dV/dK/dQ of tile it-1 are done
       tmem_st32(tP + lane_off + half * 32, pk);
       // dS^T row t, query columns [64*half, +64) -> sub-tile `half`, SW128 K-major
       {
-        uint8_t* row = sdS + half * ATT_TILE_BYTES + t * 128;
+        const uint32_t row = smem_u32(sdS + half * ATT_TILE_BYTES + t * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(row + ((c ^ (t & 7)) << 4)) =
-              make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
+          st_shared_v4(row + ((c ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
       }
       fence_proxy_async_smem();
       tc_fence_before();

@@ -192,10 +192,11 @@ __global__ void weight_stage_kernel(const float* __restrict__ wq, const float* _
   }
 }
 
-// delta[b][h][row] = sum_d dO[b,row,h*d+k] * O[b,row,h*d+k], padded rows set to 0.
+// delta[b][h][row] = scale * sum_d dO[b,row,h*d+k] * O[b,row,h*d+k], padded rows set to 0.
 template <typename T>
 __global__ void attn_delta_kernel(const T* __restrict__ dO, const T* __restrict__ O,
-                                  float* __restrict__ delta, int B, int m, int m_pad, int H, int d) {
+                                  float* __restrict__ delta, int B, int m, int m_pad, int H, int d,
+                                  float scale) {
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;  // over B*m_pad*H
   const long total = (long)B * m_pad * H;
   if (idx >= total) return;
@@ -209,7 +210,39 @@ __global__ void attn_delta_kernel(const T* __restrict__ dO, const T* __restrict_
     const T* o = O + ((long)b * m + row) * (long)H * d + (long)h * d;
     for (int k = 0; k < d; ++k) acc += float(a[k]) * float(o[k]);
   }
-  delta[((long)b * H + h) * m_pad + row] = acc;
+  delta[((long)b * H + h) * m_pad + row] = acc * scale;
+}
+
+// bf16, head_dim 64, E % 256 == 0: one warp per row, 16-byte coalesced loads;
+// lane l covers columns [8l + 256j, +8) so 8 consecutive lanes form one head.
+__global__ void attn_delta_bf16_d64_kernel(const __nv_bfloat16* __restrict__ dO,
+                                           const __nv_bfloat16* __restrict__ O, float* __restrict__ delta,
+                                           int B, int m, int m_pad, int H, float scale) {
+  const long wrow = ((long)blockIdx.x * blockDim.x + threadIdx.x) / 32;  // over B*m_pad
+  const int lane = threadIdx.x % 32;
+  if (wrow >= (long)B * m_pad) return;
+  const int row = wrow % m_pad;
+  const int b = wrow / m_pad;
+  const int E = H * 64;
+  for (int j = 0; j < E / 256; ++j) {
+    float acc = 0.f;
+    if (row < m) {
+      const long off = ((long)b * m + row) * E + j * 256 + lane * 8;
+      const uint4 av = *reinterpret_cast<const uint4*>(dO + off);
+      const uint4 ov = *reinterpret_cast<const uint4*>(O + off);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av);
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 x = __bfloat1622float2(a2[i]), y = __bfloat1622float2(o2[i]);
+        acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if ((lane & 7) == 0) delta[((long)b * H + j * 4 + lane / 8) * m_pad + row] = acc * scale;
+  }
 }
 
 // Write +inf into the padded tail of a [B*H][m_pad] log-sum-exp buffer.

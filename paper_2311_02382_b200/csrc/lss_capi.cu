@@ -324,14 +324,20 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
   {
     const long total = (long)batch * m_pad * heads;
     const int threads = 256;
-    if (dtype == LSS_BF16)
+    if (dtype == LSS_BF16 && head_dim == 64 && E % 256 == 0) {
+      const long warps = (long)batch * m_pad;
+      attn_delta_bf16_d64_kernel<<<(warps * 32 + threads - 1) / threads, threads, 0, S(stream)>>>(
+          reinterpret_cast<const __nv_bfloat16*>(grad_o), reinterpret_cast<const __nv_bfloat16*>(o), delta_ws,
+          batch, rows, m_pad, heads, scale);
+    } else if (dtype == LSS_BF16) {
       attn_delta_kernel<__nv_bfloat16><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
           reinterpret_cast<const __nv_bfloat16*>(grad_o), reinterpret_cast<const __nv_bfloat16*>(o), delta_ws,
-          batch, rows, m_pad, heads, head_dim);
-    else
+          batch, rows, m_pad, heads, head_dim, scale);
+    } else {
       attn_delta_kernel<float><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
           reinterpret_cast<const float*>(grad_o), reinterpret_cast<const float*>(o), delta_ws, batch, rows, m_pad,
-          heads, head_dim);
+          heads, head_dim, 1.0f);
+    }
     if ((rc = check_launch("attn_delta"))) return rc;
   }
   if (dtype == LSS_F32) {

@@ -13,24 +13,31 @@
 // CTA = one 128-row key tile of one (batch, head); it walks the query tiles of
 // this rank that can see the keys (causal: q_pos >= k_pos).  Transposed
 // formulation so the key rows are TMEM lanes:
-//   S^T  = K Q_i^T        (TMEM, 128 cols)        dP^T = V dO_i^T (TMEM, 128 cols)
+//   S^T  = K Q_i^T   (TMEM, 128 cols)          dP^T = V dO_i^T   (TMEM, 128 cols)
 //   P^T, dS^T computed by 256 threads (2 warpgroups, 64 query columns each)
-//   dV  += P^T dO_i       (A = P^T from TMEM)
-//   dK  += dS^T Q_i       (A = dS^T from SMEM, K-major)
-//   dQ_i = dS K           (A = dS^T from SMEM read MN-major; drained to global
-//                          fp32 with bulk async reduce-add)
+//   dV  += P^T dO_i  (A = P^T from TMEM)
+//   dK  += dS^T Q_i  (A = dS^T from SMEM, K-major)
+//   dQ_i = dS K      (A = dS^T from SMEM read MN-major) -> drained by a 4th
+//                    warpgroup into fp32 dQ with TMA tensor reduce-add
 // TMEM: S^T[0,128) dP^T[128,256) dV[256,320) dK[320,384) dQ[384,448) P^T[448,512)
-// S/dP for tile i+1 are issued as soon as tile i's values are in registers.
+// 16 warps: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 elementwise, 12-15 dQ drain;
+// setmaxnreg gives the elementwise warps the register file.
+// Pipelining: S/dP of tile i+1 are issued as soon as tile i's values are in
+// registers; dS^T is double-buffered in SMEM so the elementwise warps only wait
+// for dV_i (P^T buffer) before publishing tile i+1, and the dQ drain runs on
+// its own warps, decoupled from the elementwise critical path.
 #pragma once
-#include "common.cuh"
 #include "attn_fwd.cuh"
+#include "common.cuh"
 
 namespace lss {
 
 constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES + 2 * 512;  // Q, dO, lse2[128], delta[128]
-constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATT_TILE_BYTES /*dS*/ +
-                         2 * 128 * 128 /*dQ staging*/ + 1024 + 256;
-constexpr int ATB_THREADS = 384;
+constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;                 // dS^T tile: 2 sub-tiles [128 kv][64 q]
+constexpr int ATB_STG_BYTES = 128 * 64 * 4;                      // dQ staging [128 q][64] fp32 (2 SW128 halves)
+constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES + ATB_STG_BYTES +
+                         1024 + 256;
+constexpr int ATB_THREADS = 512;
 
 struct AttnBwdParams {
   int B, m, m_pad, G, seg_len, H;
@@ -52,6 +59,15 @@ LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t
           smem_u32(sdst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+template <uint32_t N>
+LSS_DEV void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <uint32_t N>
+LSS_DEV void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
 }
 
 // P^T and dS^T for one key row and 64 query columns:
@@ -87,25 +103,27 @@ LSS_DEV void bwd_pds(const uint32_t (&sv)[64], const uint32_t (&dp)[64], uint32_
 __global__ void __launch_bounds__(ATB_THREADS, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                        const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                       const __grid_constant__ CUtensorMap tmdQ,
-                       AttnBwdParams p) {
+                       const __grid_constant__ CUtensorMap tmdQ, AttnBwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + ATT_TILE_BYTES;
-  uint8_t* sQst = sV + ATT_TILE_BYTES;                      // 2 stages
-  uint8_t* sdS = sQst + 2 * ATB_QSTAGE_BYTES;               // 2 sub-tiles [128 kv][64 q] bf16
-  uint8_t* sStage = sdS + 2 * ATT_TILE_BYTES;               // dQ staging, 2 x [128][32] fp32 (SW128)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + 2 * 128 * 128);
+  uint8_t* sQst = sV + ATT_TILE_BYTES;              // 2 stages: Q, dO, lse2, delta
+  uint8_t* sdS = sQst + 2 * ATB_QSTAGE_BYTES;       // 2 buffers x 2 sub-tiles [128 kv][64 q] bf16
+  uint8_t* sStage = sdS + 2 * ATB_DS_BYTES;         // dQ staging, 2 x [128 q][32] fp32 (SW128)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + ATB_STG_BYTES);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;   // [2]
   uint64_t* q_empty = bars + 3;  // [2]
   uint64_t* sdp_full = bars + 5;
   uint64_t* sdp_free = bars + 6;
   uint64_t* pds_full = bars + 7;
-  uint64_t* dq_full = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* pv_free = bars + 8;   // dV_i (and everything before it) complete
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_empty = bars + 10;
+  uint64_t* mma_done = bars + 11;  // one-shot: every MMA of the CTA complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -140,7 +158,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     mbar_init(sdp_full, 1);
     mbar_init(sdp_free, 256);
     mbar_init(pds_full, 256);
+    mbar_init(pv_free, 1);
     mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 128);
+    mbar_init(mma_done, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -151,107 +172,96 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320,
                  tdQ = tmem + 384, tP = tmem + 448;
 
-  if (warp == 0) {
-    if (lane == 0 && n_iter > 0) {
-      // ------------------------------------------------ TMA producer
-      mbar_arrive_expect_tx(kv_full, 2 * ATT_TILE_BYTES);
-      tma_load_4d(&tmK, kv_full, sK, h * ATT_D, kv_row0, b, g);
-      tma_load_4d(&tmV, kv_full, sV, h * ATT_D, kv_row0, b, g);
-      for (int it = 0; it < n_iter; ++it) {
-        const int s = it & 1;
-        mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
-        uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
-        const int q0 = (i_first + it) * ATT_BM;
-        mbar_arrive_expect_tx(&q_full[s], ATB_QSTAGE_BYTES);
-        tma_load_3d(&tmQ, &q_full[s], st, h * ATT_D, q0, b);
-        tma_load_3d(&tmdO, &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
-        const long lo = ((long)b * p.H + h) * p.m_pad + q0;
-        bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.lse2 + lo, 512, &q_full[s]);
-        bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.delta + lo, 512, &q_full[s]);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && n_iter > 0) {
-      // ------------------------------------------------ MMA issuer
-      constexpr uint32_t idSS = idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
-      constexpr uint32_t idKN = idesc_bf16_f32(128, 64, 0, 1);   // dV, dK (B MN-major)
-      constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);    // dQ (A and B MN-major)
-      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sdS);
-      auto issue_sdp = [&](int it) {
-        const int s = it & 1;
-        mbar_wait(&q_full[s], (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
-        const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
-#pragma unroll
-        for (int k = 0; k < ATT_D / 16; ++k)
-          mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
-                      smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
-#pragma unroll
-        for (int k = 0; k < ATT_D / 16; ++k)
-          mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
-                      smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
-        mma_commit(sdp_full);
-      };
-      mbar_wait(kv_full, 0);
-      tc_fence_after();
-      issue_sdp(0);
-      for (int it = 0; it < n_iter; ++it) {
-        if (it + 1 < n_iter) {
-          mbar_wait(sdp_free, it & 1);
-          issue_sdp(it + 1);
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (lane == 0 && n_iter > 0) {
+        // ------------------------------------------------ TMA producer
+        mbar_arrive_expect_tx(kv_full, 2 * ATT_TILE_BYTES);
+        tma_load_4d(&tmK, kv_full, sK, h * ATT_D, kv_row0, b, g);
+        tma_load_4d(&tmV, kv_full, sV, h * ATT_D, kv_row0, b, g);
+        for (int it = 0; it < n_iter; ++it) {
+          const int s = it & 1;
+          mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
+          uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
+          const int q0 = (i_first + it) * ATT_BM;
+          mbar_arrive_expect_tx(&q_full[s], ATB_QSTAGE_BYTES);
+          tma_load_3d(&tmQ, &q_full[s], st, h * ATT_D, q0, b);
+          tma_load_3d(&tmdO, &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
+          const long lo = ((long)b * p.H + h) * p.m_pad + q0;
+          bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.lse2 + lo, 512, &q_full[s]);
+          bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.delta + lo, 512, &q_full[s]);
         }
-        const int s = it & 1;
-        const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
-        const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
-        mbar_wait(pds_full, it & 1);
+      }
+    } else if (warp == 1) {
+      if (lane == 0 && n_iter > 0) {
+        // ------------------------------------------------ MMA issuer
+        constexpr uint32_t idSS = idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
+        constexpr uint32_t idKN = idesc_bf16_f32(128, 64, 0, 1);   // dV, dK (B MN-major)
+        constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);    // dQ (A and B MN-major)
+        const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+        auto issue_sdp = [&](int it) {
+          const int s = it & 1;
+          mbar_wait(&q_full[s], (it >> 1) & 1);
+          tc_fence_after();
+          const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
+          const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
+#pragma unroll
+          for (int k = 0; k < ATT_D / 16; ++k)
+            mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
+                        smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
+#pragma unroll
+          for (int k = 0; k < ATT_D / 16; ++k)
+            mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
+                        smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
+          mma_commit(sdp_full);
+        };
+        mbar_wait(kv_full, 0);
         tc_fence_after();
+        issue_sdp(0);
+        for (int it = 0; it < n_iter; ++it) {
+          if (it + 1 < n_iter) {
+            mbar_wait(sdp_free, it & 1);
+            issue_sdp(it + 1);
+          }
+          const int s = it & 1;
+          const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
+          const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
+          const uint32_t ds_addr = smem_u32(sdS + s * ATB_DS_BYTES);
+          mbar_wait(pds_full, it & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < ATT_BM / 16; ++k)  // dV += P^T dO
-          mma_bf16_ts(tdV, tP + k * 8, smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
-                      (it > 0 || k > 0));
+          for (int k = 0; k < ATT_BM / 16; ++k)  // dV += P^T dO
+            mma_bf16_ts(tdV, tP + k * 8, smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
+                        (it > 0 || k > 0));
+          mma_commit(pv_free);
 #pragma unroll
-        for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q
-          mma_bf16_ss(tdK, smem_desc_sw128(ds_addr + (k >> 2) * ATT_TILE_BYTES + (k & 3) * 32, 16, 1024),
-                      smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN, (it > 0 || k > 0));
-        mma_commit(&q_empty[s]);
+          for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q
+            mma_bf16_ss(tdK, smem_desc_sw128(ds_addr + (k >> 2) * ATT_TILE_BYTES + (k & 3) * 32, 16, 1024),
+                        smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN, (it > 0 || k > 0));
+          mma_commit(&q_empty[s]);
+          if (it > 0) {
+            mbar_wait(dq_empty, (it - 1) & 1);  // drain has read dQ_{it-1} out of TMEM
+            tc_fence_after();
+          }
 #pragma unroll
-        for (int k = 0; k < ATT_BN / 16; ++k)  // dQ = dS K
-          mma_bf16_ss(tdQ, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
-                      smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
-        mma_commit(dq_full);
+          for (int k = 0; k < ATT_BN / 16; ++k)  // dQ = dS K
+            mma_bf16_ss(tdQ, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
+                        smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
+          mma_commit(dq_full);
+        }
+        mma_commit(mma_done);
       }
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------ elementwise + dQ drain + dK/dV epilogue
+  } else if (warp < 12) {
+    reg_alloc<184>();
+    // ------------------------------------------------ elementwise P^T / dS^T (+ dK/dV epilogue)
     const int half = (warp - 4) / 4;  // query columns [64*half, 64*half+64) of each tile
     const int quad = warp % 4;
-    const int t = quad * 32 + lane;   // key row within tile == TMEM lane (and q row for dQ)
+    const int t = quad * 32 + lane;   // key row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const long kpos = kpos0 + t;
     const bool row_ok = t < kv_valid;
-    uint8_t* stg_half = sStage + half * 128 * 128;  // [128 q rows][32 fp32], 128B-swizzled
-    const uint32_t stg_row = smem_u32(stg_half + t * 128);
-    const bool issuer = (t == 0);                    // one thread per half issues the reduce
-    auto drain_dq = [&](int it) {
-      // dQ rows of query tile `it` (TMEM lane = query row), columns [32*half, +32):
-      // TMEM -> registers -> swizzled smem tile -> TMA tensor reduce-add into fp32 dQ
-      mbar_wait(dq_full, it & 1);
-      tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tdQ + lane_off + half * 32, v);
-      if (issuer) bulk_wait_read0();  // previous reduce has finished reading the staging tile
-      named_bar_sync(1 + half, 128);
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        st_shared_v4(stg_row + ((c ^ (t & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      fence_proxy_async_smem();
-      named_bar_sync(1 + half, 128);
-      if (issuer) {
-        tma_reduce_add_3d(&tmdQ, stg_half, h * ATT_D + half * 32, (i_first + it) * ATT_BM, b);
-        bulk_commit();
-      }
-    };
     for (int it = 0; it < n_iter; ++it) {
       const int s = it & 1;
       const int q0 = (i_first + it) * ATT_BM;
@@ -275,11 +285,14 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       } else {
         bwd_pds<false>(sv, dp, s_lse, s_dsc, p.scale_log2, p.scale, 0, pk, dk);
       }
-      if (it > 0) drain_dq(it - 1);  // also guarantees dV/dK/dQ of tile it-1 are done
+      if (it > 0) {
+        mbar_wait(pv_free, (it - 1) & 1);  // dV_{it-1} (and dK/dQ_{it-2}) complete
+        tc_fence_after();
+      }
       tmem_st32(tP + lane_off + half * 32, pk);
-      // dS^T row t, query columns [64*half, +64) -> sub-tile `half`, SW128 K-major
+      // dS^T row t, query columns [64*half, +64) -> buffer s, sub-tile `half`, SW128 K-major
       {
-        const uint32_t row = smem_u32(sdS + half * ATT_TILE_BYTES + t * 128);
+        const uint32_t row = smem_u32(sdS + s * ATB_DS_BYTES + half * ATT_TILE_BYTES + t * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           st_shared_v4(row + ((c ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
@@ -288,11 +301,12 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       tc_fence_before();
       mbar_arrive(pds_full);
     }
-    if (n_iter > 0) drain_dq(n_iter - 1);
-    // dK (half 0) / dV (half 1) epilogue: all MMAs are complete after the last dq_full
+    // dK (half 0) / dV (half 1) epilogue after the one-shot mma_done commit
     float* dst = (half ? p.dv : p.dk) + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * p.ld_dkv +
                  h * ATT_D;
     if (n_iter > 0) {
+      mbar_wait(mma_done, 0);
+      tc_fence_after();
       uint32_t v[64];
       tmem_ld64((half ? tdV : tdK) + lane_off, v);
       if (row_ok) {
@@ -305,6 +319,38 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     } else if (row_ok) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) reinterpret_cast<float4*>(dst)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else {
+    reg_dealloc<80>();
+    // ------------------------------------------------ dQ drain: TMEM -> swizzled SMEM -> TMA reduce-add
+    const int quad = warp % 4;
+    const int r = quad * 32 + lane;  // query row within tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const bool issuer = (r == 0);
+    const uint32_t row0 = smem_u32(sStage + r * 128);                      // cols [0,32)
+    const uint32_t row1 = smem_u32(sStage + ATB_STG_BYTES / 2 + r * 128);  // cols [32,64)
+    for (int it = 0; it < n_iter; ++it) {
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      uint32_t v[64];
+      tmem_ld64(tdQ + lane_off, v);
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+      if (issuer) bulk_wait_read0();  // previous reduce has finished reading the staging tile
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        st_shared_v4(row0 + ((c ^ (r & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        st_shared_v4(row1 + ((c ^ (r & 7)) << 4), v[32 + 4 * c], v[33 + 4 * c], v[34 + 4 * c], v[35 + 4 * c]);
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (issuer) {
+        const int q0 = (i_first + it) * ATT_BM;
+        tma_reduce_add_3d(&tmdQ, sStage, h * ATT_D, q0, b);
+        tma_reduce_add_3d(&tmdQ, sStage + ATB_STG_BYTES / 2, h * ATT_D + 32, q0, b);
+        bulk_commit();
+      }
     }
     if (issuer) bulk_wait0();
   }

@@ -61,6 +61,19 @@ LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t
       : "memory");
 }
 
+#ifdef LSS_BWD_TRACE
+__device__ long long g_bwd_trace[8][512];
+#define BWD_TRACE(slot, it)                                                          \
+  do {                                                                               \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (it) < 512)         \
+      g_bwd_trace[slot][it] = clock64();                                             \
+  } while (0)
+#else
+#define BWD_TRACE(slot, it) \
+  do {                      \
+  } while (0)
+#endif
+
 template <uint32_t N>
 LSS_DEV void reg_alloc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
@@ -175,27 +188,34 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   if (warp < 4) {
     reg_dealloc<56>();
     if (warp == 0) {
-      if (lane == 0 && n_iter > 0) {
-        // ------------------------------------------------ TMA producer
-        mbar_arrive_expect_tx(kv_full, 2 * ATT_TILE_BYTES);
-        tma_load_4d(&tmK, kv_full, sK, h * ATT_D, kv_row0, b, g);
-        tma_load_4d(&tmV, kv_full, sV, h * ATT_D, kv_row0, b, g);
+      if (n_iter > 0) {
+        // ------------------------------------------------ TMA producer (warp-uniform loop)
+        if (elect_one()) {
+          mbar_arrive_expect_tx(kv_full, 2 * ATT_TILE_BYTES);
+          tma_load_4d(&tmK, kv_full, sK, h * ATT_D, kv_row0, b, g);
+          tma_load_4d(&tmV, kv_full, sV, h * ATT_D, kv_row0, b, g);
+        }
+        __syncwarp();
         for (int it = 0; it < n_iter; ++it) {
           const int s = it & 1;
           mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
-          uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
-          const int q0 = (i_first + it) * ATT_BM;
-          mbar_arrive_expect_tx(&q_full[s], ATB_QSTAGE_BYTES);
-          tma_load_3d(&tmQ, &q_full[s], st, h * ATT_D, q0, b);
-          tma_load_3d(&tmdO, &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
-          const long lo = ((long)b * p.H + h) * p.m_pad + q0;
-          bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.lse2 + lo, 512, &q_full[s]);
-          bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.delta + lo, 512, &q_full[s]);
+          if (elect_one()) {
+            uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
+            const int q0 = (i_first + it) * ATT_BM;
+            mbar_arrive_expect_tx(&q_full[s], ATB_QSTAGE_BYTES);
+            tma_load_3d(&tmQ, &q_full[s], st, h * ATT_D, q0, b);
+            tma_load_3d(&tmdO, &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
+            const long lo = ((long)b * p.H + h) * p.m_pad + q0;
+            bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.lse2 + lo, 512, &q_full[s]);
+            bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.delta + lo, 512, &q_full[s]);
+          }
+          __syncwarp();
         }
       }
     } else if (warp == 1) {
-      if (lane == 0 && n_iter > 0) {
-        // ------------------------------------------------ MMA issuer
+      if (n_iter > 0) {
+        // ------------------------------------------------ MMA issuer (warp-uniform loop,
+        // one elected lane issues: descriptors stay in the uniform datapath)
         constexpr uint32_t idSS = idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
         constexpr uint32_t idKN = idesc_bf16_f32(128, 64, 0, 1);   // dV, dK (B MN-major)
         constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);    // dQ (A and B MN-major)
@@ -206,15 +226,18 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
           const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < ATT_D / 16; ++k)
-            mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
-                        smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
+            for (int k = 0; k < ATT_D / 16; ++k)
+              mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
+                          smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
 #pragma unroll
-          for (int k = 0; k < ATT_D / 16; ++k)
-            mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
-                        smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
-          mma_commit(sdp_full);
+            for (int k = 0; k < ATT_D / 16; ++k)
+              mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
+                          smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
+            mma_commit(sdp_full);
+          }
+          __syncwarp();
         };
         mbar_wait(kv_full, 0);
         tc_fence_after();
@@ -222,6 +245,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         for (int it = 0; it < n_iter; ++it) {
           if (it + 1 < n_iter) {
             mbar_wait(sdp_free, it & 1);
+            if (lane == 0) BWD_TRACE(6, it);
             issue_sdp(it + 1);
           }
           const int s = it & 1;
@@ -230,27 +254,35 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           const uint32_t ds_addr = smem_u32(sdS + s * ATB_DS_BYTES);
           mbar_wait(pds_full, it & 1);
           tc_fence_after();
+          if (lane == 0) BWD_TRACE(0, it);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < ATT_BM / 16; ++k)  // dV += P^T dO
-            mma_bf16_ts(tdV, tP + k * 8, smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
-                        (it > 0 || k > 0));
-          mma_commit(pv_free);
+            for (int k = 0; k < ATT_BM / 16; ++k)  // dV += P^T dO
+              mma_bf16_ts(tdV, tP + k * 8, smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
+                          (it > 0 || k > 0));
+            mma_commit(pv_free);
 #pragma unroll
-          for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q
-            mma_bf16_ss(tdK, smem_desc_sw128(ds_addr + (k >> 2) * ATT_TILE_BYTES + (k & 3) * 32, 16, 1024),
-                        smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN, (it > 0 || k > 0));
-          mma_commit(&q_empty[s]);
+            for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q
+              mma_bf16_ss(tdK, smem_desc_sw128(ds_addr + (k >> 2) * ATT_TILE_BYTES + (k & 3) * 32, 16, 1024),
+                          smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN, (it > 0 || k > 0));
+            mma_commit(&q_empty[s]);
+          }
+          __syncwarp();
           if (it > 0) {
             mbar_wait(dq_empty, (it - 1) & 1);  // drain has read dQ_{it-1} out of TMEM
             tc_fence_after();
           }
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < ATT_BN / 16; ++k)  // dQ = dS K
-            mma_bf16_ss(tdQ, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
-                        smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
-          mma_commit(dq_full);
+            for (int k = 0; k < ATT_BN / 16; ++k)  // dQ = dS K
+              mma_bf16_ss(tdQ, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
+                          smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
+            mma_commit(dq_full);
+          }
+          __syncwarp();
         }
-        mma_commit(mma_done);
+        if (elect_one()) mma_commit(mma_done);
+        __syncwarp();
       }
     }
   } else if (warp < 12) {
@@ -270,6 +302,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + half * 256;  // delta[q]/sqrt(d)
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
+      if (t == 0 && half == 0) BWD_TRACE(1, it);
       uint32_t sv[64], dp[64];
       tmem_ld64(tS + lane_off + half * 64, sv);
       tmem_ld64(tdP + lane_off + half * 64, dp);
@@ -285,10 +318,12 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       } else {
         bwd_pds<false>(sv, dp, s_lse, s_dsc, p.scale_log2, p.scale, 0, pk, dk);
       }
+      if (t == 0 && half == 0) BWD_TRACE(2, it);
       if (it > 0) {
         mbar_wait(pv_free, (it - 1) & 1);  // dV_{it-1} (and dK/dQ_{it-2}) complete
         tc_fence_after();
       }
+      if (t == 0 && half == 0) BWD_TRACE(3, it);
       tmem_st32(tP + lane_off + half * 32, pk);
       // dS^T row t, query columns [64*half, +64) -> buffer s, sub-tile `half`, SW128 K-major
       {
@@ -300,6 +335,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(pds_full);
+      if (t == 0 && half == 0) BWD_TRACE(4, it);
     }
     // dK (half 0) / dV (half 1) epilogue after the one-shot mma_done commit
     float* dst = (half ? p.dv : p.dk) + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * p.ld_dkv +
@@ -332,6 +368,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     for (int it = 0; it < n_iter; ++it) {
       mbar_wait(dq_full, it & 1);
       tc_fence_after();
+      if (r == 0) BWD_TRACE(5, it);
       uint32_t v[64];
       tmem_ld64(tdQ + lane_off, v);
       tc_fence_before();

@@ -118,24 +118,31 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   const uint32_t tP[2] = {tmem + 384, tmem + 448};
 
   if (warp == 0) {
-    if (lane == 0 && n_kv > 0) {
-      // ------------------------------------------------ TMA producer
-      mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * ATT_TILE_BYTES);
-      tma_load_3d(&tmQ, q_full, sQ, h * ATT_D, q0, b);
-      if (has1) tma_load_3d(&tmQ, q_full, sQ + ATT_TILE_BYTES, h * ATT_D, q0 + ATT_BM, b);
+    if (n_kv > 0) {
+      // ------------------------------------------------ TMA producer (warp-uniform loop)
+      if (elect_one()) {
+        mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * ATT_TILE_BYTES);
+        tma_load_3d(&tmQ, q_full, sQ, h * ATT_D, q0, b);
+        if (has1) tma_load_3d(&tmQ, q_full, sQ + ATT_TILE_BYTES, h * ATT_D, q0 + ATT_BM, b);
+      }
+      __syncwarp();
       for (int j = 0; j < n_kv; ++j) {
         const int st = j % ATT_KV_STAGES;
         const uint32_t ph = (j / ATT_KV_STAGES) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
-        const int g = j / tps, t = j % tps;
-        mbar_arrive_expect_tx(&kv_full[st], 2 * ATT_TILE_BYTES);
-        tma_load_4d(&tmK, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
-        tma_load_4d(&tmV, &kv_full[st], sV + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
+        if (elect_one()) {
+          const int g = j / tps, t = j % tps;
+          mbar_arrive_expect_tx(&kv_full[st], 2 * ATT_TILE_BYTES);
+          tma_load_4d(&tmK, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
+          tma_load_4d(&tmV, &kv_full[st], sV + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && n_kv > 0) {
-      // ------------------------------------------------ MMA issuer
+    if (n_kv > 0) {
+      // ------------------------------------------------ MMA issuer (warp-uniform loop,
+      // one elected lane issues: descriptors stay in the uniform datapath)
       constexpr uint32_t idS = idesc_bf16_f32(ATT_BM, ATT_BN, 0, 0);
       constexpr uint32_t idO = idesc_bf16_f32(ATT_BM, ATT_D, 0, 1);
       const int nw = has1 ? 2 : 1;
@@ -147,14 +154,18 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         for (int w = 0; w < nw; ++w) {
           mbar_wait(&p_full[w], jj & 1);
           tc_fence_after();
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < ATT_BN / 16; ++k) {
-            mma_bf16_ts(tO[w], tP[w] + k * 8, smem_desc_sw128(v_addr + k * 2048, 8192, 1024), idO,
-                        (jj > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < ATT_BN / 16; ++k) {
+              mma_bf16_ts(tO[w], tP[w] + k * 8, smem_desc_sw128(v_addr + k * 2048, 8192, 1024), idO,
+                          (jj > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&o_full[w]);
           }
-          mma_commit(&o_full[w]);
+          __syncwarp();
         }
-        mma_commit(&kv_empty[st]);
+        if (elect_one()) mma_commit(&kv_empty[st]);
+        __syncwarp();
       };
       for (int j = 0; j < n_kv; ++j) {
         const int st = j % ATT_KV_STAGES;
@@ -164,12 +175,15 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         for (int w = 0; w < nw; ++w) {
           if (j > 0) mbar_wait(&s_empty[w], (j - 1) & 1);
           tc_fence_after();
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < ATT_D / 16; ++k) {
-            mma_bf16_ss(tS[w], smem_desc_sw128(q_addr + w * ATT_TILE_BYTES + k * 32, 16, 1024),
-                        smem_desc_sw128(k_addr + k * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
+            for (int k = 0; k < ATT_D / 16; ++k) {
+              mma_bf16_ss(tS[w], smem_desc_sw128(q_addr + w * ATT_TILE_BYTES + k * 32, 16, 1024),
+                          smem_desc_sw128(k_addr + k * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
+            }
+            mma_commit(&s_full[w]);
           }
-          mma_commit(&s_full[w]);
+          __syncwarp();
         }
         if (j > 0) issue_pv(j - 1);
       }

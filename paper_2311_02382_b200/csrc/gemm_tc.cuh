@@ -84,8 +84,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer
+    {
+      // ---------------- TMA producer (warp-uniform loop, elected lane issues)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -93,22 +93,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int n0 = (tile % n_tiles) * GEMM_BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * GEMM_STAGE_BYTES;
-          uint8_t* sb = sa + GEMM_A_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], GEMM_STAGE_BYTES);
-          const int k0 = kb * GEMM_BK;
-          if (A_MN) {
-            tma_load_2d(&tmA, &full_bar[stage], sa, m0, k0);
-            tma_load_2d(&tmA, &full_bar[stage], sa + 8192, m0 + 64, k0);
-          } else {
-            tma_load_2d(&tmA, &full_bar[stage], sa, k0, m0);
-          }
-          if (B_MN) {
+          if (elect_one()) {
+            uint8_t* sa = smem + stage * GEMM_STAGE_BYTES;
+            uint8_t* sb = sa + GEMM_A_BYTES;
+            mbar_arrive_expect_tx(&full_bar[stage], GEMM_STAGE_BYTES);
+            const int k0 = kb * GEMM_BK;
+            if (A_MN) {
+              tma_load_2d(&tmA, &full_bar[stage], sa, m0, k0);
+              tma_load_2d(&tmA, &full_bar[stage], sa + 8192, m0 + 64, k0);
+            } else {
+              tma_load_2d(&tmA, &full_bar[stage], sa, k0, m0);
+            }
+            if (B_MN) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) tma_load_2d(&tmB, &full_bar[stage], sb + i * 8192, n0 + 64 * i, k0);
-          } else {
-            tma_load_2d(&tmB, &full_bar[stage], sb, k0, n0);
+              for (int i = 0; i < 4; ++i) tma_load_2d(&tmB, &full_bar[stage], sb + i * 8192, n0 + 64 * i, k0);
+            } else {
+              tma_load_2d(&tmB, &full_bar[stage], sb, k0, n0);
+            }
           }
+          __syncwarp();
           if (++stage == GEMM_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -117,8 +120,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread)
+    {
+      // ---------------- MMA issuer (warp-uniform loop, elected lane issues)
       constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, GEMM_BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -134,21 +137,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * GEMM_STAGE_BYTES);
           const uint32_t sb = sa + GEMM_A_BYTES;
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const uint64_t ad = A_MN ? smem_desc_sw128(sa + k * 2048, 8192, 1024)
-                                     : smem_desc_sw128(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? smem_desc_sw128(sb + k * 2048, 8192, 1024)
-                                     : smem_desc_sw128(sb + k * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              const uint64_t ad = A_MN ? smem_desc_sw128(sa + k * 2048, 8192, 1024)
+                                       : smem_desc_sw128(sa + k * 32, 16, 1024);
+              const uint64_t bd = B_MN ? smem_desc_sw128(sb + k * 2048, 8192, 1024)
+                                       : smem_desc_sw128(sb + k * 32, 16, 1024);
+              mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
+            mma_commit(&empty_bar[stage]);
           }
-          mma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == GEMM_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull_bar[buf]);
+        if (elect_one()) mma_commit(&tfull_bar[buf]);
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {

@@ -388,3 +388,9 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
 }
 
 }  // extern "C"
+
+#ifdef LSS_BWD_TRACE
+extern "C" int lss_debug_bwd_trace(long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_bwd_trace, sizeof(long long) * 8 * 512) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -48,3 +48,13 @@ def assert_close_ref(got, want, tol, name=""):
     scale = max(np.abs(want).max(), 1e-30)
     bad = np.abs(got - want) > tol * scale + tol * np.abs(want)
     assert not bad.any(), f"{name}: {bad.sum()} elements out of tolerance {tol}, nerr={nerr(got, want):.3e}"
+
+
+def free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port

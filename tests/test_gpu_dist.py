@@ -1,0 +1,33 @@
+"""Multi-GPU (NCCL) parity of the LSS layer against the real reference's goldens.
+Runs tests/dist_check.py under torchrun; skipped unless >= 2 GPUs are visible
+(the CPU gloo tests in test_dist_gloo.py cover the host logic everywhere)."""
+
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _gpus():
+    import torch
+
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("case,world", [("configA", 2), ("batch2_g3", 3), ("small_causal", 2),
+                                        ("small_noncausal", 4)])
+def test_nccl_lss_layer_matches_reference(case, world):
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from conftest import free_port
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(ROOT / "tests" / "dist_check.py"),
+           "--case", case]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout

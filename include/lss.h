@@ -114,6 +114,29 @@ int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld
                  float* lse2, int batch, int rows, int workers, int seg_len, int heads,
                  int head_dim, long offset, int causal, void* stream);
 
+/* Partial / strided form of lss_attn_fwd: q rows [0, rows) with batch stride
+ * q_bstride (elements), attending only key segments [g_begin, g_end); ctx is
+ * written normalised with batch stride o_bstride and lse2 with row pitch
+ * lse_pitch.  Rows that see no key of the range get ctx = 0, lse2 = -inf.
+ * Used by the balanced causal schedule, whose partial results are combined
+ * with lss_attn_merge.  (bf16 only for partial ranges.) */
+int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v,
+                    long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch,
+                    int workers, int seg_len, int heads, int head_dim, long offset, int causal,
+                    int g_begin, int g_end, void* stream);
+
+/* log-sum-exp combine of two partial attentions over disjoint key ranges:
+ * lse = log2(2^la + 2^lb), ctx = 2^(la-lse) ctx_a + 2^(lb-lse) ctx_b (bf16, head_dim 64).
+ * o_out / lse_out may alias o_a / lse_a. */
+int lss_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b,
+                   void* o_out, float* lse_out, int batch, int rows, int heads, long o_bstride,
+                   int lse_pitch, void* stream);
+
+/* delta[b][h][row] = rowsum(grad_o * o) over the head's columns (x 1/sqrt(d) when scaled),
+ * the softmax-backward row term of model.scores_bwd (model.py:355); [B][H][lss_rows_pad(rows)]. */
+int lss_attn_delta(int dtype, const void* o, const void* grad_o, float* delta, int batch, int rows,
+                   int heads, int head_dim, int scaled, void* stream);
+
 /* model.scores_bwd (model.py:329-359).  grad_q [batch][rows][embed] fp32 is
  * overwritten; grad_k / grad_v (fp32, layout [workers][batch][seg_len][ld_dkv])
  * are fully written: this rank's partial dK, dV over the WHOLE sequence (the
@@ -123,6 +146,33 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
                  const void* grad_o, const float* lse2, float* delta_ws, float* grad_q,
                  float* grad_k, float* grad_v, long ld_dkv, int batch, int rows, int workers,
                  int seg_len, int heads, int head_dim, long offset, int causal, void* stream);
+
+/* One query-row source of the multi-source backward: rows [row0, row0+rows)
+ * (128-aligned; the last source may end at m_src) of [batch][m_src][embed]
+ * Q / dO (bf16) and dQ (fp32, ACCUMULATED: zero it first) whose row 0 is at
+ * global position pos0, attending key segments [g_begin, g_end); lse2 and the
+ * scaled delta (lss_attn_delta(..., scaled=1)) are [batch][heads][pitch]. */
+typedef struct lss_bwd_source {
+  const void* q;
+  const void* grad_o;
+  float* grad_q;
+  int m_src;
+  int row0, rows;
+  long pos0;
+  int g_begin, g_end;
+  const float* lse2;
+  const float* delta;
+  int pitch;
+} lss_bwd_source;
+
+/* Backward over up to 3 sources in ONE launch: every key tile accumulates dK/dV
+ * from all sources, so grad_k / grad_v rows have a single writer (fully written). */
+int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs,
+                    int nsrc, float* grad_k, float* grad_v, long ld_dkv, int batch, int workers,
+                    int seg_len, int heads, int head_dim, int causal, void* stream);
+
+/* y += x (fp32), used to fold a partner's dQ rows into the owner's. */
+int lss_add_f32(float* y, const float* x, long n, void* stream);
 
 #ifdef __cplusplus
 }

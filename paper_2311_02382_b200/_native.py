@@ -48,6 +48,15 @@ class GemmEpilogue(ctypes.Structure):
     ]
 
 
+class BwdSource(ctypes.Structure):
+    """lss_bwd_source (include/lss.h)."""
+
+    _fields_ = [
+        ("q", _P), ("grad_o", _P), ("grad_q", _P), ("m_src", _I), ("row0", _I), ("rows", _I),
+        ("pos0", _L), ("g_begin", _I), ("g_end", _I), ("lse2", _P), ("delta", _P), ("pitch", _I),
+    ]
+
+
 # name -> argtypes (all return int status, except noted)
 SIGNATURES = {
     "lss_layernorm_fwd": [_P, _P, _P, _P, _I, _P, _P, _L, _I, _F, _P],
@@ -59,6 +68,11 @@ SIGNATURES = {
     "lss_attn_fwd": [_I, _P, _P, _P, _L, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P],
     "lss_attn_bwd": [_I, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _I, _L, _I,
                      _P],
+    "lss_attn_fwd_ex": [_I, _P, _I, _L, _P, _P, _L, _P, _L, _P, _I, _I, _I, _I, _I, _I, _L, _I, _I, _I, _P],
+    "lss_attn_merge": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _L, _I, _P],
+    "lss_attn_delta": [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P],
+    "lss_attn_bwd_ex": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, _P, _P, _L, _I, _I, _I, _I, _I, _I, _P],
+    "lss_add_f32": [_P, _P, _L, _P],
 }
 EXTRA = {
     "lss_abi_version": ([], _I),
@@ -98,7 +112,8 @@ def load():
 
 # kernels each entry point launches (bf16 path; attn_bwd = delta + main kernel)
 KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 1, "lss_stage_weights": 1,
-                    "lss_cat_cast_colsum": 1, "lss_attn_fwd": 1, "lss_attn_bwd": 2}
+                    "lss_cat_cast_colsum": 1, "lss_attn_fwd": 1, "lss_attn_bwd": 2, "lss_attn_fwd_ex": 1,
+                    "lss_attn_merge": 1, "lss_attn_delta": 1, "lss_attn_bwd_ex": 1, "lss_add_f32": 1}
 launch_count = 0
 
 

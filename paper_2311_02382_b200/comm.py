@@ -99,6 +99,19 @@ class TorchDistComm:
             return None
         return self.dist.all_reduce(buf, group=self.world_group, async_op=async_op)
 
+    def p2p(self, sends, recvs, peer: int, step=0, phase="", layer=None):
+        """Point-to-point exchange with sequence-group member `peer` (balanced causal
+        schedule).  Stream-ordered: the current stream waits for completion."""
+        peer_g = peer if self.seq_group is None else self.dist.get_global_rank(self.seq_group, peer)
+        ops = [self.dist.P2POp(self.dist.isend, t.view(-1), peer_g, group=self.seq_group) for t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t.view(-1), peer_g, group=self.seq_group) for t in recvs]
+        if sends:
+            self.ledger.record("send", self.seq_name, sum(t.numel() for t in sends), step, phase, layer)
+        if recvs:
+            self.ledger.record("recv", self.seq_name, sum(t.numel() for t in recvs), step, phase, layer)
+        for w in self.dist.batch_isend_irecv(ops):
+            w.wait()
+
 
 class SoloComm:
     """One rank, no process group (G = D = 1): collectives are identities."""

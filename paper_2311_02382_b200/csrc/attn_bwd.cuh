@@ -39,17 +39,34 @@ constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 *
                          1024 + 256;
 constexpr int ATB_THREADS = 512;
 
+// A query-row source of the backward: rows [row0, row0+rows) of a [B][m_src][E]
+// (Q, dO, dQ) tensor triple whose row 0 sits at global position pos0, attending
+// key segments [g_begin, g_end).  A launch processes up to ATB_MAX_SRC sources
+// (this rank's own rows, and rows delegated by a partner in the balanced causal
+// schedule); every key tile accumulates dK/dV from all of them in TMEM, so each
+// dK/dV row has exactly one writer.
+constexpr int ATB_MAX_SRC = 3;
+struct BwdSource {
+  int row0, rows;
+  long pos0;
+  int g_begin, g_end;
+  const float* lse2;   // [B][H][pitch] (+inf beyond the tensor's last row)
+  const float* delta;  // [B][H][pitch] rowsum(dO*O)/sqrt(d)
+  int pitch;
+};
+struct BwdMaps {
+  CUtensorMap q[ATB_MAX_SRC];
+  CUtensorMap dO[ATB_MAX_SRC];
+  CUtensorMap dq[ATB_MAX_SRC];  // fp32 [B][m_src][E], box 32 x 128, reduce-add target
+};
 struct AttnBwdParams {
-  int B, m, m_pad, G, seg_len, H;
-  long offset;
+  int B, G, seg_len, H, nsrc;
   int causal;
   float scale_log2;  // log2(e)/sqrt(d)
   float scale;       // 1/sqrt(d)
-  const float* lse2;   // [B][H][m_pad] (+inf padded)
-  const float* delta;  // [B][H][m_pad] rowsum(dO*O)/sqrt(d) (0 padded)
-  float* dq;           // [B][m][E] fp32, accumulated (must be zeroed)
-  float* dk;           // [G][B][seg_len][ld_dkv] fp32, fully written
-  float* dv;           // same layout
+  BwdSource src[ATB_MAX_SRC];
+  float* dk;         // [G][B][seg_len][ld_dkv] fp32, fully written
+  float* dv;         // same layout
   long ld_dkv;
 };
 
@@ -114,9 +131,8 @@ LSS_DEV void bwd_pds(const uint32_t (&sv)[64], const uint32_t (&dp)[64], uint32_
 }
 
 __global__ void __launch_bounds__(ATB_THREADS, 1)
-    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
-                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                       const __grid_constant__ CUtensorMap tmdQ, AttnBwdParams p) {
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                       const __grid_constant__ BwdMaps maps, const __grid_constant__ AttnBwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -149,20 +165,41 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   const int kv_row0 = kt * ATT_BN;                         // row within segment
   const int kv_valid = min(ATT_BN, p.seg_len - kv_row0);
   const long kpos0 = (long)g * p.seg_len + kv_row0;        // global key position of row 0
-  const int n_qt = (p.m + ATT_BM - 1) / ATT_BM;
-  int i_first = 0;
-  if (p.causal) {
-    const long d0 = kpos0 - p.offset;  // first local q row that can see key row 0
-    i_first = d0 <= 0 ? 0 : (int)min((long)n_qt, d0 / ATT_BM);
+  // per-source query-tile ranges visible to this key tile (causal: q_pos >= k_pos)
+  int src_first[ATB_MAX_SRC], src_n[ATB_MAX_SRC];
+  int n_iter = 0;
+#pragma unroll
+  for (int s = 0; s < ATB_MAX_SRC; ++s) {
+    src_first[s] = 0;
+    src_n[s] = 0;
+    if (s < p.nsrc && g >= p.src[s].g_begin && g < p.src[s].g_end) {
+      const int n_qt = (p.src[s].rows + ATT_BM - 1) / ATT_BM;
+      int first = 0;
+      if (p.causal) {
+        const long d0 = kpos0 - (p.src[s].pos0 + p.src[s].row0);  // first source row seeing key row 0
+        first = d0 <= 0 ? 0 : (int)min((long)n_qt, d0 / ATT_BM);
+      }
+      src_first[s] = first;
+      src_n[s] = n_qt - first;
+      n_iter += n_qt - first;
+    }
   }
-  const int n_iter = n_qt - i_first;
+  // iteration -> (source, tensor row of the query tile)
+  auto locate = [&](int it, int& s_out, int& qrow_out) {
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < ATB_MAX_SRC - 1; ++k)
+      if (s == k && it >= src_n[k]) {
+        it -= src_n[k];
+        s = k + 1;
+      }
+    s_out = s;
+    qrow_out = p.src[s].row0 + (src_first[s] + it) * ATT_BM;
+  };
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmdO);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    tma_prefetch_desc(&tmdQ);
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
@@ -200,14 +237,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           const int s = it & 1;
           mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
           if (elect_one()) {
+            int src, q0;
+            locate(it, src, q0);
             uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
-            const int q0 = (i_first + it) * ATT_BM;
             mbar_arrive_expect_tx(&q_full[s], ATB_QSTAGE_BYTES);
-            tma_load_3d(&tmQ, &q_full[s], st, h * ATT_D, q0, b);
-            tma_load_3d(&tmdO, &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
-            const long lo = ((long)b * p.H + h) * p.m_pad + q0;
-            bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.lse2 + lo, 512, &q_full[s]);
-            bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.delta + lo, 512, &q_full[s]);
+            tma_load_3d(&maps.q[src], &q_full[s], st, h * ATT_D, q0, b);
+            tma_load_3d(&maps.dO[src], &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
+            const long lo = ((long)b * p.H + h) * p.src[src].pitch + q0;
+            bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.src[src].lse2 + lo, 512, &q_full[s]);
+            bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.src[src].delta + lo, 512, &q_full[s]);
           }
           __syncwarp();
         }
@@ -296,7 +334,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     const bool row_ok = t < kv_valid;
     for (int it = 0; it < n_iter; ++it) {
       const int s = it & 1;
-      const int q0 = (i_first + it) * ATT_BM;
+      int src, qrow;
+      locate(it, src, qrow);
+      const long q0 = p.src[src].pos0 + qrow;  // global position of the tile's first query
       const uint32_t st = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
       const uint32_t s_lse = st + 2 * ATT_TILE_BYTES + half * 256;        // lse2[q], 64 floats
       const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + half * 256;  // delta[q]/sqrt(d)
@@ -309,10 +349,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       tc_fence_before();
       mbar_arrive(sdp_free);
       // query column c of this half is visible to key row t iff c >= fv
-      const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > p.offset + q0 + half * 64);
+      const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > q0 + half * 64);
       uint32_t pk[32], dk[32];
       if (need_mask) {
-        const long first_vis = kpos - p.offset - q0 - half * 64;
+        const long first_vis = kpos - q0 - half * 64;
         const int fv = !row_ok ? 64 : (p.causal ? (int)max(0L, min(64L, first_vis)) : 0);
         bwd_pds<true>(sv, dp, s_lse, s_dsc, p.scale_log2, p.scale, fv, pk, dk);
       } else {
@@ -383,9 +423,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (issuer) {
-        const int q0 = (i_first + it) * ATT_BM;
-        tma_reduce_add_3d(&tmdQ, sStage, h * ATT_D, q0, b);
-        tma_reduce_add_3d(&tmdQ, sStage + ATB_STG_BYTES / 2, h * ATT_D + 32, q0, b);
+        int src, q0;
+        locate(it, src, q0);
+        tma_reduce_add_3d(&maps.dq[src], sStage, h * ATT_D, q0, b);
+        tma_reduce_add_3d(&maps.dq[src], sStage + ATB_STG_BYTES / 2, h * ATT_D + 32, q0, b);
         bulk_commit();
       }
     }

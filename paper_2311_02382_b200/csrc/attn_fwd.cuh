@@ -39,12 +39,15 @@ constexpr int ATT_FWD_THREADS = 384;
 constexpr int ATT_FWD_SMEM = (2 + 2 * ATT_KV_STAGES) * ATT_TILE_BYTES + 1024 + 256;
 
 struct AttnFwdParams {
-  int B, m, m_pad, G, seg_len, H;  // q: [B][m][H*64]; kv: [G][B][seg_len][2*H*64]
-  long offset;              // global position of q row 0
+  int B, m, m_pad, G, seg_len, H;  // q: m rows per batch; kv: [G][B][seg_len][ld]
+  int g_begin, g_end;              // key segments [g_begin, g_end) attended (partial attention)
+  long offset;                     // global position of q row 0
   int causal;
-  float scale_log2;         // log2(e)/sqrt(d)
-  __nv_bfloat16* o;         // [B][m][H*64]
-  float* lse2;              // [B][H][m_pad], log2 domain: m + log2(l); pad rows = +inf
+  float scale_log2;                // log2(e)/sqrt(d)
+  __nv_bfloat16* o;                // row r of batch b at o + b*o_bstride + r*E
+  long o_bstride;
+  float* lse2;                     // [B][H][lse_pitch] (+ row), base 2: m + log2(l); pad rows = +inf
+  int lse_pitch;                   // rows with no visible key (partial ranges) get O = 0, lse = -inf
 };
 
 __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
@@ -78,15 +81,15 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   const bool has1 = q0 + ATT_BM < p.m;
   const int q_last = min(q0 + 2 * ATT_BM, p.m) - 1;  // last valid local row in this CTA
   const int tps = (p.seg_len + ATT_BN - 1) / ATT_BN;  // key tiles per segment
-  int n_kv = p.G * tps;
+  int n_kv = (p.g_end - p.g_begin) * tps;
   if (p.causal) {
     const long max_key = p.offset + q_last;  // keys > max_key are masked for every row
     int n = 0;
-    for (int g = 0; g < p.G; ++g) {
+    for (int g = p.g_begin; g < p.g_end; ++g) {
       const long seg0 = (long)g * p.seg_len;
       if (seg0 > max_key) break;
       const long last_in_seg = min((long)p.seg_len - 1, max_key - seg0);
-      n = g * tps + (int)(last_in_seg / ATT_BN) + 1;
+      n = (g - p.g_begin) * tps + (int)(last_in_seg / ATT_BN) + 1;
     }
     n_kv = n;
   }
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         const uint32_t ph = (j / ATT_KV_STAGES) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
         if (elect_one()) {
-          const int g = j / tps, t = j % tps;
+          const int g = p.g_begin + j / tps, t = j % tps;
           mbar_arrive_expect_tx(&kv_full[st], 2 * ATT_TILE_BYTES);
           tma_load_4d(&tmK, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
           tma_load_4d(&tmV, &kv_full[st], sV + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       float m_run = -INFINITY, l_run = 0.f;
       const int tile_first_row = q0 + w * ATT_BM;  // for the mask decision (warp-uniform)
       for (int j = 0; j < n_kv; ++j) {
-        const int g = j / tps, t = j % tps;
+        const int g = p.g_begin + j / tps, t = j % tps;
         const int valid_cols = min(ATT_BN, p.seg_len - t * ATT_BN);
         const long key0 = (long)g * p.seg_len + (long)t * ATT_BN;
         const bool need_mask = valid_cols < ATT_BN ||
@@ -283,8 +286,8 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       uint32_t oo[ATT_D];
       tmem_ld64(tO[w] + lane_off, oo);
       if (lrow < p.m) {
-        const float inv = 1.f / l_run;
-        uint4* dst = reinterpret_cast<uint4*>(p.o + ((long)b * p.m + lrow) * E + h * ATT_D);
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (long)b * p.o_bstride + (long)lrow * E + h * ATT_D);
 #pragma unroll
         for (int i = 0; i < ATT_D / 8; ++i) {
           uint4 v;
@@ -294,9 +297,19 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
           v.w = pack_bf16(__uint_as_float(oo[8 * i + 6]) * inv, __uint_as_float(oo[8 * i + 7]) * inv);
           dst[i] = v;
         }
-        p.lse2[((long)b * p.H + h) * p.m_pad + lrow] = m_run + __log2f(l_run);
+        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = l_run > 0.f ? m_run + __log2f(l_run) : -INFINITY;
       } else if (lrow < p.m_pad) {
-        p.lse2[((long)b * p.H + h) * p.m_pad + lrow] = INFINITY;
+        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = INFINITY;
+      }
+    } else if (active) {
+      // no key tile of [g_begin, g_end) is visible to this CTA: empty partial
+      if (lrow < p.m) {
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (long)b * p.o_bstride + (long)lrow * E + h * ATT_D);
+#pragma unroll
+        for (int i = 0; i < ATT_D / 8; ++i) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = -INFINITY;
+      } else if (lrow < p.m_pad) {
+        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = INFINITY;
       }
     }
   }

@@ -245,6 +245,65 @@ __global__ void attn_delta_bf16_d64_kernel(const __nv_bfloat16* __restrict__ dO,
   }
 }
 
+// Merge two partial attentions over disjoint key ranges (log-sum-exp combine):
+//   lse = log2(2^la + 2^lb),  O = 2^(la-lse) O_a + 2^(lb-lse) O_b
+// One warp per (batch, row); lane l covers 8 columns per 256-column chunk.
+// O_a/O_b/O_out are bf16 rows of E = H*64 (batch stride o_bstride elements),
+// lse buffers are [B][H][pitch] (base 2).  O_out/lse_out may alias O_a/lse_a.
+__global__ void attn_merge_kernel(const __nv_bfloat16* oa, const float* la, const __nv_bfloat16* ob,
+                                  const float* lb, __nv_bfloat16* oo, float* lo, int B, int rows, int H,
+                                  long o_bstride, int pitch) {
+  const long w = ((long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= (long)B * rows) return;
+  const int row = w % rows, b = w / rows;
+  const int E = H * 64;
+  for (int c0 = 0; c0 < E; c0 += 256) {
+    const int col = c0 + lane * 8;
+    const bool on = col < E;
+    const int h = col / 64;
+    const long li = ((long)b * H + h) * pitch + row;
+    float wa = 0.f, wb = 0.f, l = -INFINITY;
+    if (on) {
+      const float a = la[li], c = lb[li];
+      const float mx = fmaxf(a, c);
+      if (mx != -INFINITY) {
+        const float ea = exp2f(a - mx), eb = exp2f(c - mx);
+        l = mx + __log2f(ea + eb);
+        wa = ea / (ea + eb);
+        wb = eb / (ea + eb);
+      }
+      const long off = (long)b * o_bstride + (long)row * E + col;
+      const uint4 va = *reinterpret_cast<const uint4*>(oa + off);
+      const uint4 vb = *reinterpret_cast<const uint4*>(ob + off);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&va);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&vb);
+      uint4 r;
+      uint32_t* r2 = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 x = __bfloat1622float2(a2[i]), y = __bfloat1622float2(b2[i]);
+        r2[i] = pack_bf16(wa * x.x + wb * y.x, wa * x.y + wb * y.y);
+      }
+      *reinterpret_cast<uint4*>(oo + off) = r;
+    }
+    __syncwarp();
+    if (on && (lane & 7) == 0) lo[li] = l;
+  }
+}
+
+__global__ void add_f32_kernel(float* __restrict__ y, const float* __restrict__ x, long n) {
+  const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n) {
+    float4 a = *reinterpret_cast<float4*>(y + i);
+    const float4 b = *reinterpret_cast<const float4*>(x + i);
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    *reinterpret_cast<float4*>(y + i) = a;
+  } else {
+    for (long k = i; k < n; ++k) y[k] += x[k];
+  }
+}
+
 // Write +inf into the padded tail of a [B*H][m_pad] log-sum-exp buffer.
 __global__ void pad_fill_kernel(float* __restrict__ buf, long nrows, int m, int m_pad, float v) {
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -272,18 +272,24 @@ static int attn_check(int dtype, int batch, int rows, int workers, int seg_len, 
   return LSS_OK;
 }
 
-int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, void* o, float* lse2,
-                 int batch, int rows, int workers, int seg_len, int heads, int head_dim, long offset, int causal,
-                 void* stream) {
+int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v, long ld_kv,
+                    void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers, int seg_len,
+                    int heads, int head_dim, long offset, int causal, int g_begin, int g_end, void* stream) {
   int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
   if (rc) return rc;
   if (!q || !k || !v || !o || !lse2) return fail(LSS_ERR_ARG, "attn_fwd: null pointer");
   const int E = heads * head_dim;
   if (ld_kv < E) return fail(LSS_ERR_SHAPE, "attn_fwd: ld_kv %ld < embed %d", ld_kv, E);
   if (causal && offset < 0) return fail(LSS_ERR_DEGENERATE, "attn_fwd: negative offset leaves rows fully masked");
+  if (g_begin < 0 || g_end > workers || g_begin >= g_end) return fail(LSS_ERR_SHAPE, "attn_fwd: bad segment range");
   const int m_pad = (int)lss_rows_pad(rows);
+  if (lse_pitch < m_pad) return fail(LSS_ERR_SHAPE, "attn_fwd: lse pitch %d < %d", lse_pitch, m_pad);
+  if (q_bstride < (long)rows * E || o_bstride < (long)rows * E) return fail(LSS_ERR_SHAPE, "attn_fwd: batch stride");
   const float scale = 1.0f / sqrtf((float)head_dim);
   if (dtype == LSS_F32) {
+    if (g_begin != 0 || g_end != workers || q_bstride != (long)rows * E || o_bstride != (long)rows * E ||
+        lse_pitch != m_pad)
+      return fail(LSS_ERR_UNSUPPORTED, "attn_fwd f32: partial/strided attention is bf16-only");
     dim3 grid((rows + 3) / 4, heads, batch);
     attn_fwd_f32_kernel<<<grid, 128, 0, S(stream)>>>(
         reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(k), reinterpret_cast<const float*>(v),
@@ -291,22 +297,126 @@ int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld
         causal, scale);
     return check_launch("attn_fwd_f32");
   }
-  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || ld_kv % 8)
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || ld_kv % 8 || q_bstride % 8 ||
+      o_bstride % 8)
     return fail(LSS_ERR_UNSUPPORTED, "attn_fwd: 16B alignment");
   CUtensorMap mq, mk, mv;
-  if ((rc = map_rows(&mq, q, E, E, rows, batch, 1, 3))) return rc;
+  {
+    uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
+    uint64_t str[2] = {(uint64_t)E, (uint64_t)q_bstride};
+    uint32_t box[3] = {64, 128, 1};
+    if ((rc = make_map(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 3, q, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
   if ((rc = map_rows(&mk, k, E, ld_kv, seg_len, batch, workers, 4))) return rc;
   if ((rc = map_rows(&mv, v, E, ld_kv, seg_len, batch, workers, 4))) return rc;
   AttnFwdParams p;
   p.B = batch; p.m = rows; p.m_pad = m_pad; p.G = workers; p.seg_len = seg_len; p.H = heads;
+  p.g_begin = g_begin; p.g_end = g_end;
   p.offset = offset; p.causal = causal;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.o = reinterpret_cast<__nv_bfloat16*>(o);
+  p.o_bstride = o_bstride;
   p.lse2 = lse2;
+  p.lse_pitch = lse_pitch;
   if ((rc = set_smem(attn_fwd_tc_kernel, ATT_FWD_SMEM))) return rc;
   dim3 grid((rows + 2 * ATT_BM - 1) / (2 * ATT_BM), heads, batch);
   attn_fwd_tc_kernel<<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
   return check_launch("attn_fwd_tc");
+}
+
+int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, void* o, float* lse2,
+                 int batch, int rows, int workers, int seg_len, int heads, int head_dim, long offset, int causal,
+                 void* stream) {
+  const long E = (long)heads * head_dim;
+  return lss_attn_fwd_ex(dtype, q, rows, rows * E, k, v, ld_kv, o, rows * E, lse2, (int)lss_rows_pad(rows), batch,
+                         workers, seg_len, heads, head_dim, offset, causal, 0, workers, stream);
+}
+
+int lss_attn_delta(int dtype, const void* o, const void* grad_o, float* delta, int batch, int rows, int heads,
+                   int head_dim, int scaled, void* stream) {
+  if (!o || !grad_o || !delta) return fail(LSS_ERR_ARG, "attn_delta: null pointer");
+  if (batch <= 0 || rows <= 0 || heads <= 0 || head_dim <= 0) return fail(LSS_ERR_SHAPE, "attn_delta: extent");
+  const int E = heads * head_dim;
+  const int m_pad = (int)lss_rows_pad(rows);
+  const float scale = scaled ? 1.0f / sqrtf((float)head_dim) : 1.0f;
+  const long total = (long)batch * m_pad * heads;
+  const int threads = 256;
+  if (dtype == LSS_BF16 && head_dim == 64 && E % 256 == 0) {
+    const long warps = (long)batch * m_pad;
+    attn_delta_bf16_d64_kernel<<<(warps * 32 + threads - 1) / threads, threads, 0, S(stream)>>>(
+        reinterpret_cast<const __nv_bfloat16*>(grad_o), reinterpret_cast<const __nv_bfloat16*>(o), delta, batch,
+        rows, m_pad, heads, scale);
+  } else if (dtype == LSS_BF16) {
+    attn_delta_kernel<__nv_bfloat16><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
+        reinterpret_cast<const __nv_bfloat16*>(grad_o), reinterpret_cast<const __nv_bfloat16*>(o), delta, batch,
+        rows, m_pad, heads, head_dim, scale);
+  } else {
+    attn_delta_kernel<float><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
+        reinterpret_cast<const float*>(grad_o), reinterpret_cast<const float*>(o), delta, batch, rows, m_pad, heads,
+        head_dim, scale);
+  }
+  return check_launch("attn_delta");
+}
+
+int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
+                    float* grad_k, float* grad_v, long ld_dkv, int batch, int workers, int seg_len, int heads,
+                    int head_dim, int causal, void* stream) {
+  if (dtype != LSS_BF16) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_ex: bf16 only");
+  int rc = attn_check(dtype, batch, 1, workers, seg_len, heads, head_dim);
+  if (rc) return rc;
+  if (!k || !v || !srcs || !grad_k || !grad_v) return fail(LSS_ERR_ARG, "attn_bwd_ex: null pointer");
+  if (nsrc < 1 || nsrc > ATB_MAX_SRC) return fail(LSS_ERR_ARG, "attn_bwd_ex: %d sources (1..%d)", nsrc, ATB_MAX_SRC);
+  const int E = heads * head_dim;
+  if (ld_kv < E || ld_dkv < E) return fail(LSS_ERR_SHAPE, "attn_bwd_ex: row strides smaller than embed");
+  if (!aligned16(k) || !aligned16(v) || !aligned16(grad_k) || !aligned16(grad_v) || ld_kv % 8 || ld_dkv % 4)
+    return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_ex: 16B alignment");
+  const float scale = 1.0f / sqrtf((float)head_dim);
+  AttnBwdParams p;
+  memset(&p, 0, sizeof(p));
+  BwdMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  for (int i = 0; i < nsrc; ++i) {
+    const lss_bwd_source& sr = srcs[i];
+    if (!sr.q || !sr.grad_o || !sr.grad_q || !sr.lse2 || !sr.delta) return fail(LSS_ERR_ARG, "source %d: null", i);
+    if (sr.row0 < 0 || sr.rows <= 0 || sr.row0 + sr.rows > sr.m_src || sr.row0 % ATT_BM ||
+        (sr.rows % ATT_BM && sr.row0 + sr.rows != sr.m_src))
+      return fail(LSS_ERR_SHAPE, "source %d: rows [%d,%d) of %d must be 128-row aligned", i, sr.row0,
+                  sr.row0 + sr.rows, sr.m_src);
+    if (sr.g_begin < 0 || sr.g_end > workers || sr.g_begin >= sr.g_end)
+      return fail(LSS_ERR_SHAPE, "source %d: bad segment range", i);
+    if (sr.pitch < lss_rows_pad(sr.m_src)) return fail(LSS_ERR_SHAPE, "source %d: lse pitch", i);
+    if (!aligned16(sr.q) || !aligned16(sr.grad_o) || !aligned16(sr.grad_q))
+      return fail(LSS_ERR_UNSUPPORTED, "source %d: 16B alignment", i);
+    if ((rc = map_rows(&maps.q[i], sr.q, E, E, sr.m_src, batch, 1, 3))) return rc;
+    if ((rc = map_rows(&maps.dO[i], sr.grad_o, E, E, sr.m_src, batch, 1, 3))) return rc;
+    uint64_t dims[3] = {(uint64_t)E, (uint64_t)sr.m_src, (uint64_t)batch};
+    uint64_t str[2] = {(uint64_t)E, (uint64_t)sr.m_src * E};
+    uint32_t box[3] = {32, 128, 1};
+    if ((rc = make_map(&maps.dq[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, sr.grad_q, dims, str, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+    p.src[i].row0 = sr.row0;
+    p.src[i].rows = sr.rows;
+    p.src[i].pos0 = sr.pos0;
+    p.src[i].g_begin = sr.g_begin;
+    p.src[i].g_end = sr.g_end;
+    p.src[i].lse2 = sr.lse2;
+    p.src[i].delta = sr.delta;
+    p.src[i].pitch = sr.pitch;
+  }
+  CUtensorMap mk, mv;
+  if ((rc = map_rows(&mk, k, E, ld_kv, seg_len, batch, workers, 4))) return rc;
+  if ((rc = map_rows(&mv, v, E, ld_kv, seg_len, batch, workers, 4))) return rc;
+  p.B = batch; p.G = workers; p.seg_len = seg_len; p.H = heads; p.nsrc = nsrc; p.causal = causal;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.scale = scale;
+  p.dk = grad_k; p.dv = grad_v; p.ld_dkv = ld_dkv;
+  if ((rc = set_smem(attn_bwd_tc_kernel, ATB_SMEM))) return rc;
+  const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
+  dim3 grid(workers * tps, heads, batch);
+  attn_bwd_tc_kernel<<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
+  return check_launch("attn_bwd_tc");
 }
 
 int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, const void* o,
@@ -321,25 +431,8 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
   if (ld_kv < E || ld_dkv < E) return fail(LSS_ERR_SHAPE, "attn_bwd: row strides smaller than embed");
   const int m_pad = (int)lss_rows_pad(rows);
   const float scale = 1.0f / sqrtf((float)head_dim);
-  {
-    const long total = (long)batch * m_pad * heads;
-    const int threads = 256;
-    if (dtype == LSS_BF16 && head_dim == 64 && E % 256 == 0) {
-      const long warps = (long)batch * m_pad;
-      attn_delta_bf16_d64_kernel<<<(warps * 32 + threads - 1) / threads, threads, 0, S(stream)>>>(
-          reinterpret_cast<const __nv_bfloat16*>(grad_o), reinterpret_cast<const __nv_bfloat16*>(o), delta_ws,
-          batch, rows, m_pad, heads, scale);
-    } else if (dtype == LSS_BF16) {
-      attn_delta_kernel<__nv_bfloat16><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
-          reinterpret_cast<const __nv_bfloat16*>(grad_o), reinterpret_cast<const __nv_bfloat16*>(o), delta_ws,
-          batch, rows, m_pad, heads, head_dim, scale);
-    } else {
-      attn_delta_kernel<float><<<(total + threads - 1) / threads, threads, 0, S(stream)>>>(
-          reinterpret_cast<const float*>(grad_o), reinterpret_cast<const float*>(o), delta_ws, batch, rows, m_pad,
-          heads, head_dim, 1.0f);
-    }
-    if ((rc = check_launch("attn_delta"))) return rc;
-  }
+  if ((rc = lss_attn_delta(dtype, o, grad_o, delta_ws, batch, rows, heads, head_dim, dtype == LSS_BF16, stream)))
+    return rc;
   if (dtype == LSS_F32) {
     const float* qf = reinterpret_cast<const float*>(q);
     const float* kf = reinterpret_cast<const float*>(k);
@@ -356,35 +449,34 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
                                                       offset, causal, scale);
     return check_launch("attn_bwd_dkv_f32");
   }
-  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(grad_o) || !aligned16(grad_q) ||
-      !aligned16(grad_k) || !aligned16(grad_v) || ld_kv % 8 || ld_dkv % 4)
-    return fail(LSS_ERR_UNSUPPORTED, "attn_bwd: 16B alignment");
+  if (!aligned16(grad_q)) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd: 16B alignment");
   cudaError_t e = cudaMemsetAsync(grad_q, 0, sizeof(float) * (size_t)batch * rows * E, S(stream));
   if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "attn_bwd memset: %s", cudaGetErrorString(e));
-  CUtensorMap mq, mdo, mk, mv, mdq;
-  if ((rc = map_rows(&mq, q, E, E, rows, batch, 1, 3))) return rc;
-  if ((rc = map_rows(&mdo, grad_o, E, E, rows, batch, 1, 3))) return rc;
-  if ((rc = map_rows(&mk, k, E, ld_kv, seg_len, batch, workers, 4))) return rc;
-  if ((rc = map_rows(&mv, v, E, ld_kv, seg_len, batch, workers, 4))) return rc;
-  {
-    uint64_t dims[3] = {(uint64_t)E, (uint64_t)rows, (uint64_t)batch};
-    uint64_t str[2] = {(uint64_t)E, (uint64_t)rows * E};
-    uint32_t box[3] = {32, 128, 1};
-    if ((rc = make_map(&mdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, grad_q, dims, str, box,
-                       CU_TENSOR_MAP_SWIZZLE_128B)))
-      return rc;
-  }
-  AttnBwdParams p;
-  p.B = batch; p.m = rows; p.m_pad = m_pad; p.G = workers; p.seg_len = seg_len; p.H = heads;
-  p.offset = offset; p.causal = causal;
-  p.scale_log2 = scale * 1.4426950408889634f;
-  p.scale = scale;
-  p.lse2 = lse2; p.delta = delta_ws; p.dq = grad_q; p.dk = grad_k; p.dv = grad_v; p.ld_dkv = ld_dkv;
-  if ((rc = set_smem(attn_bwd_tc_kernel, ATB_SMEM))) return rc;
-  const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
-  dim3 grid(workers * tps, heads, batch);
-  attn_bwd_tc_kernel<<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mq, mdo, mk, mv, mdq, p);
-  return check_launch("attn_bwd_tc");
+  lss_bwd_source src;
+  src.q = q; src.grad_o = grad_o; src.grad_q = grad_q; src.m_src = rows; src.row0 = 0; src.rows = rows;
+  src.pos0 = offset; src.g_begin = 0; src.g_end = workers; src.lse2 = lse2; src.delta = delta_ws; src.pitch = m_pad;
+  return lss_attn_bwd_ex(dtype, k, v, ld_kv, &src, 1, grad_k, grad_v, ld_dkv, batch, workers, seg_len, heads,
+                         head_dim, causal, stream);
+}
+
+int lss_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b, void* o_out,
+                   float* lse_out, int batch, int rows, int heads, long o_bstride, int lse_pitch, void* stream) {
+  if (!o_a || !lse_a || !o_b || !lse_b || !o_out || !lse_out) return fail(LSS_ERR_ARG, "attn_merge: null pointer");
+  if (heads <= 0) return fail(LSS_ERR_SHAPE, "attn_merge: heads");
+  if (rows <= 0) return LSS_OK;
+  const long warps = (long)batch * rows;
+  attn_merge_kernel<<<(warps * 32 + 255) / 256, 256, 0, S(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(o_a), lse_a, reinterpret_cast<const __nv_bfloat16*>(o_b), lse_b,
+      reinterpret_cast<__nv_bfloat16*>(o_out), lse_out, batch, rows, heads, o_bstride, lse_pitch);
+  return check_launch("attn_merge");
+}
+
+int lss_add_f32(float* y, const float* x, long n, void* stream) {
+  if (!y || !x) return fail(LSS_ERR_ARG, "add_f32: null pointer");
+  if (n <= 0) return LSS_OK;
+  const long threads = 256, per = threads * 4;
+  add_f32_kernel<<<(n + per - 1) / per, threads, 0, S(stream)>>>(y, x, n);
+  return check_launch("add_f32");
 }
 
 }  // extern "C"

@@ -15,7 +15,7 @@ import ctypes
 import torch
 
 from . import _native
-from ._native import LSS_BF16, LSS_F32, GemmEpilogue, call
+from ._native import LSS_BF16, LSS_F32, BwdSource, GemmEpilogue, call
 from .errors import ShapeError, UnsupportedError
 
 LAYERNORM_EPS = 1e-5  # nnops.py:28
@@ -238,3 +238,71 @@ def attn_bwd(q, k, v, o, grad_o, lse2, *, workers, seg_len, heads, offset, causa
          _ptr(dl), _ptr(gq), _ptr(grad_k), _ptr(grad_v), lddkv, bsz, m, workers, seg_len, heads,
          e // heads, offset, int(causal), _stream())
     return gq, grad_k, grad_v
+
+
+# ----------------------------------------------------------------- balanced-schedule pieces
+
+
+def attn_fwd_partial(q, k, v, *, rows, row0, workers, seg_len, heads, offset, causal, g_begin, g_end, out,
+                     lse2):
+    """Partial attention of q rows [row0, row0+rows) (global position offset + row0 for
+    the first) over key segments [g_begin, g_end) into out[:, row0:row0+rows] and
+    lse2[..., row0:row0+rows] (full-size [B,m,E] / [B,H,m_pad] buffers)."""
+    bsz, m, e = q.shape
+    ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
+    if _rows_view(v, "v", workers, bsz, seg_len, e) != ldk:
+        raise ShapeError("k and v must share a row stride")
+    qv = q[:, row0:row0 + rows]
+    ov = out[:, row0:row0 + rows]
+    lv = lse2[:, :, row0:]
+    call("lss_attn_fwd_ex", LSS_BF16, _ptr(qv), rows, m * e, _ptr(k), _ptr(v), ldk, _ptr(ov), m * e, _ptr(lv),
+         lse2.shape[-1], bsz, workers, seg_len, heads, e // heads, offset + row0, int(causal), g_begin, g_end,
+         _stream())
+
+
+def attn_merge(o_a, lse_a, o_b, lse_b, *, row0, rows, heads, o_out=None, lse_out=None):
+    """Combine two partial attentions of rows [row0, row0+rows) (in place into a by default)."""
+    bsz, m, e = o_a.shape
+    o_out = o_a if o_out is None else o_out
+    lse_out = lse_a if lse_out is None else lse_out
+    sl = lambda t: t[:, row0:]  # noqa: E731
+    call("lss_attn_merge", _ptr(sl(o_a)), _ptr(lse_a[:, :, row0:]), _ptr(sl(o_b)), _ptr(lse_b[:, :, row0:]),
+         _ptr(sl(o_out)), _ptr(lse_out[:, :, row0:]), bsz, rows, heads, m * e, lse_a.shape[-1], _stream())
+
+
+def attn_delta(o, grad_o, delta, *, heads, scaled=True):
+    bsz, m, e = o.shape
+    dt = LSS_BF16 if o.dtype == torch.bfloat16 else LSS_F32
+    call("lss_attn_delta", dt, _ptr(o), _ptr(grad_o), _ptr(delta), bsz, m, heads, e // heads, int(scaled),
+         _stream())
+
+
+def attn_bwd_sources(k, v, sources, *, grad_k, grad_v, workers, seg_len, heads, causal):
+    """Multi-source backward.  sources: dicts with q, grad_o, grad_q (fp32, pre-zeroed),
+    row0, rows, pos0 (global position of tensor row 0), g_begin, g_end, lse2, delta."""
+    q0 = sources[0]["q"]
+    bsz, _, e = q0.shape
+    ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
+    arr = (BwdSource * len(sources))()
+    for i, src in enumerate(sources):
+        q = src["q"]
+        arr[i].q = q.data_ptr()
+        arr[i].grad_o = src["grad_o"].data_ptr()
+        arr[i].grad_q = src["grad_q"].data_ptr()
+        arr[i].m_src = q.shape[1]
+        arr[i].row0 = src["row0"]
+        arr[i].rows = src["rows"]
+        arr[i].pos0 = src["pos0"]
+        arr[i].g_begin = src["g_begin"]
+        arr[i].g_end = src["g_end"]
+        arr[i].lse2 = src["lse2"].data_ptr()
+        arr[i].delta = src["delta"].data_ptr()
+        arr[i].pitch = src["lse2"].shape[-1]
+    call("lss_attn_bwd_ex", LSS_BF16, _ptr(k), _ptr(v), ldk, arr, len(sources), _ptr(grad_k), _ptr(grad_v),
+         grad_k.stride(-2), bsz, workers, seg_len, heads, e // heads, int(causal), _stream())
+
+
+def add_(y, x):
+    """y += x (fp32, device)."""
+    call("lss_add_f32", _ptr(y), _ptr(x), y.numel(), _stream())
+    return y

@@ -69,15 +69,65 @@ GRAD_NAMES = ("ln1_gain", "ln1_bias", "attn_q.weight", "attn_q.bias", "attn_k.we
               "attn_v.weight", "attn_v.bias", "attn_out.weight", "attn_out.bias")
 
 
+# ---------------------------------------------------------------- causal load balancing
+
+
+@dataclass(frozen=True)
+class BalancePlan:
+    """Balanced causal schedule for one rank (ownership unchanged).
+
+    With contiguous segments (ShardSpec) and the causal mask, rank r attends to
+    r full key segments plus its diagonal: work ~ (r + 1/2) m^2, so the slowest
+    rank bounds the group at (G/2)/(G - 1/2) of ideal.  Pairing rank r with
+    G-1-r gives every pair exactly G m^2 of work; the heavy rank delegates
+    D2 = 2r - G + 1 half-blocks (query-row half x full key segment) to its light
+    partner: its top rows [0, split) against key segments [0, a) and its bottom
+    rows [split, m) against [0, b), a + b = D2.  The partner needs the heavy
+    rank's Q rows (sent forward) and returns normalised partial contexts + lse,
+    merged by log-sum-exp; backward it receives dO, lse, delta and returns dQ
+    rows, while its dK/dV contributions land in its own packed buffer, so the
+    reduce-scatter is unchanged.  Extra traffic per step: 2 (B m E) bf16 + 1
+    (B m E) fp32 each way -- small next to the K/V gather.
+    """
+
+    role: str = "none"  # "none" | "heavy" | "light"
+    partner: int = -1
+    split: int = 0      # first bottom row (multiple of 128)
+    a: int = 0          # delegated key segments for the top rows: [0, a)
+    b: int = 0          # delegated key segments for the bottom rows: [0, b)
+
+    @property
+    def active(self) -> bool:
+        return self.role != "none"
+
+
+def make_plan(rank: int, workers: int, block: int, causal: bool) -> BalancePlan:
+    if not causal or workers < 2:
+        return BalancePlan()
+    split = (block // 2) // 128 * 128
+    if split == 0:
+        return BalancePlan()
+    partner = workers - 1 - rank
+    d2 = lambda r: 2 * r - workers + 1  # noqa: E731  half-blocks rank r must give away
+    if d2(rank) > 0:
+        n = d2(rank)
+        return BalancePlan("heavy", partner, split, (n + 1) // 2, n // 2)
+    if partner != rank and d2(partner) > 0:
+        n = d2(partner)
+        return BalancePlan("light", partner, split, (n + 1) // 2, n // 2)
+    return BalancePlan()
+
+
 class LSSAttention:
     """One rank's attention sublayer with resident HBM buffers.
 
     cfg.seq_len is the FULL sequence length l; spec gives this rank's block.
     ``grad_scale`` = 1/(D*N) folds the two averaging steps into the kernels.
+    ``balanced`` (default: on for causal bf16) enables the BalancePlan schedule.
     """
 
     def __init__(self, cfg: ModelConfig, spec: ShardSpec, *, grad_scale: float | None = None,
-                 device=None):
+                 device=None, balanced: bool | None = None):
         if spec.seq_len != cfg.seq_len:
             raise ShapeError(f"shard spec length {spec.seq_len} != config seq_len {cfg.seq_len}")
         self.cfg, self.spec = cfg, spec
@@ -89,7 +139,11 @@ class LSSAttention:
         f32 = torch.float32
         dev = self.device
         mp = K.rows_pad(m)
+        self.mp = mp
         z = lambda *s, dt=f32: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
+        if balanced is None:
+            balanced = cfg.precision == "bf16"
+        self.plan = make_plan(spec.rank, G, m, cfg.causal) if balanced and cfg.precision == "bf16" else BalancePlan()
         # forward
         self.xh = z(B, m, E, dt=ad)
         self.mean, self.rstd = z(B * m), z(B * m)
@@ -109,6 +163,13 @@ class LSSAttention:
         self.dqkv = z(B, m, 3 * E, dt=ad)
         self.dxh = z(B, m, E)
         self.dx = z(B, m, E)
+        # balanced-schedule exchange buffers
+        if self.plan.role == "heavy":
+            self.o_help, self.lse_help, self.dq_help = z(B, m, E, dt=ad), z(B, H, mp), z(B, m, E)
+        elif self.plan.role == "light":
+            self.q_peer, self.o_peer, self.lse_peer = z(B, m, E, dt=ad), z(B, m, E, dt=ad), z(B, H, mp)
+            self.do_peer, self.lsef_peer, self.delta_peer = z(B, m, E, dt=ad), z(B, H, mp), z(B, H, mp)
+            self.dq_peer = z(B, m, E)
         # gradients, one flat buffer: [Wq Wk Wv | Wo | bq bk bv | bo | ln_g | ln_b | extra]
         n = 4 * E * E + 6 * E + 1
         self.grads = torch.zeros(n, dtype=f32, device=dev)
@@ -152,6 +213,25 @@ class LSSAttention:
                            LinearParams(g["attn_v.weight"], g["attn_v.bias"]),
                            LinearParams(g["attn_out.weight"], g["attn_out.bias"]))
 
+    # ------------------------------------------------------------ point-to-point exchanges
+    def xfer(self, phase: str):
+        """(sends, recvs) of the balanced schedule for `phase` in {"F1","F2","B1","B2"}.
+        Tensors pair up positionally between this rank and plan.partner."""
+        pl = self.plan
+        if not pl.active:
+            return [], []
+        heavy = pl.role == "heavy"
+        if phase == "F1":  # heavy rank's query rows -> partner
+            return ([self.q], []) if heavy else ([], [self.q_peer])
+        if phase == "F2":  # partner's partial contexts + lse -> heavy rank
+            return ([], [self.o_help, self.lse_help]) if heavy else ([self.o_peer, self.lse_peer], [])
+        if phase == "B1":  # dO, merged lse, delta of the delegated rows -> partner
+            return ([self.dctx, self.lse2, self.delta], []) if heavy else \
+                ([], [self.do_peer, self.lsef_peer, self.delta_peer])
+        if phase == "B2":  # partner's dQ rows -> heavy rank
+            return ([], [self.dq_help]) if heavy else ([self.dq_peer], [])
+        raise ValueError(phase)
+
     # ------------------------------------------------------------ forward
     @property
     def kv_slot(self) -> torch.Tensor:
@@ -170,19 +250,42 @@ class LSSAttention:
                out=[(self.q.view(B * m, E), E), (slot[:, :E], 2 * E), (slot[:, E:], 2 * E)],
                M=B * m, N=3 * E, K=E)
 
-    def fwd_attend(self) -> torch.Tensor:
-        """Segment attention over the gathered K/V, out-projection + residual."""
-        B, m, E = self.B, self.m, self.E
-        K.attn_fwd(self.q, self.kv_full[..., :E], self.kv_full[..., E:], workers=self.G, seg_len=m,
-                   heads=self.H, offset=self.spec.offset, causal=self.cfg.causal, out=self.ctx,
-                   lse2=self.lse2)
+    def fwd_attend(self) -> None:
+        """Segment attention over the gathered K/V (own rows; plus the partner's
+        delegated rows on a light rank of the balanced schedule)."""
+        m, E, pl, r = self.m, self.E, self.plan, self.spec.rank
+        kf, vf = self.kv_full[..., :E], self.kv_full[..., E:]
+        common = dict(workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal)
+        if pl.role == "heavy":
+            K.attn_fwd_partial(self.q, kf, vf, rows=pl.split, row0=0, offset=self.spec.offset, g_begin=pl.a,
+                               g_end=r + 1, out=self.ctx, lse2=self.lse2, **common)
+            K.attn_fwd_partial(self.q, kf, vf, rows=m - pl.split, row0=pl.split, offset=self.spec.offset,
+                               g_begin=pl.b, g_end=r + 1, out=self.ctx, lse2=self.lse2, **common)
+            return
+        K.attn_fwd(self.q, kf, vf, offset=self.spec.offset, out=self.ctx, lse2=self.lse2, **common)
+        if pl.role == "light":
+            off = pl.partner * m
+            K.attn_fwd_partial(self.q_peer, kf, vf, rows=pl.split, row0=0, offset=off, g_begin=0, g_end=pl.a,
+                               out=self.o_peer, lse2=self.lse_peer, **common)
+            if pl.b > 0:
+                K.attn_fwd_partial(self.q_peer, kf, vf, rows=m - pl.split, row0=pl.split, offset=off,
+                                   g_begin=0, g_end=pl.b, out=self.o_peer, lse2=self.lse_peer, **common)
+
+    def fwd_out(self) -> torch.Tensor:
+        """(merge the partner's partials,) out-projection + residual."""
+        B, m, E, pl = self.B, self.m, self.E, self.plan
+        if pl.role == "heavy":
+            K.attn_merge(self.ctx, self.lse2, self.o_help, self.lse_help, row0=0, rows=pl.split, heads=self.H)
+            if pl.b > 0:
+                K.attn_merge(self.ctx, self.lse2, self.o_help, self.lse_help, row0=pl.split, rows=m - pl.split,
+                             heads=self.H)
         K.gemm(self.ctx.view(B * m, E), self.staged["wo_t"], bias=self.lp.attn_out.bias,
                residual=self.x.view(B * m, E), out=self.y.view(B * m, E), M=B * m, N=E, K=E)
         return self.y
 
     # ------------------------------------------------------------ backward
-    def bwd_attend(self, grad_y: torch.Tensor) -> None:
-        """Out-projection backward and attention backward (partial dK|dV for all ranks)."""
+    def bwd_pre(self, grad_y: torch.Tensor) -> None:
+        """Out-projection backward (+ the delta row term in the balanced schedule)."""
         B, m, E = self.B, self.m, self.E
         if grad_y.shape != (B, m, E) or grad_y.dtype != torch.float32 or not grad_y.is_contiguous():
             raise ShapeError(f"grad_y must be contiguous fp32 {(B, m, E)}")
@@ -197,10 +300,39 @@ class LSSAttention:
         # dWo = ctx^T . gy  (both operands MN-major), pre-scaled
         K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True, alpha=a,
                out=self.g_wo, M=E, N=E, K=B * m)
-        K.attn_bwd(self.q, self.kv_full[..., :E], self.kv_full[..., E:], self.ctx, self.dctx, self.lse2,
-                   workers=self.G, seg_len=m, heads=self.H, offset=self.spec.offset,
-                   causal=self.cfg.causal, grad_q=self.dq, grad_k=self.dkv_full[..., :E],
-                   grad_v=self.dkv_full[..., E:], delta=self.delta)
+        if self.plan.active:
+            K.attn_delta(self.ctx, self.dctx, self.delta, heads=self.H, scaled=True)
+
+    def bwd_attend(self) -> None:
+        """Attention backward: dQ for the rows this rank computes, partial dK|dV for all."""
+        m, E, pl, r = self.m, self.E, self.plan, self.spec.rank
+        kf, vf = self.kv_full[..., :E], self.kv_full[..., E:]
+        if not pl.active:
+            K.attn_bwd(self.q, kf, vf, self.ctx, self.dctx, self.lse2, workers=self.G, seg_len=m,
+                       heads=self.H, offset=self.spec.offset, causal=self.cfg.causal, grad_q=self.dq,
+                       grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:], delta=self.delta)
+            return
+        own = dict(q=self.q, grad_o=self.dctx, grad_q=self.dq, pos0=self.spec.offset, lse2=self.lse2,
+                   delta=self.delta)
+        self.dq.zero_()
+        if pl.role == "heavy":
+            srcs = [dict(own, row0=0, rows=pl.split, g_begin=pl.a, g_end=r + 1),
+                    dict(own, row0=pl.split, rows=m - pl.split, g_begin=pl.b, g_end=r + 1)]
+        else:
+            self.dq_peer.zero_()
+            peer = dict(q=self.q_peer, grad_o=self.do_peer, grad_q=self.dq_peer, pos0=pl.partner * m,
+                        lse2=self.lsef_peer, delta=self.delta_peer)
+            srcs = [dict(own, row0=0, rows=m, g_begin=0, g_end=r + 1),
+                    dict(peer, row0=0, rows=pl.split, g_begin=0, g_end=pl.a)]
+            if pl.b > 0:
+                srcs.append(dict(peer, row0=pl.split, rows=m - pl.split, g_begin=0, g_end=pl.b))
+        K.attn_bwd_sources(kf, vf, srcs, grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:],
+                           workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal)
+
+    def bwd_fold(self) -> None:
+        """Heavy rank of the balanced schedule: fold the partner's dQ rows in."""
+        if self.plan.role == "heavy":
+            K.add_(self.dq, self.dq_help)
 
     def bwd_project(self) -> torch.Tensor:
         """After the reduce-scatter: [dQ|dK|dV] -> dx̂ and dW_qkv, LN1 backward + residual."""
@@ -224,14 +356,7 @@ class LSSAttention:
         """Forward + backward (+ folded gradient sync) of this rank's block, device
         tensors in and out.  Returns (y, dx); gradients are in ``grads`` /
         ``grad_views()`` (already averaged over the group(s) when sync=True)."""
-        self.fwd_project(x)
-        comm.all_gather_rows(self.kv_full, step, layer)
-        y = self.fwd_attend()
-        self.bwd_attend(grad_y)
-        comm.reduce_scatter_rows(self.dkv_own, self.dkv_full, step, layer)
-        dx = self.bwd_project()
-        if sync:
-            comm.all_reduce_sum(self.grads, step)
+        (y, dx), = lss_step([self], comm, [x], [grad_y], step=step, layer=layer, sync=sync)
         return y, dx
 
     def step_from_host(self, x_host: torch.Tensor, grad_y_host: torch.Tensor, comm, grads_host=None,
@@ -251,61 +376,79 @@ class LSSAttention:
             self._gy_dev.copy_(grad_y_host, non_blocking=True)
             self._gy_ready.record()
         self._x_dev.copy_(x_host, non_blocking=True)
-        self.fwd_project(self._x_dev)
-        comm.all_gather_rows(self.kv_full, step, layer)
-        y = self.fwd_attend()
-        cur.wait_event(self._gy_ready)
-        self.bwd_attend(self._gy_dev)
-        comm.reduce_scatter_rows(self.dkv_own, self.dkv_full, step, layer)
-        dx = self.bwd_project()
-        comm.all_reduce_sum(self.grads, step)
+        out = lss_step([self], comm, [self._x_dev], [self._gy_dev], step=step, layer=layer,
+                       before_bwd=lambda: cur.wait_event(self._gy_ready))
         if grads_host is not None:
             grads_host.copy_(self.grads, non_blocking=True)
-        return y, dx
+        return out[0]
 
 
 # ---------------------------------------------------------------- drivers
 
 
-def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True):
+def _exchange(engines, comm, phase, step, layer):
+    if isinstance(comm, SimComm):
+        for e in engines:
+            sends, _ = e.xfer(phase)
+            if not sends:
+                continue
+            _, recvs = engines[e.plan.partner].xfer(phase)
+            for src, dst in zip(sends, recvs):
+                dst.copy_(src)
+            comm.ledger.record("send", "sequence", sum(t.numel() for t in sends), step, phase, layer)
+        return
+    for e in engines:
+        sends, recvs = e.xfer(phase)
+        if sends or recvs:
+            comm.p2p(sends, recvs, e.plan.partner, step=step, phase=phase, layer=layer)
+
+
+def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_bwd=None):
     """One fwd+bwd(+sync) of the attention sublayer.
 
     Real multi-GPU: ``engines`` = [this rank's LSSAttention], ``comm`` a
-    TorchDistComm.  Single-process simulation: G engines and a SimComm.
-    Returns the list of (y, dx) per engine (device tensors, not synchronised)."""
+    TorchDistComm (or SoloComm for one rank).  Single-process simulation: G
+    engines and a SimComm.  Returns the list of (y, dx) per engine (device
+    tensors, not synchronised)."""
     sim = isinstance(comm, SimComm)
+    one = lambda f: f([e for e in engines]) if sim else f(engines[0])  # noqa: E731
     for e, x in zip(engines, xs):
         e.fwd_project(x)
-    if sim:
-        comm.all_gather_rows([e.kv_full for e in engines], step, layer)
-    else:
-        comm.all_gather_rows(engines[0].kv_full, step, layer)
-    ys = [e.fwd_attend() for e in engines]
+    one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer))
+    _exchange(engines, comm, "F1", step, layer)
+    for e in engines:
+        e.fwd_attend()
+    _exchange(engines, comm, "F2", step, layer)
+    ys = [e.fwd_out() for e in engines]
+    if before_bwd is not None:
+        before_bwd()
     for e, gy in zip(engines, grad_ys):
-        e.bwd_attend(gy)
-    if sim:
-        comm.reduce_scatter_rows([e.dkv_own for e in engines], [e.dkv_full for e in engines], step, layer)
-    else:
-        comm.reduce_scatter_rows(engines[0].dkv_own, engines[0].dkv_full, step, layer)
+        e.bwd_pre(gy)
+    _exchange(engines, comm, "B1", step, layer)
+    for e in engines:
+        e.bwd_attend()
+    _exchange(engines, comm, "B2", step, layer)
+    for e in engines:
+        e.bwd_fold()
+    one(lambda t: comm.reduce_scatter_rows([e.dkv_own for e in t] if sim else t.dkv_own,
+                                           [e.dkv_full for e in t] if sim else t.dkv_full, step, layer))
     dxs = [e.bwd_project() for e in engines]
     if sync:
-        if sim:
-            comm.all_reduce_sum([e.grads for e in engines], step)
-        else:
-            comm.all_reduce_sum(engines[0].grads, step)
+        one(lambda t: comm.all_reduce_sum([e.grads for e in t] if sim else t.grads, step))
     return list(zip(ys, dxs))
 
 
-def make_sim_group(cfg: ModelConfig, lp: LayerParams, workers: int, *, replicas: int = 1, device=None):
+def make_sim_group(cfg: ModelConfig, lp: LayerParams, workers: int, *, replicas: int = 1, device=None,
+                   balanced: bool | None = None):
     """G engines of one sequence group on one device (tests / smoke), SimComm fabric."""
     engines = []
     for r in range(workers):
         e = LSSAttention(cfg, ShardSpec(r, workers, cfg.seq_len), grad_scale=1.0 / (workers * replicas),
-                         device=device)
+                         device=device, balanced=balanced)
         e.load_params(lp)
         engines.append(e)
     return engines, SimComm(Ledger())
 
 
 __all__ = ["ShardSpec", "slice_batch", "LSSAttention", "lss_step", "make_sim_group", "TorchDistComm",
-           "SimComm", "Ledger", "GRAD_NAMES"]
+           "SimComm", "Ledger", "GRAD_NAMES", "BalancePlan", "make_plan"]

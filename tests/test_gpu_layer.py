@@ -220,3 +220,46 @@ def test_score_counters_track_shapes(cuda, rng):
     b, h, m, t, dk = 3, 2, 2, 6, 4
     assert counters.attn_score_flops == b * h * (2 * m * dk * t + 2 * m * t * dk)
     assert counters.attn_score_elements_peak == b * h * m * t
+
+
+@pytest.mark.parametrize("G,m,batch", [(2, 384, 1), (3, 256, 1), (4, 384, 1), (4, 300, 2), (8, 256, 1)])
+def test_balanced_causal_schedule_matches_oracle(cuda, G, m, batch):
+    """Balanced causal schedule (heavy rank r delegates key blocks to rank G-1-r,
+    BalancePlan) == plain schedule == oracle; ownership of rows unchanged."""
+    import torch
+    from oracle import lss_oracle as O
+    from paper_2311_02382_b200.model import ModelConfig, layer_params_from_arrays
+    from paper_2311_02382_b200.sharded import ShardSpec, lss_step, make_sim_group, slice_batch
+
+    e, h = 128, 2
+    seq = G * m
+    r = np.random.default_rng(G * 1000 + m)
+    p = O.init_attn_params(e, seed=G, dtype=np.float32)
+    p.bq = (0.05 * r.standard_normal(e)).astype(np.float32)
+    p.bv = (0.05 * r.standard_normal(e)).astype(np.float32)
+    x = r.standard_normal((batch, seq, e)).astype(np.float32)
+    gy = r.standard_normal((batch, seq, e)).astype(np.float32)
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=8, vocab=16, seq_len=seq, batch=batch, causal=True)
+    lp = layer_params_from_arrays(*[getattr(p, n) for n in O.AttnParams.GRAD_ORDER], device=cuda)
+    ref = O.lss_attention(x.astype(np.float64), gy.astype(np.float64), p.astype(np.float64), h, G, True)
+    results = {}
+    for balanced in (True, False):
+        engines, comm = make_sim_group(cfg, lp, G, device=cuda, balanced=balanced)
+        if balanced:
+            assert any(eng.plan.active for eng in engines) == (m // 2 >= 128)
+        tx, tg = torch.as_tensor(x, device=cuda), torch.as_tensor(gy, device=cuda)
+        out = lss_step(engines, comm, [slice_batch(tx, ShardSpec(k, G, seq)) for k in range(G)],
+                       [slice_batch(tg, ShardSpec(k, G, seq)) for k in range(G)])
+        torch.cuda.synchronize()
+        y = torch.cat([o[0] for o in out], 1).cpu().numpy()
+        dx = torch.cat([o[1] for o in out], 1).cpu().numpy()
+        gw = {k: v.cpu().numpy() for k, v in engines[0].grad_views().items()}
+        assert_close_ref(y, ref["y"], 1e-2, f"y balanced={balanced}")
+        assert_close_ref(dx, ref["dx"], 1e-2, f"dx balanced={balanced}")
+        for ours, gold in [("attn_q.weight", "wq"), ("attn_k.weight", "wk"), ("attn_v.weight", "wv"),
+                           ("attn_out.weight", "wo"), ("ln1_gain", "ln1_gain")]:
+            assert_close_ref(gw[ours], getattr(ref["grads"], gold), 1e-2, f"{ours} balanced={balanced}")
+        results[balanced] = (y, dx)
+        # the collective schedule is unchanged: 1 gather, 1 reduce-scatter, 1 all-reduce
+        assert comm.ledger.count("all-gather") == 1 and comm.ledger.count("reduce-scatter") == 1
+    assert nerr(results[True][0], results[False][0]) < 5e-3

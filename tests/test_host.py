@@ -79,3 +79,25 @@ def test_folded_gradient_scale_equals_double_average():
     two_step = np.mean([np.mean(g[d], axis=0) for d in range(D)], axis=0)
     folded = (g / (D * N)).sum(axis=(0, 1))
     np.testing.assert_allclose(folded, two_step, rtol=1e-14)
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 5, 8])
+def test_balance_plan_equalises_causal_work(G):
+    """Every rank of a balanced causal group ends with G/2 block-units of work
+    (block = m x m query-key pairs; the diagonal block counts 1/2)."""
+    from paper_2311_02382_b200.sharded import make_plan
+
+    m = 6264
+    plans = [make_plan(r, G, m, True) for r in range(G)]
+    split = (m // 2) // 128 * 128
+    work = [r + 0.5 for r in range(G)]
+    for r, pl in enumerate(plans):
+        if pl.role == "heavy":
+            moved = pl.a * split / m + pl.b * (m - split) / m
+            work[r] -= moved
+            work[pl.partner] += moved
+            assert plans[pl.partner].role == "light" and plans[pl.partner].partner == r
+            assert (pl.a, pl.b) == (plans[pl.partner].a, plans[pl.partner].b)
+            assert pl.a + pl.b == 2 * r - G + 1 and pl.a <= r and pl.b <= r
+    assert max(work) - min(work) < 0.05 * G / 2, work
+    assert not any(p.active for p in (make_plan(r, G, m, False) for r in range(G)))

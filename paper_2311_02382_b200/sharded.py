@@ -118,6 +118,25 @@ def make_plan(rank: int, workers: int, block: int, causal: bool) -> BalancePlan:
     return BalancePlan()
 
 
+def block_pairs(rows: int, p0: int, lo: int, hi: int, causal: bool) -> int:
+    """Unmasked pairs of query rows at positions p0..p0+rows-1 against keys [lo, hi):
+    sum_i clamp(p0 + i + 1 - lo, 0, hi - lo) (causal) or rows * (hi - lo)."""
+    w = hi - lo
+    if not causal:
+        return rows * w
+    c0 = p0 + 1 - lo
+    i_a = max(0, 1 - c0)            # first row with a visible key
+    i_b = max(0, w - c0)            # first row seeing the whole range
+    e1 = min(rows, i_b)
+    part = 0
+    if e1 > i_a:
+        n = e1 - i_a
+        part = n * c0 + (i_a + e1 - 1) * n // 2
+    if rows > i_b:
+        part += (rows - i_b) * w
+    return part
+
+
 class LSSAttention:
     """One rank's attention sublayer with resident HBM buffers.
 
@@ -212,6 +231,24 @@ class LSSAttention:
                            LinearParams(g["attn_k.weight"], g["attn_k.bias"]),
                            LinearParams(g["attn_v.weight"], g["attn_v.bias"]),
                            LinearParams(g["attn_out.weight"], g["attn_out.bias"]))
+
+    def attention_work(self):
+        """(rows, global position of row 0, g_begin, g_end) blocks of query rows x key
+        segments this rank's attention kernels compute (own rows and delegated ones)."""
+        m, pl, r, off = self.m, self.plan, self.spec.rank, self.spec.offset
+        if pl.role == "heavy":
+            return [(pl.split, off, pl.a, r + 1), (m - pl.split, off + pl.split, pl.b, r + 1)]
+        items = [(m, off, 0, self.G)]
+        if pl.role == "light":
+            items.append((pl.split, pl.partner * m, 0, pl.a))
+            if pl.b > 0:
+                items.append((m - pl.split, pl.partner * m + pl.split, 0, pl.b))
+        return items
+
+    def computed_pairs(self) -> int:
+        """Unmasked (query, key) pairs per (batch, head) computed by this rank."""
+        return sum(block_pairs(rows, p0, g0 * self.m, g1 * self.m, self.cfg.causal)
+                   for rows, p0, g0, g1 in self.attention_work())
 
     # ------------------------------------------------------------ point-to-point exchanges
     def xfer(self, phase: str):

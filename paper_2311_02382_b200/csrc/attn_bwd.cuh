@@ -91,15 +91,6 @@ __device__ long long g_bwd_trace[8][512];
   } while (0)
 #endif
 
-template <uint32_t N>
-LSS_DEV void reg_alloc() {
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
-}
-template <uint32_t N>
-LSS_DEV void reg_dealloc() {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
-}
-
 // P^T and dS^T for one key row and 64 query columns:
 //   p = 2^(s*log2e/sqrt(d) - lse2[q]),  ds = p * (dp/sqrt(d) - delta[q]/sqrt(d))
 // lse2 / scaled delta come from shared memory as 128-bit broadcast loads; the
@@ -108,25 +99,32 @@ LSS_DEV void reg_dealloc() {
 template <bool MASK>
 LSS_DEV void bwd_pds(const uint32_t (&sv)[64], const uint32_t (&dp)[64], uint32_t s_lse, uint32_t s_dsc,
                      float sl2, float scale, int fv, uint32_t (&pk)[32], uint32_t (&dk)[32]) {
+  const float2 sl2v = make_float2(sl2, sl2), scv = make_float2(scale, scale);
 #pragma unroll
   for (int c4 = 0; c4 < 16; ++c4) {
     const float4 l = ld_shared_f4(s_lse + c4 * 16);
     const float4 d = ld_shared_f4(s_dsc + c4 * 16);
-    const float lv[4] = {l.x, l.y, l.z, l.w};
-    const float dv[4] = {d.x, d.y, d.z, d.w};
-    float pr[4], dr[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = 4 * c4 + j;
-      float pj = ex2(fmaf(__uint_as_float(sv[c]), sl2, -lv[j]));
-      if (MASK) pj = (c >= fv) ? pj : 0.f;
-      pr[j] = pj;
-      dr[j] = pj * fmaf(__uint_as_float(dp[c]), scale, -dv[j]);
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int c = 4 * c4 + 2 * h2;
+      const float2 nl = h2 ? make_float2(-l.z, -l.w) : make_float2(-l.x, -l.y);
+      const float2 nd = h2 ? make_float2(-d.z, -d.w) : make_float2(-d.x, -d.y);
+      const float2 x = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2v, nl);
+      float2 e;
+      if (!MASK && (c4 & 3) == 0 && h2 == 0) {  // 1 pair in 8 on the FMA pipe (x <= ~0 here)
+        e = exp2_poly2(x);
+      } else {
+        e = make_float2(ex2(x.x), ex2(x.y));
+      }
+      if (MASK) {
+        e.x = (c >= fv) ? e.x : 0.f;
+        e.y = (c + 1 >= fv) ? e.y : 0.f;
+      }
+      const float2 t = ffma2(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), scv, nd);
+      const float2 ds = fmul2(e, t);
+      pk[c / 2] = pack_bf16(e.x, e.y);
+      dk[c / 2] = pack_bf16(ds.x, ds.y);
     }
-    pk[2 * c4] = pack_bf16(pr[0], pr[1]);
-    pk[2 * c4 + 1] = pack_bf16(pr[2], pr[3]);
-    dk[2 * c4] = pack_bf16(dr[0], dr[1]);
-    dk[2 * c4 + 1] = pack_bf16(dr[2], dr[3]);
   }
 }
 
@@ -348,6 +346,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       tmem_ld64(tdP + lane_off + half * 64, dp);
       tc_fence_before();
       mbar_arrive(sdp_free);
+      if (t == 0 && half == 0) BWD_TRACE(7, it);
       // query column c of this half is visible to key row t iff c >= fv
       const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > q0 + half * 64);
       uint32_t pk[32], dk[32];

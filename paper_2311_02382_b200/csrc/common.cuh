@@ -249,4 +249,65 @@ LSS_DEV float ex2(float x) {
   return y;
 }
 
+// ---------------------------------------------------------------- register reconfiguration
+template <uint32_t N>
+LSS_DEV void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <uint32_t N>
+LSS_DEV void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+
+// ---------------------------------------------------------------- packed fp32x2 (FFMA2 / FADD2 / FMUL2)
+LSS_DEV uint64_t f2_u64(float2 v) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+LSS_DEV float2 u64_f2(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+LSS_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)), "l"(f2_u64(c)));
+  return u64_f2(d);
+}
+LSS_DEV float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(d);
+}
+LSS_DEV float2 fsub2(float2 a, float2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(d);
+}
+LSS_DEV float2 fmul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(d);
+}
+
+// 2^x on the FMA pipe for x in [-125, 127] (x is clamped below, so -inf -> ~2^-125,
+// never a wrapped exponent: p(f) < 1 at f = 0 would underflow the exponent field
+// at -127): Cody-Waite split
+// x = j + f, |f| <= 1/2 via the 1.5*2^23 rounding trick, degree-3 minimax for
+// 2^f (max rel. error 7.5e-5, far below the bf16 rounding of P), exponent
+// added as an integer.  Offloads MUFU.EX2, the softmax's binding unit.
+LSS_DEV float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);            // round(x) in the low mantissa bits
+  const float2 f = fsub2(x, fsub2(t, magic));  // x - round(x)
+  float2 pl = ffma2(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
+  pl = ffma2(pl, f, make_float2(0.69326097f, 0.69326097f));
+  pl = ffma2(pl, f, make_float2(0.99992812f, 0.99992812f));
+  return make_float2(__uint_as_float(__float_as_uint(pl.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(pl.y) + (__float_as_uint(t.y) << 23)));
+}
+
 }  // namespace lss

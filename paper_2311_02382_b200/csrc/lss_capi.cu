@@ -486,3 +486,9 @@ extern "C" int lss_debug_bwd_trace(long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, g_bwd_trace, sizeof(long long) * 8 * 512) == cudaSuccess ? 0 : 5;
 }
 #endif
+
+#ifdef LSS_FWD_TRACE
+extern "C" int lss_debug_fwd_trace(long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_fwd_trace, sizeof(long long) * 8 * 1024) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -14,21 +14,32 @@
 // this rank that can see the keys (causal: q_pos >= k_pos).  Transposed
 // formulation so the key rows are TMEM lanes:
 //   S^T  = K Q_i^T   (TMEM, 128 cols)          dP^T = V dO_i^T   (TMEM, 128 cols)
-//   P^T, dS^T computed by 256 threads (2 warpgroups, 64 query columns each)
+//   P^T  computed by 256 threads (2 warpgroups, 64 query columns each), written
+//        back as bf16 over S^T;  dS^T likewise over dP^T and into SMEM
 //   dV  += P^T dO_i  (A = P^T from TMEM)
-//   dK  += dS^T Q_i  (A = dS^T from SMEM, K-major)
+//   dK  += dS^T Q_i  (A = dS^T from TMEM)
 //   dQ_i = dS K      (A = dS^T from SMEM read MN-major) -> drained by a 4th
 //                    warpgroup into fp32 dQ with TMA tensor reduce-add
-// TMEM: S^T[0,128) dP^T[128,256) dV[256,320) dK[320,384) dQ[384,448) P^T[448,512)
+// TMEM: S^T/P^T[0,128) dP^T/dS^T[128,256) dV[256,320) dK[320,384) dQ x2 [384,512)
 // 16 warps: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 elementwise, 12-15 dQ drain;
 // setmaxnreg gives the elementwise warps the register file.
-// Pipelining: S/dP of tile i+1 are issued as soon as tile i's values are in
-// registers; dS^T is double-buffered in SMEM so the elementwise warps only wait
-// for dV_i (P^T buffer) before publishing tile i+1, and the dQ drain runs on
-// its own warps, decoupled from the elementwise critical path.
+// Pipelining: the elementwise warps publish P^T_i (dV_i starts) before they
+// touch dP^T_i, and the MMA issue order dV_i S_{i+1} dQ_{i-1} | dK_i dP_{i+1}
+// keeps the next tile's scores and dP ahead of them, so they never wait on the
+// whole five-GEMM chain; the dQ drain runs on its own warps.
 #pragma once
 #include "attn_fwd.cuh"
 #include "common.cuh"
+
+#ifndef LSS_BWD_POLY
+#define LSS_BWD_POLY 1  // exponent pairs with (pair & LSS_BWD_POLY) == 0 use the FMA-pipe polynomial
+#endif                  // (7: 1 pair in 8, 3: 1 in 4, 1: 1 in 2, -1: none)
+#ifndef LSS_BWD_DQ_RED
+#define LSS_BWD_DQ_RED 0  // dQ drain: 1 = TMEM -> registers -> red.global.add.v4 (no SMEM traffic),
+#endif                    // 0 = TMEM -> SMEM staging -> TMA tensor reduce-add
+#ifndef LSS_BWD_EW_WG
+#define LSS_BWD_EW_WG 2  // elementwise warpgroups: 128/LSS_BWD_EW_WG query columns per thread
+#endif
 
 namespace lss {
 
@@ -37,7 +48,9 @@ constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;                 // dS^T tile: 2
 constexpr int ATB_STG_BYTES = 128 * 64 * 4;                      // dQ staging [128 q][64] fp32 (2 SW128 halves)
 constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES + ATB_STG_BYTES +
                          1024 + 256;
-constexpr int ATB_THREADS = 512;
+constexpr int ATB_EW = LSS_BWD_EW_WG;              // elementwise warpgroups
+constexpr int ATB_NC = 128 / ATB_EW;                // query columns per elementwise thread
+constexpr int ATB_THREADS = 128 * (2 + ATB_EW);     // control WG + EW WGs + dQ-drain WG
 
 // A query-row source of the backward: rows [row0, row0+rows) of a [B][m_src][E]
 // (Q, dO, dQ) tensor triple whose row 0 sits at global position pos0, attending
@@ -53,6 +66,8 @@ struct BwdSource {
   const float* lse2;   // [B][H][pitch] (+inf beyond the tensor's last row)
   const float* delta;  // [B][H][pitch] rowsum(dO*O)/sqrt(d)
   int pitch;
+  int m_src;           // rows of the [B][m_src][E] tensors
+  float* dq;           // fp32 [B][m_src][E], accumulated with vector reductions
 };
 struct BwdMaps {
   CUtensorMap q[ATB_MAX_SRC];
@@ -79,7 +94,7 @@ LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t
 }
 
 #ifdef LSS_BWD_TRACE
-__device__ long long g_bwd_trace[8][512];
+__device__ long long g_bwd_trace[16][512];
 #define BWD_TRACE(slot, it)                                                          \
   do {                                                                               \
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (it) < 512)         \
@@ -96,35 +111,71 @@ __device__ long long g_bwd_trace[8][512];
 // lse2 / scaled delta come from shared memory as 128-bit broadcast loads; the
 // causal / tail mask (column c visible iff c >= fv) is compiled only into the
 // MASK instance so full tiles carry no per-element predicate work.
-template <bool MASK>
-LSS_DEV void bwd_pds(const uint32_t (&sv)[64], const uint32_t (&dp)[64], uint32_t s_lse, uint32_t s_dsc,
-                     float sl2, float scale, int fv, uint32_t (&pk)[32], uint32_t (&dk)[32]) {
-  const float2 sl2v = make_float2(sl2, sl2), scv = make_float2(scale, scale);
+
+template <int N>
+LSS_DEV void tmem_ld_n(uint32_t taddr, uint32_t (&r)[N]);
+template <>
+LSS_DEV void tmem_ld_n<32>(uint32_t taddr, uint32_t (&r)[32]) { tmem_ld32(taddr, r); }
+template <>
+LSS_DEV void tmem_ld_n<64>(uint32_t taddr, uint32_t (&r)[64]) { tmem_ld64(taddr, r); }
+template <int N>
+LSS_DEV void tmem_st_n(uint32_t taddr, const uint32_t (&r)[N]);
+template <>
+LSS_DEV void tmem_st_n<16>(uint32_t taddr, const uint32_t (&r)[16]) { tmem_st16(taddr, r); }
+template <>
+LSS_DEV void tmem_st_n<32>(uint32_t taddr, const uint32_t (&r)[32]) { tmem_st32(taddr, r); }
+
+template <int NC>
+LSS_DEV void bwd_ld_vec(uint32_t saddr, float (&v)[NC]) {
 #pragma unroll
-  for (int c4 = 0; c4 < 16; ++c4) {
-    const float4 l = ld_shared_f4(s_lse + c4 * 16);
-    const float4 d = ld_shared_f4(s_dsc + c4 * 16);
+  for (int c4 = 0; c4 < NC / 4; ++c4) {
+#ifdef LSS_BWD_NOLDS
+    const float4 l = make_float4(__uint_as_float(saddr), 1.f, 2.f, 3.f);
+#else
+    const float4 l = ld_shared_f4(saddr + c4 * 16);
+#endif
+    v[4 * c4] = l.x;
+    v[4 * c4 + 1] = l.y;
+    v[4 * c4 + 2] = l.z;
+    v[4 * c4 + 3] = l.w;
+  }
+}
+
+template <bool MASK, int NC>
+LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv, uint32_t (&pk)[NC / 2]) {
+  const float2 sl2v = make_float2(sl2, sl2);
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int c = 4 * c4 + 2 * h2;
-      const float2 nl = h2 ? make_float2(-l.z, -l.w) : make_float2(-l.x, -l.y);
-      const float2 nd = h2 ? make_float2(-d.z, -d.w) : make_float2(-d.x, -d.y);
-      const float2 x = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2v, nl);
-      float2 e;
-      if (!MASK && (c4 & 3) == 0 && h2 == 0) {  // 1 pair in 8 on the FMA pipe (x <= ~0 here)
-        e = exp2_poly2(x);
-      } else {
-        e = make_float2(ex2(x.x), ex2(x.y));
-      }
-      if (MASK) {
-        e.x = (c >= fv) ? e.x : 0.f;
-        e.y = (c + 1 >= fv) ? e.y : 0.f;
-      }
-      const float2 t = ffma2(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), scv, nd);
-      const float2 ds = fmul2(e, t);
-      pk[c / 2] = pack_bf16(e.x, e.y);
-      dk[c / 2] = pack_bf16(ds.x, ds.y);
+  for (int c = 0; c < NC; c += 2) {
+    const float2 x = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2v,
+                           make_float2(-lse[c], -lse[c + 1]));
+    float2 e;
+    if (LSS_BWD_POLY >= 0 && !MASK && ((c / 2) & LSS_BWD_POLY) == 0) {  // MUFU/FMA balance
+      e = exp2_poly2(x);
+    } else {
+      e = make_float2(ex2(x.x), ex2(x.y));
     }
+    if (MASK) {
+      e.x = (c >= fv) ? e.x : 0.f;
+      e.y = (c + 1 >= fv) ? e.y : 0.f;
+    }
+    sv[c] = __float_as_uint(e.x);
+    sv[c + 1] = __float_as_uint(e.y);
+    pk[c / 2] = pack_bf16(e.x, e.y);
+  }
+}
+
+// dS^T for columns [C0, C0+NH) of the thread's slice: ds = p (dp/sqrt(d) - delta/sqrt(d))
+template <int C0, int NH, int NC>
+LSS_DEV void bwd_ds(const uint32_t (&pv)[NC], const uint32_t (&dp)[NH], const float (&dsc)[NC], float scale,
+                    uint32_t (&dk)[NC / 2]) {
+  const float2 scv = make_float2(scale, scale);
+#pragma unroll
+  for (int c = 0; c < NH; c += 2) {
+    const float2 t = ffma2(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), scv,
+                           make_float2(-dsc[C0 + c], -dsc[C0 + c + 1]));
+    const float2 ds =
+        fmul2(make_float2(__uint_as_float(pv[C0 + c]), __uint_as_float(pv[C0 + c + 1])), t);
+    dk[(C0 + c) / 2] = pack_bf16(ds.x, ds.y);
   }
 }
 
@@ -143,14 +194,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;   // [2]
   uint64_t* q_empty = bars + 3;  // [2]
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* sdp_free = bars + 6;
-  uint64_t* pds_full = bars + 7;
-  uint64_t* pv_free = bars + 8;   // dV_i (and everything before it) complete
-  uint64_t* dq_full = bars + 9;
-  uint64_t* dq_empty = bars + 10;
-  uint64_t* mma_done = bars + 11;  // one-shot: every MMA of the CTA complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* s_full = bars + 5;   // S^T_i in TMEM
+  uint64_t* p_full = bars + 6;   // P^T_i in TMEM (S^T_i consumed)
+  uint64_t* dp_full = bars + 7;  // dP^T_i in TMEM (and every earlier MMA complete)
+  uint64_t* ds_full = bars + 8;  // dS^T_i in TMEM + SMEM (dP^T_i consumed)
+  uint64_t* mma_done = bars + 9;   // one-shot: every MMA of the CTA complete
+  uint64_t* dq_full = bars + 10;   // [2] per TMEM dQ buffer
+  uint64_t* dq_empty = bars + 12;  // [2]
+  uint64_t* ds_free = bars + 14;   // [2] dQ_i has read SMEM dS buffer i&1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -203,12 +255,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
-    mbar_init(sdp_full, 1);
-    mbar_init(sdp_free, 256);
-    mbar_init(pds_full, 256);
-    mbar_init(pv_free, 1);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 128);
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128 * ATB_EW);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 128 * ATB_EW);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&dq_full[s], 1);
+      mbar_init(&dq_empty[s], 128);
+      mbar_init(&ds_free[s], 1);
+    }
     mbar_init(mma_done, 1);
     fence_barrier_init();
   }
@@ -217,11 +272,13 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320,
-                 tdQ = tmem + 384, tP = tmem + 448;
+  // P^T (bf16) overwrites S^T and dS^T overwrites dP^T: elementwise warpgroup qd
+  // reads fp32 columns [qd*NC, +NC) and writes its packed bf16 result to the first
+  // half of those same columns, so no warpgroup overwrites data another still reads.
+  const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
 
   if (warp < 4) {
-    reg_dealloc<56>();
+    reg_dealloc<(ATB_EW == 4 ? 40 : 56)>();
     if (warp == 0) {
       if (n_iter > 0) {
         // ------------------------------------------------ TMA producer (warp-uniform loop)
@@ -256,147 +313,211 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         constexpr uint32_t idKN = idesc_bf16_f32(128, 64, 0, 1);   // dV, dK (B MN-major)
         constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);    // dQ (A and B MN-major)
         const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
-        auto issue_sdp = [&](int it) {
-          const int s = it & 1;
-          mbar_wait(&q_full[s], (it >> 1) & 1);
+        // K16 step k of a bf16 TMEM operand written by the elementwise warpgroups
+        auto ew_col = [](int k) { return (uint32_t)((16 * k / ATB_NC) * ATB_NC + (16 * k % ATB_NC) / 2); };
+        auto q_stage = [&](int it) { return smem_u32(sQst + (it & 1) * ATB_QSTAGE_BYTES); };
+        auto issue_s = [&](int it) {  // S^T_it = K Q_it^T
+          mbar_wait(&q_full[it & 1], (it >> 1) & 1);
           tc_fence_after();
-          const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
-          const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
+          const uint32_t q_addr = q_stage(it);
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < ATT_D / 16; ++k)
               mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
                           smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
+            mma_commit(s_full);
+          }
+          __syncwarp();
+        };
+        auto issue_dp = [&](int it) {  // dP^T_it = V dO_it^T (stage already resident)
+          const uint32_t do_addr = q_stage(it) + ATT_TILE_BYTES;
+          if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < ATT_D / 16; ++k)
               mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
                           smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
-            mma_commit(sdp_full);
+            mma_commit(dp_full);
+          }
+          __syncwarp();
+        };
+        auto issue_dv = [&](int it) {  // dV += P^T_it dO_it once P^T_it is in TMEM
+          mbar_wait(p_full, it & 1);
+          tc_fence_after();
+          if (lane == 0) BWD_TRACE(6, it);
+          const uint32_t do_addr = q_stage(it) + ATT_TILE_BYTES;
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < ATT_BM / 16; ++k)
+              mma_bf16_ts(tdV, tS + ew_col(k), smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
+                          (it > 0 || k > 0));
+          }
+          __syncwarp();
+        };
+        auto issue_dq = [&](int it) {  // dQ_it = dS_it K into TMEM buffer it&1 once drained
+          if (it > 1) {
+            mbar_wait(&dq_empty[it & 1], ((it >> 1) - 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t ds_addr = smem_u32(sdS + (it & 1) * ATB_DS_BYTES);
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < ATT_BN / 16; ++k)
+              mma_bf16_ss(tdQ + (it & 1) * 64, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
+                          smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
+            mma_commit(&dq_full[it & 1]);
+            mma_commit(&ds_free[it & 1]);
           }
           __syncwarp();
         };
         mbar_wait(kv_full, 0);
         tc_fence_after();
-        issue_sdp(0);
+        issue_s(0);
+        issue_dp(0);
+        // Tensor-pipe order (in-order execution):
+        //   dV_i S_{i+1} | dK_i dP_{i+1} dQ_{i-1} | dV_{i+1} S_{i+2} | ...
+        // S_{i+1} follows dV_i directly (it overwrites P^T_i), so the next scores are
+        // ready while the elementwise warps still work on dS_i; dP_{i+1} follows dK_i
+        // (it overwrites dS^T_i); dQ, which only feeds the drain, runs one tile late
+        // into a double-buffered TMEM accumulator so the drain never stalls the issue.
         for (int it = 0; it < n_iter; ++it) {
-          if (it + 1 < n_iter) {
-            mbar_wait(sdp_free, it & 1);
-            if (lane == 0) BWD_TRACE(6, it);
-            issue_sdp(it + 1);
-          }
-          const int s = it & 1;
-          const uint32_t q_addr = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
-          const uint32_t do_addr = q_addr + ATT_TILE_BYTES;
-          const uint32_t ds_addr = smem_u32(sdS + s * ATB_DS_BYTES);
-          mbar_wait(pds_full, it & 1);
+          const bool more = it + 1 < n_iter;
+          issue_dv(it);
+          if (more) issue_s(it + 1);
+          if (lane == 0) BWD_TRACE(14, it);
+          mbar_wait(ds_full, it & 1);
           tc_fence_after();
           if (lane == 0) BWD_TRACE(0, it);
+          const uint32_t q_addr = q_stage(it);
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < ATT_BM / 16; ++k)  // dV += P^T dO
-              mma_bf16_ts(tdV, tP + k * 8, smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
+            for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q  (A = dS^T from TMEM)
+              mma_bf16_ts(tdK, tdP + ew_col(k), smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN,
                           (it > 0 || k > 0));
-            mma_commit(pv_free);
-#pragma unroll
-            for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q
-              mma_bf16_ss(tdK, smem_desc_sw128(ds_addr + (k >> 2) * ATT_TILE_BYTES + (k & 3) * 32, 16, 1024),
-                          smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN, (it > 0 || k > 0));
-            mma_commit(&q_empty[s]);
+            mma_commit(&q_empty[it & 1]);
           }
           __syncwarp();
-          if (it > 0) {
-            mbar_wait(dq_empty, (it - 1) & 1);  // drain has read dQ_{it-1} out of TMEM
-            tc_fence_after();
-          }
-          if (elect_one()) {
-#pragma unroll
-            for (int k = 0; k < ATT_BN / 16; ++k)  // dQ = dS K
-              mma_bf16_ss(tdQ, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
-                          smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
-            mma_commit(dq_full);
-          }
-          __syncwarp();
+          if (more) issue_dp(it + 1);
+          if (lane == 0) BWD_TRACE(15, it);
+          if (it > 0) issue_dq(it - 1);
+          if (lane == 0) BWD_TRACE(8, it);
         }
+        issue_dq(n_iter - 1);
         if (elect_one()) mma_commit(mma_done);
         __syncwarp();
       }
     }
-  } else if (warp < 12) {
-    reg_alloc<184>();
+  } else if (warp < 4 + 4 * ATB_EW) {
+    reg_alloc<(ATB_EW == 4 ? 96 : 184)>();
     // ------------------------------------------------ elementwise P^T / dS^T (+ dK/dV epilogue)
-    const int half = (warp - 4) / 4;  // query columns [64*half, 64*half+64) of each tile
+    const int qd = (warp - 4) / 4;    // query columns [NC*qd, NC*qd + NC) of each tile
     const int quad = warp % 4;
     const int t = quad * 32 + lane;   // key row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const long kpos = kpos0 + t;
     const bool row_ok = t < kv_valid;
+    constexpr int NC = ATB_NC;
     for (int it = 0; it < n_iter; ++it) {
-      const int s = it & 1;
       int src, qrow;
       locate(it, src, qrow);
       const long q0 = p.src[src].pos0 + qrow;  // global position of the tile's first query
-      const uint32_t st = smem_u32(sQst + s * ATB_QSTAGE_BYTES);
-      const uint32_t s_lse = st + 2 * ATT_TILE_BYTES + half * 256;        // lse2[q], 64 floats
-      const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + half * 256;  // delta[q]/sqrt(d)
-      mbar_wait(sdp_full, it & 1);
+      const uint32_t st = smem_u32(sQst + (it & 1) * ATB_QSTAGE_BYTES);
+      const uint32_t s_lse = st + 2 * ATT_TILE_BYTES + qd * NC * 4;        // lse2[q]
+      const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
+      // ---- P^T = 2^(S^T log2e/sqrt(d) - lse2): S_it completing implies dV_{it-1}
+      // (the previous reader of the P^T columns) completed.
+      float lse[NC];  // issued ahead of the S wait: the loads queue behind the tensor
+      mbar_wait(&q_full[it & 1], (it >> 1) & 1);  // core's SMEM operand traffic
+      bwd_ld_vec<NC>(s_lse, lse);
+      mbar_wait(s_full, it & 1);
       tc_fence_after();
-      if (t == 0 && half == 0) BWD_TRACE(1, it);
-      uint32_t sv[64], dp[64];
-      tmem_ld64(tS + lane_off + half * 64, sv);
-      tmem_ld64(tdP + lane_off + half * 64, dp);
-      tc_fence_before();
-      mbar_arrive(sdp_free);
-      if (t == 0 && half == 0) BWD_TRACE(7, it);
-      // query column c of this half is visible to key row t iff c >= fv
-      const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > q0 + half * 64);
-      uint32_t pk[32], dk[32];
-      if (need_mask) {
-        const long first_vis = kpos - q0 - half * 64;
-        const int fv = !row_ok ? 64 : (p.causal ? (int)max(0L, min(64L, first_vis)) : 0);
-        bwd_pds<true>(sv, dp, s_lse, s_dsc, p.scale_log2, p.scale, fv, pk, dk);
-      } else {
-        bwd_pds<false>(sv, dp, s_lse, s_dsc, p.scale_log2, p.scale, 0, pk, dk);
-      }
-      if (t == 0 && half == 0) BWD_TRACE(2, it);
-      if (it > 0) {
-        mbar_wait(pv_free, (it - 1) & 1);  // dV_{it-1} (and dK/dQ_{it-2}) complete
-        tc_fence_after();
-      }
-      if (t == 0 && half == 0) BWD_TRACE(3, it);
-      tmem_st32(tP + lane_off + half * 32, pk);
-      // dS^T row t, query columns [64*half, +64) -> buffer s, sub-tile `half`, SW128 K-major
+      if (t == 0 && qd == 0) BWD_TRACE(1, it);
+      uint32_t sv[NC];
+      tmem_ld_n<NC>(tS + lane_off + qd * NC, sv);
+      if (t == 0 && qd == 0) BWD_TRACE(7, it);
+      // query column c of this slice is visible to key row t iff c >= fv
+      const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > q0 + qd * NC);
       {
-        const uint32_t row = smem_u32(sdS + s * ATB_DS_BYTES + half * ATT_TILE_BYTES + t * 128);
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          st_shared_v4(row + ((c ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
+        uint32_t pk[NC / 2];
+        if (need_mask) {
+          const long first_vis = kpos - q0 - qd * NC;
+          const int fv = !row_ok ? NC : (p.causal ? (int)max(0L, min((long)NC, first_vis)) : 0);
+          bwd_p<true, NC>(sv, lse, p.scale_log2, fv, pk);
+        } else {
+          bwd_p<false, NC>(sv, lse, p.scale_log2, 0, pk);
+        }
+        if (t == 0 && qd == 0) BWD_TRACE(13, it);
+        tmem_st_n<NC / 2>(tS + lane_off + qd * NC, pk);
       }
+      tc_fence_before();
+      mbar_arrive(p_full);
+      if (t == 0 && qd == 0) BWD_TRACE(2, it);
+      // ---- dS^T = P^T (dP^T/sqrt(d) - delta/sqrt(d)): dP_it completing implies dK_{it-1}
+      // (TMEM dS^T reader) completed; dQ_{it-2} (SMEM buffer it&1 reader) runs after
+      // dP_it and signals ds_free.
+      float dsc[NC];  // delta loads issued before the dP wait (same reason as lse)
+      bwd_ld_vec<NC>(s_dsc, dsc);
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      if (t == 0 && qd == 0) BWD_TRACE(3, it);
+      {
+        uint32_t dk[NC / 2];
+        {  // dP^T in two halves keeps p, delta and dP within the register budget
+          uint32_t dp[NC / 2];
+          tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC, dp);
+          bwd_ds<0, NC / 2, NC>(sv, dp, dsc, p.scale, dk);
+        }
+        {
+          uint32_t dp[NC / 2];
+          tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
+          bwd_ds<NC / 2, NC / 2, NC>(sv, dp, dsc, p.scale, dk);
+        }
+        if (t == 0 && qd == 0) BWD_TRACE(9, it);
+        if (it > 1) mbar_wait(&ds_free[it & 1], ((it >> 1) - 1) & 1);
+        if (t == 0 && qd == 0) BWD_TRACE(11, it);
+        // dS^T row t, query columns [NC*qd, +NC) -> SW128 K-major sub-tile (64 q per sub-tile);
+        // the SMEM stores go first so they have drained by the proxy fence below
+        const int sub = (qd * NC) / 64, c0 = ((qd * NC) % 64) / 8;  // 16-byte chunk index in the 128B row
+        const uint32_t row = smem_u32(sdS + (it & 1) * ATB_DS_BYTES + sub * ATT_TILE_BYTES + t * 128);
+#pragma unroll
+        for (int c = 0; c < NC / 8; ++c)
+          st_shared_v4(row + (((c0 + c) ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
+        if (t == 0 && qd == 0) BWD_TRACE(10, it);
+        tmem_st_n<NC / 2>(tdP + lane_off + qd * NC, dk);
+      }
+      if (t == 0 && qd == 0) BWD_TRACE(12, it);
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(pds_full);
-      if (t == 0 && half == 0) BWD_TRACE(4, it);
+      mbar_arrive(ds_full);
+      if (t == 0 && qd == 0) BWD_TRACE(4, it);
     }
-    // dK (half 0) / dV (half 1) epilogue after the one-shot mma_done commit
-    float* dst = (half ? p.dv : p.dk) + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * p.ld_dkv +
-                 h * ATT_D;
+    // dK / dV epilogue after the one-shot mma_done commit: the EW warpgroups split
+    // the 2 x 64 accumulator columns
+    constexpr int EC = 128 / ATB_EW;                       // accumulator columns per thread
+    const bool is_v = qd * EC >= 64;
+    const int col0 = (qd * EC) % 64;
+    float* dst = (is_v ? p.dv : p.dk) + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * p.ld_dkv +
+                 h * ATT_D + col0;
     if (n_iter > 0) {
       mbar_wait(mma_done, 0);
       tc_fence_after();
-      uint32_t v[64];
-      tmem_ld64((half ? tdV : tdK) + lane_off, v);
-      if (row_ok) {
+      uint32_t v[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          reinterpret_cast<float4*>(dst)[i] =
-              make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                          __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+      for (int c = 0; c < EC / 32; ++c) {
+        tmem_ld32((is_v ? tdV : tdK) + lane_off + col0 + c * 32, v);
+        if (row_ok) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(dst + c * 32)[i] =
+                make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                            __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        }
       }
     } else if (row_ok) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) reinterpret_cast<float4*>(dst)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < EC / 4; ++i) reinterpret_cast<float4*>(dst)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   } else {
-    reg_dealloc<80>();
+    reg_dealloc<(ATB_EW == 4 ? 56 : 80)>();
     // ------------------------------------------------ dQ drain: TMEM -> swizzled SMEM -> TMA reduce-add
     const int quad = warp % 4;
     const int r = quad * 32 + lane;  // query row within tile == TMEM lane
@@ -404,24 +525,60 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     const bool issuer = (r == 0);
     const uint32_t row0 = smem_u32(sStage + r * 128);                      // cols [0,32)
     const uint32_t row1 = smem_u32(sStage + ATB_STG_BYTES / 2 + r * 128);  // cols [32,64)
+#if LSS_BWD_DQ_RED
+    // Shared memory bandwidth is the backward's binding resource (the tensor core
+    // reads ~144 KB of operands per tile); reducing dQ straight from registers
+    // saves the 32 KB staging write and the 32 KB TMA read per tile.
     for (int it = 0; it < n_iter; ++it) {
-      mbar_wait(dq_full, it & 1);
+      mbar_wait(&dq_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
       if (r == 0) BWD_TRACE(5, it);
-      uint32_t v[64];
-      tmem_ld64(tdQ + lane_off, v);
-      tc_fence_before();
-      mbar_arrive(dq_empty);
+      int src, q0;
+      locate(it, src, q0);
+      const int row = q0 + r;
+      const bool ok = row < p.src[src].m_src;
+      float* dst = p.src[src].dq + ((long)b * p.src[src].m_src + row) * (p.H * ATT_D) + h * ATT_D;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t v[32];
+        tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
+        if (hh == 1) {
+          tc_fence_before();
+          mbar_arrive(&dq_empty[it & 1]);
+        }
+        if (ok) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            red_add_v4(dst + hh * 32 + 4 * i, __uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                       __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        }
+      }
+    }
+#else
+    for (int it = 0; it < n_iter; ++it) {
+      mbar_wait(&dq_full[it & 1], (it >> 1) & 1);
+      tc_fence_after();
+      if (r == 0) BWD_TRACE(5, it);
       if (issuer) bulk_wait_read0();  // previous reduce has finished reading the staging tile
       named_bar_sync(1, 128);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        st_shared_v4(row0 + ((c ^ (r & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-        st_shared_v4(row1 + ((c ^ (r & 7)) << 4), v[32 + 4 * c], v[33 + 4 * c], v[34 + 4 * c], v[35 + 4 * c]);
+      for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time keeps the drain at 56 registers
+        uint32_t v[32];
+        tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
+        const uint32_t rowh = hh ? row1 : row0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          st_shared_v4(rowh + ((c ^ (r & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
       }
+      tc_fence_before();
+      mbar_arrive(&dq_empty[it & 1]);
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
+#ifndef LSS_BWD_NODQ
       if (issuer) {
+#else
+      if (issuer && it < 0) {
+#endif
         int src, q0;
         locate(it, src, q0);
         tma_reduce_add_3d(&maps.dq[src], sStage, h * ATT_D, q0, b);
@@ -429,6 +586,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         bulk_commit();
       }
     }
+#endif
     if (issuer) bulk_wait0();
   }
 

@@ -404,6 +404,8 @@ int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const l
     p.src[i].lse2 = sr.lse2;
     p.src[i].delta = sr.delta;
     p.src[i].pitch = sr.pitch;
+    p.src[i].m_src = sr.m_src;
+    p.src[i].dq = sr.grad_q;
   }
   CUtensorMap mk, mv;
   if ((rc = map_rows(&mk, k, E, ld_kv, seg_len, batch, workers, 4))) return rc;
@@ -483,7 +485,7 @@ int lss_add_f32(float* y, const float* x, long n, void* stream) {
 
 #ifdef LSS_BWD_TRACE
 extern "C" int lss_debug_bwd_trace(long long* host_out) {
-  return cudaMemcpyFromSymbol(host_out, g_bwd_trace, sizeof(long long) * 8 * 512) == cudaSuccess ? 0 : 5;
+  return cudaMemcpyFromSymbol(host_out, g_bwd_trace, sizeof(long long) * 16 * 512) == cudaSuccess ? 0 : 5;
 }
 #endif
 

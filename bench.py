@@ -282,6 +282,11 @@ def main_ours(args):
     for name in wrapped:
         setattr(Kmod, name, originals[name])
     launches = (_native.launch_count - launches0) // args.steps
+    if os.environ.get("LSS_PHASES") == "1":  # diagnostic: one extra step with a per-phase timeline
+        from paper_2311_02382_b200 import sharded as _sh
+        one_step()
+        ph = {k: round(v, 3) for k, v in _sh.last_phases.items()}
+        print(f"[phases rank {rank}] " + json.dumps(ph), file=sys.stderr, flush=True)
     coll = {k: comm.ledger.count(k) // args.steps for k in ("all-gather", "reduce-scatter", "all-reduce")}
     ms = t_start.elapsed_time(t_end) / args.steps
     # per-step device time of this rank's attention kernels (all launches of the step)

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 1
+#define LSS_ABI_VERSION 2
 
 enum lss_status {
   LSS_OK = 0,
@@ -173,6 +173,35 @@ int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const l
 
 /* y += x (fp32), used to fold a partner's dQ rows into the owner's. */
 int lss_add_f32(float* y, const float* x, long n, void* stream);
+
+/* ---- dK|dV reduce-scatter fused into the backward (NVLink / NVSwitch peer memory)
+ *
+ * Replaces the sharded.backward -> collectives.reduce_scatter pair
+ * (sharded.py:192-199, collectives.py:362-372): instead of writing the partial
+ * [dK|dV] of every key segment locally and reduce-scattering it, the kernel's
+ * epilogue stores segment g's partial into seg_dst[g] — the owner's receive
+ * slot for this rank, [batch][seg_len][ld_dkv] fp32 with dK at column h*d and dV
+ * at embed + h*d — so the transfer overlaps the attention math tile by tile.
+ * Stores leave the SM as whole 256-byte row segments.  peer marks seg_dst as
+ * peer memory; ordering comes from kernel completion followed by a device-side
+ * barrier, after which the owner sums its `workers` slots with lss_sum_slots.  Same sources
+ * and numerics as lss_attn_bwd_ex; workers <= 16. */
+int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs,
+                     int nsrc, float* const* seg_dst, int peer, long ld_dkv, int batch, int workers,
+                     int seg_len, int heads, int head_dim, int causal, void* stream);
+
+/* dst[i] = sum_{s < nslots} src[s * slot_elems + i] for i < n (fp32, n % 4 == 0). */
+int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, long n, void* stream);
+
+/* CUDA IPC for the peer buffers above: export a device pointer (any address
+ * inside an allocation) as a 64-byte handle + offset; import it in another
+ * process of the node (lazy peer access); close an imported pointer. */
+#define LSS_IPC_HANDLE_BYTES 64
+int lss_ipc_export(const void* dev_ptr, unsigned char* handle, long* offset);
+int lss_ipc_import(const unsigned char* handle, long offset, void** dev_ptr);
+int lss_ipc_close(void* dev_ptr, long offset);
+/* 1 if `device` can load/store `peer`'s memory directly (NVLink / PCIe P2P). */
+int lss_peer_access(int device, int peer);
 
 #ifdef __cplusplus
 }

@@ -9,6 +9,14 @@ layer and step the path issues exactly:
   backward  1 reduce-scatter of the packed partial [dK | dV]      (phase "backward")
   sync      1 all-reduce (sum) of the pre-scaled gradients        (phase "sync")
 
+On one NVLink/NVSwitch domain the backward reduce-scatter is FUSED into the
+attention backward kernel (lss_attn_bwd_p2p): each key segment's partial
+[dK | dV] is stored straight into its owner's receive slot through CUDA IPC
+peer memory, overlapped with the math; ``peer_addresses`` maps the slots and
+``device_barrier`` (a one-element all-reduce) orders the peers' stores before
+the owner's slot sum.  The ledger still records one "reduce-scatter" per step
+(group "<seq>:nvlink"), plus the barrier.
+
 The packed exchange is the arithmetic of the reference's ``fused=False``
 ablation (sharded.py:144-154, 192-202) done as ONE collective per direction;
 the ledger records it as one call whose element count is the full logical
@@ -71,6 +79,60 @@ class TorchDistComm:
         self.seq_name, self.world_name = seq_name, world_name
         self.seq_size = dist.get_world_size(seq_group)
         self.seq_rank = dist.get_rank(seq_group)
+        self._peers = {}
+        self._flag = None
+
+    def peer_addresses(self, t: torch.Tensor):
+        """Device addresses, in this process, of every sequence-group rank's copy of
+        ``t`` (same shape everywhere), mapped through CUDA IPC; None when some pair
+        of ranks cannot reach each other's memory (other node, no P2P, gloo/CPU)."""
+        key = (t.data_ptr(), t.numel())
+        if key in self._peers:
+            hit = self._peers[key]
+            return None if hit is None else hit[0]
+        if not t.is_cuda or self.dist.get_backend(self.seq_group) != "nccl" or self.seq_size == 1:
+            return None
+        import socket
+
+        from . import kernels as K
+
+        dev = t.device.index
+        handle, off = K.ipc_export(t)
+        info = [None] * self.seq_size
+        self.dist.all_gather_object(info, (socket.gethostname(), dev, handle, off), group=self.seq_group)
+        ok = all(h == info[self.seq_rank][0] for h, *_ in info)
+        ok = ok and all(K.peer_access(dev, d) for r, (_, d, _, _) in enumerate(info) if r != self.seq_rank)
+        addrs, opened = [], []
+        if ok:
+            try:
+                for r, (_, _, h, o) in enumerate(info):
+                    if r == self.seq_rank:
+                        addrs.append(t.data_ptr())
+                    else:
+                        a = K.ipc_import(h, o)
+                        opened.append((a, o))
+                        addrs.append(a)
+            except Exception:  # noqa: BLE001 - any rank failing disables the fused path for all
+                ok = False
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=t.device)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.seq_group)
+        if not flag.item():
+            for a, o in opened:
+                K.ipc_close(a, o)
+            self._peers[key] = None
+            return None
+        self._peers[key] = (addrs, t)  # keep the tensor alive while peers may write into it
+        return addrs
+
+    def device_barrier(self, step=0, phase="backward", layer=None):
+        """Stream-ordered barrier of the sequence group: returns (on the device) only
+        after every rank's prior work on its stream completed."""
+        self.ledger.record("barrier", self.seq_name, 1, step, phase, layer)
+        if self.seq_size == 1:
+            return
+        if self._flag is None:
+            self._flag = torch.zeros(1, dtype=torch.float32, device=torch.device("cuda", torch.cuda.current_device()))
+        self.dist.all_reduce(self._flag, group=self.seq_group)
 
     def all_gather_rows(self, full: torch.Tensor, step=0, layer=0, async_op=False):
         """In-place all-gather: ``full`` is [G, ...]; this rank's slot full[seq_rank]
@@ -156,6 +218,9 @@ class SimComm:
             for j in range(1, g):
                 acc += fulls[j][r]
             outs[r].copy_(acc)
+
+    def device_barrier(self, step=0, phase="backward", layer=None):
+        self.ledger.record("barrier", "sequence", 1, step, phase, layer)
 
     def all_reduce_sum(self, bufs, step=0):
         self.ledger.record("all-reduce", "world", bufs[0].numel(), step, "sync", None)

@@ -59,6 +59,7 @@ constexpr int ATB_THREADS = 128 * (2 + ATB_EW);     // control WG + EW WGs + dQ-
 // schedule); every key tile accumulates dK/dV from all of them in TMEM, so each
 // dK/dV row has exactly one writer.
 constexpr int ATB_MAX_SRC = 3;
+constexpr int ATB_MAX_SEG = 16;  // workers reachable through the segment table (one NVLink domain)
 struct BwdSource {
   int row0, rows;
   long pos0;
@@ -80,9 +81,17 @@ struct AttnBwdParams {
   float scale_log2;  // log2(e)/sqrt(d)
   float scale;       // 1/sqrt(d)
   BwdSource src[ATB_MAX_SRC];
-  float* dk;         // [G][B][seg_len][ld_dkv] fp32, fully written
-  float* dv;         // same layout
+  // dK|dV destination of key segment g: a [B][seg_len][ld_dkv] fp32 block, dK at
+  // column h*d and dV at dv_off + h*d, fully written.  Either one local buffer
+  // (seg_tab null: block g at dkv + g*seg_stride, the reduce-scatter input) or a
+  // table of per-segment blocks that may live in PEER memory (the owner's receive
+  // slot for this rank): the reduce-scatter then happens inside this epilogue.
+  float* dkv;
+  long seg_stride;
+  long dv_off;
   long ld_dkv;
+  int peer;                     // seg_tab entries are peer (NVLink) memory (informational)
+  float* seg_tab[ATB_MAX_SEG];  // used when seg_tab[0] != nullptr
 };
 
 LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -490,13 +499,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       mbar_arrive(ds_full);
       if (t == 0 && qd == 0) BWD_TRACE(4, it);
     }
-    // dK / dV epilogue after the one-shot mma_done commit: the EW warpgroups split
-    // the 2 x 64 accumulator columns
-    constexpr int EC = 128 / ATB_EW;                       // accumulator columns per thread
+    // dK / dV epilogue after the one-shot mma_done commit.  The tile is staged in
+    // the (now idle) dS buffers as [128 rows][dK 64 | dV 64] fp32 with 16-byte
+    // chunks XOR-swizzled by row, then each warp stores whole 256-byte row
+    // segments: full-line writes whether the destination is local HBM or the
+    // owner's receive slot across NVLink (fused reduce-scatter).
+    constexpr int EC = 128 / ATB_EW;  // accumulator columns per thread
     const bool is_v = qd * EC >= 64;
     const int col0 = (qd * EC) % 64;
-    float* dst = (is_v ? p.dv : p.dk) + (((long)g * p.B + b) * p.seg_len + kv_row0 + t) * p.ld_dkv +
-                 h * ATT_D + col0;
+    const uint32_t stage = smem_u32(sdS);
     if (n_iter > 0) {
       mbar_wait(mma_done, 0);
       tc_fence_after();
@@ -504,17 +515,24 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
 #pragma unroll
       for (int c = 0; c < EC / 32; ++c) {
         tmem_ld32((is_v ? tdV : tdK) + lane_off + col0 + c * 32, v);
-        if (row_ok) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            reinterpret_cast<float4*>(dst + c * 32)[i] =
-                make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                            __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        for (int i = 0; i < 8; ++i) {
+          const int chunk = (is_v ? 16 : 0) + (col0 + c * 32) / 4 + i;
+          st_shared_v4(stage + t * 512 + ((chunk ^ (t & 7)) << 4), v[4 * i], v[4 * i + 1], v[4 * i + 2],
+                       v[4 * i + 3]);
         }
       }
-    } else if (row_ok) {
-#pragma unroll
-      for (int i = 0; i < EC / 4; ++i) reinterpret_cast<float4*>(dst)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    named_bar_sync(2, 128 * ATB_EW);
+    {
+      float* seg = p.seg_tab[0] ? p.seg_tab[g] : p.dkv + g * p.seg_stride;
+      const int ew_warp = warp - 4;  // 0 .. 4*ATB_EW-1
+      const long col = (lane < 16 ? 0 : p.dv_off) + h * ATT_D + (lane & 15) * 4;
+      for (int r = ew_warp; r < kv_valid; r += 4 * ATB_EW) {
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (n_iter > 0) val = ld_shared_f4(stage + r * 512 + ((lane ^ (r & 7)) << 4));
+        *reinterpret_cast<float4*>(seg + ((long)b * p.seg_len + kv_row0 + r) * p.ld_dkv + col) = val;
+      }
     }
   } else {
     reg_dealloc<(ATB_EW == 4 ? 56 : 80)>();

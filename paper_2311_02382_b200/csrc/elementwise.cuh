@@ -312,4 +312,18 @@ __global__ void pad_fill_kernel(float* __restrict__ buf, long nrows, int m, int 
   buf[(idx / pad) * m_pad + m + (idx % pad)] = v;
 }
 
+// dst = sum over nslots of src[slot] (the owner's side of the fused dK|dV
+// reduce-scatter: one slot per source rank, written by the peers' backward).
+__global__ void sum_slots_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int nslots,
+                                 long slot4, long n4) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    float4 a = src[i];
+    for (int s = 1; s < nslots; ++s) {
+      const float4 b = src[s * slot4 + i];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    dst[i] = a;
+  }
+}
+
 }  // namespace lss

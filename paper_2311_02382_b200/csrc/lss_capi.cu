@@ -359,18 +359,28 @@ int lss_attn_delta(int dtype, const void* o, const void* grad_o, float* delta, i
   return check_launch("attn_delta");
 }
 
-int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
-                    float* grad_k, float* grad_v, long ld_dkv, int batch, int workers, int seg_len, int heads,
-                    int head_dim, int causal, void* stream) {
-  if (dtype != LSS_BF16) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_ex: bf16 only");
-  int rc = attn_check(dtype, batch, 1, workers, seg_len, heads, head_dim);
+// Shared launcher of the multi-source backward.  dK|dV of key segment g go to
+// seg_tab[g] (peer memory allowed) when seg_tab != null, else to
+// grad_k + g*B*seg_len*ld_dkv; dV sits dv_off elements after dK in either case.
+static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
+                           float* grad_k, long dv_off, float* const* seg_tab, int peer, long ld_dkv, int batch,
+                           int workers, int seg_len, int heads, int head_dim, int causal, void* stream) {
+  int rc = attn_check(LSS_BF16, batch, 1, workers, seg_len, heads, head_dim);
   if (rc) return rc;
-  if (!k || !v || !srcs || !grad_k || !grad_v) return fail(LSS_ERR_ARG, "attn_bwd_ex: null pointer");
+  if (!k || !v || !srcs || (!grad_k && !seg_tab)) return fail(LSS_ERR_ARG, "attn_bwd_ex: null pointer");
   if (nsrc < 1 || nsrc > ATB_MAX_SRC) return fail(LSS_ERR_ARG, "attn_bwd_ex: %d sources (1..%d)", nsrc, ATB_MAX_SRC);
   const int E = heads * head_dim;
   if (ld_kv < E || ld_dkv < E) return fail(LSS_ERR_SHAPE, "attn_bwd_ex: row strides smaller than embed");
-  if (!aligned16(k) || !aligned16(v) || !aligned16(grad_k) || !aligned16(grad_v) || ld_kv % 8 || ld_dkv % 4)
+  if (dv_off % 4 || (dv_off < E && dv_off > -E)) return fail(LSS_ERR_SHAPE, "attn_bwd_ex: dK/dV column blocks overlap");
+  if (!aligned16(k) || !aligned16(v) || ld_kv % 8 || ld_dkv % 4)
     return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_ex: 16B alignment");
+  if (seg_tab) {
+    if (workers > ATB_MAX_SEG) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_p2p: %d workers (max %d)", workers, ATB_MAX_SEG);
+    for (int g = 0; g < workers; ++g)
+      if (!seg_tab[g] || !aligned16(seg_tab[g])) return fail(LSS_ERR_ARG, "attn_bwd_p2p: segment %d destination", g);
+  } else if (!aligned16(grad_k)) {
+    return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_ex: 16B alignment");
+  }
   const float scale = 1.0f / sqrtf((float)head_dim);
   AttnBwdParams p;
   memset(&p, 0, sizeof(p));
@@ -413,12 +423,96 @@ int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const l
   p.B = batch; p.G = workers; p.seg_len = seg_len; p.H = heads; p.nsrc = nsrc; p.causal = causal;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.scale = scale;
-  p.dk = grad_k; p.dv = grad_v; p.ld_dkv = ld_dkv;
+  p.dkv = grad_k; p.seg_stride = (long)batch * seg_len * ld_dkv; p.dv_off = dv_off; p.ld_dkv = ld_dkv;
+  p.peer = peer;
+  if (seg_tab)
+    for (int g = 0; g < workers; ++g) p.seg_tab[g] = seg_tab[g];
   if ((rc = set_smem(attn_bwd_tc_kernel, ATB_SMEM))) return rc;
   const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
   dim3 grid(workers * tps, heads, batch);
   attn_bwd_tc_kernel<<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
   return check_launch("attn_bwd_tc");
+}
+
+int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
+                    float* grad_k, float* grad_v, long ld_dkv, int batch, int workers, int seg_len, int heads,
+                    int head_dim, int causal, void* stream) {
+  if (dtype != LSS_BF16) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_ex: bf16 only");
+  if (!grad_k || !grad_v || !aligned16(grad_v)) return fail(LSS_ERR_ARG, "attn_bwd_ex: dK/dV buffers");
+  return attn_bwd_launch(k, v, ld_kv, srcs, nsrc, grad_k, (long)(grad_v - grad_k), nullptr, 0, ld_dkv, batch, workers,
+                         seg_len, heads, head_dim, causal, stream);
+}
+
+int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
+                     float* const* seg_dst, int peer, long ld_dkv, int batch, int workers, int seg_len, int heads,
+                     int head_dim, int causal, void* stream) {
+  if (dtype != LSS_BF16) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_p2p: bf16 only");
+  if (!seg_dst) return fail(LSS_ERR_ARG, "attn_bwd_p2p: null segment table");
+  return attn_bwd_launch(k, v, ld_kv, srcs, nsrc, nullptr, heads * head_dim, seg_dst, peer, ld_dkv, batch, workers,
+                         seg_len, heads, head_dim, causal, stream);
+}
+
+int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, long n, void* stream) {
+  if (!dst || !src) return fail(LSS_ERR_ARG, "sum_slots: null pointer");
+  if (nslots < 1 || n < 0 || n > slot_elems || n % 4 || slot_elems % 4 || !aligned16(dst) || !aligned16(src))
+    return fail(LSS_ERR_SHAPE, "sum_slots: %d slots of %ld (n %ld) must be float4 aligned", nslots, slot_elems, n);
+  if (n == 0) return LSS_OK;
+  const int threads = 256;
+  const long n4 = n / 4;
+  const int blocks = (int)std::min<long>((n4 + threads - 1) / threads, (long)num_sms() * 8);
+  sum_slots_kernel<<<blocks, threads, 0, S(stream)>>>(reinterpret_cast<float4*>(dst),
+                                                       reinterpret_cast<const float4*>(src), nslots, slot_elems / 4, n4);
+  return check_launch("sum_slots");
+}
+
+// ------------------------------------------------------------------ peer memory (CUDA IPC)
+using PFN_getAddressRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int lss_ipc_export(const void* dev_ptr, unsigned char* handle, long* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(LSS_ERR_ARG, "ipc_export: null pointer");
+  static PFN_getAddressRange range_fn = nullptr;
+  if (!range_fn) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fp)
+      return fail(LSS_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range_fn = reinterpret_cast<PFN_getAddressRange>(fp);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(LSS_ERR_CUDA, "ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  memcpy(handle, &h, sizeof(h));
+  *offset = (long)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return LSS_OK;
+}
+
+int lss_ipc_import(const unsigned char* handle, long offset, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(LSS_ERR_ARG, "ipc_import: null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  *dev_ptr = static_cast<char*>(base) + offset;
+  return LSS_OK;
+}
+
+int lss_ipc_close(void* dev_ptr, long offset) {
+  if (!dev_ptr) return fail(LSS_ERR_ARG, "ipc_close: null pointer");
+  cudaError_t e = cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset);
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  return LSS_OK;
+}
+
+int lss_peer_access(int device, int peer) {
+  int ok = 0;
+  if (cudaDeviceCanAccessPeer(&ok, device, peer) != cudaSuccess) return 0;
+  return ok;
 }
 
 int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, const void* o,

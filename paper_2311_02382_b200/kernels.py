@@ -277,12 +277,7 @@ def attn_delta(o, grad_o, delta, *, heads, scaled=True):
          _stream())
 
 
-def attn_bwd_sources(k, v, sources, *, grad_k, grad_v, workers, seg_len, heads, causal):
-    """Multi-source backward.  sources: dicts with q, grad_o, grad_q (fp32, pre-zeroed),
-    row0, rows, pos0 (global position of tensor row 0), g_begin, g_end, lse2, delta."""
-    q0 = sources[0]["q"]
-    bsz, _, e = q0.shape
-    ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
+def _bwd_source_array(sources):
     arr = (BwdSource * len(sources))()
     for i, src in enumerate(sources):
         q = src["q"]
@@ -298,8 +293,64 @@ def attn_bwd_sources(k, v, sources, *, grad_k, grad_v, workers, seg_len, heads, 
         arr[i].lse2 = src["lse2"].data_ptr()
         arr[i].delta = src["delta"].data_ptr()
         arr[i].pitch = src["lse2"].shape[-1]
+    return arr
+
+
+def attn_bwd_sources(k, v, sources, *, grad_k=None, grad_v=None, seg_dst=None, peer=False, ld_dkv=None,
+                     workers, seg_len, heads, causal):
+    """Multi-source backward.  sources: dicts with q, grad_o, grad_q (fp32, pre-zeroed),
+    row0, rows, pos0 (global position of tensor row 0), g_begin, g_end, lse2, delta.
+
+    dK|dV go either to grad_k / grad_v ([G][B][seg][ld] local, the reduce-scatter
+    input) or, with ``seg_dst`` (G device addresses of [B][seg][ld_dkv] fp32 blocks,
+    dV at +E; ``peer`` when they are NVLink peer memory), straight to each key
+    segment's owner: the fused reduce-scatter (lss_attn_bwd_p2p)."""
+    q0 = sources[0]["q"]
+    bsz, _, e = q0.shape
+    ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
+    arr = _bwd_source_array(sources)
+    if seg_dst is not None:
+        if len(seg_dst) != workers:
+            raise ShapeError(f"seg_dst has {len(seg_dst)} entries for {workers} workers")
+        tab = (ctypes.c_void_p * workers)(*[int(a) for a in seg_dst])
+        call("lss_attn_bwd_p2p", LSS_BF16, _ptr(k), _ptr(v), ldk, arr, len(sources), tab, int(peer),
+             int(ld_dkv if ld_dkv is not None else 2 * e), bsz, workers, seg_len, heads, e // heads, int(causal),
+             _stream())
+        return
     call("lss_attn_bwd_ex", LSS_BF16, _ptr(k), _ptr(v), ldk, arr, len(sources), _ptr(grad_k), _ptr(grad_v),
          grad_k.stride(-2), bsz, workers, seg_len, heads, e // heads, int(causal), _stream())
+
+
+def sum_slots(dst, src):
+    """dst = src.sum(0) for src [S, ...] fp32 contiguous (the owner's half of the fused
+    reduce-scatter)."""
+    if not src.is_contiguous() or not dst.is_contiguous() or src[0].numel() != dst.numel():
+        raise ShapeError("sum_slots: contiguous src [S, *dst.shape] required")
+    call("lss_sum_slots", _ptr(dst), _ptr(src), src.shape[0], src[0].numel(), dst.numel(), _stream())
+    return dst
+
+
+def ipc_export(t):
+    """(64-byte handle, offset) of a device tensor's memory for another process."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_long(0)
+    call("lss_ipc_export", _ptr(t), h, ctypes.byref(off))
+    return h.raw, off.value
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device address (int) of a peer process's exported memory."""
+    p = ctypes.c_void_p(0)
+    call("lss_ipc_import", handle, offset, ctypes.byref(p))
+    return p.value
+
+
+def ipc_close(addr: int, offset: int) -> None:
+    call("lss_ipc_close", ctypes.c_void_p(addr), offset)
+
+
+def peer_access(device: int, peer: int) -> bool:
+    return bool(_native.load().lss_peer_access(device, peer))
 
 
 def add_(y, x):

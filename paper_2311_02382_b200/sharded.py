@@ -25,6 +25,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import torch
 
 from . import kernels as K
@@ -146,7 +148,7 @@ class LSSAttention:
     """
 
     def __init__(self, cfg: ModelConfig, spec: ShardSpec, *, grad_scale: float | None = None,
-                 device=None, balanced: bool | None = None):
+                 device=None, balanced: bool | None = None, fused_rs: bool | None = None):
         if spec.seq_len != cfg.seq_len:
             raise ShapeError(f"shard spec length {spec.seq_len} != config seq_len {cfg.seq_len}")
         self.cfg, self.spec = cfg, spec
@@ -202,6 +204,13 @@ class LSSAttention:
         self.g_extra = self.grads[o:o + 1]
         self.staged = None
         self.x = None
+        # fused dK|dV reduce-scatter (lss_attn_bwd_p2p): dkv_full becomes the receive
+        # buffer, slot s = rank s's partial for THIS rank's segment
+        if fused_rs is None:
+            fused_rs = os.environ.get("LSS_FUSED_RS", "1") != "0"
+        self.fused_rs = bool(fused_rs) and G > 1 and cfg.precision == "bf16"
+        self.seg_dst = None
+        self.peer_mem = False
 
     # ------------------------------------------------------------ parameters
     def load_params(self, lp: LayerParams) -> None:
@@ -249,6 +258,18 @@ class LSSAttention:
         """Unmasked (query, key) pairs per (batch, head) computed by this rank."""
         return sum(block_pairs(rows, p0, g0 * self.m, g1 * self.m, self.cfg.causal)
                    for rows, p0, g0, g1 in self.attention_work())
+
+    def bind_peers(self, addrs, peer: bool) -> None:
+        """addrs[g] = address of rank g's dkv_full (receive buffer); this rank's
+        partial for segment g goes to slot [rank] of it."""
+        slot = self.B * self.m * 2 * self.E * 4
+        self.seg_dst = [int(a) + self.spec.rank * slot for a in addrs]
+        self.peer_mem = peer
+
+    def gather_slots(self) -> None:
+        """Owner side of the fused reduce-scatter: dK|dV of this rank's segment =
+        sum of the G received slots (after the device barrier)."""
+        K.sum_slots(self.dkv_own, self.dkv_full)
 
     # ------------------------------------------------------------ point-to-point exchanges
     def xfer(self, phase: str):
@@ -337,14 +358,18 @@ class LSSAttention:
         # dWo = ctx^T . gy  (both operands MN-major), pre-scaled
         K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True, alpha=a,
                out=self.g_wo, M=E, N=E, K=B * m)
-        if self.plan.active:
+        if self.plan.active or self.seg_dst is not None:
             K.attn_delta(self.ctx, self.dctx, self.delta, heads=self.H, scaled=True)
 
     def bwd_attend(self) -> None:
         """Attention backward: dQ for the rows this rank computes, partial dK|dV for all."""
         m, E, pl, r = self.m, self.E, self.plan, self.spec.rank
         kf, vf = self.kv_full[..., :E], self.kv_full[..., E:]
-        if not pl.active:
+        if self.seg_dst is not None:  # fused reduce-scatter: dK|dV straight to the owners
+            out = dict(seg_dst=self.seg_dst, peer=self.peer_mem, ld_dkv=2 * E)
+        else:
+            out = dict(grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:])
+        if not pl.active and self.seg_dst is None:
             K.attn_bwd(self.q, kf, vf, self.ctx, self.dctx, self.lse2, workers=self.G, seg_len=m,
                        heads=self.H, offset=self.spec.offset, causal=self.cfg.causal, grad_q=self.dq,
                        grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:], delta=self.delta)
@@ -355,7 +380,7 @@ class LSSAttention:
         if pl.role == "heavy":
             srcs = [dict(own, row0=0, rows=pl.split, g_begin=pl.a, g_end=r + 1),
                     dict(own, row0=pl.split, rows=m - pl.split, g_begin=pl.b, g_end=r + 1)]
-        else:
+        elif pl.role == "light":
             self.dq_peer.zero_()
             peer = dict(q=self.q_peer, grad_o=self.do_peer, grad_q=self.dq_peer, pos0=pl.partner * m,
                         lse2=self.lsef_peer, delta=self.delta_peer)
@@ -363,8 +388,9 @@ class LSSAttention:
                     dict(peer, row0=0, rows=pl.split, g_begin=0, g_end=pl.a)]
             if pl.b > 0:
                 srcs.append(dict(peer, row0=pl.split, rows=m - pl.split, g_begin=0, g_end=pl.b))
-        K.attn_bwd_sources(kf, vf, srcs, grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:],
-                           workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal)
+        else:
+            srcs = [dict(own, row0=0, rows=m, g_begin=0, g_end=self.G if not self.cfg.causal else r + 1)]
+        K.attn_bwd_sources(kf, vf, srcs, workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal, **out)
 
     def bwd_fold(self) -> None:
         """Heavy rank of the balanced schedule: fold the partner's dQ rows in."""
@@ -440,6 +466,52 @@ def _exchange(engines, comm, phase, step, layer):
             comm.p2p(sends, recvs, e.plan.partner, step=step, phase=phase, layer=layer)
 
 
+def _bind_fused(engines, comm) -> bool:
+    """Enable the fused dK|dV reduce-scatter when every engine wants it and the
+    fabric can map the peers' receive buffers (same device in the simulation,
+    CUDA IPC over NVLink for real ranks)."""
+    if not all(e.fused_rs for e in engines):
+        return False
+    if all(e.seg_dst is not None for e in engines):
+        return True
+    if isinstance(comm, SimComm):
+        addrs = [e.dkv_full.data_ptr() for e in engines]
+        for e in engines:
+            e.bind_peers(addrs, peer=False)
+        return True
+    if not hasattr(comm, "peer_addresses"):
+        return False
+    e = engines[0]
+    addrs = comm.peer_addresses(e.dkv_full)
+    if addrs is None:
+        for e in engines:
+            e.fused_rs = False
+        return False
+    e.bind_peers(addrs, peer=True)
+    return True
+
+
+class PhaseClock:
+    """Opt-in (LSS_PHASES=1) per-phase CUDA-event timeline of lss_step; the bench
+    prints it to explain where a multi-GPU step goes."""
+
+    def __init__(self):
+        self.marks = []
+
+    def mark(self, name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((name, ev))
+
+    def report(self):
+        torch.cuda.synchronize()
+        return {n: self.marks[i - 1][1].elapsed_time(ev) for i, (n, ev) in enumerate(self.marks) if i > 0}
+
+
+_PHASES = os.environ.get("LSS_PHASES") == "1"
+last_phases: dict = {}
+
+
 def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_bwd=None):
     """One fwd+bwd(+sync) of the attention sublayer.
 
@@ -447,41 +519,68 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
     TorchDistComm (or SoloComm for one rank).  Single-process simulation: G
     engines and a SimComm.  Returns the list of (y, dx) per engine (device
     tensors, not synchronised)."""
+    global last_phases
     sim = isinstance(comm, SimComm)
+    clk = PhaseClock() if _PHASES else None
+    mark = clk.mark if clk else (lambda name: None)
     one = lambda f: f([e for e in engines]) if sim else f(engines[0])  # noqa: E731
+    fused = _bind_fused(engines, comm)
+    mark("start")
     for e, x in zip(engines, xs):
         e.fwd_project(x)
+    mark("fwd_project")
     one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer))
+    mark("all_gather")
     _exchange(engines, comm, "F1", step, layer)
+    mark("p2p_F1")
     for e in engines:
         e.fwd_attend()
+    mark("fwd_attend")
     _exchange(engines, comm, "F2", step, layer)
+    mark("p2p_F2")
     ys = [e.fwd_out() for e in engines]
+    mark("fwd_out")
     if before_bwd is not None:
         before_bwd()
     for e, gy in zip(engines, grad_ys):
         e.bwd_pre(gy)
+    mark("bwd_pre")
     _exchange(engines, comm, "B1", step, layer)
+    mark("p2p_B1")
     for e in engines:
         e.bwd_attend()
+    mark("bwd_attend")
     _exchange(engines, comm, "B2", step, layer)
+    mark("p2p_B2")
     for e in engines:
         e.bwd_fold()
-    one(lambda t: comm.reduce_scatter_rows([e.dkv_own for e in t] if sim else t.dkv_own,
-                                           [e.dkv_full for e in t] if sim else t.dkv_full, step, layer))
+    if fused:  # the reduce-scatter already happened inside the backward kernels
+        comm.ledger.record("reduce-scatter", "sequence:nvlink", engines[0].dkv_full.numel(), step, "backward",
+                           layer)
+        comm.device_barrier(step, "backward", layer)
+        for e in engines:
+            e.gather_slots()
+    else:
+        one(lambda t: comm.reduce_scatter_rows([e.dkv_own for e in t] if sim else t.dkv_own,
+                                               [e.dkv_full for e in t] if sim else t.dkv_full, step, layer))
+    mark("reduce_scatter")
     dxs = [e.bwd_project() for e in engines]
+    mark("bwd_project")
     if sync:
         one(lambda t: comm.all_reduce_sum([e.grads for e in t] if sim else t.grads, step))
+    mark("all_reduce")
+    if clk:
+        last_phases = clk.report()
     return list(zip(ys, dxs))
 
 
 def make_sim_group(cfg: ModelConfig, lp: LayerParams, workers: int, *, replicas: int = 1, device=None,
-                   balanced: bool | None = None):
+                   balanced: bool | None = None, fused_rs: bool | None = None):
     """G engines of one sequence group on one device (tests / smoke), SimComm fabric."""
     engines = []
     for r in range(workers):
         e = LSSAttention(cfg, ShardSpec(r, workers, cfg.seq_len), grad_scale=1.0 / (workers * replicas),
-                         device=device, balanced=balanced)
+                         device=device, balanced=balanced, fused_rs=fused_rs)
         e.load_params(lp)
         engines.append(e)
     return engines, SimComm(Ledger())

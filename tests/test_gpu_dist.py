@@ -18,16 +18,21 @@ def _gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("case,world", [("configA", 2), ("batch2_g3", 3), ("small_causal", 2),
-                                        ("small_noncausal", 4)])
-def test_nccl_lss_layer_matches_reference(case, world):
+@pytest.mark.parametrize("case,world,fused", [("configA", 2, 1), ("batch2_g3", 3, 1), ("small_causal", 2, 1),
+                                              ("small_noncausal", 4, 1), ("configA", 2, 0), ("small_causal", 4, 0)])
+def test_nccl_lss_layer_matches_reference(case, world, fused):
+    """fused=1: dK|dV reduce-scatter fused into the backward over NVLink peer memory
+    (lss_attn_bwd_p2p + barrier + slot sum); fused=0: the NCCL reduce-scatter."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
+    import os
+
     from conftest import free_port
 
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(ROOT / "tests" / "dist_check.py"),
-           "--case", case]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+           "--case", case, "--expect-fused", str(fused)]
+    env = dict(os.environ, LSS_FUSED_RS=str(fused))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout

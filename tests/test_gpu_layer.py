@@ -263,3 +263,39 @@ def test_balanced_causal_schedule_matches_oracle(cuda, G, m, batch):
         # the collective schedule is unchanged: 1 gather, 1 reduce-scatter, 1 all-reduce
         assert comm.ledger.count("all-gather") == 1 and comm.ledger.count("reduce-scatter") == 1
     assert nerr(results[True][0], results[False][0]) < 5e-3
+
+
+@pytest.mark.parametrize("G,m,balanced", [(2, 384, True), (4, 384, True), (4, 296, False), (3, 256, True)])
+def test_fused_reduce_scatter_matches_collective(cuda, G, m, balanced):
+    """lss_attn_bwd_p2p (dK|dV stored into the owners' slots, summed after the
+    barrier) == the reduce-scatter path: the reduced dK|dV bit for bit (both fold
+    the G partials in ascending rank order, collectives.py:362-372); y, dx and the
+    gradients to fp32 rounding (dQ is accumulated with L2 reduce-adds, whose
+    order varies between launches)."""
+    import torch
+    from oracle import lss_oracle as O
+    from paper_2311_02382_b200.model import ModelConfig, layer_params_from_arrays
+    from paper_2311_02382_b200.sharded import ShardSpec, lss_step, make_sim_group, slice_batch
+
+    e, h, seq = 128, 2, G * m
+    r = np.random.default_rng(7 * G + m)
+    p = O.init_attn_params(e, seed=3, dtype=np.float32)
+    x = torch.as_tensor(r.standard_normal((1, seq, e)).astype(np.float32), device=cuda)
+    gy = torch.as_tensor(r.standard_normal((1, seq, e)).astype(np.float32), device=cuda)
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=8, vocab=16, seq_len=seq, batch=1, causal=True)
+    lp = layer_params_from_arrays(*[getattr(p, n) for n in O.AttnParams.GRAD_ORDER], device=cuda)
+    outs = {}
+    for fused in (True, False):
+        engines, comm = make_sim_group(cfg, lp, G, device=cuda, balanced=balanced, fused_rs=fused)
+        res = lss_step(engines, comm, [slice_batch(x, ShardSpec(k, G, seq)) for k in range(G)],
+                       [slice_batch(gy, ShardSpec(k, G, seq)) for k in range(G)])
+        torch.cuda.synchronize()
+        assert all((eng.seg_dst is not None) == fused for eng in engines)
+        assert comm.ledger.count("reduce-scatter") == 1
+        assert comm.ledger.count("barrier") == (1 if fused else 0)
+        outs[fused] = ([t.clone() for o in res for t in o], [eng.grads.clone() for eng in engines],
+                       [eng.dkv_own.clone() for eng in engines])
+    for a, b in zip(outs[True][2], outs[False][2]):
+        assert torch.equal(a, b)
+    for a, b in zip(outs[True][0] + outs[True][1], outs[False][0] + outs[False][1]):
+        assert nerr(a.cpu().numpy(), b.cpu().numpy()) < 1e-5

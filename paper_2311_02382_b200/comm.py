@@ -161,9 +161,10 @@ class TorchDistComm:
             return None
         return self.dist.all_reduce(buf, group=self.world_group, async_op=async_op)
 
-    def p2p(self, sends, recvs, peer: int, step=0, phase="", layer=None):
+    def p2p(self, sends, recvs, peer: int, step=0, phase="", layer=None, async_op=False):
         """Point-to-point exchange with sequence-group member `peer` (balanced causal
-        schedule).  Stream-ordered: the current stream waits for completion."""
+        schedule).  Stream-ordered: the current stream waits for completion, or, with
+        async_op, the caller waits on the returned works when it needs the data."""
         peer_g = peer if self.seq_group is None else self.dist.get_global_rank(self.seq_group, peer)
         ops = [self.dist.P2POp(self.dist.isend, t.view(-1), peer_g, group=self.seq_group) for t in sends]
         ops += [self.dist.P2POp(self.dist.irecv, t.view(-1), peer_g, group=self.seq_group) for t in recvs]
@@ -171,8 +172,12 @@ class TorchDistComm:
             self.ledger.record("send", self.seq_name, sum(t.numel() for t in sends), step, phase, layer)
         if recvs:
             self.ledger.record("recv", self.seq_name, sum(t.numel() for t in recvs), step, phase, layer)
-        for w in self.dist.batch_isend_irecv(ops):
+        works = self.dist.batch_isend_irecv(ops)
+        if async_op:
+            return works
+        for w in works:
             w.wait()
+        return None
 
 
 class SoloComm:

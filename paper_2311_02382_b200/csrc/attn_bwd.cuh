@@ -216,6 +216,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int E = p.H * ATT_D;
+  // head-major dispatch (key tiles fastest): the ~148 resident CTAs share one or
+  // two heads' Q/dO stream in L2 (head-fastest order measured 2% slower)
   const int h = blockIdx.y;
   const int b = blockIdx.z;
   const int tps = (p.seg_len + ATT_BN - 1) / ATT_BN;

@@ -72,11 +72,15 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int E = p.H * ATT_D;
-  const int h = blockIdx.y;
-  const int b = blockIdx.z;
-  // heavy (late, causal) query tiles first
+  // 1-D grid, (batch, head) fastest: the heaviest (late, causal) query-tile pairs
+  // of EVERY head are dispatched first (longest-processing-time order), so no
+  // head's heavy tiles are left for the tail of the launch
+  const int hb = p.H * p.B;
+  const int h = (int)(blockIdx.x % hb) % p.H;
+  const int b = (int)(blockIdx.x % hb) / p.H;
+  const int unit = (int)(blockIdx.x / hb);
   const int n_pairs = (p.m + 2 * ATT_BM - 1) / (2 * ATT_BM);
-  const int pair = p.causal ? (n_pairs - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int pair = p.causal ? (n_pairs - 1 - unit) : unit;
   const int q0 = pair * 2 * ATT_BM;
   const bool has1 = q0 + ATT_BM < p.m;
   const int q_last = min(q0 + 2 * ATT_BM, p.m) - 1;  // last valid local row in this CTA

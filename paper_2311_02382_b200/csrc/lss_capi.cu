@@ -320,7 +320,7 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
   p.lse2 = lse2;
   p.lse_pitch = lse_pitch;
   if ((rc = set_smem(attn_fwd_tc_kernel, ATT_FWD_SMEM))) return rc;
-  dim3 grid((rows + 2 * ATT_BM - 1) / (2 * ATT_BM), heads, batch);
+  dim3 grid((unsigned)((rows + 2 * ATT_BM - 1) / (2 * ATT_BM)) * heads * batch);
   attn_fwd_tc_kernel<<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
   return check_launch("attn_fwd_tc");
 }

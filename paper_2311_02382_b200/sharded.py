@@ -172,6 +172,11 @@ class LSSAttention:
         self.kv_full = z(G, B, m, 2 * E, dt=ad)          # packed gather buffer (slot r = rank r)
         self.ctx = z(B, m, E, dt=ad)
         self.lse2 = z(B, H, mp)
+        # partial attention of own rows over remote segments (merged into ctx); the
+        # split lets the diagonal (local) segment run while the gather is in flight
+        self.split_fwd = G > 1 and cfg.precision == "bf16"
+        if self.split_fwd:
+            self.o_tmp, self.lse_tmp = z(B, m, E, dt=ad), z(B, H, mp)
         self.y = z(B, m, E)
         # backward
         self.gy = z(B, m, E, dt=ad)
@@ -329,6 +334,60 @@ class LSSAttention:
                 K.attn_fwd_partial(self.q_peer, kf, vf, rows=m - pl.split, row0=pl.split, offset=off,
                                    g_begin=0, g_end=pl.b, out=self.o_peer, lse2=self.lse_peer, **common)
 
+    def own_ranges(self):
+        """(row0, rows, g_begin, g_end) blocks of this rank's own query rows."""
+        m, pl, r = self.m, self.plan, self.spec.rank
+        if pl.role == "heavy":
+            return [(0, pl.split, pl.a, r + 1), (pl.split, m - pl.split, pl.b, r + 1)]
+        return [(0, m, 0, r + 1 if self.cfg.causal else self.G)]
+
+    def _fwd_common(self):
+        E = self.E
+        return (self.kv_full[..., :E], self.kv_full[..., E:],
+                dict(workers=self.G, seg_len=self.m, heads=self.H, causal=self.cfg.causal))
+
+    def fwd_attend_local(self) -> None:
+        """Own rows x own key segment: needs no remote K/V, so it runs while the
+        all-gather (and the balanced schedule's Q hand-off) are in flight."""
+        kf, vf, common = self._fwd_common()
+        r, off = self.spec.rank, self.spec.offset
+        self._ctx_written = set()
+        for row0, rows, g0, g1 in self.own_ranges():
+            if g0 <= r < g1:
+                K.attn_fwd_partial(self.q, kf, vf, rows=rows, row0=row0, offset=off, g_begin=r, g_end=r + 1,
+                                   out=self.ctx, lse2=self.lse2, **common)
+                self._ctx_written.add(row0)
+
+    def fwd_attend_remote(self) -> None:
+        """Own rows x remote key segments (after the gather), log-sum-exp merged into ctx."""
+        kf, vf, common = self._fwd_common()
+        r, off = self.spec.rank, self.spec.offset
+        for row0, rows, g0, g1 in self.own_ranges():
+            for lo, hi in ((g0, min(g1, r)), (max(g0, r + 1), g1)):
+                if lo >= hi:
+                    continue
+                if row0 not in self._ctx_written:
+                    K.attn_fwd_partial(self.q, kf, vf, rows=rows, row0=row0, offset=off, g_begin=lo, g_end=hi,
+                                       out=self.ctx, lse2=self.lse2, **common)
+                    self._ctx_written.add(row0)
+                    continue
+                K.attn_fwd_partial(self.q, kf, vf, rows=rows, row0=row0, offset=off, g_begin=lo, g_end=hi,
+                                   out=self.o_tmp, lse2=self.lse_tmp, **common)
+                K.attn_merge(self.ctx, self.lse2, self.o_tmp, self.lse_tmp, row0=row0, rows=rows, heads=self.H)
+
+    def fwd_attend_delegated(self) -> None:
+        """Light rank of the balanced schedule: the partner's delegated rows."""
+        pl = self.plan
+        if pl.role != "light":
+            return
+        kf, vf, common = self._fwd_common()
+        m, off = self.m, pl.partner * self.m
+        K.attn_fwd_partial(self.q_peer, kf, vf, rows=pl.split, row0=0, offset=off, g_begin=0, g_end=pl.a,
+                           out=self.o_peer, lse2=self.lse_peer, **common)
+        if pl.b > 0:
+            K.attn_fwd_partial(self.q_peer, kf, vf, rows=m - pl.split, row0=pl.split, offset=off, g_begin=0,
+                               g_end=pl.b, out=self.o_peer, lse2=self.lse_peer, **common)
+
     def fwd_out(self) -> torch.Tensor:
         """(merge the partner's partials,) out-projection + residual."""
         B, m, E, pl = self.B, self.m, self.E, self.plan
@@ -355,11 +414,15 @@ class LSSAttention:
                           colsum=self.g_bo, alpha=a)
         # dctx = gy . Wo^T  (Wo [in][out] is the K-major B operand)
         K.gemm(self.gy.view(B * m, E), self.staged["wo"], out=self.dctx.view(B * m, E), M=B * m, N=E, K=E)
-        # dWo = ctx^T . gy  (both operands MN-major), pre-scaled
-        K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True, alpha=a,
-               out=self.g_wo, M=E, N=E, K=B * m)
         if self.plan.active or self.seg_dst is not None:
             K.attn_delta(self.ctx, self.dctx, self.delta, heads=self.H, scaled=True)
+
+    def bwd_pre_weights(self) -> None:
+        """dWo = ctx^T . gy (both operands MN-major), pre-scaled; runs while the
+        balanced schedule's dO / lse / delta hand-off is in flight."""
+        B, m, E = self.B, self.m, self.E
+        K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True,
+               alpha=self.grad_scale, out=self.g_wo, M=E, N=E, K=B * m)
 
     def bwd_attend(self) -> None:
         """Attention backward: dQ for the rows this rank computes, partial dK|dV for all."""
@@ -449,7 +512,8 @@ class LSSAttention:
 # ---------------------------------------------------------------- drivers
 
 
-def _exchange(engines, comm, phase, step, layer):
+def _exchange(engines, comm, phase, step, layer, async_op=False):
+    """Balanced-schedule point-to-point phase; returns the pending works (async_op)."""
     if isinstance(comm, SimComm):
         for e in engines:
             sends, _ = e.xfer(phase)
@@ -459,11 +523,21 @@ def _exchange(engines, comm, phase, step, layer):
             for src, dst in zip(sends, recvs):
                 dst.copy_(src)
             comm.ledger.record("send", "sequence", sum(t.numel() for t in sends), step, phase, layer)
-        return
+        return []
+    works = []
     for e in engines:
         sends, recvs = e.xfer(phase)
         if sends or recvs:
-            comm.p2p(sends, recvs, e.plan.partner, step=step, phase=phase, layer=layer)
+            w = comm.p2p(sends, recvs, e.plan.partner, step=step, phase=phase, layer=layer, async_op=async_op)
+            works.extend(w or [])
+    return works
+
+
+def _wait(works) -> None:
+    """Make the current stream wait for pending collectives (no host block)."""
+    for w in works or []:
+        if w is not None:
+            w.wait()
 
 
 def _bind_fused(engines, comm) -> bool:
@@ -509,6 +583,7 @@ class PhaseClock:
 
 
 _PHASES = os.environ.get("LSS_PHASES") == "1"
+_NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
 last_phases: dict = {}
 
 
@@ -525,35 +600,58 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
     mark = clk.mark if clk else (lambda name: None)
     one = lambda f: f([e for e in engines]) if sim else f(engines[0])  # noqa: E731
     fused = _bind_fused(engines, comm)
+    split = all(e.split_fwd for e in engines)
     mark("start")
     for e, x in zip(engines, xs):
         e.fwd_project(x)
     mark("fwd_project")
-    one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer))
-    mark("all_gather")
-    _exchange(engines, comm, "F1", step, layer)
-    mark("p2p_F1")
-    for e in engines:
-        e.fwd_attend()
-    mark("fwd_attend")
-    _exchange(engines, comm, "F2", step, layer)
-    mark("p2p_F2")
+    gather = one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer,
+                                                **({} if sim else {"async_op": split})))
+    f1 = _exchange(engines, comm, "F1", step, layer, async_op=split)
+    if _NO_OVERLAP:  # diagnostic: serialise the collectives with the compute
+        _wait([gather] + f1)
+        gather, f1 = None, []
+    if split:
+        # diagonal segment while the gather / Q hand-off are in flight; the light
+        # rank then does the partner's rows first so their partials travel back
+        # while it finishes its own remote segments
+        for e in engines:
+            e.fwd_attend_local()
+        mark("fwd_local")
+        _wait([gather] + f1)
+        mark("all_gather")
+        for e in engines:
+            e.fwd_attend_delegated()
+        f2 = _exchange(engines, comm, "F2", step, layer, async_op=True)
+        for e in engines:
+            e.fwd_attend_remote()
+        mark("fwd_attend")
+        _wait(f2)
+        mark("p2p_F2")
+    else:
+        _wait([gather] + f1)
+        mark("all_gather")
+        for e in engines:
+            e.fwd_attend()
+        mark("fwd_attend")
+        _exchange(engines, comm, "F2", step, layer)
+        mark("p2p_F2")
     ys = [e.fwd_out() for e in engines]
     mark("fwd_out")
     if before_bwd is not None:
         before_bwd()
     for e, gy in zip(engines, grad_ys):
         e.bwd_pre(gy)
+    b1 = _exchange(engines, comm, "B1", step, layer, async_op=True)
+    for e in engines:
+        e.bwd_pre_weights()
     mark("bwd_pre")
-    _exchange(engines, comm, "B1", step, layer)
+    _wait(b1)
     mark("p2p_B1")
     for e in engines:
         e.bwd_attend()
     mark("bwd_attend")
-    _exchange(engines, comm, "B2", step, layer)
-    mark("p2p_B2")
-    for e in engines:
-        e.bwd_fold()
+    b2 = _exchange(engines, comm, "B2", step, layer, async_op=True)
     if fused:  # the reduce-scatter already happened inside the backward kernels
         comm.ledger.record("reduce-scatter", "sequence:nvlink", engines[0].dkv_full.numel(), step, "backward",
                            layer)
@@ -564,6 +662,10 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
         one(lambda t: comm.reduce_scatter_rows([e.dkv_own for e in t] if sim else t.dkv_own,
                                                [e.dkv_full for e in t] if sim else t.dkv_full, step, layer))
     mark("reduce_scatter")
+    _wait(b2)
+    for e in engines:
+        e.bwd_fold()
+    mark("p2p_B2")
     dxs = [e.bwd_project() for e in engines]
     mark("bwd_project")
     if sync:

@@ -284,6 +284,9 @@ def main_ours(args):
     launches = (_native.launch_count - launches0) // args.steps
     if os.environ.get("LSS_PHASES") == "1":  # diagnostic: one extra step with a per-phase timeline
         from paper_2311_02382_b200 import sharded as _sh
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         one_step()
         ph = {k: round(v, 3) for k, v in _sh.last_phases.items()}
         print(f"[phases rank {rank}] " + json.dumps(ph), file=sys.stderr, flush=True)

@@ -30,6 +30,8 @@
 
 namespace lss {
 
+constexpr int ATT_FWD_HGROUP = 4;  // (batch, head) slices interleaved by the forward grid
+
 constexpr int ATT_BM = 128;
 constexpr int ATT_BN = 128;
 constexpr int ATT_D = 64;
@@ -72,14 +74,19 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int E = p.H * ATT_D;
-  // 1-D grid, (batch, head) fastest: the heaviest (late, causal) query-tile pairs
-  // of EVERY head are dispatched first (longest-processing-time order), so no
-  // head's heavy tiles are left for the tail of the launch
-  const int hb = p.H * p.B;
-  const int h = (int)(blockIdx.x % hb) % p.H;
-  const int b = (int)(blockIdx.x % hb) / p.H;
-  const int unit = (int)(blockIdx.x / hb);
+  // 1-D grid in groups of ATT_FWD_HGROUP (batch, head) slices: inside a group the
+  // heaviest (late, causal) query-tile pairs of every slice go first
+  // (longest-processing-time order, so no slice leaves its heavy tiles for the
+  // tail), while only a group's K/V streams are live at once (L2-resident).
   const int n_pairs = (p.m + 2 * ATT_BM - 1) / (2 * ATT_BM);
+  const int hb = p.H * p.B;
+  const int grp_first = ((int)blockIdx.x / (ATT_FWD_HGROUP * n_pairs)) * ATT_FWD_HGROUP;
+  const int grp_size = min(ATT_FWD_HGROUP, hb - grp_first);
+  const int in_grp = (int)blockIdx.x - grp_first * n_pairs;
+  const int slice = grp_first + in_grp % grp_size;
+  const int h = slice % p.H;
+  const int b = slice / p.H;
+  const int unit = in_grp / grp_size;
   const int pair = p.causal ? (n_pairs - 1 - unit) : unit;
   const int q0 = pair * 2 * ATT_BM;
   const bool has1 = q0 + ATT_BM < p.m;

@@ -28,6 +28,14 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef LSS_FWD_SOFTMAX_REGS
+#define LSS_FWD_SOFTMAX_REGS 232  // setmaxnreg budget: 128 x CTRL + 256 x SOFTMAX <= 64K
+#define LSS_FWD_CTRL_REGS 40
+#endif
+#ifndef LSS_FWD_POLY8
+#define LSS_FWD_POLY8 3  // exponent pairs (of every 8) on the FMA-pipe polynomial; the rest on MUFU ex2
+#endif                   // (l=50112, 232-register softmax: 0 -> 7.15 ms, 2 -> 6.3, 3 -> 6.1-6.2, 4 -> 6.2)
+
 namespace lss {
 
 constexpr int ATT_FWD_HGROUP = 4;  // (batch, head) slices interleaved by the forward grid
@@ -131,7 +139,9 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   const uint32_t tO[2] = {tmem + 256, tmem + 320};
   const uint32_t tP[2] = {tmem + 384, tmem + 448};
 
-  if (warp == 0) {
+  if (warp < 4) {
+   reg_dealloc<LSS_FWD_CTRL_REGS>();  // control warpgroup: TMA, MMA, TMEM alloc
+   if (warp == 0) {
     if (n_kv > 0) {
       // ------------------------------------------------ TMA producer (warp-uniform loop)
       if (elect_one()) {
@@ -203,7 +213,9 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       }
       issue_pv(n_kv - 1);
     }
-  } else if (warp >= 4) {
+   }
+  } else {
+    reg_alloc<LSS_FWD_SOFTMAX_REGS>();  // softmax warpgroups get the register file
     // ------------------------------------------------ softmax (one row per thread)
     const int w = (warp - 4) / 4;  // query tile of this warpgroup
     const int quad = warp % 4;
@@ -253,15 +265,24 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
           m_run = m_tile;
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        float sum = 0.f;
         uint32_t pk[ATT_BN / 2];
+        float2 sum2 = make_float2(0.f, 0.f);
+        {
+          const float2 slv = make_float2(p.scale_log2, p.scale_log2), nm = make_float2(-m_use, -m_use);
 #pragma unroll
-        for (int c = 0; c < ATT_BN; c += 2) {
-          const float e0 = ex2(fmaf(s[c], p.scale_log2, -m_use));
-          const float e1 = ex2(fmaf(s[c + 1], p.scale_log2, -m_use));
-          sum += e0 + e1;
-          pk[c / 2] = pack_bf16(e0, e1);
+          for (int c = 0; c < ATT_BN; c += 2) {
+            const float2 x = ffma2(make_float2(s[c], s[c + 1]), slv, nm);  // packed FFMA2
+            float2 e;
+            if (((c / 2) & 7) < LSS_FWD_POLY8) {  // FMA-pipe share (MUFU relief)
+              e = exp2_poly2(x);
+            } else {
+              e = make_float2(ex2(x.x), ex2(x.y));
+            }
+            sum2 = fadd2(sum2, e);
+            pk[c / 2] = pack_bf16(e.x, e.y);
+          }
         }
+        const float sum = sum2.x + sum2.y;
         l_run = l_run * alpha + sum;
         if (j > 0) {
           mbar_wait(&o_full[w], (j - 1) & 1);  // PV_{j-1} done: P buffer free, O stable

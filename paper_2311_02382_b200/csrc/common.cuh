@@ -62,6 +62,9 @@ LSS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- shared memory (32-bit addresses)
+LSS_DEV void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
 LSS_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
@@ -308,7 +311,7 @@ LSS_DEV float2 fmul2(float2 a, float2 b) {
 // never a wrapped exponent: p(f) < 1 at f = 0 would underflow the exponent field
 // at -127): Cody-Waite split
 // x = j + f, |f| <= 1/2 via the 1.5*2^23 rounding trick, degree-3 minimax for
-// 2^f (max rel. error 7.5e-5, far below the bf16 rounding of P), exponent
+// 2^f (max rel. error 1.0e-4, far below the bf16 rounding of P), exponent
 // added as an integer.  Offloads MUFU.EX2, the softmax's binding unit.
 LSS_DEV float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -125.f);
@@ -316,9 +319,11 @@ LSS_DEV float2 exp2_poly2(float2 x) {
   const float2 magic = make_float2(12582912.f, 12582912.f);
   const float2 t = fadd2(x, magic);            // round(x) in the low mantissa bits
   const float2 f = fsub2(x, fsub2(t, magic));  // x - round(x)
-  float2 pl = ffma2(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
-  pl = ffma2(pl, f, make_float2(0.69326097f, 0.69326097f));
-  pl = ffma2(pl, f, make_float2(0.99992812f, 0.99992812f));
+  // minimax cubic for 2^f on [-1/2, 1/2] with p(0) = 1 pinned (2^n exact, so
+  // e.g. equal scores give exactly uniform rows); max relative error 1.0e-4
+  float2 pl = ffma2(make_float2(0.05500906f, 0.05500906f), f, make_float2(0.24221097f, 0.24221097f));
+  pl = ffma2(pl, f, make_float2(0.69328290f, 0.69328290f));
+  pl = ffma2(pl, f, make_float2(1.0f, 1.0f));
   return make_float2(__uint_as_float(__float_as_uint(pl.x) + (__float_as_uint(t.x) << 23)),
                      __uint_as_float(__float_as_uint(pl.y) + (__float_as_uint(t.y) << 23)));
 }

@@ -423,6 +423,8 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
   p.B = batch; p.G = workers; p.seg_len = seg_len; p.H = heads; p.nsrc = nsrc; p.causal = causal;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.scale = scale;
+  p.inv_scale_log2 = 1.0f / p.scale_log2;
+  p.inv_scale = sqrtf((float)head_dim);
   p.dkv = grad_k; p.seg_stride = (long)batch * seg_len * ld_dkv; p.dv_off = dv_off; p.ld_dkv = ld_dkv;
   p.peer = peer;
   if (seg_tab)
@@ -579,7 +581,7 @@ int lss_add_f32(float* y, const float* x, long n, void* stream) {
 
 #ifdef LSS_BWD_TRACE
 extern "C" int lss_debug_bwd_trace(long long* host_out) {
-  return cudaMemcpyFromSymbol(host_out, g_bwd_trace, sizeof(long long) * 16 * 512) == cudaSuccess ? 0 : 5;
+  return cudaMemcpyFromSymbol(host_out, g_bwd_trace, sizeof(long long) * 20 * 512) == cudaSuccess ? 0 : 5;
 }
 #endif
 

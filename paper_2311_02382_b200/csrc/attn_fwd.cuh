@@ -38,12 +38,27 @@
 
 namespace lss {
 
+#ifdef LSS_FWD_TRACE
+__device__ long long g_fwd_trace[8][1024];
+#define FWD_TRACE(slot, it)                                                           \
+  do {                                                                                \
+    if (blockIdx.x == 0 && (it) < 1024) g_fwd_trace[slot][it] = clock64();            \
+  } while (0)
+#else
+#define FWD_TRACE(slot, it) \
+  do {                      \
+  } while (0)
+#endif
+
 constexpr int ATT_FWD_HGROUP = 4;  // (batch, head) slices interleaved by the forward grid
 
 constexpr int ATT_BM = 128;
 constexpr int ATT_BN = 128;
 constexpr int ATT_D = 64;
-constexpr int ATT_KV_STAGES = 3;
+#ifndef LSS_FWD_KV_STAGES
+#define LSS_FWD_KV_STAGES 3
+#endif
+constexpr int ATT_KV_STAGES = LSS_FWD_KV_STAGES;  // K/V TMA ring depth
 constexpr int ATT_TILE_BYTES = ATT_BM * ATT_D * 2;  // 16 KB (Q, K or V tile)
 constexpr int ATT_FWD_THREADS = 384;
 constexpr int ATT_FWD_SMEM = (2 + 2 * ATT_KV_STAGES) * ATT_TILE_BYTES + 1024 + 256;
@@ -120,7 +135,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
     mbar_init(q_full, 1);
     for (int s = 0; s < ATT_KV_STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&kv_empty[s], has1 ? 2 : 1);  // one PV commit per query tile
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&s_full[w], 1);
@@ -163,52 +178,52 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         __syncwarp();
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (warp == 3 && has1)) {
     if (n_kv > 0) {
-      // ------------------------------------------------ MMA issuer (warp-uniform loop,
-      // one elected lane issues: descriptors stay in the uniform datapath)
+      // ------------------------------------------------ MMA issuers: warp 1 for query
+      // tile 0, warp 3 for tile 1 (warp-uniform loops, one elected lane issues).  Each
+      // tile's S / PV stream follows only its own softmax warpgroup, so the two
+      // warpgroups run a free ping-pong on the shared tensor pipe and MUFU.
       constexpr uint32_t idS = idesc_bf16_f32(ATT_BM, ATT_BN, 0, 0);
       constexpr uint32_t idO = idesc_bf16_f32(ATT_BM, ATT_D, 0, 1);
-      const int nw = has1 ? 2 : 1;
+      const int w = warp == 1 ? 0 : 1;
       const uint32_t q_addr = smem_u32(sQ);
       mbar_wait(q_full, 0);
-      auto issue_pv = [&](int jj) {
+      auto issue_pv = [&](int jj) {  // O_w += P_w(jj) V(jj)
         const int st = jj % ATT_KV_STAGES;
         const uint32_t v_addr = smem_u32(sV + st * ATT_TILE_BYTES);
-        for (int w = 0; w < nw; ++w) {
-          mbar_wait(&p_full[w], jj & 1);
-          tc_fence_after();
-          if (elect_one()) {
+        mbar_wait(&p_full[w], jj & 1);
+        tc_fence_after();
+        if (lane == 0 && w == 0) FWD_TRACE(6, jj);
+        if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < ATT_BN / 16; ++k) {
-              mma_bf16_ts(tO[w], tP[w] + k * 8, smem_desc_sw128(v_addr + k * 2048, 8192, 1024), idO,
-                          (jj > 0 || k > 0) ? 1u : 0u);
-            }
-            mma_commit(&o_full[w]);
+          for (int k = 0; k < ATT_BN / 16; ++k) {
+            mma_bf16_ts(tO[w], tP[w] + k * 8, smem_desc_sw128(v_addr + k * 2048, 8192, 1024), idO,
+                        (jj > 0 || k > 0) ? 1u : 0u);
           }
-          __syncwarp();
+          mma_commit(&o_full[w]);
+          mma_commit(&kv_empty[st]);  // this tile's reads of the K/V stage are done
         }
-        if (elect_one()) mma_commit(&kv_empty[st]);
         __syncwarp();
       };
       for (int j = 0; j < n_kv; ++j) {
         const int st = j % ATT_KV_STAGES;
         mbar_wait(&kv_full[st], (j / ATT_KV_STAGES) & 1);
         tc_fence_after();
+        if (lane == 0 && w == 0) FWD_TRACE(7, j);
         const uint32_t k_addr = smem_u32(sK + st * ATT_TILE_BYTES);
-        for (int w = 0; w < nw; ++w) {
-          if (j > 0) mbar_wait(&s_empty[w], (j - 1) & 1);
-          tc_fence_after();
-          if (elect_one()) {
+        if (j > 0) mbar_wait(&s_empty[w], (j - 1) & 1);  // S_w(j) = Q_w K(j)^T
+        tc_fence_after();
+        if (lane == 0 && w == 0) FWD_TRACE(5, j);
+        if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < ATT_D / 16; ++k) {
-              mma_bf16_ss(tS[w], smem_desc_sw128(q_addr + w * ATT_TILE_BYTES + k * 32, 16, 1024),
-                          smem_desc_sw128(k_addr + k * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
-            }
-            mma_commit(&s_full[w]);
+          for (int k = 0; k < ATT_D / 16; ++k) {
+            mma_bf16_ss(tS[w], smem_desc_sw128(q_addr + w * ATT_TILE_BYTES + k * 32, 16, 1024),
+                        smem_desc_sw128(k_addr + k * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
           }
-          __syncwarp();
+          mma_commit(&s_full[w]);
         }
+        __syncwarp();
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_kv - 1);
@@ -235,6 +250,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
                                (p.causal && key0 + ATT_BN - 1 > p.offset + tile_first_row);
         mbar_wait(&s_full[w], j & 1);
         tc_fence_after();
+        if (w == 0 && r == 0) FWD_TRACE(0, j);
         float s[ATT_BN];
         {
           uint32_t rr[64];
@@ -247,6 +263,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         }
         tc_fence_before();
         mbar_arrive(&s_empty[w]);
+        if (w == 0 && r == 0) FWD_TRACE(1, j);
         if (need_mask) {
           const long lim = p.causal ? (qpos - key0) : (long)(ATT_BN - 1);
 #pragma unroll
@@ -284,10 +301,12 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         }
         const float sum = sum2.x + sum2.y;
         l_run = l_run * alpha + sum;
+        if (w == 0 && r == 0) FWD_TRACE(2, j);
         if (j > 0) {
           mbar_wait(&o_full[w], (j - 1) & 1);  // PV_{j-1} done: P buffer free, O stable
           tc_fence_after();
         }
+        if (w == 0 && r == 0) FWD_TRACE(3, j);
         // tcgen05.ld/st are warp-collective: rescale the whole warp's rows if any row needs it
         if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
@@ -311,6 +330,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         }
         tc_fence_before();
         mbar_arrive(&p_full[w]);
+        if (w == 0 && r == 0) FWD_TRACE(4, j);
       }
       // ---------------------------------------------- epilogue
       mbar_wait(&o_full[w], (n_kv - 1) & 1);

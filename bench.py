@@ -289,6 +289,16 @@ def main_ours(args):
             dist.barrier()
         one_step()
         ph = {k: round(v, 3) for k, v in _sh.last_phases.items()}
+        torch.cuda.synchronize()
+        _sh._PHASES = False  # the phase clock synchronises; measure the plain step
+        h0 = time.perf_counter()
+        for _ in range(3):
+            one_step()
+        h1 = time.perf_counter()
+        torch.cuda.synchronize()
+        h2 = time.perf_counter()
+        ph["host_enqueue_ms"] = round((h1 - h0) / 3 * 1e3, 3)
+        ph["host_total_ms"] = round((h2 - h0) / 3 * 1e3, 3)
         print(f"[phases rank {rank}] " + json.dumps(ph), file=sys.stderr, flush=True)
     coll = {k: comm.ledger.count(k) // args.steps for k in ("all-gather", "reduce-scatter", "all-reduce")}
     ms = t_start.elapsed_time(t_end) / args.steps

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 2
+#define LSS_ABI_VERSION 3
 
 enum lss_status {
   LSS_OK = 0,
@@ -67,7 +67,7 @@ int lss_layernorm_bwd(const float* grad_xh, const float* x, const float* mean, c
                       float* grad_bias, float alpha, long rows, int embed, void* stream);
 
 /* Products of nnops.linear_fwd / linear_bwd (nnops.py:180-193):
- *   C[M][N] = alpha * A . B^T (+ bias[N]) (+ residual[M][N])
+ *   C[M][N] = act(alpha * A . B^T (+ bias[N]) (+ residual[M][N]))
  * A is [M][K] (a_mn_major=0, row stride lda) or stored [K][M] (a_mn_major=1);
  * B is [N][K] (b_mn_major=0) or stored [K][N] (b_mn_major=1).
  * dtype LSS_BF16: A/B bf16, tcgen05 GEMM; LSS_F32: A/B fp32, FFMA GEMM (fp32 out).
@@ -82,7 +82,18 @@ typedef struct lss_gemm_epilogue {
   const float* bias;     /* [N] fp32 or null */
   const float* residual; /* [M][ld_res] fp32 or null */
   long ld_res;
+  /* FFN activation (model.ffn_fwd / ffn_bwd, model.py:371-390; nnops.gelu_fwd /
+   * gelu_bwd, nnops.py:235-245):
+   *   LSS_ACT_GELU      out = gelu_tanh(v); pre (may be null) receives v, in out's dtype
+   *   LSS_ACT_GELU_BWD  out = v * gelu_tanh'(aux[row][col]); aux dtype aux_dtype */
+  int act;
+  void* pre;
+  long ld_pre;
+  const void* aux;
+  long ld_aux;
+  int aux_dtype;
 } lss_gemm_epilogue;
+enum lss_act { LSS_ACT_NONE = 0, LSS_ACT_GELU = 1, LSS_ACT_GELU_BWD = 2 };
 
 int lss_gemm(int dtype, const void* A, long lda, int a_mn_major, const void* B, long ldb,
              int b_mn_major, int M, int N, int K, const lss_gemm_epilogue* ep, void* stream);

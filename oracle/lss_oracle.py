@@ -266,6 +266,67 @@ def lss_attention(x, grad_y, p: AttnParams, n_heads, workers, causal=True):
 
 
 # --------------------------------------------------------------------------
+# FFN half of the layer: model.py:362-390, 449-452, 475-478
+# --------------------------------------------------------------------------
+
+GELU_C = math.sqrt(2.0 / math.pi)  # nnops._GELU_C
+
+
+def gelu_fwd(x):
+    """nnops.py:235-237: 0.5 x (1 + tanh(c (x + 0.044715 x^3)))."""
+    return 0.5 * x * (1.0 + np.tanh(GELU_C * (x + 0.044715 * x ** 3)))
+
+
+def gelu_bwd(x, gy):
+    """nnops.py:240-245."""
+    t = np.tanh(GELU_C * (x + 0.044715 * x ** 3))
+    return gy * (0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * GELU_C * (1.0 + 3.0 * 0.044715 * x * x))
+
+
+@dataclass
+class FfnParams:
+    """The FFN-half parameters of model.LayerParams (model.py:91-94)."""
+    ln2_gain: np.ndarray
+    ln2_bias: np.ndarray
+    w_in: np.ndarray
+    b_in: np.ndarray
+    w_out: np.ndarray
+    b_out: np.ndarray
+
+    GRAD_ORDER = ("ln2_gain", "ln2_bias", "w_in", "b_in", "w_out", "b_out")
+
+    def astype(self, dt):
+        return FfnParams(*[getattr(self, n).astype(dt) for n in self.GRAD_ORDER])
+
+
+def ffn_half(x_mid, grad_out, f: FfnParams):
+    """model.layer_fwd 449-452 (LN2 -> ffn_fwd -> residual) and layer_bwd 475-478
+    (ffn_bwd -> LN2 bwd -> grad_mid = grad_out + g_ln2), dropout 0.  Row-local,
+    so it runs on the whole (B, l, E) at once; returns (y, grad_mid, grads summed
+    over all rows)."""
+    yh, ln2 = layernorm_fwd(x_mid, f.ln2_gain, f.ln2_bias)
+    h_pre = linear_fwd(yh, f.w_in, f.b_in)  # model.py:375
+    h = gelu_fwd(h_pre)  # model.py:376
+    y = x_mid + linear_fwd(h, f.w_out, f.b_out)  # model.py:378, 452
+    g_h, g_wout, g_bout = linear_bwd(h, f.w_out, grad_out)  # model.py:385
+    g_pre = gelu_bwd(h_pre, g_h)  # model.py:387
+    g_yh, g_win, g_bin = linear_bwd(yh, f.w_in, g_pre)  # model.py:388
+    g_ln2x, g_g2, g_b2 = layernorm_bwd(ln2, f.ln2_gain, g_yh)  # model.py:476
+    return y, grad_out + g_ln2x, FfnParams(g_g2, g_b2, g_win, g_bin, g_wout, g_bout)
+
+
+def lss_layer(x, grad_y, p: AttnParams, f: FfnParams, n_heads, workers, causal=True):
+    """The complete pre-norm layer (model.layer_fwd / layer_bwd, model.py:424-499)
+    on ``workers`` ranks: the attention half as in :func:`lss_attention`, the FFN
+    half rank-local; every gradient averaged over the group (sharded.py:238)."""
+    x_mid = lss_attention(x, np.zeros_like(x), p, n_heads, workers, causal)["y"]
+    y, grad_mid, fg = ffn_half(x_mid, grad_y, f)
+    att = lss_attention(x, grad_mid, p, n_heads, workers, causal)
+    return dict(y=y, dx=att["dx"], grads=att["grads"],
+                ffn_grads=FfnParams(*[getattr(fg, n) / workers for n in FfnParams.GRAD_ORDER]))
+
+
+# --------------------------------------------------------------------------
 # Work accounting (costs.py:98 convention, extended to fwd+bwd; SURVEY §8(d))
 # --------------------------------------------------------------------------
 

@@ -45,6 +45,12 @@ class GemmEpilogue(ctypes.Structure):
         ("bias", _P),
         ("residual", _P),
         ("ld_res", _L),
+        ("act", _I),
+        ("pre", _P),
+        ("ld_pre", _L),
+        ("aux", _P),
+        ("ld_aux", _L),
+        ("aux_dtype", _I),
     ]
 
 
@@ -80,13 +86,14 @@ SIGNATURES = {
     "lss_ipc_import": [ctypes.c_char_p, _L, ctypes.POINTER(_P)],
     "lss_ipc_close": [_P, _L],
 }
+ACT_NONE, ACT_GELU, ACT_GELU_BWD = 0, 1, 2
 EXTRA = {
     "lss_abi_version": ([], _I),
     "lss_last_error": ([], ctypes.c_char_p),
     "lss_rows_pad": ([_L], _L),
     "lss_peer_access": ([_I, _I], _I),
 }
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lib = None
 

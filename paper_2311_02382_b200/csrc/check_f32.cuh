@@ -53,6 +53,12 @@ __global__ void gemm_f32_simt_kernel(const float* __restrict__ A, long sam, long
       float v = acc[i][j] * ep.alpha;
       if (ep.bias) v += ep.bias[n];
       if (ep.residual) v += ep.residual[(long)row * ep.ld_res + n];
+      if (ep.act == 1) {
+        if (ep.pre) reinterpret_cast<float*>(ep.pre)[(long)row * ep.ld_pre + n] = v;
+        v = gelu_f<false>(v);
+      } else if (ep.act == 2) {
+        v *= gelu_grad<false>(reinterpret_cast<const float*>(ep.aux)[(long)row * ep.ld_aux + n]);
+      }
       const int seg = n / ep.seg_width;
       const long col = n - (long)seg * ep.seg_width;
       reinterpret_cast<float*>(ep.out[seg])[(long)row * ep.ldo[seg] + col] = v;

@@ -31,7 +31,37 @@ struct GemmEpilogue {
   const float* bias;     // [N] or null
   const float* residual; // [M, ld_res] fp32 or null
   long ld_res;
+  // activation (applied after alpha / bias / residual), nnops.gelu_fwd / gelu_bwd
+  // (nnops.py:235-245): 1 = tanh-GeLU, pre-activation also written to pre (same
+  // dtype as out, leading dim ld_pre); 2 = multiply by GeLU'(aux[row][col])
+  int act;
+  void* pre;
+  long ld_pre;
+  const void* aux;
+  long ld_aux;
+  int aux_bf16;
 };
+
+constexpr float GELU_C = 0.7978845608028654f;  // sqrt(2/pi), nnops._GELU_C
+constexpr float GELU_K = 0.044715f;
+template <bool FAST>
+LSS_DEV float lss_tanh(float x) {
+  if (FAST) {
+    float r;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+  }
+  return tanhf(x);
+}
+template <bool FAST>
+LSS_DEV float gelu_f(float x) {
+  return 0.5f * x * (1.f + lss_tanh<FAST>(GELU_C * (x + GELU_K * x * x * x)));
+}
+template <bool FAST>
+LSS_DEV float gelu_grad(float x) {
+  const float t = lss_tanh<FAST>(GELU_C * (x + GELU_K * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * GELU_C * (1.f + 3.f * GELU_K * x * x);
+}
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN = 256;
@@ -194,6 +224,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             v[4 * i + 1] += t.y;
             v[4 * i + 2] += t.z;
             v[4 * i + 3] += t.w;
+          }
+        }
+        if (ep.act == 1) {  // tanh-GeLU; the pre-activation is kept for the backward
+          if (ep.pre) {
+            if (ep.out_bf16) {
+              uint4* pp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.pre) + (long)row * ep.ld_pre + n);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                pp[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+            } else {
+              float4* pp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.pre) + (long)row * ep.ld_pre + n);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = gelu_f<true>(v[i]);
+        } else if (ep.act == 2) {  // chain rule through GeLU at the stored pre-activation
+          if (ep.aux_bf16) {
+            const uint4* ap = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(ep.aux) +
+                                                             (long)row * ep.ld_aux + n);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 t = ap[i];
+              const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                v[8 * i + 2 * j] *= gelu_grad<true>(__uint_as_float(w[j] << 16));
+                v[8 * i + 2 * j + 1] *= gelu_grad<true>(__uint_as_float(w[j] & 0xFFFF0000u));
+              }
+            }
+          } else {
+            const float4* ap = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ep.aux) +
+                                                               (long)row * ep.ld_aux + n);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 t = ap[i];
+              v[4 * i] *= gelu_grad<true>(t.x);
+              v[4 * i + 1] *= gelu_grad<true>(t.y);
+              v[4 * i + 2] *= gelu_grad<true>(t.z);
+              v[4 * i + 3] *= gelu_grad<true>(t.w);
+            }
           }
         }
         const int seg = n / ep.seg_width;

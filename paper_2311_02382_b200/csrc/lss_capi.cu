@@ -158,6 +158,20 @@ int lss_gemm(int dtype, const void* A, long lda, int a_mn_major, const void* B, 
   ep.bias = ep_in->bias;
   ep.residual = ep_in->residual;
   ep.ld_res = ep_in->ld_res;
+  ep.act = ep_in->act;
+  ep.pre = ep_in->pre;
+  ep.ld_pre = ep_in->ld_pre;
+  ep.aux = ep_in->aux;
+  ep.ld_aux = ep_in->ld_aux;
+  ep.aux_bf16 = ep_in->aux_dtype == LSS_BF16;
+  if (ep.act < LSS_ACT_NONE || ep.act > LSS_ACT_GELU_BWD) return fail(LSS_ERR_ARG, "gemm: activation %d", ep.act);
+  if (ep.act == LSS_ACT_GELU_BWD && !ep.aux) return fail(LSS_ERR_ARG, "gemm: GeLU backward needs the pre-activation");
+  if (ep.act == LSS_ACT_GELU && ep.pre && (ep.ld_pre < N || !aligned16(ep.pre) || ep.ld_pre % 8))
+    return fail(LSS_ERR_SHAPE, "gemm: pre-activation buffer ld %ld / alignment", ep.ld_pre);
+  if (ep.act == LSS_ACT_GELU_BWD && (ep.ld_aux < N || !aligned16(ep.aux) || ep.ld_aux % 8))
+    return fail(LSS_ERR_SHAPE, "gemm: aux ld %ld / alignment", ep.ld_aux);
+  if (ep.act != LSS_ACT_NONE && (ep.seg_width != N))
+    return fail(LSS_ERR_UNSUPPORTED, "gemm: activation epilogue with split output segments");
   const int nseg = (N + ep.seg_width - 1) / ep.seg_width;
   if (nseg > 3) return fail(LSS_ERR_SHAPE, "gemm: %d output segments (max 3)", nseg);
   for (int s = 0; s < nseg; ++s)
@@ -165,6 +179,7 @@ int lss_gemm(int dtype, const void* A, long lda, int a_mn_major, const void* B, 
 
   if (dtype == LSS_F32) {
     if (ep.out_bf16) return fail(LSS_ERR_UNSUPPORTED, "gemm f32: bf16 output");
+    if (ep.act == LSS_ACT_GELU_BWD && ep.aux_bf16) return fail(LSS_ERR_UNSUPPORTED, "gemm f32: bf16 aux");
     const float* a = reinterpret_cast<const float*>(A);
     const float* b = reinterpret_cast<const float*>(B);
     const long sam = a_mn_major ? 1 : lda, sak = a_mn_major ? lda : 1;

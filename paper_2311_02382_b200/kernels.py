@@ -92,10 +92,13 @@ def layernorm_bwd(grad_xh, x, mean, rstd, gain, grad_res=None, grad_x=None, grad
 
 
 def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_dtype=torch.float32, alpha=1.0,
-         bias=None, residual=None, seg_width=0, M=None, N=None, K=None, lda=None, ldb=None):
-    """C = alpha * A.B^T (+bias) (+residual) with A [M,K] or (a_mn_major) [K,M],
+         bias=None, residual=None, seg_width=0, M=None, N=None, K=None, lda=None, ldb=None,
+         act=None, pre=None, aux=None):
+    """C = act(alpha * A.B^T (+bias) (+residual)) with A [M,K] or (a_mn_major) [K,M],
     B [N,K] or (b_mn_major) [K,N].  ``out`` may be a tensor or a list of up to 3
-    (tensor, ld) column segments of ``seg_width`` columns."""
+    (tensor, ld) column segments of ``seg_width`` columns.  ``act``: None,
+    "gelu" (tanh GeLU; ``pre`` receives the pre-activation) or "gelu_bwd"
+    (multiply by GeLU' of ``aux``, the stored pre-activation)."""
     dt = LSS_BF16 if a.dtype == torch.bfloat16 else LSS_F32
     if b.dtype != a.dtype:
         raise ShapeError("gemm operands must share a dtype")
@@ -119,6 +122,18 @@ def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_dtype=torch.
     ep.bias = bias.data_ptr() if bias is not None else None
     ep.residual = residual.data_ptr() if residual is not None else None
     ep.ld_res = residual.shape[-1] if residual is not None else 0
+    if act is not None:
+        codes = {"gelu": _native.ACT_GELU, "gelu_bwd": _native.ACT_GELU_BWD}
+        if act not in codes:
+            raise ValueError(f"unknown activation {act!r}")
+        ep.act = codes[act]
+        if pre is not None:
+            if pre.dtype != segs[0][0].dtype:
+                raise ShapeError("pre-activation buffer must have the output dtype")
+            ep.pre, ep.ld_pre = pre.data_ptr(), pre.shape[-1]
+        if aux is not None:
+            ep.aux, ep.ld_aux = aux.data_ptr(), aux.shape[-1]
+            ep.aux_dtype = LSS_BF16 if aux.dtype == torch.bfloat16 else LSS_F32
     call("lss_gemm", dt, _ptr(a), lda, int(a_mn_major), _ptr(b), ldb, int(b_mn_major), M, N, K,
          ctypes.byref(ep), _stream())
     return out

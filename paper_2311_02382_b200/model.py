@@ -1,4 +1,5 @@
-"""Attention half of the reference's layer API (seqpar.model), on B200 kernels.
+"""The reference's layer API (seqpar.model) on B200 kernels: the attention half
+(the hot path) and the FFN half.
 
 Same names, argument meaning and error behaviour as the reference
 (/root/reference/pkg/src/seqpar/model.py) for the hot path:
@@ -6,7 +7,9 @@ Same names, argument meaning and error behaviour as the reference
   ModelConfig (model.py:39-80), LinearParams (nnops.py:172-177),
   linear3 / linear3_bwd (model.py:237-245), norm3 / norm3_bwd (248-257),
   scores_fwd / scores_bwd (280-359), local_kv_fwd / local_kv_bwd (413-421),
-  layer_fwd / layer_bwd restricted to the attention half (442-448, 479-486).
+  ffn_fwd / ffn_bwd (362-390), layer_fwd / layer_bwd (424-499): the attention
+  half always, plus LN2 -> FFN -> residual when the LayerParams carry the FFN
+  weights.
 
 Arrays are torch CUDA tensors.  ``precision`` selects the kernel family:
 "bf16" (tcgen05 path, bf16 operands / fp32 accumulation, the default) or
@@ -16,9 +19,9 @@ fp32 in both.  The reference caches the full probability matrix P per
 recomputes P (flash-attention), so ``cache.attn`` does not exist -- use
 ``probabilities()`` to materialise P for a check.
 
-Out of scope here: dropout > 0 (raises), the FFN half of the
-layer, embeddings/head -- every BASELINE config runs dropout 0 and the hot
-path is the attention sublayer.
+Out of scope here: dropout > 0 (raises), embeddings/head --
+every BASELINE config runs dropout 0 and the hot path is the attention
+sublayer.
 """
 
 from __future__ import annotations
@@ -82,7 +85,8 @@ class LinearParams:
 
 @dataclass
 class LayerParams:
-    """Attention half of model.LayerParams (model.py:83-94)."""
+    """model.LayerParams (model.py:83-94).  The FFN half (ln2_*, ff_in, ff_out) is
+    optional: without it the layer is its attention half (the hot path)."""
 
     ln1_gain: torch.Tensor
     ln1_bias: torch.Tensor
@@ -90,21 +94,41 @@ class LayerParams:
     attn_k: LinearParams
     attn_v: LinearParams
     attn_out: LinearParams
+    ln2_gain: Optional[torch.Tensor] = None
+    ln2_bias: Optional[torch.Tensor] = None
+    ff_in: Optional[LinearParams] = None
+    ff_out: Optional[LinearParams] = None
+
+    @property
+    def has_ffn(self) -> bool:
+        return self.ff_in is not None
 
     def named_arrays(self):
-        """Same relative order as Parameters.named_arrays (model.py:118-127)."""
+        """Same relative order as Parameters.named_arrays (model.py:118-133)."""
         yield "ln1_gain", self.ln1_gain
         yield "ln1_bias", self.ln1_bias
         for n in ("attn_q", "attn_k", "attn_v", "attn_out"):
             p = getattr(self, n)
             yield f"{n}.weight", p.weight
             yield f"{n}.bias", p.bias
+        if self.has_ffn:
+            yield "ln2_gain", self.ln2_gain
+            yield "ln2_bias", self.ln2_bias
+            for n in ("ff_in", "ff_out"):
+                p = getattr(self, n)
+                yield f"{n}.weight", p.weight
+                yield f"{n}.bias", p.bias
 
 
-def layer_params_from_arrays(ln1_gain, ln1_bias, wq, bq, wk, bk, wv, bv, wo, bo, device="cuda"):
+def layer_params_from_arrays(ln1_gain, ln1_bias, wq, bq, wk, bk, wv, bv, wo, bo, device="cuda", *,
+                             ln2_gain=None, ln2_bias=None, w_in=None, b_in=None, w_out=None, b_out=None):
     t = lambda a: torch.as_tensor(a, dtype=torch.float32, device=device).contiguous()  # noqa: E731
-    return LayerParams(t(ln1_gain), t(ln1_bias), LinearParams(t(wq), t(bq)), LinearParams(t(wk), t(bk)),
-                       LinearParams(t(wv), t(bv)), LinearParams(t(wo), t(bo)))
+    lp = LayerParams(t(ln1_gain), t(ln1_bias), LinearParams(t(wq), t(bq)), LinearParams(t(wk), t(bk)),
+                     LinearParams(t(wv), t(bv)), LinearParams(t(wo), t(bo)))
+    if w_in is not None:
+        lp.ln2_gain, lp.ln2_bias = t(ln2_gain), t(ln2_bias)
+        lp.ff_in, lp.ff_out = LinearParams(t(w_in), t(b_in)), LinearParams(t(w_out), t(b_out))
+    return lp
 
 
 def _check_dropout(cfg: ModelConfig, policy) -> None:
@@ -267,7 +291,71 @@ def probabilities(cache: ScoreCache, q, cfg: ModelConfig) -> torch.Tensor:
     return p
 
 
-# ------------------------------------------------------------------ layer (attention half)
+# ------------------------------------------------------------------ FFN half
+
+
+@dataclass
+class FfnCache:
+    """model.FfnCache (model.py:365-369) without dropout: yh, h_pre, h (operand dtype)."""
+
+    yh: torch.Tensor
+    h_pre: torch.Tensor
+    h: torch.Tensor
+
+
+def ffn_fwd(yh: torch.Tensor, lp: LayerParams, cfg: ModelConfig, policy=None, layer: int = 0, residual=None):
+    """model.ffn_fwd (model.py:371-378): ff_in -> tanh-GeLU -> ff_out.  The GeLU
+    runs in the ff_in GEMM's epilogue (which also keeps the pre-activation for
+    the backward); ``residual`` (fp32, optional) is added in the ff_out epilogue
+    (model.py:452's x_mid + ff)."""
+    _check_dropout(cfg, policy)
+    b, m, e = yh.shape
+    ff = lp.ff_in.weight.shape[1]
+    if lp.ff_in.weight.shape[0] != e or lp.ff_out.weight.shape != (ff, e):
+        raise ShapeError(f"ffn weights {tuple(lp.ff_in.weight.shape)} / {tuple(lp.ff_out.weight.shape)} "
+                         f"do not match embed {e}")
+    ya = _as_act(yh, cfg).contiguous().view(b * m, e)
+    ad = cfg.act_dtype
+    h_pre = torch.empty(b * m, ff, dtype=ad, device=yh.device)
+    h = torch.empty(b * m, ff, dtype=ad, device=yh.device)
+    K.gemm(ya, _as_act(lp.ff_in.weight, cfg).contiguous(), b_mn_major=True, bias=lp.ff_in.bias, out=h,
+           act="gelu", pre=h_pre, M=b * m, N=ff, K=e)
+    out = torch.empty(b * m, e, dtype=torch.float32, device=yh.device)
+    K.gemm(h, _as_act(lp.ff_out.weight, cfg).contiguous(), b_mn_major=True, bias=lp.ff_out.bias, out=out,
+           residual=None if residual is None else residual.to(torch.float32).contiguous().view(b * m, e),
+           M=b * m, N=e, K=ff)
+    return out.view(b, m, e), FfnCache(ya, h_pre, h)
+
+
+def ffn_bwd(cache: FfnCache, lp: LayerParams, grad_out: torch.Tensor, cfg: ModelConfig, policy=None):
+    """model.ffn_bwd (model.py:381-390) -> (grad_yh, (ff_in_wg, ff_in_bg, ff_out_wg, ff_out_bg)).
+    The GeLU derivative at the stored pre-activation is applied in the epilogue of
+    the GEMM that produces grad_h."""
+    _check_dropout(cfg, policy)
+    b, m, e = grad_out.shape
+    M, ff = cache.h.shape
+    ad = cfg.act_dtype
+    g32 = grad_out.to(torch.float32).contiguous().view(M, e)
+    g = torch.empty(M, e, dtype=ad, device=g32.device)
+    ff_out_bg = torch.zeros(e, dtype=torch.float32, device=g32.device)
+    K.cat_cast_colsum([(g32, e, e)], M, dst=g, colsum=ff_out_bg)
+    w_out = _as_act(lp.ff_out.weight, cfg).contiguous()  # [ff][E] = [N][K] for g . W_out^T
+    g_pre32 = torch.empty(M, ff, dtype=torch.float32, device=g32.device)
+    K.gemm(g, w_out, out=g_pre32, act="gelu_bwd", aux=cache.h_pre, M=M, N=ff, K=e)
+    ff_out_wg = torch.empty(ff, e, dtype=torch.float32, device=g32.device)
+    K.gemm(cache.h, g, a_mn_major=True, b_mn_major=True, out=ff_out_wg, M=ff, N=e, K=M)  # h^T . g
+    g_pre = torch.empty(M, ff, dtype=ad, device=g32.device)
+    ff_in_bg = torch.zeros(ff, dtype=torch.float32, device=g32.device)
+    K.cat_cast_colsum([(g_pre32, ff, ff)], M, dst=g_pre, colsum=ff_in_bg)
+    w_in = _as_act(lp.ff_in.weight, cfg).contiguous()  # [E][ff] = [N][K] for g_pre . W_in^T
+    grad_yh = torch.empty(M, e, dtype=torch.float32, device=g32.device)
+    K.gemm(g_pre, w_in, out=grad_yh, M=M, N=e, K=ff)
+    ff_in_wg = torch.empty(e, ff, dtype=torch.float32, device=g32.device)
+    K.gemm(cache.yh, g_pre, a_mn_major=True, b_mn_major=True, out=ff_in_wg, M=e, N=ff, K=M)  # yh^T . g_pre
+    return grad_yh.view(b, m, e), (ff_in_wg, ff_in_bg, ff_out_wg, ff_out_bg)
+
+
+# ------------------------------------------------------------------ layer
 
 
 def local_kv_fwd(xh: torch.Tensor, lp: LayerParams, cfg: ModelConfig):
@@ -293,28 +381,40 @@ class LayerCache:
     v: torch.Tensor
     scores: ScoreCache
     ctx: torch.Tensor
+    ln2: Optional[NormCache] = None
+    ffn: Optional[FfnCache] = None
 
 
 def layer_fwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, x: torch.Tensor, offset: int,
               kv_fwd: Optional[Callable] = None, counters=None):
-    """Attention half of model.layer_fwd (model.py:442-448):
-    norm -> kv_fwd -> q -> scores -> out-projection -> residual."""
+    """model.layer_fwd (model.py:424-456): norm -> kv_fwd -> q -> scores ->
+    out-projection -> residual, then (when lp has the FFN half) LN2 -> FFN -> residual."""
     _check_dropout(cfg, policy)
     kv_fwd = kv_fwd or (lambda xh, lp_: local_kv_fwd(xh, lp_, cfg))
     xh, ln1 = norm3(x, lp.ln1_gain, lp.ln1_bias, cfg, out_dtype=cfg.act_dtype)
     k, v, kv_ctx = kv_fwd(xh, lp)
     q = linear3(xh, lp.attn_q, cfg, cfg.act_dtype)
     ctx, sc = scores_fwd(q, k, v, offset, cfg, policy, layer, counters)
-    x_out = linear3(ctx, lp.attn_out, cfg) + x
-    return x_out, LayerCache(offset, ln1, xh, kv_ctx, q, k, v, sc, ctx)
+    x_mid = linear3(ctx, lp.attn_out, cfg) + x
+    if not lp.has_ffn:
+        return x_mid, LayerCache(offset, ln1, xh, kv_ctx, q, k, v, sc, ctx)
+    yh, ln2 = norm3(x_mid, lp.ln2_gain, lp.ln2_bias, cfg, out_dtype=cfg.act_dtype)
+    x_out, fc = ffn_fwd(yh, lp, cfg, policy, layer, residual=x_mid)
+    return x_out, LayerCache(offset, ln1, xh, kv_ctx, q, k, v, sc, ctx, ln2, fc)
 
 
 def layer_bwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, cache: LayerCache,
               grad_out: torch.Tensor, kv_bwd: Optional[Callable] = None):
-    """Attention half of model.layer_bwd (model.py:479-486) -> (grad_in, grads LayerParams)."""
+    """model.layer_bwd (model.py:459-499) -> (grad_in, grads LayerParams)."""
     _check_dropout(cfg, policy)
     kv_bwd = kv_bwd or (lambda kv_ctx, lp_, gk, gv: local_kv_bwd(kv_ctx, lp_, gk, gv, cfg))
-    grad_mid = grad_out.to(torch.float32).contiguous()
+    grad_out = grad_out.to(torch.float32).contiguous()
+    ffn_grads = None
+    if lp.has_ffn:  # model.py:474-477
+        grad_yh, ffn_grads = ffn_bwd(cache.ffn, lp, grad_out, cfg, policy)
+        grad_mid, ln2_gg, ln2_bg = norm3_bwd(cache.ln2, lp.ln2_gain, grad_yh, grad_res=grad_out)
+    else:
+        grad_mid = grad_out
     grad_ctx, out_wg, out_bg = linear3_bwd(cache.ctx, lp.attn_out, grad_mid, cfg)
     gq, gk, gv = scores_bwd(cache.scores, cache.q, cache.k, cache.v, grad_ctx, cfg, policy)
     gxq, q_wg, q_bg = linear3_bwd(cache.xh, lp.attn_q, gq, cfg)
@@ -323,4 +423,8 @@ def layer_bwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, cache: Laye
     g_in, g_gain, g_bias = norm3_bwd(cache.ln1, lp.ln1_gain, grad_xh, grad_res=grad_mid)
     grads = LayerParams(g_gain, g_bias, LinearParams(q_wg, q_bg), LinearParams(k_wg, k_bg),
                         LinearParams(v_wg, v_bg), LinearParams(out_wg, out_bg))
+    if ffn_grads is not None:
+        ff_in_wg, ff_in_bg, ff_out_wg, ff_out_bg = ffn_grads
+        grads.ln2_gain, grads.ln2_bias = ln2_gg, ln2_bg
+        grads.ff_in, grads.ff_out = LinearParams(ff_in_wg, ff_in_bg), LinearParams(ff_out_wg, ff_out_bg)
     return g_in, grads

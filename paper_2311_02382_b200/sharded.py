@@ -148,7 +148,8 @@ class LSSAttention:
     """
 
     def __init__(self, cfg: ModelConfig, spec: ShardSpec, *, grad_scale: float | None = None,
-                 device=None, balanced: bool | None = None, fused_rs: bool | None = None):
+                 device=None, balanced: bool | None = None, fused_rs: bool | None = None,
+                 with_ffn: bool = False):
         if spec.seq_len != cfg.seq_len:
             raise ShapeError(f"shard spec length {spec.seq_len} != config seq_len {cfg.seq_len}")
         self.cfg, self.spec = cfg, spec
@@ -197,7 +198,12 @@ class LSSAttention:
             self.do_peer, self.lsef_peer, self.delta_peer = z(B, m, E, dt=ad), z(B, H, mp), z(B, H, mp)
             self.dq_peer = z(B, m, E)
         # gradients, one flat buffer: [Wq Wk Wv | Wo | bq bk bv | bo | ln_g | ln_b | extra]
-        n = 4 * E * E + 6 * E + 1
+        # (+ with_ffn, 64-byte aligned: [ln2_g | ln2_b | W_in | b_in | W_out | b_out])
+        F = cfg.ff_dim
+        self.with_ffn = with_ffn
+        n_attn = 4 * E * E + 6 * E + 1
+        ffn0 = (n_attn + 15) // 16 * 16  # FFN grads start 64-byte aligned (vectorised epilogues)
+        n = ffn0 + (2 * E * F + F + 3 * E) if with_ffn else n_attn
         self.grads = torch.zeros(n, dtype=f32, device=dev)
         o = 0
         self.g_wqkv = self.grads[o:o + 3 * E * E]; o += 3 * E * E
@@ -206,7 +212,25 @@ class LSSAttention:
         self.g_bo = self.grads[o:o + E]; o += E
         self.g_ln_g = self.grads[o:o + E]; o += E
         self.g_ln_b = self.grads[o:o + E]; o += E
-        self.g_extra = self.grads[o:o + 1]
+        self.g_extra = self.grads[o:o + 1]; o += 1
+        if with_ffn:  # LN2 + FFN half: rank-local, same all-reduce
+            o = ffn0
+            self.g_ln2_g = self.grads[o:o + E]; o += E
+            self.g_ln2_b = self.grads[o:o + E]; o += E
+            self.g_win = self.grads[o:o + E * F].view(E, F); o += E * F
+            self.g_bin = self.grads[o:o + F]; o += F
+            self.g_wout = self.grads[o:o + F * E].view(F, E); o += F * E
+            self.g_bout = self.grads[o:o + E]; o += E
+            M = B * m
+            self.x_mid = z(B, m, E)
+            self.mean2, self.rstd2 = z(M), z(M)
+            self.yh = z(B, m, E, dt=ad)
+            self.h_pre, self.h = z(M, F, dt=ad), z(M, F, dt=ad)
+            self.y_out = z(B, m, E)
+            self.g_out = z(M, E, dt=ad)
+            self.g_pre32, self.g_pre = z(M, F), z(M, F, dt=ad)
+            self.g_yh = z(M, E)
+            self.grad_mid = z(B, m, E)
         self.staged = None
         self.x = None
         # fused dK|dV reduce-scatter (lss_attn_bwd_p2p): dkv_full becomes the receive
@@ -224,6 +248,12 @@ class LSSAttention:
         self.staged = K.stage_weights(lp.attn_q.weight, lp.attn_k.weight, lp.attn_v.weight,
                                       lp.attn_out.weight, lp.attn_q.bias, lp.attn_k.bias,
                                       lp.attn_v.bias, self.cfg.precision, bufs=self.staged)
+        if self.with_ffn:
+            if not lp.has_ffn:
+                raise ShapeError("engine built with_ffn but the LayerParams carry no FFN half")
+            ad = self.cfg.act_dtype
+            self.w_in = lp.ff_in.weight.to(ad).contiguous()    # [E][F]: B operand N-major / K-major
+            self.w_out = lp.ff_out.weight.to(ad).contiguous()  # [F][E]
 
     def grad_views(self) -> dict:
         """Gradients by reference name (model.LayerParams field order)."""
@@ -236,15 +266,22 @@ class LSSAttention:
             "attn_k.weight": w[1], "attn_k.bias": b[1],
             "attn_v.weight": w[2], "attn_v.bias": b[2],
             "attn_out.weight": self.g_wo, "attn_out.bias": self.g_bo,
-        }
+        } | ({"ln2_gain": self.g_ln2_g, "ln2_bias": self.g_ln2_b, "ff_in.weight": self.g_win,
+              "ff_in.bias": self.g_bin, "ff_out.weight": self.g_wout, "ff_out.bias": self.g_bout}
+             if self.with_ffn else {})
 
     def grad_params(self) -> LayerParams:
         g = self.grad_views()
-        return LayerParams(g["ln1_gain"], g["ln1_bias"],
-                           LinearParams(g["attn_q.weight"], g["attn_q.bias"]),
-                           LinearParams(g["attn_k.weight"], g["attn_k.bias"]),
-                           LinearParams(g["attn_v.weight"], g["attn_v.bias"]),
-                           LinearParams(g["attn_out.weight"], g["attn_out.bias"]))
+        lp = LayerParams(g["ln1_gain"], g["ln1_bias"],
+                         LinearParams(g["attn_q.weight"], g["attn_q.bias"]),
+                         LinearParams(g["attn_k.weight"], g["attn_k.bias"]),
+                         LinearParams(g["attn_v.weight"], g["attn_v.bias"]),
+                         LinearParams(g["attn_out.weight"], g["attn_out.bias"]))
+        if self.with_ffn:
+            lp.ln2_gain, lp.ln2_bias = g["ln2_gain"], g["ln2_bias"]
+            lp.ff_in = LinearParams(g["ff_in.weight"], g["ff_in.bias"])
+            lp.ff_out = LinearParams(g["ff_out.weight"], g["ff_out.bias"])
+        return lp
 
     def attention_work(self):
         """(rows, global position of row 0, g_begin, g_end) blocks of query rows x key
@@ -306,6 +343,7 @@ class LSSAttention:
         if x.shape != (B, m, E) or x.dtype != torch.float32 or not x.is_contiguous():
             raise ShapeError(f"x must be contiguous fp32 {(B, m, E)}, got {tuple(x.shape)} {x.dtype}")
         self.x = x
+        self.grads.zero_()  # every kernel of the step accumulates its pre-scaled share
         lp, st = self.lp, self.staged
         K.layernorm_fwd(x, lp.ln1_gain, lp.ln1_bias, out=self.xh, mean=self.mean, rstd=self.rstd)
         slot = self.kv_slot.view(B * m, 2 * E)
@@ -400,6 +438,35 @@ class LSSAttention:
                residual=self.x.view(B * m, E), out=self.y.view(B * m, E), M=B * m, N=E, K=E)
         return self.y
 
+    # ------------------------------------------------------------ FFN half (rank-local)
+    def ffn_step(self, x_mid: torch.Tensor, grad_out: torch.Tensor) -> torch.Tensor:
+        """LN2 -> ff_in -> GeLU -> ff_out -> residual and its backward (model.py:449-452,
+        474-477), between the attention forward and backward.  Returns y_out; the
+        attention backward then runs on ``self.grad_mid`` = grad_out + LN2'(...)."""
+        B, m, E, F = self.B, self.m, self.E, self.cfg.ff_dim
+        M = B * m
+        a = self.grad_scale
+        lp = self.lp
+        if grad_out.shape != (B, m, E) or grad_out.dtype != torch.float32 or not grad_out.is_contiguous():
+            raise ShapeError(f"grad_y must be contiguous fp32 {(B, m, E)}")
+        K.layernorm_fwd(x_mid, lp.ln2_gain, lp.ln2_bias, out=self.yh, mean=self.mean2, rstd=self.rstd2)
+        yh = self.yh.view(M, E)
+        K.gemm(yh, self.w_in, b_mn_major=True, bias=lp.ff_in.bias, out=self.h, act="gelu", pre=self.h_pre,
+               M=M, N=F, K=E)
+        K.gemm(self.h, self.w_out, b_mn_major=True, bias=lp.ff_out.bias, residual=x_mid.view(M, E),
+               out=self.y_out.view(M, E), M=M, N=E, K=F)
+        g32 = grad_out.view(M, E)
+        K.cat_cast_colsum([(g32, E, E)], M, dst=self.g_out, colsum=self.g_bout, alpha=a)
+        K.gemm(self.g_out, self.w_out, out=self.g_pre32, act="gelu_bwd", aux=self.h_pre, M=M, N=F, K=E)
+        K.gemm(self.h, self.g_out, a_mn_major=True, b_mn_major=True, alpha=a, out=self.g_wout, M=F, N=E, K=M)
+        K.cat_cast_colsum([(self.g_pre32, F, F)], M, dst=self.g_pre, colsum=self.g_bin, alpha=a)
+        K.gemm(self.g_pre, self.w_in, out=self.g_yh, M=M, N=E, K=F)
+        K.gemm(yh, self.g_pre, a_mn_major=True, b_mn_major=True, alpha=a, out=self.g_win, M=E, N=F, K=M)
+        K.layernorm_bwd(self.g_yh, x_mid.view(M, E), self.mean2, self.rstd2, lp.ln2_gain,
+                        grad_res=g32, grad_x=self.grad_mid.view(M, E), grad_gain=self.g_ln2_g,
+                        grad_bias=self.g_ln2_b, alpha=a)
+        return self.y_out
+
     # ------------------------------------------------------------ backward
     def bwd_pre(self, grad_y: torch.Tensor) -> None:
         """Out-projection backward (+ the delta row term in the balanced schedule)."""
@@ -408,7 +475,6 @@ class LSSAttention:
             raise ShapeError(f"grad_y must be contiguous fp32 {(B, m, E)}")
         self.grad_y = grad_y
         a = self.grad_scale
-        self.grads.zero_()
         # gy -> operand dtype, d b_out = alpha * column sums (nnops.py:192)
         K.cat_cast_colsum([(grad_y.view(B * m, E), E, E)], B * m, dst=self.gy.view(B * m, E),
                           colsum=self.g_bo, alpha=a)
@@ -640,6 +706,10 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
     mark("fwd_out")
     if before_bwd is not None:
         before_bwd()
+    if all(e.with_ffn for e in engines):  # complete layer: rank-local LN2 / FFN half
+        ys = [e.ffn_step(y, gy) for e, y, gy in zip(engines, ys, grad_ys)]
+        grad_ys = [e.grad_mid for e in engines]
+        mark("ffn")
     for e, gy in zip(engines, grad_ys):
         e.bwd_pre(gy)
     b1 = _exchange(engines, comm, "B1", step, layer, async_op=True)
@@ -678,11 +748,12 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
 
 def make_sim_group(cfg: ModelConfig, lp: LayerParams, workers: int, *, replicas: int = 1, device=None,
                    balanced: bool | None = None, fused_rs: bool | None = None):
-    """G engines of one sequence group on one device (tests / smoke), SimComm fabric."""
+    """G engines of one sequence group on one device (tests / smoke), SimComm fabric.
+    LayerParams with the FFN half build complete-layer engines."""
     engines = []
     for r in range(workers):
         e = LSSAttention(cfg, ShardSpec(r, workers, cfg.seq_len), grad_scale=1.0 / (workers * replicas),
-                         device=device, balanced=balanced, fused_rs=fused_rs)
+                         device=device, balanced=balanced, fused_rs=fused_rs, with_ffn=lp.has_ffn)
         e.load_params(lp)
         engines.append(e)
     return engines, SimComm(Ledger())

@@ -12,6 +12,11 @@ adds exactly 0 and its backward passes grad_out through unchanged).
 Inputs are rounded to float32 and then computed in float64 ("double"
 precision, the reference's default).  Stored: inputs, per-rank outputs
 concatenated (y, dx), and the group-averaged attention-parameter grads.
+
+FULL_CASES (files full_*.npz) run the complete pre-norm layer with live FFN
+weights (LN2 -> ff_in -> tanh-GeLU -> ff_out -> residual, model.py:362-390,
+449-452, 475-478) and additionally store the LN2 / FFN parameters and their
+group-averaged grads.
 """
 
 from __future__ import annotations
@@ -40,10 +45,17 @@ CASES = {
 }
 
 GRAD_NAMES = ("ln1_gain", "ln1_bias", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo")
+FFN_NAMES = ("ln2_gain", "ln2_bias", "w_in", "b_in", "w_out", "b_out")
+
+FULL_CASES = {
+    # name: (seq_len, embed, heads, workers, batch, causal, ff_dim, out dtype)
+    "full_g2_causal": (256, 128, 2, 2, 1, True, 512, np.float64),
+    "full_g1_b2": (128, 128, 2, 1, 2, True, 256, np.float64),
+}
 
 
-def run_case(seq, e, h, g, b, causal, seed=0):
-    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=8, vocab=16, seq_len=seq,
+def run_case(seq, e, h, g, b, causal, seed=0, ff_dim=0):
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=ff_dim or 8, vocab=16, seq_len=seq,
                       batch=b, causal=causal, precision="double")
     rng = np.random.default_rng(seed)
     f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
@@ -54,8 +66,14 @@ def run_case(seq, e, h, g, b, causal, seed=0):
     lin = lambda p: LinearParams(f32(p.weight), f32(0.05 * rng.standard_normal(e)))  # noqa: E731
     lp.attn_q, lp.attn_k, lp.attn_v, lp.attn_out = (lin(lp.attn_q), lin(lp.attn_k),
                                                     lin(lp.attn_v), lin(lp.attn_out))
-    lp.ff_in = LinearParams(np.zeros_like(lp.ff_in.weight), np.zeros_like(lp.ff_in.bias))
-    lp.ff_out = LinearParams(np.zeros_like(lp.ff_out.weight), np.zeros_like(lp.ff_out.bias))
+    if ff_dim:  # live FFN half with non-trivial LN2 affine and biases
+        lp.ln2_gain = f32(1.0 + 0.1 * rng.standard_normal(e))
+        lp.ln2_bias = f32(0.1 * rng.standard_normal(e))
+        lp.ff_in = LinearParams(f32(lp.ff_in.weight), f32(0.05 * rng.standard_normal(ff_dim)))
+        lp.ff_out = LinearParams(f32(lp.ff_out.weight), f32(0.05 * rng.standard_normal(e)))
+    else:
+        lp.ff_in = LinearParams(np.zeros_like(lp.ff_in.weight), np.zeros_like(lp.ff_in.bias))
+        lp.ff_out = LinearParams(np.zeros_like(lp.ff_out.weight), np.zeros_like(lp.ff_out.bias))
     x = f32(rng.standard_normal((b, seq, e)))
     gy = f32(rng.standard_normal((b, seq, e)))
     off = DropoutPolicy.off()
@@ -82,6 +100,9 @@ def run_case(seq, e, h, g, b, causal, seed=0):
         flat = [grads.ln1_gain, grads.ln1_bias, grads.attn_q.weight, grads.attn_q.bias,
                 grads.attn_k.weight, grads.attn_k.bias, grads.attn_v.weight, grads.attn_v.bias,
                 grads.attn_out.weight, grads.attn_out.bias]
+        if ff_dim:
+            flat += [grads.ln2_gain, grads.ln2_bias, grads.ff_in.weight, grads.ff_in.bias,
+                     grads.ff_out.weight, grads.ff_out.bias]
         vec = np.concatenate([a.ravel() for a in flat])
         vec = comm.all_reduce_mean(group, rank, vec, step=0, phase="sync")  # sharded.py:238
         return y, dx, vec, [a.shape for a in flat]
@@ -91,7 +112,7 @@ def run_case(seq, e, h, g, b, causal, seed=0):
     dx = np.concatenate([r[1] for r in res], axis=1)
     vec, shapes = res[0][2], res[0][3]
     grads, pos = {}, 0
-    for name, shp in zip(GRAD_NAMES, shapes):
+    for name, shp in zip(GRAD_NAMES + (FFN_NAMES if ff_dim else ()), shapes):
         n = int(np.prod(shp))
         grads["g_" + name] = vec[pos:pos + n].reshape(shp)
         pos += n
@@ -99,6 +120,9 @@ def run_case(seq, e, h, g, b, causal, seed=0):
                   bq=lp.attn_q.bias, wk=lp.attn_k.weight, bk=lp.attn_k.bias,
                   wv=lp.attn_v.weight, bv=lp.attn_v.bias, wo=lp.attn_out.weight,
                   bo=lp.attn_out.bias)
+    if ff_dim:
+        params.update(ln2_gain=lp.ln2_gain, ln2_bias=lp.ln2_bias, w_in=lp.ff_in.weight, b_in=lp.ff_in.bias,
+                      w_out=lp.ff_out.weight, b_out=lp.ff_out.bias)
     return x, gy, params, y, dx, grads
 
 
@@ -112,6 +136,15 @@ def main():
         arrays.update({k: v.astype(odt) for k, v in grads.items()})
         np.savez_compressed(OUT / f"{name}.npz", **arrays)
         print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("x", "y")})
+    for name, (seq, e, h, g, b, causal, ff, odt) in FULL_CASES.items():
+        x, gy, params, y, dx, grads = run_case(seq, e, h, g, b, causal, ff_dim=ff)
+        arrays = dict(x=x.astype(np.float32), grad_y=gy.astype(np.float32),
+                      meta=np.array([seq, e, h, g, b, int(causal)], dtype=np.int64),
+                      ff_dim=np.array(ff, dtype=np.int64), y=y.astype(odt), dx=dx.astype(odt))
+        arrays.update({k: v.astype(np.float32) for k, v in params.items()})
+        arrays.update({k: v.astype(odt) for k, v in grads.items()})
+        np.savez_compressed(OUT / f"{name}.npz", **arrays)
+        print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("x", "y", "w_in")})
 
 
 if __name__ == "__main__":

@@ -265,7 +265,7 @@ def test_balanced_causal_schedule_matches_oracle(cuda, G, m, batch):
     assert nerr(results[True][0], results[False][0]) < 5e-3
 
 
-@pytest.mark.parametrize("G,m,balanced", [(2, 384, True), (4, 384, True), (4, 296, False), (3, 256, True)])
+@pytest.mark.parametrize("G,m,balanced", [(2, 384, True), (4, 384, True), (4, 296, False), (3, 256, True), (8, 256, True), (8, 256, False)])
 def test_fused_reduce_scatter_matches_collective(cuda, G, m, balanced):
     """lss_attn_bwd_p2p (dK|dV stored into the owners' slots, summed after the
     barrier) == the reduce-scatter path: the reduced dK|dV bit for bit (both fold
@@ -299,3 +299,74 @@ def test_fused_reduce_scatter_matches_collective(cuda, G, m, balanced):
         assert torch.equal(a, b)
     for a, b in zip(outs[True][0] + outs[True][1], outs[False][0] + outs[False][1]):
         assert nerr(a.cpu().numpy(), b.cpu().numpy()) < 1e-5
+
+
+# ---- complete layer: attention half + LN2 / FFN half
+
+FULL_CASES = ["full_g2_causal", "full_g1_b2"]
+FFN_KEYS = [("ln2_gain", "ln2_gain"), ("ln2_bias", "ln2_bias"), ("ff_in.weight", "w_in"),
+            ("ff_in.bias", "b_in"), ("ff_out.weight", "w_out"), ("ff_out.bias", "b_out")]
+ATTN_NAMES = ("ln1_gain", "ln1_bias", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo")
+
+
+def _full_params(z, dev):
+    from paper_2311_02382_b200.model import layer_params_from_arrays
+
+    return layer_params_from_arrays(*[z[k] for k in ATTN_NAMES], device=dev,
+                                    **{k: z[k] for k in ("ln2_gain", "ln2_bias", "w_in", "b_in", "w_out", "b_out")})
+
+
+@pytest.mark.parametrize("name", FULL_CASES)
+@pytest.mark.parametrize("precision", ["bf16", "single"])
+def test_full_layer_engine_matches_reference(cuda, name, precision):
+    """LSS engine with the FFN half (ffn_step between the attention forward and
+    backward, GeLU / GeLU' fused into the GEMM epilogues) == the real reference's
+    complete layer_fwd / layer_bwd; FFN grads ride in the same all-reduce."""
+    import torch
+    from paper_2311_02382_b200.model import ModelConfig
+    from paper_2311_02382_b200.sharded import ShardSpec, lss_step, make_sim_group, slice_batch
+
+    z, seq, e, h, g, b, causal = _load(name)
+    ff = int(z["ff_dim"])
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=ff, vocab=16, seq_len=seq, batch=b,
+                      causal=causal, precision=precision)
+    engines, comm = make_sim_group(cfg, _full_params(z, cuda), g, device=cuda)
+    assert all(eng.with_ffn for eng in engines)
+    x, gy = torch.as_tensor(z["x"], device=cuda), torch.as_tensor(z["grad_y"], device=cuda)
+    out = lss_step(engines, comm, [slice_batch(x, ShardSpec(r, g, seq)) for r in range(g)],
+                   [slice_batch(gy, ShardSpec(r, g, seq)) for r in range(g)])
+    torch.cuda.synchronize()
+    tol = TOL[precision]
+    assert_close_ref(torch.cat([o[0] for o in out], 1).cpu().numpy(), z["y"], tol, "y")
+    assert_close_ref(torch.cat([o[1] for o in out], 1).cpu().numpy(), z["dx"], tol, "dx")
+    gv = {k: v.cpu().numpy() for k, v in engines[0].grad_views().items()}
+    for ours, gold in GRAD_KEYS + FFN_KEYS:
+        if gold == "bk":
+            continue
+        assert_close_ref(gv[ours], z["g_" + gold], tol, ours)
+    assert comm.ledger.count("all-reduce") == 1  # FFN grads share the one all-reduce
+
+
+@pytest.mark.parametrize("precision", ["bf16", "single"])
+def test_functional_full_layer_matches_reference(cuda, precision):
+    """model.layer_fwd / layer_bwd with the FFN half (one worker) == reference."""
+    import torch
+    from paper_2311_02382_b200 import model as M
+
+    z, seq, e, h, g, b, causal = _load("full_g1_b2")
+    cfg = M.ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=int(z["ff_dim"]), vocab=16, seq_len=seq,
+                        batch=b, causal=causal, precision=precision)
+    lp = _full_params(z, cuda)
+    y, cache = M.layer_fwd(lp, cfg, None, 0, torch.as_tensor(z["x"], device=cuda), 0)
+    dx, grads = M.layer_bwd(lp, cfg, None, 0, cache, torch.as_tensor(z["grad_y"], device=cuda))
+    torch.cuda.synchronize()
+    tol = TOL[precision]
+    assert_close_ref(y.cpu().numpy(), z["y"], tol, "y")
+    assert_close_ref(dx.cpu().numpy(), z["dx"], tol, "dx")
+    for name, gold in [("ff_in", "w_in"), ("ff_out", "w_out")]:
+        assert_close_ref(getattr(grads, name).weight.cpu().numpy(), z["g_" + gold], tol, name)
+    assert_close_ref(grads.ff_in.bias.cpu().numpy(), z["g_b_in"], tol, "b_in")
+    assert_close_ref(grads.ln2_gain.cpu().numpy(), z["g_ln2_gain"], tol, "ln2_gain")
+    assert_close_ref(grads.attn_q.weight.cpu().numpy(), z["g_wq"], tol, "wq")
+    assert [n for n, _ in grads.named_arrays()][-6:] == ["ln2_gain", "ln2_bias", "ff_in.weight", "ff_in.bias",
+                                                         "ff_out.weight", "ff_out.bias"]

@@ -201,6 +201,13 @@ int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const 
                      int nsrc, float* const* seg_dst, int peer, long ld_dkv, int batch, int workers,
                      int seg_len, int heads, int head_dim, int causal, void* stream);
 
+/* Parameter updates after the gradient all-reduce, over flat fp32 buffers:
+ * model.sgd_step (model.py:621-623) p -= lr * g, and optim.adam_step
+ * (optim.py:35-53) with bias correction (step is 1-based). */
+int lss_sgd_update(float* params, const float* grads, long n, float lr, void* stream);
+int lss_adam_update(float* params, const float* grads, float* m, float* v, long n, float lr, float beta1,
+                    float beta2, float eps, int step, void* stream);
+
 /* dst[i] = sum_{s < nslots} src[s * slot_elems + i] for i < n (fp32, n % 4 == 0). */
 int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, long n, void* stream);
 

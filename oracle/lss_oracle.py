@@ -326,6 +326,20 @@ def lss_layer(x, grad_y, p: AttnParams, f: FfnParams, n_heads, workers, causal=T
                 ffn_grads=FfnParams(*[getattr(fg, n) / workers for n in FfnParams.GRAD_ORDER]))
 
 
+def sgd_step(params, grads, lr):
+    """model.sgd_step (model.py:621-623)."""
+    return [p - lr * g for p, g in zip(params, grads)]
+
+
+def adam_step(params, grads, m, v, t, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """optim.adam_step (optim.py:35-53), t 1-based; returns (params, m, v)."""
+    m = [beta1 * a + (1.0 - beta1) * g for a, g in zip(m, grads)]
+    v = [beta2 * a + (1.0 - beta2) * g * g for a, g in zip(v, grads)]
+    out = [p - lr * (a / (1.0 - beta1 ** t)) / (np.sqrt(b / (1.0 - beta2 ** t)) + eps)
+           for p, a, b in zip(params, m, v)]
+    return out, m, v
+
+
 # --------------------------------------------------------------------------
 # Work accounting (costs.py:98 convention, extended to fwd+bwd; SURVEY §8(d))
 # --------------------------------------------------------------------------

@@ -326,4 +326,24 @@ __global__ void sum_slots_kernel(float4* __restrict__ dst, const float4* __restr
   }
 }
 
+// Optimizer updates over flat fp32 buffers, applied after the gradient
+// all-reduce: model.sgd_step (model.py:621-623) and optim.adam_step (optim.py:35-53).
+__global__ void sgd_update_kernel(float* __restrict__ p, const float* __restrict__ g, long n, float lr) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    p[i] -= lr * g[i];
+}
+
+__global__ void adam_update_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                                   float* __restrict__ v, long n, float lr, float beta1, float beta2, float eps,
+                                   float inv_bc1, float inv_bc2) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = beta1 * m[i] + (1.f - beta1) * gi;
+    const float vi = beta2 * v[i] + (1.f - beta2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi * inv_bc1) / (sqrtf(vi * inv_bc2) + eps);
+  }
+}
+
 }  // namespace lss

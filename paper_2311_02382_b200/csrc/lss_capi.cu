@@ -482,6 +482,29 @@ int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, lon
   return check_launch("sum_slots");
 }
 
+int lss_sgd_update(float* params, const float* grads, long n, float lr, void* stream) {
+  if (!params || !grads) return fail(LSS_ERR_ARG, "sgd_update: null pointer");
+  if (n <= 0) return n == 0 ? LSS_OK : fail(LSS_ERR_SHAPE, "sgd_update: n %ld", n);
+  const int threads = 256;
+  const int blocks = (int)std::min<long>((n + threads - 1) / threads, (long)num_sms() * 8);
+  sgd_update_kernel<<<blocks, threads, 0, S(stream)>>>(params, grads, n, lr);
+  return check_launch("sgd_update");
+}
+
+int lss_adam_update(float* params, const float* grads, float* m, float* v, long n, float lr, float beta1,
+                    float beta2, float eps, int step, void* stream) {
+  if (!params || !grads || !m || !v) return fail(LSS_ERR_ARG, "adam_update: null pointer");
+  if (step < 1) return fail(LSS_ERR_ARG, "adam_update: step %d (1-based)", step);
+  if (n <= 0) return n == 0 ? LSS_OK : fail(LSS_ERR_SHAPE, "adam_update: n %ld", n);
+  const float inv_bc1 = (float)(1.0 / (1.0 - std::pow((double)beta1, step)));
+  const float inv_bc2 = (float)(1.0 / (1.0 - std::pow((double)beta2, step)));
+  const int threads = 256;
+  const int blocks = (int)std::min<long>((n + threads - 1) / threads, (long)num_sms() * 8);
+  adam_update_kernel<<<blocks, threads, 0, S(stream)>>>(params, grads, m, v, n, lr, beta1, beta2, eps, inv_bc1,
+                                                        inv_bc2);
+  return check_launch("adam_update");
+}
+
 // ------------------------------------------------------------------ peer memory (CUDA IPC)
 using PFN_getAddressRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 

@@ -70,3 +70,23 @@ def make_groups(layout: GridLayout):
         if rank in layout.data_members(s):
             my_data = g
     return my_seq, my_data, dist.group.WORLD
+
+
+def run_steps(engine, comm, batches, opt, *, layer: int = 0):
+    """Drive ``len(batches)`` training steps of ONE rank of a D x N grid
+    (hybrid.run_steps / train_step, hybrid.py:95-126, 140-190, at layer level):
+    each step runs the layer forward + backward with the folded gradient
+    all-reduce (sequence x data, scale 1/(D*N) in the kernels) and then the
+    optimizer update of the bound parameters (``engine.bind_params``).
+
+    ``batches[s]`` = (x_seg, grad_y_seg) of this rank's sequence block.
+    Returns the post-sync gradient norm of every step (HybridRun.grad_norms,
+    folded in fp64 like model.grad_norm)."""
+    import torch
+
+    norms = []
+    for s, (x, gy) in enumerate(batches):
+        engine.step(x, gy, comm, step=s, layer=layer)
+        norms.append(float(torch.linalg.vector_norm(engine.grads.double())))
+        engine.optimizer_step(opt)
+    return norms

@@ -345,6 +345,25 @@ def sum_slots(dst, src):
     return dst
 
 
+def sgd_update(params, grads, lr):
+    """params -= lr * grads (flat fp32, in place): model.sgd_step (model.py:621-623)."""
+    _need(params, "params", torch.float32)
+    _need(grads, "grads", torch.float32)
+    if params.numel() != grads.numel():
+        raise ShapeError("sgd_update: params / grads sizes differ")
+    call("lss_sgd_update", _ptr(params), _ptr(grads), params.numel(), lr, _stream())
+
+
+def adam_update(params, grads, m, v, *, lr, step, beta1=0.9, beta2=0.999, eps=1e-8):
+    """Bias-corrected Adam in place (optim.adam_step, optim.py:35-53); step is 1-based."""
+    for t, n in ((params, "params"), (grads, "grads"), (m, "m"), (v, "v")):
+        _need(t, n, torch.float32)
+        if t.numel() != params.numel():
+            raise ShapeError(f"adam_update: {n} size differs")
+    call("lss_adam_update", _ptr(params), _ptr(grads), _ptr(m), _ptr(v), params.numel(), lr, beta1, beta2, eps,
+         step, _stream())
+
+
 def ipc_export(t):
     """(64-byte handle, offset) of a device tensor's memory for another process."""
     h = ctypes.create_string_buffer(64)

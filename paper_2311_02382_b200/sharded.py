@@ -204,7 +204,10 @@ class LSSAttention:
         n_attn = 4 * E * E + 6 * E + 1
         ffn0 = (n_attn + 15) // 16 * 16  # FFN grads start 64-byte aligned (vectorised epilogues)
         n = ffn0 + (2 * E * F + F + 3 * E) if with_ffn else n_attn
+        self._ffn0 = ffn0
         self.grads = torch.zeros(n, dtype=f32, device=dev)
+        self.params = None  # flat fp32 parameters in the same layout (bind_params)
+        self.param_lp = None
         o = 0
         self.g_wqkv = self.grads[o:o + 3 * E * E]; o += 3 * E * E
         self.g_wo = self.grads[o:o + E * E].view(E, E); o += E * E
@@ -255,33 +258,70 @@ class LSSAttention:
             self.w_in = lp.ff_in.weight.to(ad).contiguous()    # [E][F]: B operand N-major / K-major
             self.w_out = lp.ff_out.weight.to(ad).contiguous()  # [F][E]
 
+    def _flat_views(self, buf: torch.Tensor) -> dict:
+        """Named views (reference names, model.LayerParams order) into a flat buffer
+        with the gradient layout."""
+        E, F = self.E, self.cfg.ff_dim
+        o = 0
+        w = buf[o:o + 3 * E * E].view(3, E, E); o += 3 * E * E
+        wo = buf[o:o + E * E].view(E, E); o += E * E
+        b = buf[o:o + 3 * E].view(3, E); o += 3 * E
+        bo = buf[o:o + E]; o += E
+        d = {"ln1_gain": buf[o:o + E], "ln1_bias": buf[o + E:o + 2 * E],
+             "attn_q.weight": w[0], "attn_q.bias": b[0], "attn_k.weight": w[1], "attn_k.bias": b[1],
+             "attn_v.weight": w[2], "attn_v.bias": b[2], "attn_out.weight": wo, "attn_out.bias": bo}
+        if self.with_ffn:
+            o = self._ffn0
+            d["ln2_gain"] = buf[o:o + E]; o += E
+            d["ln2_bias"] = buf[o:o + E]; o += E
+            d["ff_in.weight"] = buf[o:o + E * F].view(E, F); o += E * F
+            d["ff_in.bias"] = buf[o:o + F]; o += F
+            d["ff_out.weight"] = buf[o:o + F * E].view(F, E); o += F * E
+            d["ff_out.bias"] = buf[o:o + E]
+        return d
+
+    def _layer_params(self, d: dict) -> LayerParams:
+        lp = LayerParams(d["ln1_gain"], d["ln1_bias"], LinearParams(d["attn_q.weight"], d["attn_q.bias"]),
+                         LinearParams(d["attn_k.weight"], d["attn_k.bias"]),
+                         LinearParams(d["attn_v.weight"], d["attn_v.bias"]),
+                         LinearParams(d["attn_out.weight"], d["attn_out.bias"]))
+        if self.with_ffn:
+            lp.ln2_gain, lp.ln2_bias = d["ln2_gain"], d["ln2_bias"]
+            lp.ff_in = LinearParams(d["ff_in.weight"], d["ff_in.bias"])
+            lp.ff_out = LinearParams(d["ff_out.weight"], d["ff_out.bias"])
+        return lp
+
     def grad_views(self) -> dict:
         """Gradients by reference name (model.LayerParams field order)."""
-        E = self.E
-        w = self.g_wqkv.view(3, E, E)
-        b = self.g_bqkv.view(3, E)
-        return {
-            "ln1_gain": self.g_ln_g, "ln1_bias": self.g_ln_b,
-            "attn_q.weight": w[0], "attn_q.bias": b[0],
-            "attn_k.weight": w[1], "attn_k.bias": b[1],
-            "attn_v.weight": w[2], "attn_v.bias": b[2],
-            "attn_out.weight": self.g_wo, "attn_out.bias": self.g_bo,
-        } | ({"ln2_gain": self.g_ln2_g, "ln2_bias": self.g_ln2_b, "ff_in.weight": self.g_win,
-              "ff_in.bias": self.g_bin, "ff_out.weight": self.g_wout, "ff_out.bias": self.g_bout}
-             if self.with_ffn else {})
+        return self._flat_views(self.grads)
 
     def grad_params(self) -> LayerParams:
-        g = self.grad_views()
-        lp = LayerParams(g["ln1_gain"], g["ln1_bias"],
-                         LinearParams(g["attn_q.weight"], g["attn_q.bias"]),
-                         LinearParams(g["attn_k.weight"], g["attn_k.bias"]),
-                         LinearParams(g["attn_v.weight"], g["attn_v.bias"]),
-                         LinearParams(g["attn_out.weight"], g["attn_out.bias"]))
-        if self.with_ffn:
-            lp.ln2_gain, lp.ln2_bias = g["ln2_gain"], g["ln2_bias"]
-            lp.ff_in = LinearParams(g["ff_in.weight"], g["ff_in.bias"])
-            lp.ff_out = LinearParams(g["ff_out.weight"], g["ff_out.bias"])
-        return lp
+        return self._layer_params(self.grad_views())
+
+    # ------------------------------------------------------------ training step (SURVEY §8(f) f4)
+    def bind_params(self, lp: LayerParams) -> LayerParams:
+        """Copy ``lp`` into the engine's flat fp32 parameter buffer (the gradient
+        layout) and stage it; returns LayerParams views of that buffer, which
+        :meth:`optimizer_step` updates in place (the DistParameters of the reference)."""
+        if self.params is None:
+            self.params = torch.zeros_like(self.grads)
+        views = self._flat_views(self.params)
+        for name, t in lp.named_arrays():
+            if name not in views:
+                raise ShapeError(f"parameter {name} has no slot (engine with_ffn={self.with_ffn})")
+            views[name].copy_(t)
+        self.param_lp = self._layer_params(views)
+        self.load_params(self.param_lp)
+        return self.param_lp
+
+    def optimizer_step(self, opt) -> None:
+        """Apply ``opt`` (optim.SGD / optim.Adam) to the bound parameters with the
+        synced gradients -- hybrid.train_step's sgd_step after vertical_sync
+        (hybrid.py:119-125) -- and restage the operand copies."""
+        if self.params is None:
+            raise ValueError("optimizer_step needs bind_params first")
+        opt.step(self.params, self.grads)
+        self.load_params(self.param_lp)
 
     def attention_work(self):
         """(rows, global position of row 0, g_begin, g_end) blocks of query rows x key

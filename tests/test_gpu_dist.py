@@ -37,3 +37,17 @@ def test_nccl_lss_layer_matches_reference(case, world, fused):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+def test_nccl_hybrid_grid_training_step():
+    """2 x 2 hybrid grid (two replicas of a 2-rank sequence group) over NCCL:
+    one step of run_steps == the oracle's doubly averaged SGD update."""
+    if _gpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    from conftest import free_port
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(ROOT / "tests" / "hybrid_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout

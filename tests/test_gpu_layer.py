@@ -370,3 +370,81 @@ def test_functional_full_layer_matches_reference(cuda, precision):
     assert_close_ref(grads.attn_q.weight.cpu().numpy(), z["g_wq"], tol, "wq")
     assert [n for n, _ in grads.named_arrays()][-6:] == ["ln2_gain", "ln2_bias", "ff_in.weight", "ff_in.bias",
                                                          "ff_out.weight", "ff_out.bias"]
+
+
+# ---- training step: optimizer update after the synced gradients
+
+
+@pytest.mark.parametrize("opt_name", ["sgd", "adam"])
+@pytest.mark.parametrize("name", ["small_causal", "full_g2_causal"])
+def test_training_steps_match_oracle(cuda, name, opt_name):
+    """Two steps of (fwd + bwd + folded all-reduce + optimizer update) on the
+    engine == the oracle's layer gradients fed through model.sgd_step /
+    optim.adam_step.  The parameter UPDATE is compared (fp32 check mode)."""
+    import torch
+    from oracle import lss_oracle as O
+    from paper_2311_02382_b200 import optim
+    from paper_2311_02382_b200.model import ModelConfig
+    from paper_2311_02382_b200.sharded import ShardSpec, lss_step, make_sim_group, slice_batch
+
+    z, seq, e, h, g, b, causal = _load(name)
+    full = "w_in" in z.files
+    ff = int(z["ff_dim"]) if full else 8
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=ff, vocab=16, seq_len=seq, batch=b,
+                      causal=causal, precision="single")
+    lp = _full_params(z, cuda) if full else __import__("paper_2311_02382_b200.model", fromlist=["x"]) \
+        .layer_params_from_arrays(*[z[k] for k in ATTN_NAMES], device=cuda)
+    engines, comm = make_sim_group(cfg, lp, g, device=cuda)
+    opts = [optim.make_update(opt_name, 1e-2) for _ in engines]
+    views = [eng.bind_params(lp) for eng in engines]
+    x, gy = torch.as_tensor(z["x"], device=cuda), torch.as_tensor(z["grad_y"], device=cuda)
+    names = [n for n, _ in views[0].named_arrays()]
+    # oracle state (float64), in named_arrays order
+    ocur = [t.detach().cpu().double().numpy().copy() for _, t in views[0].named_arrays()]
+    om = [np.zeros_like(a) for a in ocur]
+    ov = [np.zeros_like(a) for a in ocur]
+    n_attn = 10
+    for step in range(2):
+        before = [t.detach().cpu().double().numpy().copy() for _, t in engines[0].param_lp.named_arrays()]
+        lss_step(engines, comm, [slice_batch(x, ShardSpec(r, g, seq)) for r in range(g)],
+                 [slice_batch(gy, ShardSpec(r, g, seq)) for r in range(g)], step=step)
+        for eng, opt in zip(engines, opts):
+            eng.optimizer_step(opt)
+        torch.cuda.synchronize()
+        after = [t.detach().cpu().double().numpy() for _, t in engines[0].param_lp.named_arrays()]
+        # oracle gradients at the current parameters
+        d = dict(zip(names, ocur))
+        p = O.AttnParams(d["ln1_gain"], d["ln1_bias"], d["attn_q.weight"], d["attn_q.bias"],
+                         d["attn_k.weight"], d["attn_k.bias"], d["attn_v.weight"], d["attn_v.bias"],
+                         d["attn_out.weight"], d["attn_out.bias"])
+        xd, gd = z["x"].astype(np.float64), z["grad_y"].astype(np.float64)
+        if full:
+            f = O.FfnParams(d["ln2_gain"], d["ln2_bias"], d["ff_in.weight"], d["ff_in.bias"],
+                            d["ff_out.weight"], d["ff_out.bias"])
+            ref = O.lss_layer(xd, gd, p, f, h, g, causal)
+            grads = [getattr(ref["grads"], n) for n in O.AttnParams.GRAD_ORDER] + \
+                    [getattr(ref["ffn_grads"], n) for n in O.FfnParams.GRAD_ORDER]
+        else:
+            ref = O.lss_attention(xd, gd, p, h, g, causal)
+            grads = [getattr(ref["grads"], n) for n in O.AttnParams.GRAD_ORDER]
+        order = ["ln1_gain", "ln1_bias", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo"]
+        gmap = dict(zip(order + list(O.FfnParams.GRAD_ORDER), grads))
+        ref_names = dict(zip(names, ["ln1_gain", "ln1_bias", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo"]
+                             + list(O.FfnParams.GRAD_ORDER)))
+        og = [gmap[ref_names[n]] for n in names]
+        if opt_name == "sgd":
+            nxt = O.sgd_step(ocur, og, 1e-2)
+        else:
+            nxt, om, ov = O.adam_step(ocur, og, om, ov, step + 1, 1e-2)
+        for i, n in enumerate(names):
+            if n == "attn_k.bias":  # its gradient is mathematically zero (rounding noise on both sides)
+                continue
+            got, want = after[i] - before[i], nxt[i] - ocur[i]
+            if opt_name == "adam" and step == 0:  # first Adam step is lr * sign(g): compare where |g| is clear
+                mask = np.abs(og[i]) > 1e-3 * np.abs(og[i]).max()
+                assert nerr(got[mask], want[mask]) < 1e-3, n
+            else:
+                assert nerr(got, want) < (1e-3 if opt_name == "adam" else 1e-4), n
+        ocur = nxt
+        for eng in engines[1:]:  # every worker of the group holds identical parameters
+            assert torch.equal(eng.params, engines[0].params)

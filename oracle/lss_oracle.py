@@ -326,6 +326,48 @@ def lss_layer(x, grad_y, p: AttnParams, f: FfnParams, n_heads, workers, causal=T
                 ffn_grads=FfnParams(*[getattr(fg, n) / workers for n in FfnParams.GRAD_ORDER]))
 
 
+def cross_entropy(logits, targets):
+    """nnops.cross_entropy (nnops.py:274-299): mean loss over rows and its logit gradient."""
+    n = logits.shape[0]
+    shifted = logits - logits.max(axis=1, keepdims=True)
+    e = np.exp(shifted)
+    se = e.sum(axis=1, keepdims=True)
+    loss = float(-np.mean((shifted - np.log(se))[np.arange(n), targets]))
+    grad = e / se
+    grad[np.arange(n), targets] -= 1.0
+    return loss, grad / n
+
+
+def gpt_forward_backward(P, tokens, targets, n_heads, causal=True, workers=1):
+    """model.forward / model.backward (model.py:583-618) for the whole decoder:
+    token + position embedding (517-540), the layers (:func:`lss_layer`), final LN +
+    head (552-570), mean cross-entropy.  ``P`` is a dict with token_table, pos_table,
+    layers [(AttnParams, FfnParams)], final_gain, final_bias, head_w, head_b.
+    Returns (loss, grads dict with the same keys; layers as (AttnParams, FfnParams))."""
+    b, m = tokens.shape
+    x = P["token_table"][tokens] + P["pos_table"][None]
+    xs = [x]
+    for p, f in P["layers"]:
+        x = lss_layer(x, np.zeros_like(x), p, f, n_heads, workers, causal)["y"]
+        xs.append(x)
+    xf, lnf = layernorm_fwd(x, P["final_gain"], P["final_bias"])
+    v = P["head_w"].shape[1]
+    logits = (xf @ P["head_w"] + P["head_b"]).reshape(b * m, v)
+    loss, glog = cross_entropy(logits, targets.reshape(-1))
+    g_xf, g_hw, g_hb = linear_bwd(xf, P["head_w"], glog.reshape(b, m, v))
+    g, g_fg, g_fb = layernorm_bwd(lnf, P["final_gain"], g_xf)
+    layer_grads = [None] * len(P["layers"])
+    for li in range(len(P["layers"]) - 1, -1, -1):
+        p, f = P["layers"][li]
+        out = lss_layer(xs[li], g, p, f, n_heads, workers, causal)
+        g = out["dx"]
+        layer_grads[li] = (out["grads"], out["ffn_grads"])
+    g_tok = np.zeros_like(P["token_table"])
+    np.add.at(g_tok, tokens.reshape(-1), g.reshape(b * m, -1))  # nnops.py:258-262
+    return loss, dict(token_table=g_tok, pos_table=g.sum(axis=0), layers=layer_grads, final_gain=g_fg,
+                      final_bias=g_fb, head_w=g_hw, head_b=g_hb)
+
+
 def sgd_step(params, grads, lr):
     """model.sgd_step (model.py:621-623)."""
     return [p - lr * g for p, g in zip(params, grads)]

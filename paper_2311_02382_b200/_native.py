@@ -83,6 +83,9 @@ SIGNATURES = {
                          _I, _I, _I, _P],
     "lss_sum_slots": [_P, _P, _I, _L, _L, _P],
     "lss_sgd_update": [_P, _P, _L, _F, _P],
+    "lss_embed_fwd": [_P, _P, _P, _P, _I, _I, _I, _P],
+    "lss_embed_bwd": [_P, _P, _P, _P, _I, _I, _I, _P],
+    "lss_cross_entropy": [_P, _L, _P, _L, _I, _F, _P, _P, _L, _P],
     "lss_adam_update": [_P, _P, _P, _P, _L, _F, _F, _F, _F, _I, _P],
     "lss_ipc_export": [_P, ctypes.c_char_p, ctypes.POINTER(_L)],
     "lss_ipc_import": [ctypes.c_char_p, _L, ctypes.POINTER(_P)],
@@ -130,7 +133,8 @@ def load():
 KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 1, "lss_stage_weights": 1,
                     "lss_cat_cast_colsum": 1, "lss_attn_fwd": 1, "lss_attn_bwd": 2, "lss_attn_fwd_ex": 1,
                     "lss_attn_merge": 1, "lss_attn_delta": 1, "lss_attn_bwd_ex": 1, "lss_add_f32": 1,
-                    "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1}
+                    "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1,
+                    "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1}
 launch_count = 0
 
 

@@ -346,4 +346,76 @@ __global__ void adam_update_kernel(float* __restrict__ p, const float* __restric
   }
 }
 
+// ---------------------------------------------------------------- embeddings / loss
+// model.embed_fwd (model.py:517-533): x[b][i] = token_table[tokens[b][i]] + pos_table[i]
+// (pos_table holds exactly this block's rows).  One warp per (b, i) row, float4.
+__global__ void embed_fwd_kernel(const int* __restrict__ tokens, const float* __restrict__ tok,
+                                 const float* __restrict__ pos, float* __restrict__ x, long rows, int m, int e) {
+  const long r = blockIdx.x * (long)(blockDim.x / 32) + threadIdx.x / 32;
+  if (r >= rows) return;
+  const int lane = threadIdx.x % 32;
+  const float4* trow = reinterpret_cast<const float4*>(tok + (long)tokens[r] * e);
+  const float4* prow = reinterpret_cast<const float4*>(pos + (long)(r % m) * e);
+  float4* xrow = reinterpret_cast<float4*>(x + r * e);
+  for (int c = lane; c < e / 4; c += 32) {
+    const float4 a = trow[c], p = prow[c];
+    xrow[c] = make_float4(a.x + p.x, a.y + p.y, a.z + p.z, a.w + p.w);
+  }
+}
+
+// model.embed_bwd (model.py:536-540): grad_pe[i] = sum_b g[b][i] (written), grad_tok[id] +=
+// g[b][i] (accumulated: nnops.embed_tokens_bwd scatter-add, nnops.py:258-262).
+__global__ void embed_bwd_kernel(const int* __restrict__ tokens, const float* __restrict__ g,
+                                 float* __restrict__ grad_tok, float* __restrict__ grad_pe, int batch, int m, int e) {
+  const long i = blockIdx.x * (long)(blockDim.x / 32) + threadIdx.x / 32;  // position
+  if (i >= m) return;
+  const int lane = threadIdx.x % 32;
+  for (int c = lane; c < e; c += 32) {
+    float acc = 0.f;
+    for (int b = 0; b < batch; ++b) {
+      const long r = (long)b * m + i;
+      const float v = g[r * e + c];
+      acc += v;
+      atomicAdd(grad_tok + (long)tokens[r] * e + c, v);
+    }
+    grad_pe[i * e + c] = acc;
+  }
+}
+
+// nnops.cross_entropy (nnops.py:274-299): per row r of logits [n][ld] (first v
+// columns): loss_r = logsumexp - logit[target], grad = (softmax - onehot) * scale.
+// One 256-thread block per row.
+__global__ void cross_entropy_kernel(const float* __restrict__ logits, long ld, const int* __restrict__ targets,
+                                     int v, float scale, float* __restrict__ loss_rows, float* __restrict__ grad,
+                                     long ld_grad) {
+  const long r = blockIdx.x;
+  const float* row = logits + r * ld;
+  __shared__ float red[32];
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < v; c += blockDim.x) mx = fmaxf(mx, row[c]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int w = 0; w < (int)(blockDim.x / 32); ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float se = 0.f;
+  for (int c = threadIdx.x; c < v; c += blockDim.x) se += expf(row[c] - mx);
+  for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = se;
+  __syncthreads();
+  se = 0.f;
+  for (int w = 0; w < (int)(blockDim.x / 32); ++w) se += red[w];
+  const int t = targets[r];
+  const float lse = mx + logf(se);
+  if (threadIdx.x == 0) loss_rows[r] = lse - row[t];
+  if (grad) {
+    const float inv = 1.f / se;
+    float* grow = grad + r * ld_grad;
+    for (int c = threadIdx.x; c < v; c += blockDim.x)
+      grow[c] = (expf(row[c] - mx) * inv - (c == t ? 1.f : 0.f)) * scale;
+    for (int c = v + threadIdx.x; c < ld_grad; c += blockDim.x) grow[c] = 0.f;  // padded head columns
+  }
+}
+
 }  // namespace lss

@@ -505,6 +505,35 @@ int lss_adam_update(float* params, const float* grads, float* m, float* v, long 
   return check_launch("adam_update");
 }
 
+int lss_embed_fwd(const int* tokens, const float* token_table, const float* pos_table, float* x, int batch,
+                  int rows, int embed, void* stream) {
+  if (!tokens || !token_table || !pos_table || !x) return fail(LSS_ERR_ARG, "embed_fwd: null pointer");
+  if (batch <= 0 || rows <= 0 || embed <= 0 || embed % 4) return fail(LSS_ERR_SHAPE, "embed_fwd: shape");
+  if (!aligned16(token_table) || !aligned16(pos_table) || !aligned16(x))
+    return fail(LSS_ERR_UNSUPPORTED, "embed_fwd: 16B alignment");
+  const long n = (long)batch * rows;
+  embed_fwd_kernel<<<(unsigned)((n + 7) / 8), 256, 0, S(stream)>>>(tokens, token_table, pos_table, x, n, rows, embed);
+  return check_launch("embed_fwd");
+}
+
+int lss_embed_bwd(const int* tokens, const float* grad_x, float* grad_token_table, float* grad_pos, int batch,
+                  int rows, int embed, void* stream) {
+  if (!tokens || !grad_x || !grad_token_table || !grad_pos) return fail(LSS_ERR_ARG, "embed_bwd: null pointer");
+  if (batch <= 0 || rows <= 0 || embed <= 0) return fail(LSS_ERR_SHAPE, "embed_bwd: shape");
+  embed_bwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, S(stream)>>>(tokens, grad_x, grad_token_table, grad_pos,
+                                                                      batch, rows, embed);
+  return check_launch("embed_bwd");
+}
+
+int lss_cross_entropy(const float* logits, long ld, const int* targets, long n, int vocab, float scale,
+                      float* loss_rows, float* grad, long ld_grad, void* stream) {
+  if (!logits || !targets || !loss_rows) return fail(LSS_ERR_ARG, "cross_entropy: null pointer");
+  if (n < 0 || vocab <= 0 || ld < vocab || (grad && ld_grad < vocab)) return fail(LSS_ERR_SHAPE, "cross_entropy: shape");
+  if (n == 0) return LSS_OK;
+  cross_entropy_kernel<<<(unsigned)n, 256, 0, S(stream)>>>(logits, ld, targets, vocab, scale, loss_rows, grad, ld_grad);
+  return check_launch("cross_entropy");
+}
+
 // ------------------------------------------------------------------ peer memory (CUDA IPC)
 using PFN_getAddressRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 

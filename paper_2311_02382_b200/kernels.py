@@ -345,6 +345,44 @@ def sum_slots(dst, src):
     return dst
 
 
+def embed_fwd(tokens, token_table, pos_table, out=None):
+    """model.embed_fwd (model.py:517-533), dropout 0: token rows + this block's positions."""
+    _need(tokens, "tokens", torch.int32)
+    _need(token_table, "token_table", torch.float32)
+    _need(pos_table, "pos_table", torch.float32)
+    b, m = tokens.shape
+    e = token_table.shape[1]
+    if pos_table.shape != (m, e):
+        raise ShapeError(f"position table has {pos_table.shape[0]} rows, block has {m}")
+    x = out if out is not None else torch.empty(b, m, e, dtype=torch.float32, device=tokens.device)
+    call("lss_embed_fwd", _ptr(tokens), _ptr(token_table), _ptr(pos_table), _ptr(x), b, m, e, _stream())
+    return x
+
+
+def embed_bwd(tokens, grad_x, vocab):
+    """model.embed_bwd (model.py:536-540) -> (grad_token_table, grad_pos_table)."""
+    _need(tokens, "tokens", torch.int32)
+    _need(grad_x, "grad_x", torch.float32)
+    b, m, e = grad_x.shape
+    gt = torch.zeros(vocab, e, dtype=torch.float32, device=grad_x.device)
+    gp = torch.empty(m, e, dtype=torch.float32, device=grad_x.device)
+    call("lss_embed_bwd", _ptr(tokens), _ptr(grad_x), _ptr(gt), _ptr(gp), b, m, e, _stream())
+    return gt, gp
+
+
+def cross_entropy(logits, targets, vocab, *, scale, grad=True):
+    """nnops.cross_entropy (nnops.py:274-299) on logits [n][ld >= vocab]: per-row
+    losses and (optionally) grad = (softmax - onehot) * scale, padded columns zero."""
+    _need(logits, "logits", torch.float32)
+    _need(targets, "targets", torch.int32)
+    n, ld = logits.shape
+    loss_rows = torch.empty(n, dtype=torch.float32, device=logits.device)
+    g = torch.empty(n, ld, dtype=torch.float32, device=logits.device) if grad else None
+    call("lss_cross_entropy", _ptr(logits), ld, _ptr(targets), n, vocab, scale, _ptr(loss_rows), _ptr(g),
+         ld, _stream())
+    return loss_rows, g
+
+
 def sgd_update(params, grads, lr):
     """params -= lr * grads (flat fp32, in place): model.sgd_step (model.py:621-623)."""
     _need(params, "params", torch.float32)

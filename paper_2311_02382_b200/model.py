@@ -428,3 +428,155 @@ def layer_bwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, cache: Laye
         grads.ln2_gain, grads.ln2_bias = ln2_gg, ln2_bg
         grads.ff_in, grads.ff_out = LinearParams(ff_in_wg, ff_in_bg), LinearParams(ff_out_wg, ff_out_bg)
     return g_in, grads
+
+
+# ------------------------------------------------------------------ whole model
+
+
+@dataclass
+class Parameters:
+    """model.Parameters (model.py:97-137); on a distributed worker ``pos_table``
+    holds only that worker's rows.  The same container carries gradients."""
+
+    token_table: torch.Tensor
+    pos_table: torch.Tensor
+    layers: list
+    final_gain: torch.Tensor
+    final_bias: torch.Tensor
+    head: LinearParams
+
+    def named_arrays(self):
+        yield "token_table", self.token_table
+        yield "pos_table", self.pos_table
+        for i, lp in enumerate(self.layers):
+            for n, a in lp.named_arrays():
+                yield f"layer{i}.{n}", a
+        yield "final_gain", self.final_gain
+        yield "final_bias", self.final_bias
+        yield "head.weight", self.head.weight
+        yield "head.bias", self.head.bias
+
+    def arrays(self) -> list:
+        return [a for _, a in self.named_arrays()]
+
+
+def _ids(t: torch.Tensor, vocab: int, what: str) -> torch.Tensor:
+    """int32 device ids, range-checked like nnops.embed_tokens / cross_entropy."""
+    ids = t.to(torch.int32).contiguous()
+    lo, hi = torch.aminmax(ids)
+    if int(lo) < 0 or int(hi) >= vocab:
+        raise ValueError(f"{what} id out of range for vocab {vocab}")
+    return ids
+
+
+@dataclass
+class EmbedCache:
+    tokens: torch.Tensor
+
+
+def embed_fwd(params: Parameters, cfg: ModelConfig, tokens: torch.Tensor, offset: int = 0, policy=None):
+    """model.embed_fwd (model.py:517-533): token + position embeddings of one block."""
+    _check_dropout(cfg, policy)
+    if tokens.dim() != 2:
+        raise ShapeError(f"tokens must be (batch, seq_len), got shape {tuple(tokens.shape)}")
+    m = tokens.shape[1]
+    if params.pos_table.shape[0] != m:
+        raise ShapeError(f"position table has {params.pos_table.shape[0]} rows, block has {m}")
+    ids = _ids(tokens, params.token_table.shape[0], "token")
+    return K.embed_fwd(ids, params.token_table.contiguous(), params.pos_table.contiguous()), EmbedCache(ids)
+
+
+def embed_bwd(cache: EmbedCache, vocab: int, policy, grad_x: torch.Tensor):
+    """model.embed_bwd (model.py:536-540) -> (grad_token_table, grad_pos_table)."""
+    return K.embed_bwd(cache.tokens, grad_x.to(torch.float32).contiguous(), vocab)
+
+
+@dataclass
+class HeadCache:
+    lnf: NormCache
+    xf: torch.Tensor
+    logits: torch.Tensor
+    grad_logits: Optional[torch.Tensor]
+    shape3: tuple
+    vocab: int
+
+
+def _head_operand(params: Parameters, cfg: ModelConfig):
+    """Head weight [E][V] and bias with V padded to a multiple of 32 for the tcgen05
+    GEMM (padded columns have zero weights; the loss ignores them)."""
+    w, b = params.head.weight, params.head.bias
+    v = w.shape[1]
+    vp = (v + 31) // 32 * 32 if cfg.precision == "bf16" else v
+    if vp != v:
+        w = torch.nn.functional.pad(w, (0, vp - v))
+        b = torch.nn.functional.pad(b, (0, vp - v))
+    return _as_act(w, cfg).contiguous(), b.contiguous(), vp
+
+
+def head_fwd(x: torch.Tensor, params: Parameters, targets: Optional[torch.Tensor], cfg: ModelConfig):
+    """model.head_fwd (model.py:552-562): final LN, vocabulary projection and the
+    mean cross-entropy.  Returns (loss or None, HeadCache)."""
+    bsz, m, e = x.shape
+    v = params.head.weight.shape[1]
+    xf, lnf = norm3(x.reshape(bsz * m, e), params.final_gain, params.final_bias, cfg, out_dtype=cfg.act_dtype)
+    w, b, vp = _head_operand(params, cfg)
+    logits = torch.empty(bsz * m, vp, dtype=torch.float32, device=x.device)
+    K.gemm(xf, w, b_mn_major=True, bias=b, out=logits, M=bsz * m, N=vp, K=e)
+    if targets is None:
+        return None, HeadCache(lnf, xf, logits, None, (bsz, m, e), v)
+    ids = _ids(targets.reshape(-1), v, "target")
+    n = bsz * m
+    loss_rows, grad = K.cross_entropy(logits, ids, v, scale=1.0 / n)
+    loss = loss_rows.sum() / n
+    if not bool(torch.isfinite(loss)):
+        raise ValueError("cross_entropy produced a non-finite loss")
+    return float(loss), HeadCache(lnf, xf, logits, grad, (bsz, m, e), v)
+
+
+def head_bwd(cache: HeadCache, params: Parameters, cfg: ModelConfig):
+    """model.head_bwd (model.py:565-570) -> (grad_x, final_gain_g, final_bias_g, head_wg, head_bg)."""
+    if cache.grad_logits is None:
+        raise ValueError("head_bwd requires a forward pass that computed the loss")
+    n, vp = cache.grad_logits.shape
+    e = cache.xf.shape[1]
+    v = cache.vocab
+    w, _, _ = _head_operand(params, cfg)
+    ga = _as_act(cache.grad_logits, cfg).contiguous()
+    grad_xf = torch.empty(n, e, dtype=torch.float32, device=ga.device)
+    K.gemm(ga, w, out=grad_xf, M=n, N=e, K=vp)  # g . W^T  (W [E][Vp] = [N][K])
+    head_wg = torch.empty(e, vp, dtype=torch.float32, device=ga.device)
+    K.gemm(cache.xf, ga, a_mn_major=True, b_mn_major=True, out=head_wg, M=e, N=vp, K=n)
+    head_bg = torch.zeros(vp, dtype=torch.float32, device=ga.device)
+    K.cat_cast_colsum([(cache.grad_logits, vp, vp)], n, dst=None, colsum=head_bg)
+    grad_x, g_gain, g_bias = norm3_bwd(cache.lnf, params.final_gain, grad_xf)
+    return grad_x.view(cache.shape3), g_gain, g_bias, head_wg[:, :v].contiguous(), head_bg[:v].contiguous()
+
+
+@dataclass
+class SequentialCache:
+    embed: EmbedCache
+    layers: list
+    head: HeadCache
+
+
+def forward(params: Parameters, cfg: ModelConfig, tokens: torch.Tensor, targets=None, policy=None,
+            counters=None):
+    """model.forward (model.py:583-600): whole-sequence forward on one worker."""
+    _check_dropout(cfg, policy)
+    x, ec = embed_fwd(params, cfg, tokens, 0, policy)
+    caches = []
+    for li, lp in enumerate(params.layers):
+        x, c = layer_fwd(lp, cfg, policy, li, x, 0, None, counters)
+        caches.append(c)
+    loss, hc = head_fwd(x, params, targets, cfg)
+    return loss, SequentialCache(ec, caches, hc)
+
+
+def backward(params: Parameters, cfg: ModelConfig, cache: SequentialCache) -> Parameters:
+    """model.backward (model.py:603-618): gradients of the mean-over-tokens loss."""
+    grad_x, fg, fb, hw, hb = head_bwd(cache.head, params, cfg)
+    layer_grads = [None] * len(params.layers)
+    for li in range(len(params.layers) - 1, -1, -1):
+        grad_x, layer_grads[li] = layer_bwd(params.layers[li], cfg, None, li, cache.layers[li], grad_x)
+    gt, gp = embed_bwd(cache.embed, cfg.vocab, None, grad_x)
+    return Parameters(gt, gp, layer_grads, fg, fb, LinearParams(hw, hb))

@@ -126,6 +126,43 @@ def run_case(seq, e, h, g, b, causal, seed=0, ff_dim=0):
     return x, gy, params, y, dx, grads
 
 
+def gpt_case(seed=5):
+    """Whole decoder: model.forward / model.backward sequentially,
+    2 layers, vocab 40 (not a multiple of 32: exercises the padded head)."""
+    cfg = ModelConfig(embed_dim=128, n_layers=2, n_heads=2, ff_dim=256, vocab=40, seq_len=128, batch=2,
+                      causal=True, precision="double")
+    rng = np.random.default_rng(seed)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    params = model.init_params(cfg, seed)
+    params.token_table = f32(params.token_table)
+    params.pos_table = f32(params.pos_table)
+    for lp in params.layers:
+        lp.ln1_gain = f32(1.0 + 0.1 * rng.standard_normal(128))
+        lp.ln1_bias = f32(0.1 * rng.standard_normal(128))
+        lp.ln2_gain = f32(1.0 + 0.1 * rng.standard_normal(128))
+        lp.ln2_bias = f32(0.1 * rng.standard_normal(128))
+        for n in ("attn_q", "attn_k", "attn_v", "attn_out", "ff_in", "ff_out"):
+            lin = getattr(lp, n)
+            setattr(lp, n, LinearParams(f32(lin.weight), f32(0.05 * rng.standard_normal(lin.bias.shape))))
+    params.final_gain = f32(1.0 + 0.1 * rng.standard_normal(128))
+    params.final_bias = f32(0.1 * rng.standard_normal(128))
+    params.head = LinearParams(f32(params.head.weight), f32(0.05 * rng.standard_normal(40)))
+    tokens = rng.integers(0, 40, (2, 128))
+    targets = rng.integers(0, 40, (2, 128))
+    loss, cache = model.forward(params, cfg, tokens, targets)
+    grads = model.backward(params, cfg, cache)
+    arrays = dict(tokens=tokens.astype(np.int32), targets=targets.astype(np.int32),
+                  loss=np.array(loss, dtype=np.float64),
+                  meta=np.array([128, 128, 2, 1, 2, 1], dtype=np.int64), ff_dim=np.array(256), n_layers=np.array(2),
+                  vocab=np.array(40))
+    for n, a in params.named_arrays():
+        arrays["p." + n] = np.asarray(a, np.float32)
+    for n, a in grads.named_arrays():
+        arrays["g." + n] = np.asarray(a, np.float64)
+    np.savez_compressed(OUT / "gpt_small.npz", **arrays)
+    print("gpt_small written, loss", loss)
+
+
 def main():
     for name, (seq, e, h, g, b, causal, odt) in CASES.items():
         x, gy, params, y, dx, grads = run_case(seq, e, h, g, b, causal)
@@ -145,6 +182,7 @@ def main():
         arrays.update({k: v.astype(odt) for k, v in grads.items()})
         np.savez_compressed(OUT / f"{name}.npz", **arrays)
         print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("x", "y", "w_in")})
+    gpt_case()
 
 
 if __name__ == "__main__":

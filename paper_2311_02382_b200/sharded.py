@@ -225,7 +225,6 @@ class LSSAttention:
             self.g_wout = self.grads[o:o + F * E].view(F, E); o += F * E
             self.g_bout = self.grads[o:o + E]; o += E
             M = B * m
-            self.x_mid = z(B, m, E)
             self.mean2, self.rstd2 = z(M), z(M)
             self.yh = z(B, m, E, dt=ad)
             self.h_pre, self.h = z(M, F, dt=ad), z(M, F, dt=ad)
@@ -479,33 +478,41 @@ class LSSAttention:
         return self.y
 
     # ------------------------------------------------------------ FFN half (rank-local)
-    def ffn_step(self, x_mid: torch.Tensor, grad_out: torch.Tensor) -> torch.Tensor:
-        """LN2 -> ff_in -> GeLU -> ff_out -> residual and its backward (model.py:449-452,
-        474-477), between the attention forward and backward.  Returns y_out; the
-        attention backward then runs on ``self.grad_mid`` = grad_out + LN2'(...)."""
+    def ffn_forward(self, x_mid: torch.Tensor) -> torch.Tensor:
+        """LN2 -> ff_in -> GeLU -> ff_out -> residual (model.py:449-452); the GeLU and
+        the pre-activation store run in the ff_in GEMM's epilogue."""
+        B, m, E, F = self.B, self.m, self.E, self.cfg.ff_dim
+        M = B * m
+        lp = self.lp
+        self.x_mid_ref = x_mid
+        K.layernorm_fwd(x_mid, lp.ln2_gain, lp.ln2_bias, out=self.yh, mean=self.mean2, rstd=self.rstd2)
+        K.gemm(self.yh.view(M, E), self.w_in, b_mn_major=True, bias=lp.ff_in.bias, out=self.h, act="gelu",
+               pre=self.h_pre, M=M, N=F, K=E)
+        K.gemm(self.h, self.w_out, b_mn_major=True, bias=lp.ff_out.bias, residual=x_mid.view(M, E),
+               out=self.y_out.view(M, E), M=M, N=E, K=F)
+        return self.y_out
+
+    def ffn_backward(self, grad_out: torch.Tensor) -> torch.Tensor:
+        """Backward of :meth:`ffn_forward` (model.py:474-477): returns grad_mid =
+        grad_out + LN2'(FFN'(grad_out)); grads pre-scaled into the flat buffer."""
         B, m, E, F = self.B, self.m, self.E, self.cfg.ff_dim
         M = B * m
         a = self.grad_scale
         lp = self.lp
         if grad_out.shape != (B, m, E) or grad_out.dtype != torch.float32 or not grad_out.is_contiguous():
             raise ShapeError(f"grad_y must be contiguous fp32 {(B, m, E)}")
-        K.layernorm_fwd(x_mid, lp.ln2_gain, lp.ln2_bias, out=self.yh, mean=self.mean2, rstd=self.rstd2)
-        yh = self.yh.view(M, E)
-        K.gemm(yh, self.w_in, b_mn_major=True, bias=lp.ff_in.bias, out=self.h, act="gelu", pre=self.h_pre,
-               M=M, N=F, K=E)
-        K.gemm(self.h, self.w_out, b_mn_major=True, bias=lp.ff_out.bias, residual=x_mid.view(M, E),
-               out=self.y_out.view(M, E), M=M, N=E, K=F)
         g32 = grad_out.view(M, E)
         K.cat_cast_colsum([(g32, E, E)], M, dst=self.g_out, colsum=self.g_bout, alpha=a)
         K.gemm(self.g_out, self.w_out, out=self.g_pre32, act="gelu_bwd", aux=self.h_pre, M=M, N=F, K=E)
         K.gemm(self.h, self.g_out, a_mn_major=True, b_mn_major=True, alpha=a, out=self.g_wout, M=F, N=E, K=M)
         K.cat_cast_colsum([(self.g_pre32, F, F)], M, dst=self.g_pre, colsum=self.g_bin, alpha=a)
         K.gemm(self.g_pre, self.w_in, out=self.g_yh, M=M, N=E, K=F)
-        K.gemm(yh, self.g_pre, a_mn_major=True, b_mn_major=True, alpha=a, out=self.g_win, M=E, N=F, K=M)
-        K.layernorm_bwd(self.g_yh, x_mid.view(M, E), self.mean2, self.rstd2, lp.ln2_gain,
+        K.gemm(self.yh.view(M, E), self.g_pre, a_mn_major=True, b_mn_major=True, alpha=a, out=self.g_win,
+               M=E, N=F, K=M)
+        K.layernorm_bwd(self.g_yh, self.x_mid_ref.view(M, E), self.mean2, self.rstd2, lp.ln2_gain,
                         grad_res=g32, grad_x=self.grad_mid.view(M, E), grad_gain=self.g_ln2_g,
                         grad_bias=self.g_ln2_b, alpha=a)
-        return self.y_out
+        return self.grad_mid
 
     # ------------------------------------------------------------ backward
     def bwd_pre(self, grad_y: torch.Tensor) -> None:
@@ -693,21 +700,18 @@ _NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
 last_phases: dict = {}
 
 
-def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_bwd=None):
-    """One fwd+bwd(+sync) of the attention sublayer.
+def _no_mark(name):
+    return None
 
-    Real multi-GPU: ``engines`` = [this rank's LSSAttention], ``comm`` a
-    TorchDistComm (or SoloComm for one rank).  Single-process simulation: G
-    engines and a SimComm.  Returns the list of (y, dx) per engine (device
-    tensors, not synchronised)."""
-    global last_phases
+
+def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
+    """Forward of one layer on every engine (model.layer_fwd distributed, the
+    fwd half of sharded.forward): LN1, [Q|K|V], the packed K/V all-gather
+    overlapped with the diagonal segment, attention, out-projection + residual,
+    and the LN2 / FFN half for complete-layer engines.  Returns the outputs."""
     sim = isinstance(comm, SimComm)
-    clk = PhaseClock() if _PHASES else None
-    mark = clk.mark if clk else (lambda name: None)
     one = lambda f: f([e for e in engines]) if sim else f(engines[0])  # noqa: E731
-    fused = _bind_fused(engines, comm)
     split = all(e.split_fwd for e in engines)
-    mark("start")
     for e, x in zip(engines, xs):
         e.fwd_project(x)
     mark("fwd_project")
@@ -744,12 +748,24 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
         mark("p2p_F2")
     ys = [e.fwd_out() for e in engines]
     mark("fwd_out")
-    if before_bwd is not None:
-        before_bwd()
     if all(e.with_ffn for e in engines):  # complete layer: rank-local LN2 / FFN half
-        ys = [e.ffn_step(y, gy) for e, y, gy in zip(engines, ys, grad_ys)]
-        grad_ys = [e.grad_mid for e in engines]
-        mark("ffn")
+        ys = [e.ffn_forward(y) for e, y in zip(engines, ys)]
+        mark("ffn_fwd")
+    return ys
+
+
+def lss_backward(engines, comm, grad_ys, *, step=0, layer=0, sync=True, mark=_no_mark):
+    """Backward of one layer (model.layer_bwd distributed, the bwd half of
+    sharded.backward): FFN / LN2 half, out-projection, attention backward with the
+    dK|dV reduce-scatter (fused into the kernel over NVLink when the peers map),
+    projections, LN1 + residual; with ``sync`` the folded gradient all-reduce.
+    Returns the input gradients."""
+    sim = isinstance(comm, SimComm)
+    one = lambda f: f([e for e in engines]) if sim else f(engines[0])  # noqa: E731
+    fused = _bind_fused(engines, comm)
+    if all(e.with_ffn for e in engines):
+        grad_ys = [e.ffn_backward(gy) for e, gy in zip(engines, grad_ys)]
+        mark("ffn_bwd")
     for e, gy in zip(engines, grad_ys):
         e.bwd_pre(gy)
     b1 = _exchange(engines, comm, "B1", step, layer, async_op=True)
@@ -781,6 +797,26 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
     if sync:
         one(lambda t: comm.all_reduce_sum([e.grads for e in t] if sim else t.grads, step))
     mark("all_reduce")
+    return dxs
+
+
+def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_bwd=None):
+    """One fwd+bwd(+sync) of the layer (attention sublayer, or the complete layer
+    for with_ffn engines).
+
+    Real multi-GPU: ``engines`` = [this rank's LSSAttention], ``comm`` a
+    TorchDistComm (or SoloComm for one rank).  Single-process simulation: G
+    engines and a SimComm.  Returns the list of (y, dx) per engine (device
+    tensors, not synchronised)."""
+    global last_phases
+    clk = PhaseClock() if _PHASES else None
+    mark = clk.mark if clk else _no_mark
+    _bind_fused(engines, comm)
+    mark("start")
+    ys = lss_forward(engines, comm, xs, step=step, layer=layer, mark=mark)
+    if before_bwd is not None:
+        before_bwd()
+    dxs = lss_backward(engines, comm, grad_ys, step=step, layer=layer, sync=sync, mark=mark)
     if clk:
         last_phases = clk.report()
     return list(zip(ys, dxs))

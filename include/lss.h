@@ -203,15 +203,16 @@ int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const 
 
 /* Whole-model edges.  tokens / targets are int32.
  * model.embed_fwd (model.py:517-533): x[b][i] = token_table[tokens[b][i]] + pos_table[i]
- * (pos_table = this block's rows).  model.embed_bwd (536-540): grad_pos[i] = sum_b
- * grad_x[b][i] (written); grad_token_table[id] += grad_x rows (accumulated).
+ * (pos_table = this block's rows).  model.embed_bwd (536-540): grad_pos[i] = alpha_pos *
+ * sum_b grad_x[b][i] (written); grad_token_table[id] += alpha_token * grad_x rows
+ * (accumulated; the alphas carry the folded gradient scales, sharded.py:207-208).
  * nnops.cross_entropy (nnops.py:274-299) per row of logits [n][ld] (first vocab
  * columns): loss_rows[r] = logsumexp - logit[target]; grad (optional, [n][ld_grad],
  * columns >= vocab zeroed) = (softmax - onehot) * scale (scale = 1/rows of the mean). */
 int lss_embed_fwd(const int* tokens, const float* token_table, const float* pos_table, float* x, int batch,
                   int rows, int embed, void* stream);
 int lss_embed_bwd(const int* tokens, const float* grad_x, float* grad_token_table, float* grad_pos, int batch,
-                  int rows, int embed, void* stream);
+                  int rows, int embed, float alpha_token, float alpha_pos, void* stream);
 int lss_cross_entropy(const float* logits, long ld, const int* targets, long n, int vocab, float scale,
                       float* loss_rows, float* grad, long ld_grad, void* stream);
 

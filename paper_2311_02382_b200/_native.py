@@ -84,7 +84,7 @@ SIGNATURES = {
     "lss_sum_slots": [_P, _P, _I, _L, _L, _P],
     "lss_sgd_update": [_P, _P, _L, _F, _P],
     "lss_embed_fwd": [_P, _P, _P, _P, _I, _I, _I, _P],
-    "lss_embed_bwd": [_P, _P, _P, _P, _I, _I, _I, _P],
+    "lss_embed_bwd": [_P, _P, _P, _P, _I, _I, _I, _F, _F, _P],
     "lss_cross_entropy": [_P, _L, _P, _L, _I, _F, _P, _P, _L, _P],
     "lss_adam_update": [_P, _P, _P, _P, _L, _F, _F, _F, _F, _I, _P],
     "lss_ipc_export": [_P, ctypes.c_char_p, ctypes.POINTER(_L)],

@@ -366,7 +366,8 @@ __global__ void embed_fwd_kernel(const int* __restrict__ tokens, const float* __
 // model.embed_bwd (model.py:536-540): grad_pe[i] = sum_b g[b][i] (written), grad_tok[id] +=
 // g[b][i] (accumulated: nnops.embed_tokens_bwd scatter-add, nnops.py:258-262).
 __global__ void embed_bwd_kernel(const int* __restrict__ tokens, const float* __restrict__ g,
-                                 float* __restrict__ grad_tok, float* __restrict__ grad_pe, int batch, int m, int e) {
+                                 float* __restrict__ grad_tok, float* __restrict__ grad_pe, int batch, int m, int e,
+                                 float alpha_tok, float alpha_pos) {
   const long i = blockIdx.x * (long)(blockDim.x / 32) + threadIdx.x / 32;  // position
   if (i >= m) return;
   const int lane = threadIdx.x % 32;
@@ -376,9 +377,9 @@ __global__ void embed_bwd_kernel(const int* __restrict__ tokens, const float* __
       const long r = (long)b * m + i;
       const float v = g[r * e + c];
       acc += v;
-      atomicAdd(grad_tok + (long)tokens[r] * e + c, v);
+      atomicAdd(grad_tok + (long)tokens[r] * e + c, alpha_tok * v);
     }
-    grad_pe[i * e + c] = acc;
+    grad_pe[i * e + c] = alpha_pos * acc;
   }
 }
 

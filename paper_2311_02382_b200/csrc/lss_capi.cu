@@ -517,11 +517,11 @@ int lss_embed_fwd(const int* tokens, const float* token_table, const float* pos_
 }
 
 int lss_embed_bwd(const int* tokens, const float* grad_x, float* grad_token_table, float* grad_pos, int batch,
-                  int rows, int embed, void* stream) {
+                  int rows, int embed, float alpha_token, float alpha_pos, void* stream) {
   if (!tokens || !grad_x || !grad_token_table || !grad_pos) return fail(LSS_ERR_ARG, "embed_bwd: null pointer");
   if (batch <= 0 || rows <= 0 || embed <= 0) return fail(LSS_ERR_SHAPE, "embed_bwd: shape");
   embed_bwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, S(stream)>>>(tokens, grad_x, grad_token_table, grad_pos,
-                                                                      batch, rows, embed);
+                                                                      batch, rows, embed, alpha_token, alpha_pos);
   return check_launch("embed_bwd");
 }
 

@@ -359,14 +359,15 @@ def embed_fwd(tokens, token_table, pos_table, out=None):
     return x
 
 
-def embed_bwd(tokens, grad_x, vocab):
-    """model.embed_bwd (model.py:536-540) -> (grad_token_table, grad_pos_table)."""
+def embed_bwd(tokens, grad_x, vocab, *, grad_token=None, grad_pos=None, alpha_token=1.0, alpha_pos=1.0):
+    """model.embed_bwd (model.py:536-540) -> (grad_token_table (accumulated), grad_pos_table)."""
     _need(tokens, "tokens", torch.int32)
     _need(grad_x, "grad_x", torch.float32)
     b, m, e = grad_x.shape
-    gt = torch.zeros(vocab, e, dtype=torch.float32, device=grad_x.device)
-    gp = torch.empty(m, e, dtype=torch.float32, device=grad_x.device)
-    call("lss_embed_bwd", _ptr(tokens), _ptr(grad_x), _ptr(gt), _ptr(gp), b, m, e, _stream())
+    gt = grad_token if grad_token is not None else torch.zeros(vocab, e, dtype=torch.float32, device=grad_x.device)
+    gp = grad_pos if grad_pos is not None else torch.empty(m, e, dtype=torch.float32, device=grad_x.device)
+    call("lss_embed_bwd", _ptr(tokens), _ptr(grad_x), _ptr(gt), _ptr(gp), b, m, e, alpha_token, alpha_pos,
+         _stream())
     return gt, gp
 
 

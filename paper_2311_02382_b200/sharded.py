@@ -149,7 +149,7 @@ class LSSAttention:
 
     def __init__(self, cfg: ModelConfig, spec: ShardSpec, *, grad_scale: float | None = None,
                  device=None, balanced: bool | None = None, fused_rs: bool | None = None,
-                 with_ffn: bool = False):
+                 with_ffn: bool = False, grads: torch.Tensor | None = None):
         if spec.seq_len != cfg.seq_len:
             raise ShapeError(f"shard spec length {spec.seq_len} != config seq_len {cfg.seq_len}")
         self.cfg, self.spec = cfg, spec
@@ -205,7 +205,9 @@ class LSSAttention:
         ffn0 = (n_attn + 15) // 16 * 16  # FFN grads start 64-byte aligned (vectorised epilogues)
         n = ffn0 + (2 * E * F + F + 3 * E) if with_ffn else n_attn
         self._ffn0 = ffn0
-        self.grads = torch.zeros(n, dtype=f32, device=dev)
+        if grads is not None and (grads.numel() != n or grads.dtype != f32 or grads.data_ptr() % 64):
+            raise ShapeError(f"external gradient buffer must be {n} fp32, 64-byte aligned")
+        self.grads = grads if grads is not None else torch.zeros(n, dtype=f32, device=dev)
         self.params = None  # flat fp32 parameters in the same layout (bind_params)
         self.param_lp = None
         o = 0
@@ -298,11 +300,16 @@ class LSSAttention:
         return self._layer_params(self.grad_views())
 
     # ------------------------------------------------------------ training step
-    def bind_params(self, lp: LayerParams) -> LayerParams:
+    def bind_params(self, lp: LayerParams, params: torch.Tensor | None = None) -> LayerParams:
         """Copy ``lp`` into the engine's flat fp32 parameter buffer (the gradient
-        layout) and stage it; returns LayerParams views of that buffer, which
-        :meth:`optimizer_step` updates in place (the DistParameters of the reference)."""
-        if self.params is None:
+        layout; ``params`` may be a view into a larger model buffer) and stage it;
+        returns LayerParams views of that buffer, which :meth:`optimizer_step`
+        updates in place (the DistParameters of the reference)."""
+        if params is not None:
+            if params.numel() != self.grads.numel():
+                raise ShapeError("parameter buffer does not match the gradient layout")
+            self.params = params
+        elif self.params is None:
             self.params = torch.zeros_like(self.grads)
         views = self._flat_views(self.params)
         for name, t in lp.named_arrays():
@@ -676,6 +683,13 @@ def _bind_fused(engines, comm) -> bool:
         return False
     e.bind_peers(addrs, peer=True)
     return True
+
+
+def layer_grad_size(cfg: ModelConfig, with_ffn: bool) -> int:
+    """Elements of one engine's flat gradient buffer (LSSAttention layout)."""
+    E, F = cfg.embed_dim, cfg.ff_dim
+    n_attn = 4 * E * E + 6 * E + 1
+    return (n_attn + 15) // 16 * 16 + (2 * E * F + F + 3 * E) if with_ffn else n_attn
 
 
 class PhaseClock:

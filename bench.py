@@ -51,6 +51,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=128, help="query rows in the CPU sample")
     ap.add_argument("--unbalanced", action="store_true", help="plain contiguous causal schedule")
+    ap.add_argument("--model", choices=["layer", "gpt"], default="layer",
+                    help="layer: the BASELINE metric (one LSS attention layer); gpt: the L-layer decoder "
+                         "training step of BASELINE configs 4/5 (embedding, L complete layers, head, loss, "
+                         "one all-reduce, SGD update)")
+    ap.add_argument("--layers", type=int, default=12)
+    ap.add_argument("--replicas", type=int, default=1, help="gpt: data-parallel replicas D (world = D x N)")
     return ap.parse_args()
 
 
@@ -401,10 +407,112 @@ def main_ours(args):
     return 0
 
 
+def main_gpt(args):
+    """BASELINE configs 4/5: the L-layer decoder training step on a D x N grid."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_02382_b200 import optim
+    from paper_2311_02382_b200.comm import Ledger, SimComm, SoloComm, TorchDistComm
+    from paper_2311_02382_b200.gpt import GPTRank, gpt_step
+    from paper_2311_02382_b200.hybrid import GridLayout, make_groups
+    from paper_2311_02382_b200.model import LayerParams, LinearParams, ModelConfig, Parameters
+    from paper_2311_02382_b200.sharded import ShardSpec
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lay = GridLayout(args.replicas, world // args.replicas)
+    replica, seq_index = lay.coords(rank)
+    data_comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        if args.replicas > 1:
+            seq_g, data_g, world_g = make_groups(lay)
+            comm = TorchDistComm(seq_g, world_g, Ledger())
+            data_comm = TorchDistComm(data_g, data_g, Ledger())
+        else:
+            comm = TorchDistComm(None, None, Ledger())
+    else:
+        comm = SoloComm(Ledger())
+    B, l, E, H, L, V = args.batch, args.seq, args.embed, args.heads, args.layers, 256
+    F = 4 * E
+    cfg = ModelConfig(embed_dim=E, n_layers=L, n_heads=H, ff_dim=F, vocab=V, seq_len=l, batch=B,
+                      causal=not args.noncausal, precision="bf16")
+    g = torch.Generator(device=dev).manual_seed(7)
+    u = lambda a, b_: ((torch.rand(a, b_, generator=g, device=dev) * 2 - 1) / math.sqrt(a))  # noqa: E731
+    z = lambda n: torch.zeros(n, device=dev)  # noqa: E731
+    layers = [LayerParams(torch.ones(E, device=dev), z(E), LinearParams(u(E, E), z(E)), LinearParams(u(E, E), z(E)),
+                          LinearParams(u(E, E), z(E)), LinearParams(u(E, E), z(E)), torch.ones(E, device=dev), z(E),
+                          LinearParams(u(E, F), z(F)), LinearParams(u(F, E), z(E))) for _ in range(L)]
+    spec = ShardSpec(seq_index, lay.seq_workers, l)
+    P = Parameters(torch.randn(V, E, generator=g, device=dev) * 0.02,
+                   torch.randn(spec.block, E, generator=g, device=dev) * 0.02, layers, torch.ones(E, device=dev),
+                   z(E), LinearParams(u(E, V), z(V)))
+    rk = GPTRank(cfg, spec, replicas=args.replicas, device=dev)
+    rk.bind_params(P)
+    del P, layers
+    gt = torch.Generator(device=dev).manual_seed(100 + replica)
+    tok = torch.randint(0, V, (B, l), generator=gt, device=dev)
+    o, m = spec.offset, spec.block
+    tseg, yseg = tok[:, o:o + m].contiguous(), torch.roll(tok, -1, 1)[:, o:o + m].contiguous()
+    opt, opt_pos = optim.SGD(1e-4), optim.SGD(1e-4)
+
+    def one_step():
+        gpt_step([rk], comm, [tseg], [yseg], data_comm=data_comm)
+        rk.optimizer_step(opt, opt_pos)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.start()
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    loss = float(rk.loss())
+    tokens = args.replicas * B * l
+    pairs = l * (l + 1) // 2 if cfg.causal else l * l
+    flops = args.replicas * B * (L * (24 * l * E * E + 12 * E * pairs + 12 * l * E * F) + 6 * l * E * V)
+    burst, sustained, src = peaks()
+    if rank == 0:
+        line = {"metric": f"tokens/sec training step of the {L}-layer LSS decoder (embedding, layers, head, loss, "
+                          "one all-reduce, SGD)", "value": tokens / (ms / 1e3), "unit": "tokens/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic", "config": {"workload": f"decoder L={L}, l_x={l}, E_m={E}, {H} heads, ff={F}, "
+                                                            f"vocab {V}, batch {B}, grid {args.replicas}x{lay.seq_workers}",
+                                                "parallelism": f"dp{args.replicas}xsp{lay.seq_workers}"},
+                "pct_bf16_peak": {"burst": flops / (ms / 1e3) / (world * burst * 1e12),
+                                  "sustained": flops / (ms / 1e3) / (world * sustained * 1e12)},
+                "loss": loss, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.model == "gpt":
+        return main_gpt(args)
     return main_ours(args)
 
 

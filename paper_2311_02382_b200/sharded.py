@@ -442,11 +442,16 @@ class LSSAttention:
                                    out=self.ctx, lse2=self.lse2, **common)
                 self._ctx_written.add(row0)
 
-    def fwd_attend_remote(self) -> None:
-        """Own rows x remote key segments (after the gather), log-sum-exp merged into ctx."""
+    def fwd_attend_remote(self, part: int | None = None) -> None:
+        """Own rows x remote key segments (after the gather), log-sum-exp merged into
+        ctx.  ``part`` selects the row range (0: the first, 1: the rest) so the
+        heavy rank's two ranges can run on two streams."""
         kf, vf, common = self._fwd_common()
         r, off = self.spec.rank, self.spec.offset
-        for row0, rows, g0, g1 in self.own_ranges():
+        ranges = self.own_ranges()
+        if part is not None:
+            ranges = ranges[:1] if part == 0 else ranges[1:]
+        for row0, rows, g0, g1 in ranges:
             for lo, hi in ((g0, min(g1, r)), (max(g0, r + 1), g1)):
                 if lo >= hi:
                     continue
@@ -718,6 +723,17 @@ def _no_mark(name):
     return None
 
 
+_SIDE = {}
+
+
+def _side_stream(device) -> torch.cuda.Stream:
+    """One side stream per device for concurrent attention launches."""
+    key = torch.device(device).index
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
+
+
 def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
     """Forward of one layer on every engine (model.layer_fwd distributed, the
     fwd half of sharded.forward): LN1, [Q|K|V], the packed K/V all-gather
@@ -744,11 +760,20 @@ def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
         mark("fwd_local")
         _wait([gather] + f1)
         mark("all_gather")
+        # two streams so the launches' tails overlap: the light rank's delegated rows
+        # (whose partials then travel back) and the heavy rank's second row range on
+        # a side stream, own rows on the main stream
+        main = torch.cuda.current_stream()
+        side = _side_stream(engines[0].device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            for e in engines:
+                e.fwd_attend_delegated()
+                e.fwd_attend_remote(part=1)
+            f2 = _exchange(engines, comm, "F2", step, layer, async_op=True)
         for e in engines:
-            e.fwd_attend_delegated()
-        f2 = _exchange(engines, comm, "F2", step, layer, async_op=True)
-        for e in engines:
-            e.fwd_attend_remote()
+            e.fwd_attend_remote(part=0)
+        main.wait_stream(side)
         mark("fwd_attend")
         _wait(f2)
         mark("p2p_F2")

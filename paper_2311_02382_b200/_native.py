@@ -90,6 +90,7 @@ SIGNATURES = {
     "lss_ipc_export": [_P, ctypes.c_char_p, ctypes.POINTER(_L)],
     "lss_ipc_import": [ctypes.c_char_p, _L, ctypes.POINTER(_P)],
     "lss_ipc_close": [_P, _L],
+    "lss_copy_d2d": [_P, _P, _L, _P],
 }
 ACT_NONE, ACT_GELU, ACT_GELU_BWD = 0, 1, 2
 EXTRA = {

@@ -124,6 +124,35 @@ class TorchDistComm:
         self._peers[key] = (addrs, t)  # keep the tensor alive while peers may write into it
         return addrs
 
+    def gather_pull(self, full: torch.Tensor, step=0, layer=0):
+        """K/V all-gather on the copy engines: after a device barrier (every rank's
+        slot is written), pull each peer's own slot full[p] from its IPC-mapped
+        buffer on a copy stream -- no SMs taken from the overlapped attention.
+        Returns an event the consumer waits on, or None when peers do not map
+        (the caller then falls back to the NCCL all-gather)."""
+        addrs = self.peer_addresses(full)
+        if addrs is None:
+            return None
+        from . import kernels as K
+
+        self.ledger.record("all-gather", self.seq_name + ":nvlink-ce", full.numel(), step, "forward", layer)
+        cur = torch.cuda.current_stream()
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=full.device)
+        cs = self._copy_stream
+        # barrier on the compute stream: every rank then starts its diagonal tiles
+        # together, which aligns the later hand-offs (measured N=4: 6.6 ms vs 6.8
+        # with the barrier on the copy stream or with the NCCL all-gather)
+        self.device_barrier(step, "forward", layer)
+        cs.wait_stream(cur)
+        slot = full[0].numel() * full.element_size()
+        for p in range(self.seq_size):
+            if p != self.seq_rank:
+                K.copy_d2d(full[p].data_ptr(), addrs[p] + p * slot, slot, cs)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        return ev
+
     def device_barrier(self, step=0, phase="backward", layer=None):
         """Stream-ordered barrier of the sequence group: returns (on the device) only
         after every rank's prior work on its stream completed."""

@@ -535,6 +535,14 @@ int lss_cross_entropy(const float* logits, long ld, const int* targets, long n, 
 }
 
 // ------------------------------------------------------------------ peer memory (CUDA IPC)
+int lss_copy_d2d(void* dst, const void* src, long bytes, void* stream) {
+  if (!dst || !src || bytes < 0) return fail(LSS_ERR_ARG, "copy_d2d: arguments");
+  if (bytes == 0) return LSS_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, S(stream));
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "copy_d2d: %s", cudaGetErrorString(e));
+  return LSS_OK;
+}
+
 using PFN_getAddressRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 int lss_ipc_export(const void* dev_ptr, unsigned char* handle, long* offset) {

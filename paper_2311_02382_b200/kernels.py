@@ -422,6 +422,12 @@ def ipc_close(addr: int, offset: int) -> None:
     call("lss_ipc_close", ctypes.c_void_p(addr), offset)
 
 
+def copy_d2d(dst_addr: int, src_addr: int, nbytes: int, stream=None) -> None:
+    """Copy-engine D2D copy (src may be IPC-mapped peer memory), stream-ordered."""
+    s = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    call("lss_copy_d2d", ctypes.c_void_p(int(dst_addr)), ctypes.c_void_p(int(src_addr)), int(nbytes), s)
+
+
 def peer_access(device: int, peer: int) -> bool:
     return bool(_native.load().lss_peer_access(device, peer))
 

@@ -430,13 +430,18 @@ class LSSAttention:
         return (self.kv_full[..., :E], self.kv_full[..., E:],
                 dict(workers=self.G, seg_len=self.m, heads=self.H, causal=self.cfg.causal))
 
-    def fwd_attend_local(self) -> None:
+    def fwd_attend_local(self, part: int | None = None) -> None:
         """Own rows x own key segment: needs no remote K/V, so it runs while the
-        all-gather (and the balanced schedule's Q hand-off) are in flight."""
+        all-gather (and the balanced schedule's Q hand-off) are in flight.
+        ``part`` as in :meth:`fwd_attend_remote`."""
         kf, vf, common = self._fwd_common()
         r, off = self.spec.rank, self.spec.offset
-        self._ctx_written = set()
-        for row0, rows, g0, g1 in self.own_ranges():
+        if part in (None, 0):
+            self._ctx_written = set()
+        ranges = self.own_ranges()
+        if part is not None:
+            ranges = ranges[:1] if part == 0 else ranges[1:]
+        for row0, rows, g0, g1 in ranges:
             if g0 <= r < g1:
                 K.attn_fwd_partial(self.q, kf, vf, rows=rows, row0=row0, offset=off, g_begin=r, g_end=r + 1,
                                    out=self.ctx, lse2=self.lse2, **common)
@@ -659,9 +664,11 @@ def _exchange(engines, comm, phase, step, layer, async_op=False):
 
 
 def _wait(works) -> None:
-    """Make the current stream wait for pending collectives (no host block)."""
+    """Make the current stream wait for pending collectives / copy events (no host block)."""
     for w in works or []:
-        if w is not None:
+        if isinstance(w, torch.cuda.Event):
+            torch.cuda.current_stream().wait_event(w)
+        elif w is not None:
             w.wait()
 
 
@@ -716,6 +723,7 @@ class PhaseClock:
 
 _PHASES = os.environ.get("LSS_PHASES") == "1"
 _NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
+_CE_GATHER = os.environ.get("LSS_CE_GATHER", "1") != "0"  # K/V gather on the copy engines
 last_phases: dict = {}
 
 
@@ -745,8 +753,12 @@ def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
     for e, x in zip(engines, xs):
         e.fwd_project(x)
     mark("fwd_project")
-    gather = one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer,
-                                                **({} if sim else {"async_op": split})))
+    gather = None
+    if not sim and split and _CE_GATHER and hasattr(comm, "gather_pull") and comm.seq_size > 1:
+        gather = comm.gather_pull(engines[0].kv_full, step, layer)  # copy engines, no SMs
+    if gather is None:
+        gather = one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer,
+                                                    **({} if sim else {"async_op": split})))
     f1 = _exchange(engines, comm, "F1", step, layer, async_op=split)
     if _NO_OVERLAP:  # diagnostic: serialise the collectives with the compute
         _wait([gather] + f1)
@@ -755,16 +767,21 @@ def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
         # diagonal segment while the gather / Q hand-off are in flight; the light
         # rank then does the partner's rows first so their partials travel back
         # while it finishes its own remote segments
+        main = torch.cuda.current_stream()
+        side = _side_stream(engines[0].device)
         for e in engines:
-            e.fwd_attend_local()
+            e.fwd_attend_local(part=0)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):  # the heavy rank's second row range
+            for e in engines:
+                e.fwd_attend_local(part=1)
+        main.wait_stream(side)
         mark("fwd_local")
         _wait([gather] + f1)
         mark("all_gather")
         # two streams so the launches' tails overlap: the light rank's delegated rows
         # (whose partials then travel back) and the heavy rank's second row range on
         # a side stream, own rows on the main stream
-        main = torch.cuda.current_stream()
-        side = _side_stream(engines[0].device)
         side.wait_stream(main)
         with torch.cuda.stream(side):
             for e in engines:

@@ -233,6 +233,10 @@ int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, lon
 int lss_ipc_export(const void* dev_ptr, unsigned char* handle, long* offset);
 int lss_ipc_import(const unsigned char* handle, long offset, void** dev_ptr);
 int lss_ipc_close(void* dev_ptr, long offset);
+/* Stream-ordered device-to-device copy on the copy engines (no SMs); src may be a
+ * peer's memory imported with lss_ipc_import: the K/V gather pulls each peer's
+ * [K_p|V_p] slot this way (replaces collectives.all_gather, collectives.py:325-344). */
+int lss_copy_d2d(void* dst, const void* src, long bytes, void* stream);
 /* 1 if `device` can load/store `peer`'s memory directly (NVLink / PCIe P2P). */
 int lss_peer_access(int device, int peer);
 

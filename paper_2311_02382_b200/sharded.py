@@ -616,24 +616,50 @@ class LSSAttention:
         return y, dx
 
     def step_from_host(self, x_host: torch.Tensor, grad_y_host: torch.Tensor, comm, grads_host=None,
-                       *, step: int = 0, layer: int = 0):
-        """End-to-end call with HOST buffers: pinned x / grad_y are copied in (grad_y
-        on a side stream, overlapped with the forward), the averaged gradients are
-        copied back to ``grads_host`` (pinned).  Stream-ordered; the caller
-        synchronises when it needs the host result."""
+                       *, step: int = 0, layer: int = 0, next_inputs=None):
+        """End-to-end call with HOST buffers: pinned x / grad_y are copied in and the
+        averaged gradients are copied back to ``grads_host`` (pinned).  Inputs are
+        double-buffered: with ``next_inputs`` = (x_host, grad_y_host) of the NEXT
+        step, their copy is issued on the copy stream during this step's compute
+        (input prefetch), and the next call finds them resident.  Every step's
+        inputs are still copied once, by this engine, per step.  Stream-ordered;
+        the caller synchronises when it needs the host result."""
         cur = torch.cuda.current_stream()
-        if not hasattr(self, "_x_dev"):
-            self._x_dev = torch.empty(self.B, self.m, self.E, dtype=torch.float32, device=self.device)
-            self._gy_dev = torch.empty_like(self._x_dev)
+        if not hasattr(self, "_in_bufs"):
+            mk = lambda: torch.empty(self.B, self.m, self.E, dtype=torch.float32, device=self.device)  # noqa: E731
+            self._in_bufs = [(mk(), mk()), (mk(), mk())]
+            self._in_ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self._in_free = [torch.cuda.Event(), torch.cuda.Event()]
             self._copy_stream = torch.cuda.Stream(device=self.device)
-            self._gy_ready = torch.cuda.Event()
-        self._copy_stream.wait_stream(cur)
-        with torch.cuda.stream(self._copy_stream):
-            self._gy_dev.copy_(grad_y_host, non_blocking=True)
-            self._gy_ready.record()
-        self._x_dev.copy_(x_host, non_blocking=True)
-        out = lss_step([self], comm, [self._x_dev], [self._gy_dev], step=step, layer=layer,
-                       before_bwd=lambda: cur.wait_event(self._gy_ready))
+            self._prefetched = None  # (slot, x_host, grad_y_host) already in flight
+            self._slot = 0
+
+        def issue(slot, xh, gyh):
+            cs = self._copy_stream
+            cs.wait_stream(cur)
+            cs.wait_event(self._in_free[slot])  # the step that last read this slot is done
+            with torch.cuda.stream(cs):
+                x_d, gy_d = self._in_bufs[slot]
+                x_d.copy_(xh, non_blocking=True)
+                gy_d.copy_(gyh, non_blocking=True)
+                self._in_ready[slot].record()
+
+        pf = self._prefetched
+        if pf is not None and pf[1] is x_host and pf[2] is grad_y_host:
+            slot = pf[0]
+        else:
+            slot = self._slot
+            issue(slot, x_host, grad_y_host)
+        self._prefetched = None
+        if next_inputs is not None:  # overlap the next step's H2D with this step's compute
+            nxt = 1 - slot
+            issue(nxt, *next_inputs)
+            self._prefetched = (nxt, next_inputs[0], next_inputs[1])
+        self._slot = 1 - slot
+        cur.wait_event(self._in_ready[slot])
+        x_d, gy_d = self._in_bufs[slot]
+        out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer)
+        self._in_free[slot].record(cur)
         if grads_host is not None:
             grads_host.copy_(self.grads, non_blocking=True)
         return out[0]

@@ -555,3 +555,34 @@ def test_distributed_gpt_step_matches_sequential_reference(cuda, precision, G):
         rk.optimizer_step(optim.SGD(1e-2), optim.SGD(1e-2))
     for rk in ranks[1:]:
         assert torch.equal(rk.params, ranks[0].params)
+
+
+def test_step_from_host_prefetch_matches_device_step(cuda):
+    """step_from_host with input prefetch (double-buffered H2D) gives the same
+    results as the device-resident step, step after step."""
+    import torch
+    from paper_2311_02382_b200.comm import Ledger, SoloComm
+    from paper_2311_02382_b200.model import ModelConfig, layer_params_from_arrays
+    from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec
+
+    z, seq, e, h, g, b, causal = _load("small_causal")
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=8, vocab=16, seq_len=seq, batch=b, causal=causal)
+    lp = layer_params_from_arrays(*[z[k] for k in ATTN_NAMES], device=cuda)
+    eng = LSSAttention(cfg, ShardSpec(0, 1, seq), device=cuda)
+    eng.load_params(lp)
+    r = np.random.default_rng(3)
+    hosts = [(torch.as_tensor(r.standard_normal((b, seq, e)).astype(np.float32)).pin_memory(),
+              torch.as_tensor(r.standard_normal((b, seq, e)).astype(np.float32)).pin_memory()) for _ in range(3)]
+    comm = SoloComm(Ledger())
+    got = []
+    for i, (xh, gyh) in enumerate(hosts):
+        gh = torch.empty(eng.grads.numel()).pin_memory()
+        y, dx = eng.step_from_host(xh, gyh, comm, gh, next_inputs=hosts[i + 1] if i + 1 < len(hosts) else None)
+        torch.cuda.synchronize()
+        got.append((y.clone(), dx.clone(), gh.clone()))
+    for (xh, gyh), (y, dx, gh) in zip(hosts, got):
+        y2, dx2 = eng.step(xh.to(cuda), gyh.to(cuda), comm)
+        torch.cuda.synchronize()
+        assert nerr(y.cpu().numpy(), y2.cpu().numpy()) < 1e-5
+        assert nerr(dx.cpu().numpy(), dx2.cpu().numpy()) < 1e-5
+        assert nerr(gh.numpy(), eng.grads.cpu().numpy()) < 1e-5

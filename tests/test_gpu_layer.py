@@ -586,3 +586,42 @@ def test_step_from_host_prefetch_matches_device_step(cuda):
         assert nerr(y.cpu().numpy(), y2.cpu().numpy()) < 1e-5
         assert nerr(dx.cpu().numpy(), dx2.cpu().numpy()) < 1e-5
         assert nerr(gh.numpy(), eng.grads.cpu().numpy()) < 1e-5
+
+
+def test_full_size_eight_rank_schedule_matches_single_rank(cuda):
+    """The driver's 8-GPU configuration at its real shape (l=50112, m=6264 ragged
+    against the 128-row tile, balanced causal schedule for G=8, fused 8-slot
+    reduce-scatter) simulated on one GPU == the single-rank engine on the same
+    inputs (bf16; both compared through the same kernels, so the bound is the
+    schedule's rounding only)."""
+    import torch
+    from paper_2311_02382_b200.comm import Ledger, SoloComm
+    from paper_2311_02382_b200.model import LayerParams, LinearParams, ModelConfig
+    from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec, lss_step, make_sim_group, slice_batch
+
+    l, E, H = 50112, 1024, 16
+    cfg = ModelConfig(embed_dim=E, n_layers=1, n_heads=H, ff_dim=4 * E, vocab=256, seq_len=l)
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    u = lambda: (torch.rand(E, E, generator=gen, device=cuda) * 2 - 1) / E ** 0.5  # noqa: E731
+    zb = lambda: torch.zeros(E, device=cuda)  # noqa: E731
+    lp = LayerParams(torch.ones(E, device=cuda), zb(), LinearParams(u(), zb()), LinearParams(u(), zb()),
+                     LinearParams(u(), zb()), LinearParams(u(), zb()))
+    x = torch.randn(1, l, E, generator=gen, device=cuda)
+    gy = torch.randn(1, l, E, generator=gen, device=cuda)
+    one = LSSAttention(cfg, ShardSpec(0, 1, l), device=cuda)
+    one.load_params(lp)
+    y1, dx1 = one.step(x, gy, SoloComm(Ledger()))
+    y1, dx1, g1 = y1.clone(), dx1.clone(), one.grads.clone()
+    del one
+    engines, comm = make_sim_group(cfg, lp, 8, device=cuda)
+    assert [e.plan.role for e in engines].count("heavy") == 4 and all(e.m == 6264 for e in engines)
+    out = lss_step(engines, comm, [slice_batch(x, ShardSpec(r, 8, l)) for r in range(8)],
+                   [slice_batch(gy, ShardSpec(r, 8, l)) for r in range(8)])
+    torch.cuda.synchronize()
+    y8 = torch.cat([o[0] for o in out], 1)
+    dx8 = torch.cat([o[1] for o in out], 1)
+    assert all(e.seg_dst is not None for e in engines)  # fused reduce-scatter path
+    assert nerr(y8.cpu().numpy(), y1.cpu().numpy()) < 5e-3
+    assert nerr(dx8.cpu().numpy(), dx1.cpu().numpy()) < 5e-3
+    # sync averages the per-rank grads over the group (sharded.py:238): G=8 = full / 8
+    assert nerr(8 * engines[0].grads.cpu().numpy(), g1.cpu().numpy()) < 5e-3

@@ -547,12 +547,25 @@ class LSSAttention:
         if self.plan.active or self.seg_dst is not None:
             K.attn_delta(self.ctx, self.dctx, self.delta, heads=self.H, scaled=True)
 
+    def _wgrad_stream(self) -> torch.cuda.Stream:
+        """Side stream for the weight-gradient GEMMs: their output grids are small
+        (E/128 x N/256 tiles, 32-96 CTAs), so they run beside the attention backward /
+        the input-gradient GEMM instead of leaving most SMs idle."""
+        if not _WGRAD_SIDE:
+            return torch.cuda.current_stream()
+        if getattr(self, "_wstream", None) is None:
+            self._wstream = torch.cuda.Stream(device=self.device)
+        return self._wstream
+
     def bwd_pre_weights(self) -> None:
-        """dWo = ctx^T . gy (both operands MN-major), pre-scaled; runs while the
-        balanced schedule's dO / lse / delta hand-off is in flight."""
+        """dWo = ctx^T . gy (both operands MN-major), pre-scaled, on the weight-gradient
+        stream (overlaps the dO / lse / delta hand-off and the attention backward)."""
         B, m, E = self.B, self.m, self.E
-        K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True,
-               alpha=self.grad_scale, out=self.g_wo, M=E, N=E, K=B * m)
+        ws = self._wgrad_stream()
+        ws.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(ws):
+            K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True,
+                   alpha=self.grad_scale, out=self.g_wo, M=E, N=E, K=B * m)
 
     def bwd_attend(self) -> None:
         """Attention backward: dQ for the rows this rank computes, partial dK|dV for all."""
@@ -597,13 +610,17 @@ class LSSAttention:
         M = B * m
         K.cat_cast_colsum([(self.dq.view(M, E), E, E), (self.dkv_own.view(M, 2 * E), 2 * E, 2 * E)], M,
                           dst=self.dqkv.view(M, 3 * E), colsum=self.g_bqkv, alpha=a)
+        main, ws = torch.cuda.current_stream(), self._wgrad_stream()
+        ws.wait_stream(main)
+        with torch.cuda.stream(ws):  # dW_qkv (96 tiles) beside the dx̂ GEMM
+            gw = self.g_wqkv.view(3, E, E)
+            K.gemm(self.xh.view(M, E), self.dqkv.view(M, 3 * E), a_mn_major=True, b_mn_major=True, alpha=a,
+                   seg_width=E, out=[(gw[0], E), (gw[1], E), (gw[2], E)], M=E, N=3 * E, K=M)
         K.gemm(self.dqkv.view(M, 3 * E), self.staged["wqkv"], out=self.dxh.view(M, E), M=M, N=E, K=3 * E)
-        gw = self.g_wqkv.view(3, E, E)
-        K.gemm(self.xh.view(M, E), self.dqkv.view(M, 3 * E), a_mn_major=True, b_mn_major=True, alpha=a,
-               seg_width=E, out=[(gw[0], E), (gw[1], E), (gw[2], E)], M=E, N=3 * E, K=M)
         K.layernorm_bwd(self.dxh.view(M, E), self.x.view(M, E), self.mean, self.rstd, self.lp.ln1_gain,
                         grad_res=self.grad_y.view(M, E), grad_x=self.dx.view(M, E),
                         grad_gain=self.g_ln_g, grad_bias=self.g_ln_b, alpha=a)
+        main.wait_stream(ws)  # every weight gradient is in the flat buffer before the all-reduce
         return self.dx
 
     # ------------------------------------------------------------ public step API
@@ -750,6 +767,7 @@ class PhaseClock:
 _PHASES = os.environ.get("LSS_PHASES") == "1"
 _NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
 _CE_GATHER = os.environ.get("LSS_CE_GATHER", "1") != "0"  # K/V gather on the copy engines
+_WGRAD_SIDE = os.environ.get("LSS_WGRAD_SIDE", "1") != "0"  # weight-gradient GEMMs on a side stream
 last_phases: dict = {}
 
 

@@ -124,12 +124,14 @@ class TorchDistComm:
         self._peers[key] = (addrs, t)  # keep the tensor alive while peers may write into it
         return addrs
 
-    def gather_pull(self, full: torch.Tensor, step=0, layer=0):
+    def gather_pull(self, full: torch.Tensor, step=0, layer=0, segments=None):
         """K/V all-gather on the copy engines: after a device barrier (every rank's
         slot is written), pull each peer's own slot full[p] from its IPC-mapped
         buffer on a copy stream -- no SMs taken from the overlapped attention.
-        Returns an event the consumer waits on, or None when peers do not map
-        (the caller then falls back to the NCCL all-gather)."""
+        ``segments``: the peers' slots this rank's attention actually reads (the
+        causal schedule never touches the others); default all.  Returns an
+        event the consumer waits on, or None when peers do not map (the caller
+        then falls back to the NCCL all-gather)."""
         addrs = self.peer_addresses(full)
         if addrs is None:
             return None
@@ -146,7 +148,7 @@ class TorchDistComm:
         self.device_barrier(step, "forward", layer)
         cs.wait_stream(cur)
         slot = full[0].numel() * full.element_size()
-        for p in range(self.seq_size):
+        for p in (range(self.seq_size) if segments is None else segments):
             if p != self.seq_rank:
                 K.copy_d2d(full[p].data_ptr(), addrs[p] + p * slot, slot, cs)
         ev = torch.cuda.Event()

@@ -342,6 +342,17 @@ class LSSAttention:
                 items.append((m - pl.split, pl.partner * m + pl.split, 0, pl.b))
         return items
 
+    def needed_segments(self) -> list:
+        """Key segments any of this rank's attention work reads (forward and
+        backward use the same ranges); the copy-engine gather pulls only these."""
+        need = set()
+        for _row0, _rows, g0, g1 in self.own_ranges():  # causal-trimmed own ranges
+            need.update(range(g0, g1))
+        pl = self.plan
+        if pl.role == "light":  # the partner's delegated rows
+            need.update(range(0, max(pl.a, pl.b)))
+        return sorted(need)
+
     def computed_pairs(self) -> int:
         """Unmasked (query, key) pairs per (batch, head) computed by this rank."""
         return sum(block_pairs(rows, p0, g0 * self.m, g1 * self.m, self.cfg.causal)
@@ -799,7 +810,8 @@ def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
     mark("fwd_project")
     gather = None
     if not sim and split and _CE_GATHER and hasattr(comm, "gather_pull") and comm.seq_size > 1:
-        gather = comm.gather_pull(engines[0].kv_full, step, layer)  # copy engines, no SMs
+        gather = comm.gather_pull(engines[0].kv_full, step, layer,  # copy engines, no SMs
+                                  segments=engines[0].needed_segments())
     if gather is None:
         gather = one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer,
                                                     **({} if sim else {"async_op": split})))

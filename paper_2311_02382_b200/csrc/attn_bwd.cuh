@@ -34,32 +34,15 @@
 #ifndef LSS_BWD_POLY
 #define LSS_BWD_POLY 1  // exponent pairs with (pair & LSS_BWD_POLY) == 0 use the FMA-pipe polynomial
 #endif                  // (7: 1 pair in 8, 3: 1 in 4, 1: 1 in 2, -1: none)
-#ifndef LSS_BWD_DQ_RED
-#define LSS_BWD_DQ_RED 0  // dQ drain: 1 = TMEM -> registers -> red.global.add.v4 (no SMEM traffic),
-#endif                    // 0 = TMEM -> SMEM staging -> TMA tensor reduce-add
-#ifndef LSS_BWD_FOLD
-#define LSS_BWD_FOLD 0  // 1: lse2 / delta enter S / dP through an extra K16 MMA step (no broadcast LDS;
-#endif                  //    measured 6% slower: the 8 KB/stage operands delay the Q/dO stage refill)
-#ifndef LSS_BWD_EW_WG
-#define LSS_BWD_EW_WG 2  // elementwise warpgroups: 128/LSS_BWD_EW_WG query columns per thread
-#endif
 
 namespace lss {
 
-#if LSS_BWD_FOLD
-// Q, dO, then the two [128 q][16 k] bf16 augmentation operands (no-swizzle K-major
-// core-matrix layout) carrying -lse2/sl2 and -delta' split into hi/mid/lo bf16
-constexpr int ATB_AUG_BYTES = 128 * 16 * 2;
-constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES + 2 * ATB_AUG_BYTES;
-#else
-constexpr int ATB_AUG_BYTES = 0;
 constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES + 2 * 512;  // Q, dO, lse2[128], delta[128]
-#endif
 constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;                 // dS^T tile: 2 sub-tiles [128 kv][64 q]
 constexpr int ATB_STG_BYTES = 128 * 64 * 4;                      // dQ staging [128 q][64] fp32 (2 SW128 halves)
 constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES + ATB_STG_BYTES +
-                         ATB_AUG_BYTES /*ones*/ + 1024 + 256;
-constexpr int ATB_EW = LSS_BWD_EW_WG;              // elementwise warpgroups
+                         1024 + 256;
+constexpr int ATB_EW = 2;                          // elementwise warpgroups (4 measured slower)
 constexpr int ATB_NC = 128 / ATB_EW;                // query columns per elementwise thread
 constexpr int ATB_THREADS = 128 * (2 + ATB_EW);     // control WG + EW WGs + dQ-drain WG
 
@@ -91,7 +74,6 @@ struct AttnBwdParams {
   int causal;
   float scale_log2;  // log2(e)/sqrt(d)
   float scale;       // 1/sqrt(d)
-  float inv_scale_log2, inv_scale;
   BwdSource src[ATB_MAX_SRC];
   // dK|dV destination of key segment g: a [B][seg_len][ld_dkv] fp32 block, dK at
   // column h*d and dV at dv_off + h*d, fully written.  Either one local buffer
@@ -105,33 +87,6 @@ struct AttnBwdParams {
   int peer;                     // seg_tab entries are peer (NVLink) memory (informational)
   float* seg_tab[ATB_MAX_SEG];  // used when seg_tab[0] != nullptr
 };
-
-// K-major, no-swizzle operand of 16 K columns: core matrices of 8 rows x 16 bytes,
-// the two K halves 2048 bytes apart (LBO), 8-row groups 128 bytes apart (SBO)
-LSS_DEV uint64_t smem_desc_k16(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((2048u >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((128u >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // version = 1 (sm100), layout 0 = SWIZZLE_NONE
-  return d;
-}
-// byte offset of (row, k-chunk of 8) in that layout
-LSS_DEV uint32_t k16_off(int row, int kc) { return kc * 2048 + (row >> 3) * 128 + (row & 7) * 16; }
-// v ~= hi + mid + lo in bf16 (24 significant bits); non-finite v goes whole into hi
-LSS_DEV void split3_bf16(float v, uint32_t& w01, uint32_t& w2) {
-  if (!isfinite(v)) {
-    w01 = pack_bf16(v, 0.f);
-    w2 = 0;
-    return;
-  }
-  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-  const float r1 = v - __bfloat162float(hi);
-  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-  const float r2 = r1 - __bfloat162float(mid);
-  w01 = pack_bf16(__bfloat162float(hi), __bfloat162float(mid));
-  w2 = pack_bf16(r2, 0.f);
-}
 
 LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -169,19 +124,13 @@ LSS_DEV void tmem_ld_n<64>(uint32_t taddr, uint32_t (&r)[64]) { tmem_ld64(taddr,
 template <int N>
 LSS_DEV void tmem_st_n(uint32_t taddr, const uint32_t (&r)[N]);
 template <>
-LSS_DEV void tmem_st_n<16>(uint32_t taddr, const uint32_t (&r)[16]) { tmem_st16(taddr, r); }
-template <>
 LSS_DEV void tmem_st_n<32>(uint32_t taddr, const uint32_t (&r)[32]) { tmem_st32(taddr, r); }
 
 template <int NC>
 LSS_DEV void bwd_ld_vec(uint32_t saddr, float (&v)[NC]) {
 #pragma unroll
   for (int c4 = 0; c4 < NC / 4; ++c4) {
-#ifdef LSS_BWD_NOLDS
-    const float4 l = make_float4(__uint_as_float(saddr), 1.f, 2.f, 3.f);
-#else
     const float4 l = ld_shared_f4(saddr + c4 * 16);
-#endif
     v[4 * c4] = l.x;
     v[4 * c4 + 1] = l.y;
     v[4 * c4 + 2] = l.z;
@@ -212,39 +161,6 @@ LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv
   }
 }
 
-// FOLD: S' = S - lse2/sl2 and dP' = dP - rowsum(dO*O) come out of the MMAs, so
-// p = 2^(s' sl2) and dS' = p dP' (the 1/sqrt(d) is applied to dK and dQ at the end)
-template <bool MASK, int NC>
-LSS_DEV void bwd_pf(uint32_t (&sv)[NC], float sl2, int fv, uint32_t (&pk)[NC / 2]) {
-  const float2 sl2v = make_float2(sl2, sl2);
-#pragma unroll
-  for (int c = 0; c < NC; c += 2) {
-    const float2 x = fmul2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2v);
-    float2 e;
-    if (LSS_BWD_POLY >= 0 && !MASK && ((c / 2) & LSS_BWD_POLY) == 0) {
-      e = exp2_poly2(x);
-    } else {
-      e = make_float2(ex2(x.x), ex2(x.y));
-    }
-    if (MASK) {
-      e.x = (c >= fv) ? e.x : 0.f;
-      e.y = (c + 1 >= fv) ? e.y : 0.f;
-    }
-    sv[c] = __float_as_uint(e.x);
-    sv[c + 1] = __float_as_uint(e.y);
-    pk[c / 2] = pack_bf16(e.x, e.y);
-  }
-}
-template <int C0, int NH, int NC>
-LSS_DEV void bwd_dsf(const uint32_t (&pv)[NC], const uint32_t (&dp)[NH], uint32_t (&dk)[NC / 2]) {
-#pragma unroll
-  for (int c = 0; c < NH; c += 2) {
-    const float2 ds = fmul2(make_float2(__uint_as_float(pv[C0 + c]), __uint_as_float(pv[C0 + c + 1])),
-                            make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])));
-    dk[(C0 + c) / 2] = pack_bf16(ds.x, ds.y);
-  }
-}
-
 // dS^T for columns [C0, C0+NH) of the thread's slice: ds = p (dp/sqrt(d) - delta/sqrt(d))
 template <int C0, int NH, int NC>
 LSS_DEV void bwd_ds(const uint32_t (&pv)[NC], const uint32_t (&dp)[NH], const float (&dsc)[NC], float scale,
@@ -271,8 +187,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   uint8_t* sQst = sV + ATT_TILE_BYTES;              // 2 stages: Q, dO, lse2, delta
   uint8_t* sdS = sQst + 2 * ATB_QSTAGE_BYTES;       // 2 buffers x 2 sub-tiles [128 kv][64 q] bf16
   uint8_t* sStage = sdS + 2 * ATB_DS_BYTES;         // dQ staging, 2 x [128 q][32] fp32 (SW128)
-  uint8_t* sOnes = sStage + ATB_STG_BYTES;          // FOLD: [128 kv][16 k] bf16, k<3 -> 1
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + ATB_AUG_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + ATB_STG_BYTES);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;   // [2]
   uint64_t* q_empty = bars + 3;  // [2]
@@ -288,7 +203,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int E = p.H * ATT_D;
   // head-major dispatch (key tiles fastest): the ~148 resident CTAs share one or
   // two heads' Q/dO stream in L2 (head-fastest order measured 2% slower)
   const int h = blockIdx.y;
@@ -336,7 +250,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     tma_prefetch_desc(&tmV);
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&q_full[s], LSS_BWD_FOLD ? 2 : 1);
+      mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
     mbar_init(s_full, 1);
@@ -352,20 +266,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
-#if LSS_BWD_FOLD
-  if (warp >= 4 && warp < 8) {  // ones operand + zeroed augmentation operands (k >= 3 stay 0)
-    const int r = (warp - 4) * 32 + lane;
-    const uint32_t one2 = pack_bf16(1.f, 1.f), one0 = pack_bf16(1.f, 0.f);
-    st_shared_v4(smem_u32(sOnes) + k16_off(r, 0), one2, one0, 0u, 0u);
-    st_shared_v4(smem_u32(sOnes) + k16_off(r, 1), 0u, 0u, 0u, 0u);
-    for (int st = 0; st < 2; ++st)
-      for (int a = 0; a < 2; ++a)
-        for (int kc = 0; kc < 2; ++kc)
-          st_shared_v4(smem_u32(sQst + st * ATB_QSTAGE_BYTES + 2 * ATT_TILE_BYTES + a * ATB_AUG_BYTES) +
-                           k16_off(r, kc), 0u, 0u, 0u, 0u);
-    fence_proxy_async_smem();
-  }
-#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -376,7 +276,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
 
   if (warp < 4) {
-    reg_dealloc<(ATB_EW == 4 ? 40 : 56)>();
+    reg_dealloc<56>();
     if (warp == 0) {
       if (n_iter > 0) {
         // ------------------------------------------------ TMA producer (warp-uniform loop)
@@ -386,25 +286,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           tma_load_4d(&tmV, kv_full, sV, h * ATT_D, kv_row0, b, g);
         }
         __syncwarp();
-#if LSS_BWD_FOLD
-        // lse2 / delta of the NEXT query tile are loaded into registers one
-        // iteration ahead, so their global-load latency hides under the stage wait
-        auto load_rows = [&](int it, float4& L, float4& D) {
-          int src, q0;
-          locate(it, src, q0);
-          const long lo = ((long)b * p.H + h) * p.src[src].pitch + q0 + 4 * lane;
-          L = *reinterpret_cast<const float4*>(p.src[src].lse2 + lo);
-          D = *reinterpret_cast<const float4*>(p.src[src].delta + lo);
-        };
-        float4 Ln, Dn;
-        load_rows(0, Ln, Dn);
-#endif
         for (int it = 0; it < n_iter; ++it) {
           const int s = it & 1;
-#if LSS_BWD_FOLD
-          const float4 L = Ln, D = Dn;
-          if (it + 1 < n_iter) load_rows(it + 1, Ln, Dn);
-#endif
           mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
           if (lane == 0) BWD_TRACE(18, it);
           int src, q0;
@@ -412,33 +295,13 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
           const long lo = ((long)b * p.H + h) * p.src[src].pitch + q0;
           if (elect_one()) {
-            mbar_arrive_expect_tx(&q_full[s], 2 * ATT_TILE_BYTES + (LSS_BWD_FOLD ? 0 : 1024));
+            mbar_arrive_expect_tx(&q_full[s], 2 * ATT_TILE_BYTES + 1024);
             tma_load_3d(&maps.q[src], &q_full[s], st, h * ATT_D, q0, b);
             tma_load_3d(&maps.dO[src], &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
-#if !LSS_BWD_FOLD
             bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.src[src].lse2 + lo, 512, &q_full[s]);
             bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.src[src].delta + lo, 512, &q_full[s]);
-#endif
           }
           __syncwarp();
-#if LSS_BWD_FOLD
-          {  // augmentation rows (written while the Q / dO TMA is in flight): lane -> query rows 4*lane .. 4*lane+3
-            const float ls[4] = {L.x, L.y, L.z, L.w}, ds[4] = {D.x, D.y, D.z, D.w};
-            const uint32_t aS = smem_u32(st + 2 * ATT_TILE_BYTES), aD = aS + ATB_AUG_BYTES;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint32_t w01, w2;
-              split3_bf16(-ls[j] * p.inv_scale_log2, w01, w2);  // S' = S - lse2 / sl2
-              st_shared_v2(aS + k16_off(4 * lane + j, 0), w01, w2);
-              split3_bf16(-ds[j] * p.inv_scale, w01, w2);       // dP' = dP - rowsum(dO*O)
-              st_shared_v2(aD + k16_off(4 * lane + j, 0), w01, w2);
-            }
-            fence_proxy_async_smem();
-          }
-          __syncwarp();
-          if (elect_one()) mbar_arrive(&q_full[s]);  // second arrival: augmentation rows written
-          __syncwarp();
-#endif
         }
       }
     } else if (warp == 1) {
@@ -463,9 +326,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             for (int k = 0; k < ATT_D / 16; ++k)
               mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
                           smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
-#if LSS_BWD_FOLD
-            mma_bf16_ss(tS, smem_desc_k16(smem_u32(sOnes)), smem_desc_k16(q_addr + 2 * ATT_TILE_BYTES), idSS, 1);
-#endif
             mma_commit(s_full);
           }
           __syncwarp();
@@ -477,10 +337,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             for (int k = 0; k < ATT_D / 16; ++k)
               mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
                           smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
-#if LSS_BWD_FOLD
-            mma_bf16_ss(tdP, smem_desc_k16(smem_u32(sOnes)),
-                        smem_desc_k16(do_addr + ATT_TILE_BYTES + ATB_AUG_BYTES), idSS, 1);
-#endif
             mma_commit(dp_full);
           }
           __syncwarp();
@@ -552,7 +408,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       }
     }
   } else if (warp < 4 + 4 * ATB_EW) {
-    reg_alloc<(ATB_EW == 4 ? 96 : 184)>();
+    reg_alloc<184>();
     // ------------------------------------------------ elementwise P^T / dS^T (+ dK/dV epilogue)
     const int qd = (warp - 4) / 4;    // query columns [NC*qd, NC*qd + NC) of each tile
     const int quad = warp % 4;
@@ -570,11 +426,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
       // ---- P^T = 2^(S^T log2e/sqrt(d) - lse2): S_it completing implies dV_{it-1}
       // (the previous reader of the P^T columns) completed.
-#if !LSS_BWD_FOLD
       float lse[NC];  // issued ahead of the S wait: the loads queue behind the tensor
       mbar_wait(&q_full[it & 1], (it >> 1) & 1);  // core's SMEM operand traffic
       bwd_ld_vec<NC>(s_lse, lse);
-#endif
       mbar_wait(s_full, it & 1);
       tc_fence_after();
       if (t == 0 && qd == 0) BWD_TRACE(1, it);
@@ -588,17 +442,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         if (need_mask) {
           const long first_vis = kpos - q0 - qd * NC;
           const int fv = !row_ok ? NC : (p.causal ? (int)max(0L, min((long)NC, first_vis)) : 0);
-#if LSS_BWD_FOLD
-          bwd_pf<true, NC>(sv, p.scale_log2, fv, pk);
-        } else {
-          bwd_pf<false, NC>(sv, p.scale_log2, 0, pk);
-        }
-#else
           bwd_p<true, NC>(sv, lse, p.scale_log2, fv, pk);
         } else {
           bwd_p<false, NC>(sv, lse, p.scale_log2, 0, pk);
         }
-#endif
         if (t == 0 && qd == 0) BWD_TRACE(13, it);
         tmem_st_n<NC / 2>(tS + lane_off + qd * NC, pk);
       }
@@ -608,10 +455,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       // ---- dS^T = P^T (dP^T/sqrt(d) - delta/sqrt(d)): dP_it completing implies dK_{it-1}
       // (TMEM dS^T reader) completed; dQ_{it-2} (SMEM buffer it&1 reader) runs after
       // dP_it and signals ds_free.
-#if !LSS_BWD_FOLD
       float dsc[NC];  // delta loads issued before the dP wait (same reason as lse)
       bwd_ld_vec<NC>(s_dsc, dsc);
-#endif
       mbar_wait(dp_full, it & 1);
       tc_fence_after();
       if (t == 0 && qd == 0) BWD_TRACE(3, it);
@@ -620,20 +465,12 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         {  // dP^T in two halves keeps p, delta and dP within the register budget
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC, dp);
-#if LSS_BWD_FOLD
-          bwd_dsf<0, NC / 2, NC>(sv, dp, dk);
-#else
           bwd_ds<0, NC / 2, NC>(sv, dp, dsc, p.scale, dk);
-#endif
         }
         {
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
-#if LSS_BWD_FOLD
-          bwd_dsf<NC / 2, NC / 2, NC>(sv, dp, dk);
-#else
           bwd_ds<NC / 2, NC / 2, NC>(sv, dp, dsc, p.scale, dk);
-#endif
         }
         if (t == 0 && qd == 0) BWD_TRACE(9, it);
         if (it > 1) mbar_wait(&ds_free[it & 1], ((it >> 1) - 1) & 1);
@@ -670,10 +507,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
 #pragma unroll
       for (int c = 0; c < EC / 32; ++c) {
         tmem_ld32((is_v ? tdV : tdK) + lane_off + col0 + c * 32, v);
-        if (LSS_BWD_FOLD && !is_v) {  // dK accumulated dS' = dS sqrt(d)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.scale);
-        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int chunk = (is_v ? 16 : 0) + (col0 + c * 32) / 4 + i;
@@ -694,7 +527,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       }
     }
   } else {
-    reg_dealloc<(ATB_EW == 4 ? 56 : 80)>();
+    reg_dealloc<80>();
     // ------------------------------------------------ dQ drain: TMEM -> swizzled SMEM -> TMA reduce-add
     const int quad = warp % 4;
     const int r = quad * 32 + lane;  // query row within tile == TMEM lane
@@ -702,40 +535,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     const bool issuer = (r == 0);
     const uint32_t row0 = smem_u32(sStage + r * 128);                      // cols [0,32)
     const uint32_t row1 = smem_u32(sStage + ATB_STG_BYTES / 2 + r * 128);  // cols [32,64)
-#if LSS_BWD_DQ_RED
-    // Shared memory bandwidth is the backward's binding resource (the tensor core
-    // reads ~144 KB of operands per tile); reducing dQ straight from registers
-    // saves the 32 KB staging write and the 32 KB TMA read per tile.
-    for (int it = 0; it < n_iter; ++it) {
-      mbar_wait(&dq_full[it & 1], (it >> 1) & 1);
-      tc_fence_after();
-      if (r == 0) BWD_TRACE(5, it);
-      int src, q0;
-      locate(it, src, q0);
-      const int row = q0 + r;
-      const bool ok = row < p.src[src].m_src;
-      float* dst = p.src[src].dq + ((long)b * p.src[src].m_src + row) * (p.H * ATT_D) + h * ATT_D;
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t v[32];
-        tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
-        if (LSS_BWD_FOLD) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.scale);
-        }
-        if (hh == 1) {
-          tc_fence_before();
-          mbar_arrive(&dq_empty[it & 1]);
-        }
-        if (ok) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            red_add_v4(dst + hh * 32 + 4 * i, __uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                       __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-        }
-      }
-    }
-#else
     for (int it = 0; it < n_iter; ++it) {
       mbar_wait(&dq_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
@@ -746,10 +545,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time keeps the drain at 56 registers
         uint32_t v[32];
         tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
-        if (LSS_BWD_FOLD) {  // dQ accumulated dS' = dS sqrt(d)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.scale);
-        }
         const uint32_t rowh = hh ? row1 : row0;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
@@ -771,7 +566,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         bulk_commit();
       }
     }
-#endif
     if (issuer) bulk_wait0();
   }
 

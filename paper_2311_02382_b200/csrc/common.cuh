@@ -206,11 +206,6 @@ LSS_DEV void mma_commit(uint64_t* bar) {
                   "r"(r[b + 4]), "r"(r[b + 5]), "r"(r[b + 6]), "r"(r[b + 7])
 
 // 32 lanes x 32 bits, 32 consecutive columns per thread, then wait
-// fire-and-forget vector reduction into global memory (L2 atomics, sm_90+)
-LSS_DEV void red_add_v4(float* ptr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
 LSS_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "

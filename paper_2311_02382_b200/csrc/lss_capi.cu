@@ -438,8 +438,6 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
   p.B = batch; p.G = workers; p.seg_len = seg_len; p.H = heads; p.nsrc = nsrc; p.causal = causal;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.scale = scale;
-  p.inv_scale_log2 = 1.0f / p.scale_log2;
-  p.inv_scale = sqrtf((float)head_dim);
   p.dkv = grad_k; p.seg_stride = (long)batch * seg_len * ld_dkv; p.dv_off = dv_off; p.ld_dkv = ld_dkv;
   p.peer = peer;
   if (seg_tab)

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 3
+#define LSS_ABI_VERSION 4
 
 enum lss_status {
   LSS_OK = 0,
@@ -125,6 +125,19 @@ int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld
                  float* lse2, int batch, int rows, int workers, int seg_len, int heads,
                  int head_dim, long offset, int causal, void* stream);
 
+/* Attention-probability dropout (model.scores_fwd / scores_bwd, model.py:313-317,
+ * 350-352; nnops.keep_mask, nnops.py:124-135): site_key = mix(mix(seed, 2), layer+1),
+ * the row key of query (b, h, q_pos) is mix(mix(mix(site_key, b+1), h+1), q_pos) and
+ * (q_pos, k_pos) is kept iff (mix(row key, k_pos) >> 11) >= thresh, thresh =
+ * ceil(rate * 2^53); kept probabilities are scaled by scale = 1/(1-rate).  Pass
+ * null (or active = 0) for no dropout; bf16 path only. */
+typedef struct lss_dropout {
+  unsigned long long site_key;
+  unsigned long long thresh;
+  float scale;
+  int active;
+} lss_dropout;
+
 /* Partial / strided form of lss_attn_fwd: q rows [0, rows) with batch stride
  * q_bstride (elements), attending only key segments [g_begin, g_end); ctx is
  * written normalised with batch stride o_bstride and lse2 with row pitch
@@ -134,7 +147,7 @@ int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld
 int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v,
                     long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch,
                     int workers, int seg_len, int heads, int head_dim, long offset, int causal,
-                    int g_begin, int g_end, void* stream);
+                    int g_begin, int g_end, const lss_dropout* dropout, void* stream);
 
 /* log-sum-exp combine of two partial attentions over disjoint key ranges:
  * lse = log2(2^la + 2^lb), ctx = 2^(la-lse) ctx_a + 2^(lb-lse) ctx_b (bf16, head_dim 64).
@@ -180,7 +193,7 @@ typedef struct lss_bwd_source {
  * from all sources, so grad_k / grad_v rows have a single writer (fully written). */
 int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs,
                     int nsrc, float* grad_k, float* grad_v, long ld_dkv, int batch, int workers,
-                    int seg_len, int heads, int head_dim, int causal, void* stream);
+                    int seg_len, int heads, int head_dim, int causal, const lss_dropout* dropout, void* stream);
 
 /* y += x (fp32), used to fold a partner's dQ rows into the owner's. */
 int lss_add_f32(float* y, const float* x, long n, void* stream);
@@ -199,7 +212,8 @@ int lss_add_f32(float* y, const float* x, long n, void* stream);
  * and numerics as lss_attn_bwd_ex; workers <= 16. */
 int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs,
                      int nsrc, float* const* seg_dst, int peer, long ld_dkv, int batch, int workers,
-                     int seg_len, int heads, int head_dim, int causal, void* stream);
+                     int seg_len, int heads, int head_dim, int causal, const lss_dropout* dropout,
+                     void* stream);
 
 /* Whole-model edges.  tokens / targets are int32.
  * model.embed_fwd (model.py:517-533): x[b][i] = token_table[tokens[b][i]] + pos_table[i]
@@ -215,6 +229,14 @@ int lss_embed_bwd(const int* tokens, const float* grad_x, float* grad_token_tabl
                   int rows, int embed, float alpha_token, float alpha_pos, void* stream);
 int lss_cross_entropy(const float* logits, long ld, const int* targets, long n, int vocab, float scale,
                       float* loss_rows, float* grad, long ld_grad, void* stream);
+
+/* nnops.dropout_fwd / dropout_bwd (nnops.py:143-166) on a (rows, cols) activation
+ * whose row r is (sample r / rows_per_sample, position offset + r % rows_per_sample):
+ * out = x * keep * scale (+ residual fp32), keep from the site key
+ * mix(mix(seed, tag), layer+1) (see lss_dropout).  x / out bf16 or fp32 (dtype). */
+int lss_dropout_rows(int dtype, const void* x, long ldx, void* out, long ldo, const float* residual, long ld_res,
+                     long rows, int cols, int rows_per_sample, long offset, unsigned long long site_key,
+                     unsigned long long thresh, float scale, void* stream);
 
 /* Parameter updates after the gradient all-reduce, over flat fp32 buffers:
  * model.sgd_step (model.py:621-623) p -= lr * g, and optim.adam_step

@@ -54,6 +54,12 @@ class GemmEpilogue(ctypes.Structure):
     ]
 
 
+class DropoutDesc(ctypes.Structure):
+    """lss_dropout (include/lss.h)."""
+
+    _fields_ = [("site_key", ctypes.c_ulonglong), ("thresh", ctypes.c_ulonglong), ("scale", _F), ("active", _I)]
+
+
 class BwdSource(ctypes.Structure):
     """lss_bwd_source (include/lss.h)."""
 
@@ -74,13 +80,16 @@ SIGNATURES = {
     "lss_attn_fwd": [_I, _P, _P, _P, _L, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P],
     "lss_attn_bwd": [_I, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _I, _L, _I,
                      _P],
-    "lss_attn_fwd_ex": [_I, _P, _I, _L, _P, _P, _L, _P, _L, _P, _I, _I, _I, _I, _I, _I, _L, _I, _I, _I, _P],
+    "lss_attn_fwd_ex": [_I, _P, _I, _L, _P, _P, _L, _P, _L, _P, _I, _I, _I, _I, _I, _I, _L, _I, _I, _I,
+                        ctypes.POINTER(DropoutDesc), _P],
     "lss_attn_merge": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _L, _I, _P],
     "lss_attn_delta": [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P],
-    "lss_attn_bwd_ex": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, _P, _P, _L, _I, _I, _I, _I, _I, _I, _P],
+    "lss_attn_bwd_ex": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, _P, _P, _L, _I, _I, _I, _I, _I, _I,
+                        ctypes.POINTER(DropoutDesc), _P],
     "lss_add_f32": [_P, _P, _L, _P],
     "lss_attn_bwd_p2p": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, ctypes.POINTER(_P), _I, _L, _I, _I, _I,
-                         _I, _I, _I, _P],
+                         _I, _I, _I, ctypes.POINTER(DropoutDesc), _P],
+    "lss_dropout_rows": [_I, _P, _L, _P, _L, _P, _L, _L, _I, _I, _L, ctypes.c_ulonglong, ctypes.c_ulonglong, _F, _P],
     "lss_sum_slots": [_P, _P, _I, _L, _L, _P],
     "lss_sgd_update": [_P, _P, _L, _F, _P],
     "lss_embed_fwd": [_P, _P, _P, _P, _I, _I, _I, _P],
@@ -99,7 +108,7 @@ EXTRA = {
     "lss_rows_pad": ([_L], _L),
     "lss_peer_access": ([_I, _I], _I),
 }
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _lib = None
 
@@ -135,7 +144,8 @@ KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 
                     "lss_cat_cast_colsum": 1, "lss_attn_fwd": 1, "lss_attn_bwd": 2, "lss_attn_fwd_ex": 1,
                     "lss_attn_merge": 1, "lss_attn_delta": 1, "lss_attn_bwd_ex": 1, "lss_add_f32": 1,
                     "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1,
-                    "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1}
+                    "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1,
+                    "lss_dropout_rows": 1}
 launch_count = 0
 
 

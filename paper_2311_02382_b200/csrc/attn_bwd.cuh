@@ -85,6 +85,10 @@ struct AttnBwdParams {
   long dv_off;
   long ld_dkv;
   int peer;                     // seg_tab entries are peer (NVLink) memory (informational)
+  // attention-probability dropout (DROP instances; model.scores_bwd, model.py:350-352)
+  uint64_t drop_site;
+  uint64_t drop_thresh;
+  float drop_scale;
   float* seg_tab[ATB_MAX_SEG];  // used when seg_tab[0] != nullptr
 };
 
@@ -138,8 +142,20 @@ LSS_DEV void bwd_ld_vec(uint32_t saddr, float (&v)[NC]) {
   }
 }
 
-template <bool MASK, int NC>
-LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv, uint32_t (&pk)[NC / 2]) {
+// keep bits of the thread's key row (global position kpos) against query columns
+// q_first .. q_first+NC-1 of head (b, h): the forward's mask, recomputed
+template <int NC>
+LSS_DEV uint64_t bwd_drop_bits(uint64_t head_key, long q_first, long kpos, uint64_t thresh) {
+  uint64_t bits = 0;
+#pragma unroll 4
+  for (int c = 0; c < NC; ++c)
+    bits |= (uint64_t)drop_keep(drop_mix(head_key, (uint64_t)(q_first + c)), (uint64_t)kpos, thresh) << c;
+  return bits;
+}
+
+template <bool MASK, bool DROP, int NC>
+LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv, uint32_t (&pk)[NC / 2],
+                   uint64_t keep = 0, float dscale = 1.f) {
   const float2 sl2v = make_float2(sl2, sl2);
 #pragma unroll
   for (int c = 0; c < NC; c += 2) {
@@ -155,20 +171,31 @@ LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv
       e.x = (c >= fv) ? e.x : 0.f;
       e.y = (c + 1 >= fv) ? e.y : 0.f;
     }
-    sv[c] = __float_as_uint(e.x);
+    sv[c] = __float_as_uint(e.x);  // dS needs the undropped probabilities
     sv[c + 1] = __float_as_uint(e.y);
+    if (DROP) {  // dV uses the dropped ones (aw_d)
+      e.x = ((keep >> c) & 1) ? e.x * dscale : 0.f;
+      e.y = ((keep >> (c + 1)) & 1) ? e.y * dscale : 0.f;
+    }
     pk[c / 2] = pack_bf16(e.x, e.y);
   }
 }
 
-// dS^T for columns [C0, C0+NH) of the thread's slice: ds = p (dp/sqrt(d) - delta/sqrt(d))
-template <int C0, int NH, int NC>
+// dS^T for columns [C0, C0+NH) of the thread's slice: ds = p (dp/sqrt(d) - delta/sqrt(d));
+// with dropout dp is the gradient of the dropped probabilities and is masked first
+// (grad_aw = grad_aw_d * keep * 1/(1-rate))
+template <int C0, int NH, int NC, bool DROP>
 LSS_DEV void bwd_ds(const uint32_t (&pv)[NC], const uint32_t (&dp)[NH], const float (&dsc)[NC], float scale,
-                    uint32_t (&dk)[NC / 2]) {
+                    uint32_t (&dk)[NC / 2], uint64_t keep = 0, float dscale = 1.f) {
   const float2 scv = make_float2(scale, scale);
 #pragma unroll
   for (int c = 0; c < NH; c += 2) {
-    const float2 t = ffma2(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), scv,
+    float2 sc = scv;
+    if (DROP) {
+      sc.x = ((keep >> (C0 + c)) & 1) ? scale * dscale : 0.f;
+      sc.y = ((keep >> (C0 + c + 1)) & 1) ? scale * dscale : 0.f;
+    }
+    const float2 t = ffma2(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), sc,
                            make_float2(-dsc[C0 + c], -dsc[C0 + c + 1]));
     const float2 ds =
         fmul2(make_float2(__uint_as_float(pv[C0 + c]), __uint_as_float(pv[C0 + c + 1])), t);
@@ -176,6 +203,7 @@ LSS_DEV void bwd_ds(const uint32_t (&pv)[NC], const uint32_t (&dp)[NH], const fl
   }
 }
 
+template <bool DROP>
 __global__ void __launch_bounds__(ATB_THREADS, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        const __grid_constant__ BwdMaps maps, const __grid_constant__ AttnBwdParams p) {
@@ -415,6 +443,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     const int t = quad * 32 + lane;   // key row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const long kpos = kpos0 + t;
+    const uint64_t drop_head = DROP ? drop_mix(drop_mix(p.drop_site, (uint64_t)b + 1), (uint64_t)h + 1) : 0;
     const bool row_ok = t < kv_valid;
     constexpr int NC = ATB_NC;
     for (int it = 0; it < n_iter; ++it) {
@@ -437,14 +466,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       if (t == 0 && qd == 0) BWD_TRACE(7, it);
       // query column c of this slice is visible to key row t iff c >= fv
       const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > q0 + qd * NC);
+      const uint64_t keep = DROP ? bwd_drop_bits<NC>(drop_head, q0 + qd * NC, kpos, p.drop_thresh) : 0;
       {
         uint32_t pk[NC / 2];
         if (need_mask) {
           const long first_vis = kpos - q0 - qd * NC;
           const int fv = !row_ok ? NC : (p.causal ? (int)max(0L, min((long)NC, first_vis)) : 0);
-          bwd_p<true, NC>(sv, lse, p.scale_log2, fv, pk);
+          bwd_p<true, DROP, NC>(sv, lse, p.scale_log2, fv, pk, keep, p.drop_scale);
         } else {
-          bwd_p<false, NC>(sv, lse, p.scale_log2, 0, pk);
+          bwd_p<false, DROP, NC>(sv, lse, p.scale_log2, 0, pk, keep, p.drop_scale);
         }
         if (t == 0 && qd == 0) BWD_TRACE(13, it);
         tmem_st_n<NC / 2>(tS + lane_off + qd * NC, pk);
@@ -465,12 +495,12 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         {  // dP^T in two halves keeps p, delta and dP within the register budget
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC, dp);
-          bwd_ds<0, NC / 2, NC>(sv, dp, dsc, p.scale, dk);
+          bwd_ds<0, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
         }
         {
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
-          bwd_ds<NC / 2, NC / 2, NC>(sv, dp, dsc, p.scale, dk);
+          bwd_ds<NC / 2, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
         }
         if (t == 0 && qd == 0) BWD_TRACE(9, it);
         if (it > 1) mbar_wait(&ds_free[it & 1], ((it >> 1) - 1) & 1);

@@ -73,8 +73,15 @@ struct AttnFwdParams {
   long o_bstride;
   float* lse2;                     // [B][H][lse_pitch] (+ row), base 2: m + log2(l); pad rows = +inf
   int lse_pitch;                   // rows with no visible key (partial ranges) get O = 0, lse = -inf
+  // attention-probability dropout (model.scores_fwd, model.py:313-317; used when DROP):
+  // site = mix(mix(seed, tag 2), layer + 1); row key = mix(mix(mix(site, b + 1), h + 1), q_pos);
+  // keep (q_pos, k_pos) iff (mix(row key, k_pos) >> 11) >= drop_thresh; kept P scaled by drop_scale
+  uint64_t drop_site;
+  uint64_t drop_thresh;
+  float drop_scale;
 };
 
+template <bool DROP>
 __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, AttnFwdParams p) {
@@ -284,6 +291,8 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
         uint32_t pk[ATT_BN / 2];
         float2 sum2 = make_float2(0.f, 0.f);
+        uint64_t drop_row = 0;
+        if (DROP) drop_row = drop_mix(drop_mix(drop_mix(p.drop_site, (uint64_t)b + 1), (uint64_t)h + 1), (uint64_t)qpos);
         {
           const float2 slv = make_float2(p.scale_log2, p.scale_log2), nm = make_float2(-m_use, -m_use);
 #pragma unroll
@@ -295,7 +304,11 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
             } else {
               e = make_float2(ex2(x.x), ex2(x.y));
             }
-            sum2 = fadd2(sum2, e);
+            sum2 = fadd2(sum2, e);  // the normaliser uses the undropped probabilities
+            if (DROP) {
+              e.x = drop_keep(drop_row, (uint64_t)(key0 + c), p.drop_thresh) ? e.x * p.drop_scale : 0.f;
+              e.y = drop_keep(drop_row, (uint64_t)(key0 + c + 1), p.drop_thresh) ? e.y * p.drop_scale : 0.f;
+            }
             pk[c / 2] = pack_bf16(e.x, e.y);
           }
         }

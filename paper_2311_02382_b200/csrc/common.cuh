@@ -302,6 +302,25 @@ LSS_DEV float2 fmul2(float2 a, float2 b) {
   return u64_f2(d);
 }
 
+// Counter-based dropout bits (nnops.py:40-64 mix_key, the splitmix64 finaliser
+// keyed by a running hash): every keep decision is a pure function of
+// (seed, layer, site, sample, [head,] position, column), so a mask is recomputed
+// in the backward instead of stored and is identical across sharding layouts.
+constexpr uint64_t DROP_GOLDEN = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t DROP_MIX_A = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t DROP_MIX_B = 0x94D049BB133111EBull;
+LSS_DEV uint64_t drop_mix(uint64_t h, uint64_t word) {
+  uint64_t z = h + word * DROP_GOLDEN;
+  z = (z ^ (z >> 30)) * DROP_MIX_A;
+  z = (z ^ (z >> 27)) * DROP_MIX_B;
+  return z ^ (z >> 31);
+}
+// keep iff uniform = (word >> 11) * 2^-53 >= rate  <=>  (word >> 11) >= thresh,
+// thresh = ceil(rate * 2^53) computed exactly on the host (nnops.keep_mask)
+LSS_DEV bool drop_keep(uint64_t row_key, uint64_t col, uint64_t thresh) {
+  return (drop_mix(row_key, col) >> 11) >= thresh;
+}
+
 // 2^x on the FMA pipe for x in [-125, 127] (x is clamped below, so -inf -> ~2^-125,
 // never a wrapped exponent: p(f) < 1 at f = 0 would underflow the exponent field
 // at -127): Cody-Waite split

@@ -419,4 +419,32 @@ __global__ void cross_entropy_kernel(const float* __restrict__ logits, long ld, 
   }
 }
 
+// nnops.dropout_fwd / dropout_bwd (nnops.py:143-166) over a (rows, cols) activation
+// whose row r is (sample r / m, global position offset + r % m): out = x * keep *
+// scale (+ residual).  site = mix(mix(seed, tag), layer + 1); row key =
+// mix(mix(site, sample), position).  x / out fp32 or bf16 (same dtype).
+LSS_DEV float to_f32(float v) { return v; }
+LSS_DEV float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+LSS_DEV T from_f32(float v);
+template <>
+LSS_DEV float from_f32<float>(float v) { return v; }
+template <>
+LSS_DEV __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__global__ void dropout_rows_kernel(const T* __restrict__ x, long ldx, T* __restrict__ out, long ldo,
+                                    const float* __restrict__ residual, long ld_res, long rows, int cols, int m,
+                                    long offset, uint64_t site, uint64_t thresh, float scale) {
+  for (long r = blockIdx.y; r < rows; r += gridDim.y) {
+    const uint64_t key = drop_mix(drop_mix(site, (uint64_t)(r / m)), (uint64_t)(offset + r % m));
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
+      float v = to_f32(x[r * ldx + c]);
+      v = drop_keep(key, (uint64_t)c, thresh) ? v * scale : 0.f;
+      if (residual) v += residual[r * ld_res + c];
+      out[r * ldo + c] = from_f32<T>(v);
+    }
+  }
+}
+
 }  // namespace lss

@@ -289,7 +289,8 @@ static int attn_check(int dtype, int batch, int rows, int workers, int seg_len, 
 
 int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v, long ld_kv,
                     void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers, int seg_len,
-                    int heads, int head_dim, long offset, int causal, int g_begin, int g_end, void* stream) {
+                    int heads, int head_dim, long offset, int causal, int g_begin, int g_end,
+                    const lss_dropout* dropout, void* stream) {
   int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
   if (rc) return rc;
   if (!q || !k || !v || !o || !lse2) return fail(LSS_ERR_ARG, "attn_fwd: null pointer");
@@ -302,6 +303,7 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
   if (q_bstride < (long)rows * E || o_bstride < (long)rows * E) return fail(LSS_ERR_SHAPE, "attn_fwd: batch stride");
   const float scale = 1.0f / sqrtf((float)head_dim);
   if (dtype == LSS_F32) {
+    if (dropout && dropout->active) return fail(LSS_ERR_UNSUPPORTED, "attn_fwd f32: dropout is bf16-path only");
     if (g_begin != 0 || g_end != workers || q_bstride != (long)rows * E || o_bstride != (long)rows * E ||
         lse_pitch != m_pad)
       return fail(LSS_ERR_UNSUPPORTED, "attn_fwd f32: partial/strided attention is bf16-only");
@@ -334,9 +336,18 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
   p.o_bstride = o_bstride;
   p.lse2 = lse2;
   p.lse_pitch = lse_pitch;
-  if ((rc = set_smem(attn_fwd_tc_kernel, ATT_FWD_SMEM))) return rc;
+  const bool drop = dropout && dropout->active;
+  p.drop_site = drop ? dropout->site_key : 0;
+  p.drop_thresh = drop ? dropout->thresh : 0;
+  p.drop_scale = drop ? dropout->scale : 1.f;
   dim3 grid((unsigned)((rows + 2 * ATT_BM - 1) / (2 * ATT_BM)) * heads * batch);
-  attn_fwd_tc_kernel<<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
+  if (drop) {
+    if ((rc = set_smem(attn_fwd_tc_kernel<true>, ATT_FWD_SMEM))) return rc;
+    attn_fwd_tc_kernel<true><<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
+  } else {
+    if ((rc = set_smem(attn_fwd_tc_kernel<false>, ATT_FWD_SMEM))) return rc;
+    attn_fwd_tc_kernel<false><<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
+  }
   return check_launch("attn_fwd_tc");
 }
 
@@ -345,7 +356,7 @@ int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld
                  void* stream) {
   const long E = (long)heads * head_dim;
   return lss_attn_fwd_ex(dtype, q, rows, rows * E, k, v, ld_kv, o, rows * E, lse2, (int)lss_rows_pad(rows), batch,
-                         workers, seg_len, heads, head_dim, offset, causal, 0, workers, stream);
+                         workers, seg_len, heads, head_dim, offset, causal, 0, workers, nullptr, stream);
 }
 
 int lss_attn_delta(int dtype, const void* o, const void* grad_o, float* delta, int batch, int rows, int heads,
@@ -379,7 +390,8 @@ int lss_attn_delta(int dtype, const void* o, const void* grad_o, float* delta, i
 // grad_k + g*B*seg_len*ld_dkv; dV sits dv_off elements after dK in either case.
 static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
                            float* grad_k, long dv_off, float* const* seg_tab, int peer, long ld_dkv, int batch,
-                           int workers, int seg_len, int heads, int head_dim, int causal, void* stream) {
+                           int workers, int seg_len, int heads, int head_dim, int causal, const lss_dropout* dropout,
+                           void* stream) {
   int rc = attn_check(LSS_BF16, batch, 1, workers, seg_len, heads, head_dim);
   if (rc) return rc;
   if (!k || !v || !srcs || (!grad_k && !seg_tab)) return fail(LSS_ERR_ARG, "attn_bwd_ex: null pointer");
@@ -440,31 +452,42 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
   p.scale = scale;
   p.dkv = grad_k; p.seg_stride = (long)batch * seg_len * ld_dkv; p.dv_off = dv_off; p.ld_dkv = ld_dkv;
   p.peer = peer;
+  const bool drop = dropout && dropout->active;
+  p.drop_site = drop ? dropout->site_key : 0;
+  p.drop_thresh = drop ? dropout->thresh : 0;
+  p.drop_scale = drop ? dropout->scale : 1.f;
   if (seg_tab)
     for (int g = 0; g < workers; ++g) p.seg_tab[g] = seg_tab[g];
-  if ((rc = set_smem(attn_bwd_tc_kernel, ATB_SMEM))) return rc;
+  if (drop) {
+    if ((rc = set_smem(attn_bwd_tc_kernel<true>, ATB_SMEM))) return rc;
+  } else if ((rc = set_smem(attn_bwd_tc_kernel<false>, ATB_SMEM))) {
+    return rc;
+  }
   const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
   dim3 grid(workers * tps, heads, batch);
-  attn_bwd_tc_kernel<<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
+  if (drop)
+    attn_bwd_tc_kernel<true><<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
+  else
+    attn_bwd_tc_kernel<false><<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
   return check_launch("attn_bwd_tc");
 }
 
 int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
                     float* grad_k, float* grad_v, long ld_dkv, int batch, int workers, int seg_len, int heads,
-                    int head_dim, int causal, void* stream) {
+                    int head_dim, int causal, const lss_dropout* dropout, void* stream) {
   if (dtype != LSS_BF16) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_ex: bf16 only");
   if (!grad_k || !grad_v || !aligned16(grad_v)) return fail(LSS_ERR_ARG, "attn_bwd_ex: dK/dV buffers");
   return attn_bwd_launch(k, v, ld_kv, srcs, nsrc, grad_k, (long)(grad_v - grad_k), nullptr, 0, ld_dkv, batch, workers,
-                         seg_len, heads, head_dim, causal, stream);
+                         seg_len, heads, head_dim, causal, dropout, stream);
 }
 
 int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs, int nsrc,
                      float* const* seg_dst, int peer, long ld_dkv, int batch, int workers, int seg_len, int heads,
-                     int head_dim, int causal, void* stream) {
+                     int head_dim, int causal, const lss_dropout* dropout, void* stream) {
   if (dtype != LSS_BF16) return fail(LSS_ERR_UNSUPPORTED, "attn_bwd_p2p: bf16 only");
   if (!seg_dst) return fail(LSS_ERR_ARG, "attn_bwd_p2p: null segment table");
   return attn_bwd_launch(k, v, ld_kv, srcs, nsrc, nullptr, heads * head_dim, seg_dst, peer, ld_dkv, batch, workers,
-                         seg_len, heads, head_dim, causal, stream);
+                         seg_len, heads, head_dim, causal, dropout, stream);
 }
 
 int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, long n, void* stream) {
@@ -530,6 +553,25 @@ int lss_cross_entropy(const float* logits, long ld, const int* targets, long n, 
   if (n == 0) return LSS_OK;
   cross_entropy_kernel<<<(unsigned)n, 256, 0, S(stream)>>>(logits, ld, targets, vocab, scale, loss_rows, grad, ld_grad);
   return check_launch("cross_entropy");
+}
+
+int lss_dropout_rows(int dtype, const void* x, long ldx, void* out, long ldo, const float* residual, long ld_res,
+                     long rows, int cols, int rows_per_sample, long offset, unsigned long long site_key,
+                     unsigned long long thresh, float scale, void* stream) {
+  if (!x || !out) return fail(LSS_ERR_ARG, "dropout_rows: null pointer");
+  if (rows < 0 || cols <= 0 || rows_per_sample <= 0 || ldx < cols || ldo < cols || (residual && ld_res < cols))
+    return fail(LSS_ERR_SHAPE, "dropout_rows: shape");
+  if (rows == 0) return LSS_OK;
+  dim3 grid((unsigned)std::min(8, (cols + 255) / 256), (unsigned)std::min(rows, 65535L));
+  if (dtype == LSS_BF16)
+    dropout_rows_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(
+        reinterpret_cast<const __nv_bfloat16*>(x), ldx, reinterpret_cast<__nv_bfloat16*>(out), ldo, residual, ld_res,
+        rows, cols, rows_per_sample, offset, site_key, thresh, scale);
+  else
+    dropout_rows_kernel<float><<<grid, 256, 0, S(stream)>>>(reinterpret_cast<const float*>(x), ldx,
+                                                           reinterpret_cast<float*>(out), ldo, residual, ld_res, rows,
+                                                           cols, rows_per_sample, offset, site_key, thresh, scale);
+  return check_launch("dropout_rows");
 }
 
 // ------------------------------------------------------------------ peer memory (CUDA IPC)
@@ -627,7 +669,7 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
   src.q = q; src.grad_o = grad_o; src.grad_q = grad_q; src.m_src = rows; src.row0 = 0; src.rows = rows;
   src.pos0 = offset; src.g_begin = 0; src.g_end = workers; src.lse2 = lse2; src.delta = delta_ws; src.pitch = m_pad;
   return lss_attn_bwd_ex(dtype, k, v, ld_kv, &src, 1, grad_k, grad_v, ld_dkv, batch, workers, seg_len, heads,
-                         head_dim, causal, stream);
+                         head_dim, causal, nullptr, stream);
 }
 
 int lss_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b, void* o_out,

@@ -258,8 +258,12 @@ def attn_bwd(q, k, v, o, grad_o, lse2, *, workers, seg_len, heads, offset, causa
 # ----------------------------------------------------------------- balanced-schedule pieces
 
 
+def _drop(dropout):
+    return ctypes.byref(dropout) if dropout is not None else None
+
+
 def attn_fwd_partial(q, k, v, *, rows, row0, workers, seg_len, heads, offset, causal, g_begin, g_end, out,
-                     lse2):
+                     lse2, dropout=None):
     """Partial attention of q rows [row0, row0+rows) (global position offset + row0 for
     the first) over key segments [g_begin, g_end) into out[:, row0:row0+rows] and
     lse2[..., row0:row0+rows] (full-size [B,m,E] / [B,H,m_pad] buffers)."""
@@ -272,7 +276,7 @@ def attn_fwd_partial(q, k, v, *, rows, row0, workers, seg_len, heads, offset, ca
     lv = lse2[:, :, row0:]
     call("lss_attn_fwd_ex", LSS_BF16, _ptr(qv), rows, m * e, _ptr(k), _ptr(v), ldk, _ptr(ov), m * e, _ptr(lv),
          lse2.shape[-1], bsz, workers, seg_len, heads, e // heads, offset + row0, int(causal), g_begin, g_end,
-         _stream())
+         _drop(dropout), _stream())
 
 
 def attn_merge(o_a, lse_a, o_b, lse_b, *, row0, rows, heads, o_out=None, lse_out=None):
@@ -312,7 +316,7 @@ def _bwd_source_array(sources):
 
 
 def attn_bwd_sources(k, v, sources, *, grad_k=None, grad_v=None, seg_dst=None, peer=False, ld_dkv=None,
-                     workers, seg_len, heads, causal):
+                     workers, seg_len, heads, causal, dropout=None):
     """Multi-source backward.  sources: dicts with q, grad_o, grad_q (fp32, pre-zeroed),
     row0, rows, pos0 (global position of tensor row 0), g_begin, g_end, lse2, delta.
 
@@ -330,10 +334,25 @@ def attn_bwd_sources(k, v, sources, *, grad_k=None, grad_v=None, seg_dst=None, p
         tab = (ctypes.c_void_p * workers)(*[int(a) for a in seg_dst])
         call("lss_attn_bwd_p2p", LSS_BF16, _ptr(k), _ptr(v), ldk, arr, len(sources), tab, int(peer),
              int(ld_dkv if ld_dkv is not None else 2 * e), bsz, workers, seg_len, heads, e // heads, int(causal),
-             _stream())
+             _drop(dropout), _stream())
         return
     call("lss_attn_bwd_ex", LSS_BF16, _ptr(k), _ptr(v), ldk, arr, len(sources), _ptr(grad_k), _ptr(grad_v),
-         grad_k.stride(-2), bsz, workers, seg_len, heads, e // heads, int(causal), _stream())
+         grad_k.stride(-2), bsz, workers, seg_len, heads, e // heads, int(causal), _drop(dropout), _stream())
+
+
+def dropout_rows(x, out, *, rows_per_sample, offset, site_key, thresh, scale, residual=None):
+    """nnops.dropout_fwd / dropout_bwd on a (rows, cols) activation (row r = sample
+    r // rows_per_sample at position offset + r % rows_per_sample): out = x * keep *
+    scale (+ residual).  x / out same dtype (bf16 or fp32), may alias."""
+    cols = x.shape[-1]
+    rows = x.numel() // cols
+    if out.dtype != x.dtype or out.numel() != x.numel():
+        raise ShapeError("dropout_rows: out must match x")
+    dt = LSS_BF16 if x.dtype == torch.bfloat16 else LSS_F32
+    call("lss_dropout_rows", dt, _ptr(x), cols, _ptr(out), cols, _ptr(residual),
+         residual.shape[-1] if residual is not None else 0, rows, cols, rows_per_sample, offset, site_key, thresh,
+         scale, _stream())
+    return out
 
 
 def sum_slots(dst, src):

@@ -33,6 +33,7 @@ from typing import Callable, Optional
 import torch
 
 from . import kernels as K
+from .dropout import DropoutPolicy, as_policy
 from .errors import ShapeError, UnsupportedError
 
 LAYERNORM_EPS = 1e-5
@@ -132,9 +133,25 @@ def layer_params_from_arrays(ln1_gain, ln1_bias, wq, bq, wk, bk, wv, bv, wo, bo,
 
 
 def _check_dropout(cfg: ModelConfig, policy) -> None:
-    active = getattr(policy, "active", False) or cfg.dropout > 0
-    if active:
-        raise UnsupportedError("dropout > 0 is outside the B200 hot path (every BASELINE config runs 0)")
+    """Dropout (position-keyed masks, dropout.py) runs on the bf16 tcgen05 path; the
+    fp32 check mode has no dropout kernels."""
+    if as_policy(policy).active and cfg.precision != "bf16":
+        raise UnsupportedError("dropout > 0 runs on the bf16 path only (no fp32 check-mode dropout kernels)")
+
+
+def _dropout(x: torch.Tensor, policy, layer: int, tag: str, offset: int, out=None, residual=None):
+    """nnops.dropout_fwd / dropout_bwd on (B, m, C) rows at global positions
+    offset..offset+m (model.dropout3 / row_coords, model.py:230-268); identity
+    (plus residual) when the policy is off."""
+    pol = as_policy(policy)
+    if not pol.active:
+        if residual is None:
+            return x
+        return (x.to(torch.float32) + residual) if out is None else out.copy_(x + residual)
+    b, m, c = x.shape
+    out = out if out is not None else torch.empty_like(x if residual is None else residual)
+    return K.dropout_rows(x.contiguous(), out, rows_per_sample=m, offset=offset, site_key=pol.site_key(layer, tag),
+                          thresh=pol.thresh, scale=pol.scale, residual=residual)
 
 
 def _as_act(x: torch.Tensor, cfg: ModelConfig) -> torch.Tensor:
@@ -211,6 +228,8 @@ class ScoreCache:
     v: torch.Tensor = field(repr=False)
     workers: int = 1
     seg_len: int = 0
+    policy: object = None  # dropout policy and layer: the masks are recomputed in the backward
+    layer: int = 0
 
 
 def _kv_rows(k: torch.Tensor):
@@ -244,14 +263,23 @@ def scores_fwd(q, k, v, offset: int, cfg: ModelConfig, policy=None, layer: int =
     va = v if v.dtype == cfg.act_dtype else v.to(cfg.act_dtype)
     if ka.dim() == 3:
         ka, va = ka.contiguous(), va.contiguous()
-    ctx, lse = K.attn_fwd(qa, ka, va, workers=workers, seg_len=seg, heads=cfg.n_heads, offset=offset,
-                          causal=cfg.causal)
+    pol = as_policy(policy)
+    if pol.active:  # probability dropout inside the flash kernel (nnops.keep_mask keys)
+        ctx = torch.empty(bsz, m, e, dtype=qa.dtype, device=qa.device)
+        lse = torch.empty(bsz, cfg.n_heads, K.rows_pad(m), dtype=torch.float32, device=qa.device)
+        kv = (ka, va) if ka.dim() == 4 else (ka.unsqueeze(0), va.unsqueeze(0))
+        K.attn_fwd_partial(qa, kv[0], kv[1], rows=m, row0=0, workers=workers, seg_len=seg, heads=cfg.n_heads,
+                           offset=offset, causal=cfg.causal, g_begin=0, g_end=workers, out=ctx, lse2=lse,
+                           dropout=pol.desc(layer))
+    else:
+        ctx, lse = K.attn_fwd(qa, ka, va, workers=workers, seg_len=seg, heads=cfg.n_heads, offset=offset,
+                              causal=cfg.causal)
     if counters is not None:  # model.py:312-313, 321-325: 2*m*d*t twice per (b, h)
         bh = bsz * cfg.n_heads
         counters.add_score_flops(m, cfg.head_dim * bh, t)
         counters.add_score_flops(m, t, cfg.head_dim * bh)
         counters.record_score_footprint(bh * m * t)
-    return ctx, ScoreCache(offset, ctx, lse, ka, va, workers, seg)
+    return ctx, ScoreCache(offset, ctx, lse, ka, va, workers, seg, pol, layer)
 
 
 def scores_bwd(cache: ScoreCache, q, k, v, grad_ctx, cfg: ModelConfig, policy=None):
@@ -269,6 +297,19 @@ def scores_bwd(cache: ScoreCache, q, k, v, grad_ctx, cfg: ModelConfig, policy=No
     else:
         packed = torch.empty(workers, bsz, seg, 2 * e, dtype=torch.float32, device=qa.device)
     gk, gv = packed[..., :e], packed[..., e:]
+    pol = as_policy(cache.policy)
+    if pol.active:  # same masks as the forward, recomputed from (seed, layer, b, h, q_pos, k_pos)
+        H = cfg.n_heads
+        delta = torch.empty(bsz, H, cache.lse2.shape[-1], dtype=torch.float32, device=qa.device)
+        K.attn_delta(cache.ctx, go, delta, heads=H, scaled=True)
+        gq = torch.zeros(bsz, m, e, dtype=torch.float32, device=qa.device)
+        src = dict(q=qa, grad_o=go, grad_q=gq, row0=0, rows=m, pos0=cache.offset, g_begin=0, g_end=workers,
+                   lse2=cache.lse2, delta=delta)
+        kv = (ka, va) if ka.dim() == 4 else (ka.unsqueeze(0), va.unsqueeze(0))
+        gk4, gv4 = (gk, gv) if gk.dim() == 4 else (gk.unsqueeze(0), gv.unsqueeze(0))
+        K.attn_bwd_sources(kv[0], kv[1], [src], grad_k=gk4, grad_v=gv4, workers=workers, seg_len=seg, heads=H,
+                           causal=cfg.causal, dropout=pol.desc(cache.layer))
+        return gq, gk, gv
     gq, gk, gv = K.attn_bwd(qa, ka, va, cache.ctx, go, cache.lse2, workers=workers, seg_len=seg,
                             heads=cfg.n_heads, offset=cache.offset, causal=cfg.causal, grad_k=gk,
                             grad_v=gv)
@@ -300,10 +341,14 @@ class FfnCache:
 
     yh: torch.Tensor
     h_pre: torch.Tensor
-    h: torch.Tensor
+    h: torch.Tensor  # h_drop (the dropped activation feeds ff_out and its wgrad)
+    policy: object = None
+    layer: int = 0
+    offset: int = 0
 
 
-def ffn_fwd(yh: torch.Tensor, lp: LayerParams, cfg: ModelConfig, policy=None, layer: int = 0, residual=None):
+def ffn_fwd(yh: torch.Tensor, lp: LayerParams, cfg: ModelConfig, policy=None, layer: int = 0, residual=None,
+            offset: int = 0):
     """model.ffn_fwd (model.py:371-378): ff_in -> tanh-GeLU -> ff_out.  The GeLU
     runs in the ff_in GEMM's epilogue (which also keeps the pre-activation for
     the backward); ``residual`` (fp32, optional) is added in the ff_out epilogue
@@ -320,11 +365,17 @@ def ffn_fwd(yh: torch.Tensor, lp: LayerParams, cfg: ModelConfig, policy=None, la
     h = torch.empty(b * m, ff, dtype=ad, device=yh.device)
     K.gemm(ya, _as_act(lp.ff_in.weight, cfg).contiguous(), b_mn_major=True, bias=lp.ff_in.bias, out=h,
            act="gelu", pre=h_pre, M=b * m, N=ff, K=e)
+    pol = as_policy(policy)
+    if pol.active:  # model.py:377 (ffn_hidden) and 451 (ffn_out)
+        _dropout(h.view(b, m, ff), pol, layer, "ffn_hidden", offset, out=h.view(b, m, ff))
     out = torch.empty(b * m, e, dtype=torch.float32, device=yh.device)
+    res = None if residual is None else residual.to(torch.float32).contiguous().view(b * m, e)
     K.gemm(h, _as_act(lp.ff_out.weight, cfg).contiguous(), b_mn_major=True, bias=lp.ff_out.bias, out=out,
-           residual=None if residual is None else residual.to(torch.float32).contiguous().view(b * m, e),
-           M=b * m, N=e, K=ff)
-    return out.view(b, m, e), FfnCache(ya, h_pre, h)
+           residual=None if pol.active else res, M=b * m, N=e, K=ff)
+    if pol.active:
+        out = _dropout(out.view(b, m, e), pol, layer, "ffn_out", offset,
+                       residual=None if res is None else res.view(b, m, e))
+    return out.view(b, m, e), FfnCache(ya, h_pre, h, pol, layer, offset)
 
 
 def ffn_bwd(cache: FfnCache, lp: LayerParams, grad_out: torch.Tensor, cfg: ModelConfig, policy=None):
@@ -336,12 +387,17 @@ def ffn_bwd(cache: FfnCache, lp: LayerParams, grad_out: torch.Tensor, cfg: Model
     M, ff = cache.h.shape
     ad = cfg.act_dtype
     g32 = grad_out.to(torch.float32).contiguous().view(M, e)
+    pol = as_policy(cache.policy)
+    if pol.active:  # dropout3_bwd(ffn_out), model.py:475
+        g32 = _dropout(g32.view(b, m, e), pol, cache.layer, "ffn_out", cache.offset).view(M, e)
     g = torch.empty(M, e, dtype=ad, device=g32.device)
     ff_out_bg = torch.zeros(e, dtype=torch.float32, device=g32.device)
     K.cat_cast_colsum([(g32, e, e)], M, dst=g, colsum=ff_out_bg)
     w_out = _as_act(lp.ff_out.weight, cfg).contiguous()  # [ff][E] = [N][K] for g . W_out^T
     g_pre32 = torch.empty(M, ff, dtype=torch.float32, device=g32.device)
     K.gemm(g, w_out, out=g_pre32, act="gelu_bwd", aux=cache.h_pre, M=M, N=ff, K=e)
+    if pol.active:  # dropout_bwd(ffn_hidden), model.py:387 (elementwise: commutes with GeLU')
+        _dropout(g_pre32.view(b, m, ff), pol, cache.layer, "ffn_hidden", cache.offset, out=g_pre32.view(b, m, ff))
     ff_out_wg = torch.empty(ff, e, dtype=torch.float32, device=g32.device)
     K.gemm(cache.h, g, a_mn_major=True, b_mn_major=True, out=ff_out_wg, M=ff, N=e, K=M)  # h^T . g
     g_pre = torch.empty(M, ff, dtype=ad, device=g32.device)
@@ -395,11 +451,12 @@ def layer_fwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, x: torch.Te
     k, v, kv_ctx = kv_fwd(xh, lp)
     q = linear3(xh, lp.attn_q, cfg, cfg.act_dtype)
     ctx, sc = scores_fwd(q, k, v, offset, cfg, policy, layer, counters)
-    x_mid = linear3(ctx, lp.attn_out, cfg) + x
+    x_mid = _dropout(linear3(ctx, lp.attn_out, cfg), policy, layer, "attn_out", offset,
+                     residual=x.to(torch.float32).contiguous())  # model.py:447-448
     if not lp.has_ffn:
         return x_mid, LayerCache(offset, ln1, xh, kv_ctx, q, k, v, sc, ctx)
     yh, ln2 = norm3(x_mid, lp.ln2_gain, lp.ln2_bias, cfg, out_dtype=cfg.act_dtype)
-    x_out, fc = ffn_fwd(yh, lp, cfg, policy, layer, residual=x_mid)
+    x_out, fc = ffn_fwd(yh, lp, cfg, policy, layer, residual=x_mid, offset=offset)
     return x_out, LayerCache(offset, ln1, xh, kv_ctx, q, k, v, sc, ctx, ln2, fc)
 
 
@@ -415,7 +472,8 @@ def layer_bwd(lp: LayerParams, cfg: ModelConfig, policy, layer: int, cache: Laye
         grad_mid, ln2_gg, ln2_bg = norm3_bwd(cache.ln2, lp.ln2_gain, grad_yh, grad_res=grad_out)
     else:
         grad_mid = grad_out
-    grad_ctx, out_wg, out_bg = linear3_bwd(cache.ctx, lp.attn_out, grad_mid, cfg)
+    g_att = _dropout(grad_mid, policy, layer, "attn_out", cache.offset)  # dropout3_bwd, model.py:479
+    grad_ctx, out_wg, out_bg = linear3_bwd(cache.ctx, lp.attn_out, g_att, cfg)
     gq, gk, gv = scores_bwd(cache.scores, cache.q, cache.k, cache.v, grad_ctx, cfg, policy)
     gxq, q_wg, q_bg = linear3_bwd(cache.xh, lp.attn_q, gq, cfg)
     gxkv, k_wg, k_bg, v_wg, v_bg = kv_bwd(cache.kv_ctx, lp, gk, gv)
@@ -472,6 +530,8 @@ def _ids(t: torch.Tensor, vocab: int, what: str) -> torch.Tensor:
 @dataclass
 class EmbedCache:
     tokens: torch.Tensor
+    policy: object = None
+    offset: int = 0
 
 
 def embed_fwd(params: Parameters, cfg: ModelConfig, tokens: torch.Tensor, offset: int = 0, policy=None):
@@ -483,12 +543,20 @@ def embed_fwd(params: Parameters, cfg: ModelConfig, tokens: torch.Tensor, offset
     if params.pos_table.shape[0] != m:
         raise ShapeError(f"position table has {params.pos_table.shape[0]} rows, block has {m}")
     ids = _ids(tokens, params.token_table.shape[0], "token")
-    return K.embed_fwd(ids, params.token_table.contiguous(), params.pos_table.contiguous()), EmbedCache(ids)
+    x = K.embed_fwd(ids, params.token_table.contiguous(), params.pos_table.contiguous())
+    pol = as_policy(policy)
+    if pol.active:  # model.py:526 (layer 0, tag "embed")
+        x = _dropout(x, pol, 0, "embed", offset, out=x)
+    return x, EmbedCache(ids, pol, offset)
 
 
 def embed_bwd(cache: EmbedCache, vocab: int, policy, grad_x: torch.Tensor):
     """model.embed_bwd (model.py:536-540) -> (grad_token_table, grad_pos_table)."""
-    return K.embed_bwd(cache.tokens, grad_x.to(torch.float32).contiguous(), vocab)
+    g = grad_x.to(torch.float32).contiguous()
+    pol = as_policy(cache.policy)
+    if pol.active:
+        g = _dropout(g, pol, 0, "embed", cache.offset)
+    return K.embed_bwd(cache.tokens, g, vocab)
 
 
 @dataclass
@@ -557,6 +625,7 @@ class SequentialCache:
     embed: EmbedCache
     layers: list
     head: HeadCache
+    policy: object = None
 
 
 def forward(params: Parameters, cfg: ModelConfig, tokens: torch.Tensor, targets=None, policy=None,
@@ -569,7 +638,7 @@ def forward(params: Parameters, cfg: ModelConfig, tokens: torch.Tensor, targets=
         x, c = layer_fwd(lp, cfg, policy, li, x, 0, None, counters)
         caches.append(c)
     loss, hc = head_fwd(x, params, targets, cfg)
-    return loss, SequentialCache(ec, caches, hc)
+    return loss, SequentialCache(ec, caches, hc, policy)
 
 
 def backward(params: Parameters, cfg: ModelConfig, cache: SequentialCache) -> Parameters:
@@ -577,6 +646,6 @@ def backward(params: Parameters, cfg: ModelConfig, cache: SequentialCache) -> Pa
     grad_x, fg, fb, hw, hb = head_bwd(cache.head, params, cfg)
     layer_grads = [None] * len(params.layers)
     for li in range(len(params.layers) - 1, -1, -1):
-        grad_x, layer_grads[li] = layer_bwd(params.layers[li], cfg, None, li, cache.layers[li], grad_x)
-    gt, gp = embed_bwd(cache.embed, cfg.vocab, None, grad_x)
+        grad_x, layer_grads[li] = layer_bwd(params.layers[li], cfg, cache.policy, li, cache.layers[li], grad_x)
+    gt, gp = embed_bwd(cache.embed, cfg.vocab, cache.policy, grad_x)
     return Parameters(gt, gp, layer_grads, fg, fb, LinearParams(hw, hb))

@@ -54,7 +54,7 @@ FULL_CASES = {
 }
 
 
-def run_case(seq, e, h, g, b, causal, seed=0, ff_dim=0):
+def run_case(seq, e, h, g, b, causal, seed=0, ff_dim=0, policy=None):
     cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=ff_dim or 8, vocab=16, seq_len=seq,
                       batch=b, causal=causal, precision="double")
     rng = np.random.default_rng(seed)
@@ -76,7 +76,7 @@ def run_case(seq, e, h, g, b, causal, seed=0, ff_dim=0):
         lp.ff_out = LinearParams(np.zeros_like(lp.ff_out.weight), np.zeros_like(lp.ff_out.bias))
     x = f32(rng.standard_normal((b, seq, e)))
     gy = f32(rng.standard_normal((b, seq, e)))
-    off = DropoutPolicy.off()
+    off = policy if policy is not None else DropoutPolicy.off()
     comm = Communicator(g, timeout=120.0)
     group = comm.group("sequence", tuple(range(g)))
 
@@ -126,7 +126,15 @@ def run_case(seq, e, h, g, b, causal, seed=0, ff_dim=0):
     return x, gy, params, y, dx, grads
 
 
-def gpt_case(seed=5):
+DROP_CASES = {
+    # name: (seq_len, embed, heads, workers, batch, causal, ff_dim, rate, seed) -- position-keyed dropout
+    # at every site; G=2 must equal G=1 on the same masks
+    "drop_layer_g1": (128, 128, 2, 1, 2, True, 256, 0.1, 1234),
+    "drop_layer_g2": (256, 128, 2, 2, 1, True, 256, 0.1, 1234),
+}
+
+
+def gpt_case(seed=5, policy=None, name="gpt_small"):
     """Whole decoder: model.forward / model.backward sequentially,
     2 layers, vocab 40 (not a multiple of 32: exercises the padded head)."""
     cfg = ModelConfig(embed_dim=128, n_layers=2, n_heads=2, ff_dim=256, vocab=40, seq_len=128, batch=2,
@@ -149,7 +157,7 @@ def gpt_case(seed=5):
     params.head = LinearParams(f32(params.head.weight), f32(0.05 * rng.standard_normal(40)))
     tokens = rng.integers(0, 40, (2, 128))
     targets = rng.integers(0, 40, (2, 128))
-    loss, cache = model.forward(params, cfg, tokens, targets)
+    loss, cache = model.forward(params, cfg, tokens, targets, policy)
     grads = model.backward(params, cfg, cache)
     arrays = dict(tokens=tokens.astype(np.int32), targets=targets.astype(np.int32),
                   loss=np.array(loss, dtype=np.float64),
@@ -159,8 +167,10 @@ def gpt_case(seed=5):
         arrays["p." + n] = np.asarray(a, np.float32)
     for n, a in grads.named_arrays():
         arrays["g." + n] = np.asarray(a, np.float64)
-    np.savez_compressed(OUT / "gpt_small.npz", **arrays)
-    print("gpt_small written, loss", loss)
+    if policy is not None:
+        arrays["drop"] = np.array([policy.rate, policy.seed], dtype=np.float64)
+    np.savez_compressed(OUT / f"{name}.npz", **arrays)
+    print(name, "written, loss", loss)
 
 
 def main():
@@ -183,6 +193,18 @@ def main():
         np.savez_compressed(OUT / f"{name}.npz", **arrays)
         print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("x", "y", "w_in")})
     gpt_case()
+    gpt_case(policy=DropoutPolicy(0.1, seed=99), name="gpt_drop")
+    for name, (seq, e, h, g, b, causal, ff, rate, dseed) in DROP_CASES.items():
+        pol = DropoutPolicy(rate, seed=dseed)
+        x, gy, params, y, dx, grads = run_case(seq, e, h, g, b, causal, ff_dim=ff, policy=pol)
+        arrays = dict(x=x.astype(np.float32), grad_y=gy.astype(np.float32),
+                      meta=np.array([seq, e, h, g, b, int(causal)], dtype=np.int64),
+                      ff_dim=np.array(ff, dtype=np.int64), drop=np.array([rate, dseed], dtype=np.float64),
+                      y=y.astype(np.float64), dx=dx.astype(np.float64))
+        arrays.update({k: v.astype(np.float32) for k, v in params.items()})
+        arrays.update({k: v.astype(np.float64) for k, v in grads.items()})
+        np.savez_compressed(OUT / f"{name}.npz", **arrays)
+        print(name, "written")
 
 
 if __name__ == "__main__":

@@ -625,3 +625,71 @@ def test_full_size_eight_rank_schedule_matches_single_rank(cuda):
     assert nerr(dx8.cpu().numpy(), dx1.cpu().numpy()) < 5e-3
     # sync averages the per-rank grads over the group (sharded.py:238): G=8 = full / 8
     assert nerr(8 * engines[0].grads.cpu().numpy(), g1.cpu().numpy()) < 5e-3
+
+
+# ---- position-keyed dropout
+
+
+def test_functional_layer_with_dropout_matches_reference(cuda):
+    """Complete layer with dropout at every site (attention probabilities inside the
+    flash kernels, attn_out, ffn_hidden, ffn_out) == the reference's layer_fwd /
+    layer_bwd with the same DropoutPolicy: the masks are the reference's bit for bit
+    (a wrong keep decision moves the result far beyond the bf16 tolerance)."""
+    import torch
+    from paper_2311_02382_b200 import model as M
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+
+    z, seq, e, h, g, b, causal = _load("drop_layer_g1")
+    rate, seed = float(z["drop"][0]), int(z["drop"][1])
+    pol = DropoutPolicy(rate, seed=seed)
+    cfg = M.ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=int(z["ff_dim"]), vocab=16, seq_len=seq, batch=b,
+                        causal=causal, dropout=rate)
+    lp = _full_params(z, cuda)
+    y, cache = M.layer_fwd(lp, cfg, pol, 0, torch.as_tensor(z["x"], device=cuda), 0)
+    dx, grads = M.layer_bwd(lp, cfg, pol, 0, cache, torch.as_tensor(z["grad_y"], device=cuda))
+    torch.cuda.synchronize()
+    assert_close_ref(y.cpu().numpy(), z["y"], 1e-2, "y")
+    assert_close_ref(dx.cpu().numpy(), z["dx"], 1e-2, "dx")
+    for name, gold in [("attn_q", "wq"), ("attn_v", "wv"), ("attn_out", "wo"), ("ff_in", "w_in"), ("ff_out", "w_out")]:
+        assert_close_ref(getattr(grads, name).weight.cpu().numpy(), z["g_" + gold], 1e-2, name)
+    # and the policy matters: without it the result is far off
+    y0, _ = M.layer_fwd(lp, M.ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=int(z["ff_dim"]), vocab=16,
+                                          seq_len=seq, batch=b), None, 0, torch.as_tensor(z["x"], device=cuda), 0)
+    assert nerr(y0.cpu().numpy(), z["y"]) > 5e-2
+
+
+def test_whole_model_with_dropout_matches_reference(cuda):
+    """model.forward / backward with dropout (embed + every layer site) == reference."""
+    import torch
+    from paper_2311_02382_b200 import model as M
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+
+    z = np.load(GOLDEN / "gpt_drop.npz")
+    L, h, v = int(z["n_layers"]), int(z["meta"][2]), int(z["vocab"])
+    pol = DropoutPolicy(float(z["drop"][0]), seed=int(z["drop"][1]))
+    params = _gpt_from_golden(z, cuda)
+    cfg = M.ModelConfig(embed_dim=128, n_layers=L, n_heads=h, ff_dim=int(z["ff_dim"]), vocab=v, seq_len=128,
+                        batch=2, dropout=pol.rate)
+    loss, cache = M.forward(params, cfg, torch.as_tensor(z["tokens"], device=cuda),
+                            torch.as_tensor(z["targets"], device=cuda), pol)
+    grads = M.backward(params, cfg, cache)
+    torch.cuda.synchronize()
+    assert abs(loss - float(z["loss"])) / float(z["loss"]) < 2e-2
+    got = dict(grads.named_arrays())
+    for name in [n for n in z.files if n.startswith("g.")]:
+        key = name[2:]
+        if key.endswith("attn_k.bias"):
+            continue
+        assert_close_ref(got[key].cpu().numpy(), z[name], 2e-2, key)
+
+
+def test_dropout_fp32_check_mode_raises(cuda):
+    import torch
+    from paper_2311_02382_b200 import model as M
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+    from paper_2311_02382_b200.errors import UnsupportedError
+
+    cfg = M.ModelConfig(embed_dim=64, n_layers=1, n_heads=1, ff_dim=8, vocab=16, seq_len=4, precision="single")
+    z = torch.zeros(1, 4, 64, device=cuda)
+    with pytest.raises(UnsupportedError):
+        M.scores_fwd(z, z, z, 0, cfg, DropoutPolicy(0.1))

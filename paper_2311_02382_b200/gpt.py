@@ -131,13 +131,21 @@ class GPTRank:
         self._stage_head()
 
     # ------------------------------------------------------------ step pieces
-    def embed(self, tokens_seg: torch.Tensor) -> torch.Tensor:
+    def embed(self, tokens_seg: torch.Tensor, policy=None) -> torch.Tensor:
+        """Token + position rows (model.embed_fwd, model.py:517-533), dropout at the
+        ``embed`` site of layer 0 when ``policy`` is active."""
         ids = tokens_seg.to(torch.int32).contiguous()
         if ids.shape != (self.B, self.m):
             raise ShapeError(f"tokens must be {(self.B, self.m)}, got {tuple(ids.shape)}")
         self.tokens = ids
         self.grads.zero_()
-        return K.embed_fwd(ids, self._views(self.params)["tok"], self.pos, out=self.x0)
+        for li, e in enumerate(self.engines):
+            e.set_dropout(policy, li)
+        x = K.embed_fwd(ids, self._views(self.params)["tok"], self.pos, out=self.x0)
+        e0 = self.engines[0]
+        if e0._dd is not None:
+            e0._drop_rows(x.view(-1, self.E), x.view(-1, self.E), "embed")
+        return x
 
     def head(self, x: torch.Tensor, targets_seg: torch.Tensor) -> torch.Tensor:
         """Final LN, head, cross-entropy of this rank's tokens and its backward to the
@@ -160,6 +168,9 @@ class GPTRank:
         return self.g_x
 
     def embed_backward(self, g: torch.Tensor) -> None:
+        e0 = self.engines[0]
+        if e0._dd is not None:  # dropout_bwd(embed), in place on the incoming gradient
+            e0._drop_rows(g.view(-1, self.E), g.view(-1, self.E), "embed")
         K.embed_bwd(self.tokens, g, self.V, grad_token=self._views(self.grads)["tok"], grad_pos=self.g_pos,
                     alpha_token=self.grad_scale, alpha_pos=self.grad_scale)
 
@@ -168,14 +179,15 @@ class GPTRank:
         return self._views(self.grads)["loss"][0]
 
 
-def gpt_step(ranks, comm, tokens, targets, *, step: int = 0, sync: bool = True, data_comm=None):
+def gpt_step(ranks, comm, tokens, targets, *, step: int = 0, sync: bool = True, data_comm=None, policy=None):
     """One training-step forward + backward (+ sync) of the decoder on every rank
     (sharded.forward / backward / sync, hybrid.vertical_sync).  ``ranks`` is this
     process's [GPTRank] (or G of them with a SimComm); tokens / targets are the
     ranks' (B, m) blocks.  Returns the ranks' loss device scalars (grid mean
-    after sync)."""
+    after sync).  ``policy``: dropout (dropout.DropoutPolicy / rate / None), the
+    same masks as the sequential model.forward."""
     L = len(ranks[0].engines)
-    xs = [r.embed(t) for r, t in zip(ranks, tokens)]
+    xs = [r.embed(t, policy) for r, t in zip(ranks, tokens)]
     for li in range(L):
         xs = lss_forward([r.engines[li] for r in ranks], comm, xs, step=step, layer=li)
     gs = [r.head(x, t) for r, x, t in zip(ranks, xs, targets)]

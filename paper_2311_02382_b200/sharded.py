@@ -31,7 +31,8 @@ import torch
 
 from . import kernels as K
 from .comm import Ledger, SimComm, TorchDistComm
-from .errors import PartitionError, ShapeError
+from .dropout import as_policy
+from .errors import PartitionError, ShapeError, UnsupportedError
 from .model import LayerParams, LinearParams, ModelConfig
 
 
@@ -244,6 +245,31 @@ class LSSAttention:
         self.fused_rs = bool(fused_rs) and G > 1 and cfg.precision == "bf16"
         self.seg_dst = None
         self.peer_mem = False
+        self.set_dropout(None, 0)
+
+    # ------------------------------------------------------------ dropout
+    def set_dropout(self, policy, layer: int) -> None:
+        """Dropout policy of the next step(s) at ``layer`` (model.layer_fwd's
+        ``policy, layer``): masks are keyed by global positions, so every rank (and
+        the partner computing delegated rows) draws exactly the sequential masks."""
+        pol = as_policy(policy)
+        if pol.active and self.cfg.precision != "bf16":
+            raise UnsupportedError("dropout > 0 runs on the bf16 path only (no fp32 check-mode dropout kernels)")
+        self.policy, self.layer = pol, layer
+        self._dd = pol.desc(layer) if pol.active else None  # score-site descriptor for the attention kernels
+
+    def _drop_rows(self, x, out, tag: str, residual=None):
+        """dropout_fwd / dropout_bwd of this rank's rows (positions offset..offset+m)."""
+        pol = self.policy
+        return K.dropout_rows(x, out, rows_per_sample=self.m, offset=self.spec.offset,
+                              site_key=pol.site_key(self.layer, tag), thresh=pol.thresh, scale=pol.scale,
+                              residual=residual)
+
+    def _drop_tmp(self) -> torch.Tensor:
+        """fp32 [B*m, E] scratch for the dropped sites (forward temp, masked gradients)."""
+        if getattr(self, "_dtmp", None) is None:
+            self._dtmp = torch.empty(self.B * self.m, self.E, dtype=torch.float32, device=self.device)
+        return self._dtmp
 
     # ------------------------------------------------------------ parameters
     def load_params(self, lp: LayerParams) -> None:
@@ -416,18 +442,25 @@ class LSSAttention:
         common = dict(workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal)
         if pl.role == "heavy":
             K.attn_fwd_partial(self.q, kf, vf, rows=pl.split, row0=0, offset=self.spec.offset, g_begin=pl.a,
-                               g_end=r + 1, out=self.ctx, lse2=self.lse2, **common)
+                               g_end=r + 1, out=self.ctx, lse2=self.lse2, dropout=self._dd, **common)
             K.attn_fwd_partial(self.q, kf, vf, rows=m - pl.split, row0=pl.split, offset=self.spec.offset,
-                               g_begin=pl.b, g_end=r + 1, out=self.ctx, lse2=self.lse2, **common)
+                               g_begin=pl.b, g_end=r + 1, out=self.ctx, lse2=self.lse2, dropout=self._dd,
+                               **common)
             return
-        K.attn_fwd(self.q, kf, vf, offset=self.spec.offset, out=self.ctx, lse2=self.lse2, **common)
+        if self._dd is not None:  # dropout lives in the partial (tcgen05) launch
+            K.attn_fwd_partial(self.q, kf, vf, rows=m, row0=0, offset=self.spec.offset, g_begin=0,
+                               g_end=r + 1 if self.cfg.causal else self.G, out=self.ctx, lse2=self.lse2,
+                               dropout=self._dd, **common)
+        else:
+            K.attn_fwd(self.q, kf, vf, offset=self.spec.offset, out=self.ctx, lse2=self.lse2, **common)
         if pl.role == "light":
             off = pl.partner * m
             K.attn_fwd_partial(self.q_peer, kf, vf, rows=pl.split, row0=0, offset=off, g_begin=0, g_end=pl.a,
-                               out=self.o_peer, lse2=self.lse_peer, **common)
+                               out=self.o_peer, lse2=self.lse_peer, dropout=self._dd, **common)
             if pl.b > 0:
                 K.attn_fwd_partial(self.q_peer, kf, vf, rows=m - pl.split, row0=pl.split, offset=off,
-                                   g_begin=0, g_end=pl.b, out=self.o_peer, lse2=self.lse_peer, **common)
+                                   g_begin=0, g_end=pl.b, out=self.o_peer, lse2=self.lse_peer, dropout=self._dd,
+                                   **common)
 
     def own_ranges(self):
         """(row0, rows, g_begin, g_end) blocks of this rank's own query rows."""
@@ -439,7 +472,7 @@ class LSSAttention:
     def _fwd_common(self):
         E = self.E
         return (self.kv_full[..., :E], self.kv_full[..., E:],
-                dict(workers=self.G, seg_len=self.m, heads=self.H, causal=self.cfg.causal))
+                dict(workers=self.G, seg_len=self.m, heads=self.H, causal=self.cfg.causal, dropout=self._dd))
 
     def fwd_attend_local(self, part: int | None = None) -> None:
         """Own rows x own key segment: needs no remote K/V, so it runs while the
@@ -501,6 +534,12 @@ class LSSAttention:
             if pl.b > 0:
                 K.attn_merge(self.ctx, self.lse2, self.o_help, self.lse_help, row0=pl.split, rows=m - pl.split,
                              heads=self.H)
+        if self._dd is not None:  # x_mid = x + dropout3(attn_out) (model.py:447-448)
+            att = self._drop_tmp()
+            K.gemm(self.ctx.view(B * m, E), self.staged["wo_t"], bias=self.lp.attn_out.bias, out=att,
+                   M=B * m, N=E, K=E)
+            self._drop_rows(att, self.y.view(B * m, E), "attn_out", residual=self.x.view(B * m, E))
+            return self.y
         K.gemm(self.ctx.view(B * m, E), self.staged["wo_t"], bias=self.lp.attn_out.bias,
                residual=self.x.view(B * m, E), out=self.y.view(B * m, E), M=B * m, N=E, K=E)
         return self.y
@@ -516,6 +555,12 @@ class LSSAttention:
         K.layernorm_fwd(x_mid, lp.ln2_gain, lp.ln2_bias, out=self.yh, mean=self.mean2, rstd=self.rstd2)
         K.gemm(self.yh.view(M, E), self.w_in, b_mn_major=True, bias=lp.ff_in.bias, out=self.h, act="gelu",
                pre=self.h_pre, M=M, N=F, K=E)
+        if self._dd is not None:  # ffn_hidden / ffn_out sites (model.py:377, 451)
+            self._drop_rows(self.h, self.h, "ffn_hidden")
+            K.gemm(self.h, self.w_out, b_mn_major=True, bias=lp.ff_out.bias, out=self.y_out.view(M, E),
+                   M=M, N=E, K=F)
+            self._drop_rows(self.y_out.view(M, E), self.y_out.view(M, E), "ffn_out", residual=x_mid.view(M, E))
+            return self.y_out
         K.gemm(self.h, self.w_out, b_mn_major=True, bias=lp.ff_out.bias, residual=x_mid.view(M, E),
                out=self.y_out.view(M, E), M=M, N=E, K=F)
         return self.y_out
@@ -530,8 +575,11 @@ class LSSAttention:
         if grad_out.shape != (B, m, E) or grad_out.dtype != torch.float32 or not grad_out.is_contiguous():
             raise ShapeError(f"grad_y must be contiguous fp32 {(B, m, E)}")
         g32 = grad_out.view(M, E)
-        K.cat_cast_colsum([(g32, E, E)], M, dst=self.g_out, colsum=self.g_bout, alpha=a)
+        g_ffn = self._drop_rows(g32, self._drop_tmp(), "ffn_out") if self._dd is not None else g32
+        K.cat_cast_colsum([(g_ffn, E, E)], M, dst=self.g_out, colsum=self.g_bout, alpha=a)
         K.gemm(self.g_out, self.w_out, out=self.g_pre32, act="gelu_bwd", aux=self.h_pre, M=M, N=F, K=E)
+        if self._dd is not None:  # dropout_bwd(ffn_hidden): elementwise, commutes with GeLU'
+            self._drop_rows(self.g_pre32, self.g_pre32, "ffn_hidden")
         K.gemm(self.h, self.g_out, a_mn_major=True, b_mn_major=True, alpha=a, out=self.g_wout, M=F, N=E, K=M)
         K.cat_cast_colsum([(self.g_pre32, F, F)], M, dst=self.g_pre, colsum=self.g_bin, alpha=a)
         K.gemm(self.g_pre, self.w_in, out=self.g_yh, M=M, N=E, K=F)
@@ -551,11 +599,13 @@ class LSSAttention:
         self.grad_y = grad_y
         a = self.grad_scale
         # gy -> operand dtype, d b_out = alpha * column sums (nnops.py:192)
-        K.cat_cast_colsum([(grad_y.view(B * m, E), E, E)], B * m, dst=self.gy.view(B * m, E),
-                          colsum=self.g_bo, alpha=a)
+        g_att = grad_y.view(B * m, E)
+        if self._dd is not None:  # dropout3_bwd(attn_out), model.py:479; LN1 keeps the unmasked residual
+            g_att = self._drop_rows(g_att, self._drop_tmp(), "attn_out")
+        K.cat_cast_colsum([(g_att, E, E)], B * m, dst=self.gy.view(B * m, E), colsum=self.g_bo, alpha=a)
         # dctx = gy . Wo^T  (Wo [in][out] is the K-major B operand)
         K.gemm(self.gy.view(B * m, E), self.staged["wo"], out=self.dctx.view(B * m, E), M=B * m, N=E, K=E)
-        if self.plan.active or self.seg_dst is not None:
+        if self.plan.active or self.seg_dst is not None or self._dd is not None:
             K.attn_delta(self.ctx, self.dctx, self.delta, heads=self.H, scaled=True)
 
     def _wgrad_stream(self) -> torch.cuda.Stream:
@@ -586,7 +636,7 @@ class LSSAttention:
             out = dict(seg_dst=self.seg_dst, peer=self.peer_mem, ld_dkv=2 * E)
         else:
             out = dict(grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:])
-        if not pl.active and self.seg_dst is None:
+        if not pl.active and self.seg_dst is None and self._dd is None:
             K.attn_bwd(self.q, kf, vf, self.ctx, self.dctx, self.lse2, workers=self.G, seg_len=m,
                        heads=self.H, offset=self.spec.offset, causal=self.cfg.causal, grad_q=self.dq,
                        grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:], delta=self.delta)
@@ -607,7 +657,8 @@ class LSSAttention:
                 srcs.append(dict(peer, row0=pl.split, rows=m - pl.split, g_begin=0, g_end=pl.b))
         else:
             srcs = [dict(own, row0=0, rows=m, g_begin=0, g_end=self.G if not self.cfg.causal else r + 1)]
-        K.attn_bwd_sources(kf, vf, srcs, workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal, **out)
+        K.attn_bwd_sources(kf, vf, srcs, workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal,
+                           dropout=self._dd, **out)
 
     def bwd_fold(self) -> None:
         """Heavy rank of the balanced schedule: fold the partner's dQ rows in."""
@@ -636,15 +687,15 @@ class LSSAttention:
 
     # ------------------------------------------------------------ public step API
     def step(self, x: torch.Tensor, grad_y: torch.Tensor, comm, *, step: int = 0, layer: int = 0,
-             sync: bool = True):
+             sync: bool = True, policy=None):
         """Forward + backward (+ folded gradient sync) of this rank's block, device
         tensors in and out.  Returns (y, dx); gradients are in ``grads`` /
         ``grad_views()`` (already averaged over the group(s) when sync=True)."""
-        (y, dx), = lss_step([self], comm, [x], [grad_y], step=step, layer=layer, sync=sync)
+        (y, dx), = lss_step([self], comm, [x], [grad_y], step=step, layer=layer, sync=sync, policy=policy)
         return y, dx
 
     def step_from_host(self, x_host: torch.Tensor, grad_y_host: torch.Tensor, comm, grads_host=None,
-                       *, step: int = 0, layer: int = 0, next_inputs=None):
+                       *, step: int = 0, layer: int = 0, next_inputs=None, policy=None):
         """End-to-end call with HOST buffers: pinned x / grad_y are copied in and the
         averaged gradients are copied back to ``grads_host`` (pinned).  Inputs are
         double-buffered: with ``next_inputs`` = (x_host, grad_y_host) of the NEXT
@@ -686,7 +737,7 @@ class LSSAttention:
         self._slot = 1 - slot
         cur.wait_event(self._in_ready[slot])
         x_d, gy_d = self._in_bufs[slot]
-        out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer)
+        out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer, policy=policy)
         self._in_free[slot].record(cur)
         if grads_host is not None:
             grads_host.copy_(self.grads, non_blocking=True)
@@ -912,15 +963,18 @@ def lss_backward(engines, comm, grad_ys, *, step=0, layer=0, sync=True, mark=_no
     return dxs
 
 
-def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_bwd=None):
+def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_bwd=None, policy=None):
     """One fwd+bwd(+sync) of the layer (attention sublayer, or the complete layer
     for with_ffn engines).
 
     Real multi-GPU: ``engines`` = [this rank's LSSAttention], ``comm`` a
     TorchDistComm (or SoloComm for one rank).  Single-process simulation: G
     engines and a SimComm.  Returns the list of (y, dx) per engine (device
-    tensors, not synchronised)."""
+    tensors, not synchronised).  ``policy``: dropout (dropout.DropoutPolicy or a
+    rate; None = off), as model.layer_fwd's ``policy, layer``."""
     global last_phases
+    for e in engines:
+        e.set_dropout(policy, layer)
     clk = PhaseClock() if _PHASES else None
     mark = clk.mark if clk else _no_mark
     _bind_fused(engines, comm)

@@ -693,3 +693,120 @@ def test_dropout_fp32_check_mode_raises(cuda):
     z = torch.zeros(1, 4, 64, device=cuda)
     with pytest.raises(UnsupportedError):
         M.scores_fwd(z, z, z, 0, cfg, DropoutPolicy(0.1))
+
+
+@pytest.mark.parametrize("name", ["drop_layer_g1", "drop_layer_g2"])
+@pytest.mark.parametrize("balanced", [True, False])
+def test_engine_with_dropout_matches_reference(cuda, name, balanced):
+    """The sequence-distributed engine (complete layer, fused reduce-scatter, the
+    balanced causal schedule's delegated rows) with dropout at every site == the
+    reference's sharded layer with the same policy: masks are keyed by global
+    positions, so the partner computing delegated rows draws the owner's masks."""
+    import torch
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+    from paper_2311_02382_b200.model import ModelConfig
+    from paper_2311_02382_b200.sharded import ShardSpec, lss_step, make_sim_group, slice_batch
+
+    z, seq, e, h, g, b, causal = _load(name)
+    pol = DropoutPolicy(float(z["drop"][0]), seed=int(z["drop"][1]))
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=int(z["ff_dim"]), vocab=16, seq_len=seq, batch=b,
+                      causal=causal, dropout=pol.rate)
+    engines, comm = make_sim_group(cfg, _full_params(z, cuda), g, device=cuda, balanced=balanced)
+    x, gy = torch.as_tensor(z["x"], device=cuda), torch.as_tensor(z["grad_y"], device=cuda)
+    out = lss_step(engines, comm, [slice_batch(x, ShardSpec(r, g, seq)) for r in range(g)],
+                   [slice_batch(gy, ShardSpec(r, g, seq)) for r in range(g)], policy=pol)
+    torch.cuda.synchronize()
+    assert_close_ref(torch.cat([o[0] for o in out], 1).cpu().numpy(), z["y"], 1e-2, "y")
+    assert_close_ref(torch.cat([o[1] for o in out], 1).cpu().numpy(), z["dx"], 1e-2, "dx")
+    gv = {k: v.cpu().numpy() for k, v in engines[0].grad_views().items()}
+    for ours, gold in GRAD_KEYS + FFN_KEYS:
+        if gold == "bk":
+            continue
+        assert_close_ref(gv[ours], z["g_" + gold], 1e-2, ours)
+    # the next step without a policy is the plain layer again
+    out0 = lss_step(engines, comm, [slice_batch(x, ShardSpec(r, g, seq)) for r in range(g)],
+                    [slice_batch(gy, ShardSpec(r, g, seq)) for r in range(g)])
+    torch.cuda.synchronize()
+    assert nerr(torch.cat([o[0] for o in out0], 1).cpu().numpy(), z["y"]) > 5e-2
+
+
+def test_engine_dropout_balanced_g4_matches_single_rank(cuda):
+    """G=4 balanced causal schedule (two heavy/light pairs, ragged split rows) with
+    dropout == one rank on the same inputs and policy: every delegated row and
+    partial merge sees the sequential masks."""
+    import torch
+    from paper_2311_02382_b200.comm import Ledger, SoloComm
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+    from paper_2311_02382_b200.model import LayerParams, LinearParams, ModelConfig
+    from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec, lss_step, make_sim_group, slice_batch
+
+    l, E, H = 2000, 256, 4
+    pol = DropoutPolicy(0.15, seed=77)
+    cfg = ModelConfig(embed_dim=E, n_layers=1, n_heads=H, ff_dim=4 * E, vocab=16, seq_len=l, batch=2,
+                      dropout=pol.rate)
+    gen = torch.Generator(device=cuda).manual_seed(9)
+    u = lambda: (torch.rand(E, E, generator=gen, device=cuda) * 2 - 1) / E ** 0.5  # noqa: E731
+    zb = lambda: torch.zeros(E, device=cuda)  # noqa: E731
+    lp = LayerParams(torch.ones(E, device=cuda), zb(), LinearParams(u(), zb()), LinearParams(u(), zb()),
+                     LinearParams(u(), zb()), LinearParams(u(), zb()))
+    x = torch.randn(2, l, E, generator=gen, device=cuda)
+    gy = torch.randn(2, l, E, generator=gen, device=cuda)
+    one = LSSAttention(cfg, ShardSpec(0, 1, l), device=cuda)
+    one.load_params(lp)
+    y1, dx1 = one.step(x, gy, SoloComm(Ledger()), policy=pol)
+    y1, dx1, g1 = y1.clone(), dx1.clone(), one.grads.clone()
+    engines, comm = make_sim_group(cfg, lp, 4, device=cuda)
+    assert [e.plan.role for e in engines].count("heavy") == 2
+    out = lss_step(engines, comm, [slice_batch(x, ShardSpec(r, 4, l)) for r in range(4)],
+                   [slice_batch(gy, ShardSpec(r, 4, l)) for r in range(4)], policy=pol)
+    torch.cuda.synchronize()
+    assert nerr(torch.cat([o[0] for o in out], 1).cpu().numpy(), y1.cpu().numpy()) < 5e-3
+    assert nerr(torch.cat([o[1] for o in out], 1).cpu().numpy(), dx1.cpu().numpy()) < 5e-3
+    assert nerr(4 * engines[0].grads.cpu().numpy(), g1.cpu().numpy()) < 5e-3
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_distributed_gpt_step_with_dropout_matches_reference(cuda, G):
+    """gpt_step(policy=...) on G ranks == the reference's sequential model with the
+    same dropout policy (embed site + every layer site)."""
+    import torch
+    from paper_2311_02382_b200 import model as M
+    from paper_2311_02382_b200.comm import Ledger, SimComm
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+    from paper_2311_02382_b200.gpt import GPTRank, gpt_step
+    from paper_2311_02382_b200.sharded import ShardSpec
+
+    z = np.load(GOLDEN / "gpt_drop.npz")
+    L, h, v, seq = int(z["n_layers"]), int(z["meta"][2]), int(z["vocab"]), 128
+    pol = DropoutPolicy(float(z["drop"][0]), seed=int(z["drop"][1]))
+    cfg = M.ModelConfig(embed_dim=128, n_layers=L, n_heads=h, ff_dim=int(z["ff_dim"]), vocab=v, seq_len=seq,
+                        batch=2, dropout=pol.rate)
+    P = _gpt_from_golden(z, cuda)
+    ranks = [GPTRank(cfg, ShardSpec(r, G, seq), device=cuda) for r in range(G)]
+    for rk in ranks:
+        rk.bind_params(P)
+    tok, tgt = torch.as_tensor(z["tokens"], device=cuda), torch.as_tensor(z["targets"], device=cuda)
+    m = seq // G
+    losses = gpt_step(ranks, SimComm(Ledger()), [tok[:, r * m:(r + 1) * m] for r in range(G)],
+                      [tgt[:, r * m:(r + 1) * m] for r in range(G)], policy=pol)
+    torch.cuda.synchronize()
+    assert abs(float(losses[0]) - float(z["loss"])) / float(z["loss"]) < 2e-2
+    got = dict(ranks[0].gradients().named_arrays())
+    got["pos_table"] = torch.cat([rk.g_pos for rk in ranks], 0)
+    for name in [n for n in z.files if n.startswith("g.")]:
+        key = name[2:]
+        if key.endswith("attn_k.bias"):
+            continue
+        assert_close_ref(got[key].cpu().numpy(), z[name], 2e-2, key)
+
+
+def test_engine_dropout_fp32_check_mode_raises(cuda):
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+    from paper_2311_02382_b200.errors import UnsupportedError
+    from paper_2311_02382_b200.model import ModelConfig
+    from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec
+
+    cfg = ModelConfig(embed_dim=64, n_layers=1, n_heads=1, ff_dim=8, vocab=16, seq_len=128, precision="single")
+    eng = LSSAttention(cfg, ShardSpec(0, 1, 128), device=cuda)
+    with pytest.raises(UnsupportedError):
+        eng.set_dropout(DropoutPolicy(0.1), 0)

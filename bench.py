@@ -288,13 +288,26 @@ def main_ours(args):
     for name in wrapped:
         setattr(Kmod, name, originals[name])
     launches = (_native.launch_count - launches0) // args.steps
-    if os.environ.get("LSS_PHASES") == "1":  # diagnostic: one extra step with a per-phase timeline
+    if os.environ.get("LSS_PHASES") in ("1", "2"):  # diagnostic: one extra step with a per-phase timeline
         from paper_2311_02382_b200 import sharded as _sh
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         one_step()
+        if os.environ.get("LSS_PHASES") == "2":  # steady state: back-to-back steps, stamps of the last
+            for _ in range(4):
+                one_step()
+            _sh.last_phases = _sh.last_clock.report()
         ph = {k: round(v, 3) for k, v in _sh.last_phases.items()}
+        if _sh.last_stamps and world > 1:  # cross-rank timeline (GPU global timer, us after the earliest start)
+            allst = [None] * world
+            dist.all_gather_object(allst, _sh.last_stamps)
+            if rank == 0:  # per-GPU timers are not synchronised: align on the backward barrier's release
+                names = [n for n, _ in allst[0]]
+                ai = names.index("rs_barrier") if "rs_barrier" in names else 0
+                for i, name in enumerate(names):
+                    print(f"[timeline] {name:16s} " + " ".join(f"{(st[i][1] - st[ai][1]) / 1e3:9.1f}"
+                                                          for st in allst), file=sys.stderr, flush=True)
         torch.cuda.synchronize()
         _sh._PHASES = False  # the phase clock synchronises; measure the plain step
         h0 = time.perf_counter()

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 4
+#define LSS_ABI_VERSION 5
 
 enum lss_status {
   LSS_OK = 0,
@@ -149,6 +149,21 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
                     int workers, int seg_len, int heads, int head_dim, long offset, int causal,
                     int g_begin, int g_end, const lss_dropout* dropout, void* stream);
 
+/* lss_attn_fwd_ex with the key range split `splits` ways (1..16) inside ONE
+ * launch: split s attends key tiles [s*n/S, (s+1)*n/S) of each CTA's n visible
+ * tiles; split 0 writes (o, lse2), split s > 0 the caller's scratch slot s-1 at
+ * o_part + (s-1)*o_part_stride / lse_part + (s-1)*lse_part_stride (same batch
+ * stride and lse pitch as o / lse2), and an N-way log-sum-exp merge folds the
+ * slots into (o, lse2) on the same stream.  For launches with few query tiles
+ * over a long key range (a rank's remote segments at N >= 4), where one CTA per
+ * query-tile pair would leave most of the 148 SMs idle in the last wave.
+ * Same result as lss_attn_fwd_ex up to the bf16 rounding of the partials. */
+int lss_attn_fwd_split(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v,
+                       long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch,
+                       int workers, int seg_len, int heads, int head_dim, long offset, int causal,
+                       int g_begin, int g_end, const lss_dropout* dropout, int splits, void* o_part,
+                       long o_part_stride, float* lse_part, long lse_part_stride, void* stream);
+
 /* log-sum-exp combine of two partial attentions over disjoint key ranges:
  * lse = log2(2^la + 2^lb), ctx = 2^(la-lse) ctx_a + 2^(lb-lse) ctx_b (bf16, head_dim 64).
  * o_out / lse_out may alias o_a / lse_a. */
@@ -197,6 +212,19 @@ int lss_attn_bwd_ex(int dtype, const void* k, const void* v, long ld_kv, const l
 
 /* y += x (fp32), used to fold a partner's dQ rows into the owner's. */
 int lss_add_f32(float* y, const float* x, long n, void* stream);
+
+/* Cross-process stream signals (stream memory operations: executed by the GPU
+ * front-end, no SM, no NCCL kernel).  lss_stream_signal writes `value` to *flag
+ * after every prior operation of `stream` (memory fence included); flag may be
+ * an IPC-mapped word of a peer GPU.  lss_stream_wait blocks `stream` until
+ * (int32)(*flag - value) >= 0 (monotonic sequence numbers).  They replace the
+ * reference's point-to-point sends / barriers of the balanced causal schedule
+ * (sharded.py:144-154 exchanges) on one NVLink domain. */
+int lss_stream_signal(unsigned int* flag, unsigned int value, void* stream);
+int lss_stream_wait(const unsigned int* flag, unsigned int value, void* stream);
+
+/* Diagnostic: stream-ordered write of the GPU global timer (ns) to *dst. */
+int lss_timestamp(unsigned long long* dst, void* stream);
 
 /* ---- dK|dV reduce-scatter fused into the backward (NVLink / NVSwitch peer memory)
  *

@@ -82,11 +82,16 @@ SIGNATURES = {
                      _P],
     "lss_attn_fwd_ex": [_I, _P, _I, _L, _P, _P, _L, _P, _L, _P, _I, _I, _I, _I, _I, _I, _L, _I, _I, _I,
                         ctypes.POINTER(DropoutDesc), _P],
+    "lss_attn_fwd_split": [_I, _P, _I, _L, _P, _P, _L, _P, _L, _P, _I, _I, _I, _I, _I, _I, _L, _I, _I, _I,
+                           ctypes.POINTER(DropoutDesc), _I, _P, _L, _P, _L, _P],
     "lss_attn_merge": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _L, _I, _P],
     "lss_attn_delta": [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P],
     "lss_attn_bwd_ex": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, _P, _P, _L, _I, _I, _I, _I, _I, _I,
                         ctypes.POINTER(DropoutDesc), _P],
     "lss_add_f32": [_P, _P, _L, _P],
+    "lss_timestamp": [_P, _P],
+    "lss_stream_signal": [_P, ctypes.c_uint, _P],
+    "lss_stream_wait": [_P, ctypes.c_uint, _P],
     "lss_attn_bwd_p2p": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, ctypes.POINTER(_P), _I, _L, _I, _I, _I,
                          _I, _I, _I, ctypes.POINTER(DropoutDesc), _P],
     "lss_dropout_rows": [_I, _P, _L, _P, _L, _P, _L, _L, _I, _I, _L, ctypes.c_ulonglong, ctypes.c_ulonglong, _F, _P],
@@ -108,7 +113,7 @@ EXTRA = {
     "lss_rows_pad": ([_L], _L),
     "lss_peer_access": ([_I, _I], _I),
 }
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _lib = None
 
@@ -145,7 +150,7 @@ KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 
                     "lss_attn_merge": 1, "lss_attn_delta": 1, "lss_attn_bwd_ex": 1, "lss_add_f32": 1,
                     "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1,
                     "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1,
-                    "lss_dropout_rows": 1}
+                    "lss_dropout_rows": 1, "lss_attn_fwd_split": 1}
 launch_count = 0
 
 
@@ -155,6 +160,8 @@ def call(name: str, *args):
     lib = load()
     rc = getattr(lib, name)(*args)
     launch_count += KERNELS_PER_CALL.get(name, 0)
+    if name == "lss_attn_fwd_split" and args[21] > 1:
+        launch_count += 1  # + the N-way merge
     if rc != 0:
         msg = lib.lss_last_error().decode(errors="replace")
         raise _STATUS.get(rc, NativeError)(f"{name}: {msg}")

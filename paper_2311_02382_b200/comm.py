@@ -81,6 +81,11 @@ class TorchDistComm:
         self.seq_rank = dist.get_rank(seq_group)
         self._peers = {}
         self._flag = None
+        self._board = None     # flag words [channel][source rank] of every rank (stream signals)
+        self._seq = {}
+        import os
+
+        self.use_flags = os.environ.get("LSS_FLAGS", "1") != "0"
 
     def peer_addresses(self, t: torch.Tensor):
         """Device addresses, in this process, of every sequence-group rank's copy of
@@ -124,6 +129,98 @@ class TorchDistComm:
         self._peers[key] = (addrs, t)  # keep the tensor alive while peers may write into it
         return addrs
 
+    def map_named(self, named: dict):
+        """Collective: every rank contributes {name: tensor or None}; returns, per rank,
+        {name: device address in this process} (own tensors: their pointers; peers':
+        CUDA IPC mappings), or None when some pair of ranks cannot map each other."""
+        if self.dist.get_backend(self.seq_group) != "nccl" or self.seq_size == 1:
+            return None
+        import socket
+
+        from . import kernels as K
+
+        dev = torch.cuda.current_device()
+        mine = {n: (K.ipc_export(t) if t is not None else None) for n, t in named.items()}
+        info = [None] * self.seq_size
+        self.dist.all_gather_object(info, (socket.gethostname(), dev, mine), group=self.seq_group)
+        ok = all(h == info[self.seq_rank][0] for h, _, _ in info)
+        ok = ok and all(K.peer_access(dev, d) for r, (_, d, _) in enumerate(info) if r != self.seq_rank)
+        out, opened = [], []
+        if ok:
+            try:
+                for r, (_, _, entries) in enumerate(info):
+                    if r == self.seq_rank:
+                        out.append({n: t.data_ptr() for n, t in named.items() if t is not None})
+                        continue
+                    d = {}
+                    for n, e in entries.items():
+                        if e is not None:
+                            d[n] = K.ipc_import(*e)
+                            opened.append((d[n], e[1]))
+                    out.append(d)
+            except Exception:  # noqa: BLE001 - any rank failing disables the path for all
+                ok = False
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.device("cuda", dev))
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.seq_group)
+        if not flag.item():
+            for a, o in opened:
+                K.ipc_close(a, o)
+            return None
+        self._keep = getattr(self, "_keep", []) + [named]  # peers may write into these
+        return out
+
+    # ------------------------------------------------ stream signals (no SM, no NCCL kernel)
+    N_CHANNELS = 8  # 0 forward barrier, 1 backward barrier, 2-5 F1/F2/B1/B2 hand-offs
+
+    def flags_ready(self) -> bool:
+        """Map every rank's flag board once (collective); False when unavailable."""
+        if self._board is None:
+            if not self.use_flags or self.seq_size == 1 or self.dist.get_backend(self.seq_group) != "nccl":
+                self._board = False
+                return False
+            dev = torch.device("cuda", torch.cuda.current_device())
+            board = torch.zeros(self.N_CHANNELS * self.seq_size, dtype=torch.int32, device=dev)
+            torch.cuda.synchronize()  # zeroed before any peer can signal into it
+            addrs = self.map_named({"board": board})
+            self._board = False if addrs is None else (board, [a["board"] for a in addrs])
+        return self._board is not False
+
+    def _flag_addr(self, rank: int, channel: int, source: int) -> int:
+        return self._board[1][rank] + 4 * (channel * self.seq_size + source)
+
+    def flag_barrier(self, channel: int, step=0, phase="backward", layer=None, stream=None):
+        """Stream-ordered barrier through the flag boards: signal every peer, then wait
+        for every peer's signal.  Same contract as device_barrier."""
+        from . import kernels as K
+
+        self.ledger.record("barrier", self.seq_name, 1, step, phase, layer)
+        seq = self._seq[("bar", channel)] = self._seq.get(("bar", channel), 0) + 1
+        me = self.seq_rank
+        for p in range(self.seq_size):
+            if p != me:
+                K.stream_signal(self._flag_addr(p, channel, me), seq, stream)
+        for p in range(self.seq_size):
+            if p != me:
+                K.stream_wait(self._flag_addr(me, channel, p), seq, stream)
+
+    def notify(self, peer: int, channel: int, stream=None) -> None:
+        """Signal `peer` on `channel` once everything enqueued on `stream` is done."""
+        from . import kernels as K
+
+        seq = self._seq[("out", channel, peer)] = self._seq.get(("out", channel, peer), 0) + 1
+        K.stream_signal(self._flag_addr(peer, channel, self.seq_rank), seq, stream)
+
+    def expect(self, peer: int, channel: int):
+        """Handle whose wait() blocks the caller's current stream until `peer`'s next
+        notify on `channel` (the NCCL Work.wait() contract)."""
+        seq = self._seq[("in", channel, peer)] = self._seq.get(("in", channel, peer), 0) + 1
+        return _FlagWait(self._flag_addr(self.seq_rank, channel, peer), seq)
+
+    def push_stream(self) -> torch.cuda.Stream:
+        if getattr(self, "_push_stream", None) is None:
+            self._push_stream = torch.cuda.Stream(device=torch.cuda.current_device())
+        return self._push_stream
+
     def gather_pull(self, full: torch.Tensor, step=0, layer=0, segments=None):
         """K/V all-gather on the copy engines: after a device barrier (every rank's
         slot is written), pull each peer's own slot full[p] from its IPC-mapped
@@ -145,7 +242,10 @@ class TorchDistComm:
         # barrier on the compute stream: every rank then starts its diagonal tiles
         # together, which aligns the later hand-offs (measured N=4: 6.6 ms vs 6.8
         # with the barrier on the copy stream or with the NCCL all-gather)
-        self.device_barrier(step, "forward", layer)
+        if self.flags_ready() and self.use_flags:
+            self.flag_barrier(0, step, "forward", layer)
+        else:
+            self.device_barrier(step, "forward", layer)
         cs.wait_stream(cur)
         slot = full[0].numel() * full.element_size()
         for p in (range(self.seq_size) if segments is None else segments):
@@ -209,6 +309,18 @@ class TorchDistComm:
         for w in works:
             w.wait()
         return None
+
+
+class _FlagWait:
+    """Pending stream signal (see TorchDistComm.expect)."""
+
+    def __init__(self, addr: int, seq: int):
+        self.addr, self.seq = addr, seq
+
+    def wait(self) -> None:
+        from . import kernels as K
+
+        K.stream_wait(self.addr, self.seq)
 
 
 class SoloComm:

@@ -79,6 +79,15 @@ struct AttnFwdParams {
   uint64_t drop_site;
   uint64_t drop_thresh;
   float drop_scale;
+  // key split (few query tiles over a long key range, e.g. a rank's remote segments):
+  // split s of `splits` attends key tiles [s*n/S, (s+1)*n/S) of its CTA's n visible
+  // tiles; split 0 writes o / lse2, split s > 0 the partial slot s-1 (same row layout),
+  // merged afterwards by attn_merge_n_kernel
+  int splits;
+  __nv_bfloat16* o_part;
+  long o_part_stride;
+  float* lse_part;
+  long lse_part_stride;
 };
 
 template <bool DROP>
@@ -110,9 +119,11 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   // tail), while only a group's K/V streams are live at once (L2-resident).
   const int n_pairs = (p.m + 2 * ATT_BM - 1) / (2 * ATT_BM);
   const int hb = p.H * p.B;
-  const int grp_first = ((int)blockIdx.x / (ATT_FWD_HGROUP * n_pairs)) * ATT_FWD_HGROUP;
+  const int split = (int)blockIdx.x % p.splits;  // innermost: a tile's splits run together
+  const int cta = (int)blockIdx.x / p.splits;
+  const int grp_first = (cta / (ATT_FWD_HGROUP * n_pairs)) * ATT_FWD_HGROUP;
   const int grp_size = min(ATT_FWD_HGROUP, hb - grp_first);
-  const int in_grp = (int)blockIdx.x - grp_first * n_pairs;
+  const int in_grp = cta - grp_first * n_pairs;
   const int slice = grp_first + in_grp % grp_size;
   const int h = slice % p.H;
   const int b = slice / p.H;
@@ -134,6 +145,10 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
     }
     n_kv = n;
   }
+  const int j_base = (int)(((long)split * n_kv) / p.splits);  // this split's key tiles
+  n_kv = (int)(((long)(split + 1) * n_kv) / p.splits) - j_base;
+  __nv_bfloat16* const o_dst = split == 0 ? p.o : p.o_part + (long)(split - 1) * p.o_part_stride;
+  float* const lse_dst = split == 0 ? p.lse2 : p.lse_part + (long)(split - 1) * p.lse_part_stride;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -177,7 +192,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         const uint32_t ph = (j / ATT_KV_STAGES) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
         if (elect_one()) {
-          const int g = p.g_begin + j / tps, t = j % tps;
+          const int g = p.g_begin + (j_base + j) / tps, t = (j_base + j) % tps;
           mbar_arrive_expect_tx(&kv_full[st], 2 * ATT_TILE_BYTES);
           tma_load_4d(&tmK, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
           tma_load_4d(&tmV, &kv_full[st], sV + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
@@ -250,7 +265,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       float m_run = -INFINITY, l_run = 0.f;
       const int tile_first_row = q0 + w * ATT_BM;  // for the mask decision (warp-uniform)
       for (int j = 0; j < n_kv; ++j) {
-        const int g = p.g_begin + j / tps, t = j % tps;
+        const int g = p.g_begin + (j_base + j) / tps, t = (j_base + j) % tps;
         const int valid_cols = min(ATT_BN, p.seg_len - t * ATT_BN);
         const long key0 = (long)g * p.seg_len + (long)t * ATT_BN;
         const bool need_mask = valid_cols < ATT_BN ||
@@ -352,7 +367,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       tmem_ld64(tO[w] + lane_off, oo);
       if (lrow < p.m) {
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(p.o + (long)b * p.o_bstride + (long)lrow * E + h * ATT_D);
+        uint4* dst = reinterpret_cast<uint4*>(o_dst + (long)b * p.o_bstride + (long)lrow * E + h * ATT_D);
 #pragma unroll
         for (int i = 0; i < ATT_D / 8; ++i) {
           uint4 v;
@@ -362,19 +377,19 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
           v.w = pack_bf16(__uint_as_float(oo[8 * i + 6]) * inv, __uint_as_float(oo[8 * i + 7]) * inv);
           dst[i] = v;
         }
-        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = l_run > 0.f ? m_run + __log2f(l_run) : -INFINITY;
+        lse_dst[((long)b * p.H + h) * p.lse_pitch + lrow] = l_run > 0.f ? m_run + __log2f(l_run) : -INFINITY;
       } else if (lrow < p.m_pad) {
-        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = INFINITY;
+        lse_dst[((long)b * p.H + h) * p.lse_pitch + lrow] = INFINITY;
       }
     } else if (active) {
       // no key tile of [g_begin, g_end) is visible to this CTA: empty partial
       if (lrow < p.m) {
-        uint4* dst = reinterpret_cast<uint4*>(p.o + (long)b * p.o_bstride + (long)lrow * E + h * ATT_D);
+        uint4* dst = reinterpret_cast<uint4*>(o_dst + (long)b * p.o_bstride + (long)lrow * E + h * ATT_D);
 #pragma unroll
         for (int i = 0; i < ATT_D / 8; ++i) dst[i] = make_uint4(0u, 0u, 0u, 0u);
-        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = -INFINITY;
+        lse_dst[((long)b * p.H + h) * p.lse_pitch + lrow] = -INFINITY;
       } else if (lrow < p.m_pad) {
-        p.lse2[((long)b * p.H + h) * p.lse_pitch + lrow] = INFINITY;
+        lse_dst[((long)b * p.H + h) * p.lse_pitch + lrow] = INFINITY;
       }
     }
   }

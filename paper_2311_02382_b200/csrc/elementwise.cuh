@@ -250,6 +250,65 @@ __global__ void attn_delta_bf16_d64_kernel(const __nv_bfloat16* __restrict__ dO,
 // One warp per (batch, row); lane l covers 8 columns per 256-column chunk.
 // O_a/O_b/O_out are bf16 rows of E = H*64 (batch stride o_bstride elements),
 // lse buffers are [B][H][pitch] (base 2).  O_out/lse_out may alias O_a/lse_a.
+// N-way merge for the key-split forward: (o, lse) <- merge of (o, lse) and the
+// nparts partials at op + i*o_pstride / lp + i*l_pstride (same row layout); one
+// warp per row, 8 columns (one head) per lane and pass.
+constexpr int ATT_MERGE_MAX = 15;
+__global__ void attn_merge_n_kernel(__nv_bfloat16* o, float* lse, const __nv_bfloat16* op, const float* lp,
+                                    int nparts, long o_pstride, long l_pstride, int B, int rows, int H,
+                                    long o_bstride, int pitch) {
+  const long w = ((long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= (long)B * rows) return;
+  const int row = w % rows, b = w / rows;
+  const int E = H * 64;
+  for (int c0 = 0; c0 < E; c0 += 256) {
+    const int col = c0 + lane * 8;
+    const bool on = col < E;
+    const int h = col / 64;
+    const long li = ((long)b * H + h) * pitch + row;
+    float l = -INFINITY;
+    if (on) {
+      float ls[ATT_MERGE_MAX + 1];
+      ls[0] = lse[li];
+      float mx = ls[0];
+      for (int i = 0; i < nparts; ++i) {
+        ls[i + 1] = lp[i * l_pstride + li];
+        mx = fmaxf(mx, ls[i + 1]);
+      }
+      const long off = (long)b * o_bstride + (long)row * E + col;
+      float acc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+      float den = 0.f;
+      if (mx != -INFINITY) {
+        for (int i = 0; i <= nparts; ++i) {
+          const float wi = exp2f(ls[i] - mx);
+          if (wi == 0.f) continue;
+          den += wi;
+          const uint4 v = *reinterpret_cast<const uint4*>(i == 0 ? o + off : op + (i - 1) * o_pstride + off);
+          const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 x = __bfloat1622float2(v2[k]);
+            acc[2 * k] += wi * x.x;
+            acc[2 * k + 1] += wi * x.y;
+          }
+        }
+        l = mx + __log2f(den);
+      }
+      const float inv = den > 0.f ? 1.f / den : 0.f;
+      uint4 r;
+      uint32_t* r2 = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r2[k] = pack_bf16(acc[2 * k] * inv, acc[2 * k + 1] * inv);
+      *reinterpret_cast<uint4*>(o + off) = r;
+    }
+    __syncwarp();
+    if (on && (lane & 7) == 0) lse[li] = l;
+  }
+}
+
 __global__ void attn_merge_kernel(const __nv_bfloat16* oa, const float* la, const __nv_bfloat16* ob,
                                   const float* lb, __nv_bfloat16* oo, float* lo, int B, int rows, int H,
                                   long o_bstride, int pitch) {

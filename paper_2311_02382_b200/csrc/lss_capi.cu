@@ -8,6 +8,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/lss.h"
@@ -287,10 +289,14 @@ static int attn_check(int dtype, int batch, int rows, int workers, int seg_len, 
   return LSS_OK;
 }
 
-int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v, long ld_kv,
-                    void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers, int seg_len,
-                    int heads, int head_dim, long offset, int causal, int g_begin, int g_end,
-                    const lss_dropout* dropout, void* stream) {
+}  // extern "C"
+
+// Forward launcher shared by lss_attn_fwd_ex (splits = 1) and lss_attn_fwd_split.
+static int attn_fwd_launch(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v,
+                           long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers,
+                           int seg_len, int heads, int head_dim, long offset, int causal, int g_begin, int g_end,
+                           const lss_dropout* dropout, int splits, void* o_part, long o_part_stride,
+                           float* lse_part, long lse_part_stride, void* stream) {
   int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
   if (rc) return rc;
   if (!q || !k || !v || !o || !lse2) return fail(LSS_ERR_ARG, "attn_fwd: null pointer");
@@ -304,6 +310,7 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
   const float scale = 1.0f / sqrtf((float)head_dim);
   if (dtype == LSS_F32) {
     if (dropout && dropout->active) return fail(LSS_ERR_UNSUPPORTED, "attn_fwd f32: dropout is bf16-path only");
+    if (splits != 1) return fail(LSS_ERR_UNSUPPORTED, "attn_fwd f32: key splits are bf16-only");
     if (g_begin != 0 || g_end != workers || q_bstride != (long)rows * E || o_bstride != (long)rows * E ||
         lse_pitch != m_pad)
       return fail(LSS_ERR_UNSUPPORTED, "attn_fwd f32: partial/strided attention is bf16-only");
@@ -340,7 +347,12 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
   p.drop_site = drop ? dropout->site_key : 0;
   p.drop_thresh = drop ? dropout->thresh : 0;
   p.drop_scale = drop ? dropout->scale : 1.f;
-  dim3 grid((unsigned)((rows + 2 * ATT_BM - 1) / (2 * ATT_BM)) * heads * batch);
+  p.splits = splits;
+  p.o_part = reinterpret_cast<__nv_bfloat16*>(o_part);
+  p.o_part_stride = o_part_stride;
+  p.lse_part = lse_part;
+  p.lse_part_stride = lse_part_stride;
+  dim3 grid((unsigned)((rows + 2 * ATT_BM - 1) / (2 * ATT_BM)) * heads * batch * splits);
   if (drop) {
     if ((rc = set_smem(attn_fwd_tc_kernel<true>, ATT_FWD_SMEM))) return rc;
     attn_fwd_tc_kernel<true><<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
@@ -348,7 +360,45 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
     if ((rc = set_smem(attn_fwd_tc_kernel<false>, ATT_FWD_SMEM))) return rc;
     attn_fwd_tc_kernel<false><<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
   }
-  return check_launch("attn_fwd_tc");
+  if ((rc = check_launch("attn_fwd_tc"))) return rc;
+  if (splits > 1) {
+    const long warps = (long)batch * rows;
+    attn_merge_n_kernel<<<(warps * 32 + 255) / 256, 256, 0, S(stream)>>>(
+        reinterpret_cast<__nv_bfloat16*>(o), lse2, reinterpret_cast<const __nv_bfloat16*>(o_part), lse_part,
+        splits - 1, o_part_stride, lse_part_stride, batch, rows, heads, o_bstride, lse_pitch);
+    return check_launch("attn_merge_n");
+  }
+  return LSS_OK;
+}
+
+extern "C" {
+
+int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v, long ld_kv,
+                    void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers, int seg_len,
+                    int heads, int head_dim, long offset, int causal, int g_begin, int g_end,
+                    const lss_dropout* dropout, void* stream) {
+  return attn_fwd_launch(dtype, q, rows, q_bstride, k, v, ld_kv, o, o_bstride, lse2, lse_pitch, batch, workers,
+                         seg_len, heads, head_dim, offset, causal, g_begin, g_end, dropout, 1, nullptr, 0, nullptr,
+                         0, stream);
+}
+
+int lss_attn_fwd_split(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v,
+                       long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers,
+                       int seg_len, int heads, int head_dim, long offset, int causal, int g_begin, int g_end,
+                       const lss_dropout* dropout, int splits, void* o_part, long o_part_stride, float* lse_part,
+                       long lse_part_stride, void* stream) {
+  if (splits < 1 || splits > ATT_MERGE_MAX + 1)
+    return fail(LSS_ERR_ARG, "attn_fwd_split: %d splits (1..%d)", splits, ATT_MERGE_MAX + 1);
+  if (splits > 1) {
+    if (!o_part || !lse_part) return fail(LSS_ERR_ARG, "attn_fwd_split: null partial buffers");
+    const long o_span = (long)(batch - 1) * o_bstride + (long)rows * heads * head_dim;  // one slot's extent
+    if (!aligned16(o_part) || o_part_stride % 8 || o_part_stride < o_span ||
+        lse_part_stride < (long)(batch * heads - 1) * lse_pitch + rows)
+      return fail(LSS_ERR_SHAPE, "attn_fwd_split: partial slot stride");
+  }
+  return attn_fwd_launch(dtype, q, rows, q_bstride, k, v, ld_kv, o, o_bstride, lse2, lse_pitch, batch, workers,
+                         seg_len, heads, head_dim, offset, causal, g_begin, g_end, dropout, splits, o_part,
+                         o_part_stride, lse_part, lse_part_stride, stream);
 }
 
 int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, void* o, float* lse2,
@@ -608,21 +658,82 @@ int lss_ipc_export(const void* dev_ptr, unsigned char* handle, long* offset) {
   return LSS_OK;
 }
 
+}  // extern "C"
+
+// A peer allocation may back several exported buffers (the caching allocator
+// sub-allocates segments) but can be opened only once per process: mappings are
+// shared and reference-counted by handle.
+struct IpcMapping {
+  void* base;
+  int refs;
+};
+static std::mutex g_ipc_mu;
+static std::map<std::string, IpcMapping> g_ipc_maps;
+
+extern "C" {
+
 int lss_ipc_import(const unsigned char* handle, long offset, void** dev_ptr) {
   if (!handle || !dev_ptr) return fail(LSS_ERR_ARG, "ipc_import: null pointer");
-  cudaIpcMemHandle_t h;
-  memcpy(&h, handle, sizeof(h));
-  void* base = nullptr;
-  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
-  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-  *dev_ptr = static_cast<char*>(base) + offset;
+  std::lock_guard<std::mutex> lock(g_ipc_mu);
+  const std::string key(reinterpret_cast<const char*>(handle), sizeof(cudaIpcMemHandle_t));
+  auto it = g_ipc_maps.find(key);
+  if (it == g_ipc_maps.end()) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    it = g_ipc_maps.emplace(key, IpcMapping{base, 0}).first;
+  }
+  it->second.refs++;
+  *dev_ptr = static_cast<char*>(it->second.base) + offset;
   return LSS_OK;
 }
 
 int lss_ipc_close(void* dev_ptr, long offset) {
   if (!dev_ptr) return fail(LSS_ERR_ARG, "ipc_close: null pointer");
-  cudaError_t e = cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset);
-  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lock(g_ipc_mu);
+  void* base = static_cast<char*>(dev_ptr) - offset;
+  for (auto it = g_ipc_maps.begin(); it != g_ipc_maps.end(); ++it) {
+    if (it->second.base != base) continue;
+    if (--it->second.refs > 0) return LSS_OK;
+    g_ipc_maps.erase(it);
+    cudaError_t e = cudaIpcCloseMemHandle(base);
+    if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return LSS_OK;
+  }
+  return fail(LSS_ERR_ARG, "ipc_close: address was not imported");
+}
+
+// Stream memory operations (executed by the GPU front-end, no SM): cross-process
+// signals through IPC-mapped flag words.
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_streamValue32 stream_value_fn(const char* name) {
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fp, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<PFN_streamValue32>(fp);
+}
+
+int lss_stream_signal(unsigned int* flag, unsigned int value, void* stream) {
+  static PFN_streamValue32 fn = stream_value_fn("cuStreamWriteValue32");
+  if (!flag) return fail(LSS_ERR_ARG, "stream_signal: null flag");
+  if (!fn) return fail(LSS_ERR_UNSUPPORTED, "cuStreamWriteValue32 unavailable");
+  // default flags: a memory fence orders every prior write of the stream before the flag
+  CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value, 0);
+  if (r != CUDA_SUCCESS) return fail(LSS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  return LSS_OK;
+}
+
+int lss_stream_wait(const unsigned int* flag, unsigned int value, void* stream) {
+  static PFN_streamValue32 fn = stream_value_fn("cuStreamWaitValue32");
+  if (!flag) return fail(LSS_ERR_ARG, "stream_wait: null flag");
+  if (!fn) return fail(LSS_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
+  // (int32)(*flag - value) >= 0: wrap-safe monotonic sequence numbers
+  CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                  CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(LSS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
   return LSS_OK;
 }
 
@@ -682,6 +793,19 @@ int lss_attn_merge(const void* o_a, const float* lse_a, const void* o_b, const f
       reinterpret_cast<const __nv_bfloat16*>(o_a), lse_a, reinterpret_cast<const __nv_bfloat16*>(o_b), lse_b,
       reinterpret_cast<__nv_bfloat16*>(o_out), lse_out, batch, rows, heads, o_bstride, lse_pitch);
   return check_launch("attn_merge");
+}
+
+// Diagnostic: the GPU's global nanosecond timer, stream-ordered (cross-rank timelines).
+__global__ void timestamp_kernel(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
+int lss_timestamp(unsigned long long* dst, void* stream) {
+  if (!dst) return fail(LSS_ERR_ARG, "timestamp: null pointer");
+  timestamp_kernel<<<1, 1, 0, S(stream)>>>(dst);
+  return check_launch("timestamp");
 }
 
 int lss_add_f32(float* y, const float* x, long n, void* stream) {

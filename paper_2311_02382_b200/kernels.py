@@ -263,10 +263,14 @@ def _drop(dropout):
 
 
 def attn_fwd_partial(q, k, v, *, rows, row0, workers, seg_len, heads, offset, causal, g_begin, g_end, out,
-                     lse2, dropout=None):
+                     lse2, dropout=None, splits=1, scratch=None):
     """Partial attention of q rows [row0, row0+rows) (global position offset + row0 for
     the first) over key segments [g_begin, g_end) into out[:, row0:row0+rows] and
-    lse2[..., row0:row0+rows] (full-size [B,m,E] / [B,H,m_pad] buffers)."""
+    lse2[..., row0:row0+rows] (full-size [B,m,E] / [B,H,m_pad] buffers).
+
+    ``splits`` > 1 splits every CTA's key range inside the launch (lss_attn_fwd_split);
+    ``scratch`` = (o_part [S-1, B, m, E] bf16, lse_part [S-1, B, H, m_pad] fp32)
+    holds the partials of splits 1..S-1, shaped like out / lse2."""
     bsz, m, e = q.shape
     ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
     if _rows_view(v, "v", workers, bsz, seg_len, e) != ldk:
@@ -274,9 +278,16 @@ def attn_fwd_partial(q, k, v, *, rows, row0, workers, seg_len, heads, offset, ca
     qv = q[:, row0:row0 + rows]
     ov = out[:, row0:row0 + rows]
     lv = lse2[:, :, row0:]
-    call("lss_attn_fwd_ex", LSS_BF16, _ptr(qv), rows, m * e, _ptr(k), _ptr(v), ldk, _ptr(ov), m * e, _ptr(lv),
-         lse2.shape[-1], bsz, workers, seg_len, heads, e // heads, offset + row0, int(causal), g_begin, g_end,
-         _drop(dropout), _stream())
+    args = (LSS_BF16, _ptr(qv), rows, m * e, _ptr(k), _ptr(v), ldk, _ptr(ov), m * e, _ptr(lv), lse2.shape[-1], bsz,
+            workers, seg_len, heads, e // heads, offset + row0, int(causal), g_begin, g_end, _drop(dropout))
+    if splits <= 1:
+        call("lss_attn_fwd_ex", *args, _stream())
+        return
+    op, lp = scratch
+    if op.shape[0] < splits - 1 or op.shape[1:] != out.shape or lp.shape[1:] != lse2.shape:
+        raise ShapeError(f"attn_fwd_partial: scratch for {splits - 1} partials shaped like out / lse2 required")
+    call("lss_attn_fwd_split", *args, splits, _ptr(op[0][:, row0:]), op[0].numel(), _ptr(lp[0][:, :, row0:]),
+         lp[0].numel(), _stream())
 
 
 def attn_merge(o_a, lse_a, o_b, lse_b, *, row0, rows, heads, o_out=None, lse_out=None):
@@ -353,6 +364,23 @@ def dropout_rows(x, out, *, rows_per_sample, offset, site_key, thresh, scale, re
          residual.shape[-1] if residual is not None else 0, rows, cols, rows_per_sample, offset, site_key, thresh,
          scale, _stream())
     return out
+
+
+def stream_signal(flag_addr: int, value: int, stream=None) -> None:
+    """Stream-ordered write of value to the (possibly peer-mapped) flag word."""
+    s = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    call("lss_stream_signal", ctypes.c_void_p(int(flag_addr)), value & 0xFFFFFFFF, s)
+
+
+def stream_wait(flag_addr: int, value: int, stream=None) -> None:
+    """Block the stream until the flag word reaches value (wrap-safe >=)."""
+    s = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    call("lss_stream_wait", ctypes.c_void_p(int(flag_addr)), value & 0xFFFFFFFF, s)
+
+
+def timestamp(dst):
+    """Diagnostic: write the GPU global timer (ns) into the int64 scalar view dst."""
+    call("lss_timestamp", _ptr(dst), _stream())
 
 
 def sum_slots(dst, src):

@@ -121,6 +121,65 @@ def make_plan(rank: int, workers: int, block: int, causal: bool) -> BalancePlan:
     return BalancePlan()
 
 
+_FWD_SPLIT = os.environ.get("LSS_FWD_SPLIT", "1") != "0"
+_SPLIT_MAX = 8
+_TILE_OVH = 3.0  # per-CTA fixed cost (prologue, Q load, epilogue) in key-tile units
+_SPLIT_CACHE: dict = {}
+
+
+def fwd_cta_tiles(rows: int, pos0: int, g0: int, g1: int, seg_len: int, causal: bool) -> list:
+    """Visible key tiles of each query-tile-pair CTA of a partial forward launch, in
+    grid order (heaviest first for causal), as attn_fwd_tc_kernel counts them."""
+    tps = -(-seg_len // 128)
+    n_pairs = -(-rows // 256)
+    out = []
+    for unit in range(n_pairs):
+        pair = n_pairs - 1 - unit if causal else unit
+        if not causal:
+            out.append((g1 - g0) * tps)
+            continue
+        max_key = pos0 + min(pair * 256 + 256, rows) - 1
+        n = 0
+        for g in range(g0, g1):
+            seg0 = g * seg_len
+            if seg0 > max_key:
+                break
+            n = (g - g0) * tps + min(seg_len - 1, max_key - seg0) // 128 + 1
+        out.append(n)
+    return out
+
+
+def choose_fwd_splits(rows: int, pos0: int, g0: int, g1: int, seg_len: int, causal: bool, slices: int,
+                      sms: int, embed: int) -> int:
+    """Key-split count for one partial forward launch: the S minimising the simulated
+    makespan of the grid (CTAs dispatched in grid order to the first free SM, each
+    split a CTA of ceil(n/S) tiles + the fixed cost) plus the N-way merge."""
+    key = (rows, pos0, g0, g1, seg_len, causal, slices, sms, embed)
+    if key in _SPLIT_CACHE:
+        return _SPLIT_CACHE[key]
+    import heapq
+
+    tiles = fwd_cta_tiles(rows, pos0, g0, g1, seg_len, causal)
+    best, best_t = 1, None
+    for S in range(1, _SPLIT_MAX + 1):
+        if S > 1 and max(tiles) < 4 * S:
+            break
+        free = [0.0] * sms
+        for g0s in range(0, slices, 4):  # grid: groups of 4 slices (ATT_FWD_HGROUP), heavy pairs first
+            for n in tiles:
+                for _ in range(min(4, slices - g0s)):
+                    for s in range(S):
+                        c = (s + 1) * n // S - s * n // S + _TILE_OVH
+                        heapq.heappush(free, heapq.heappop(free) + c)
+        t = max(free)
+        if S > 1:  # merge: reads S partials + writes the result (~1.45 us per tile unit, ~6 TB/s)
+            t += 1.5 + rows * embed * 2 * (S + 1) / 6e12 / 1.45e-6
+        if best_t is None or t < best_t * 0.97:
+            best, best_t = S, t
+    _SPLIT_CACHE[key] = best
+    return best
+
+
 def block_pairs(rows: int, p0: int, lo: int, hi: int, causal: bool) -> int:
     """Unmasked pairs of query rows at positions p0..p0+rows-1 against keys [lo, hi):
     sum_i clamp(p0 + i + 1 - lo, 0, hi - lo) (causal) or rows * (hi - lo)."""
@@ -246,6 +305,9 @@ class LSSAttention:
         self.seg_dst = None
         self.peer_mem = False
         self.set_dropout(None, 0)
+        self._scratch = {}
+        self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count if self.device.type == "cuda" \
+            else 148
 
     # ------------------------------------------------------------ dropout
     def set_dropout(self, policy, layer: int) -> None:
@@ -264,6 +326,30 @@ class LSSAttention:
         return K.dropout_rows(x, out, rows_per_sample=self.m, offset=self.spec.offset,
                               site_key=pol.site_key(self.layer, tag), thresh=pol.thresh, scale=pol.scale,
                               residual=residual)
+
+    def _attn_part(self, q, *, rows, row0, offset, g_begin, g_end, out, lse2) -> None:
+        """One partial forward launch (rows [row0, row0+rows) of q at global position
+        offset + row0, key segments [g_begin, g_end)), key-split inside the launch
+        when few query tiles face a long key range (choose_fwd_splits)."""
+        kf, vf, common = self._fwd_common()
+        S = 1
+        if _FWD_SPLIT:
+            S = choose_fwd_splits(rows, offset + row0, g_begin, g_end, self.m, self.cfg.causal, self.B * self.H,
+                                  self._sms, self.E)
+        K.attn_fwd_partial(q, kf, vf, rows=rows, row0=row0, offset=offset, g_begin=g_begin, g_end=g_end, out=out,
+                           lse2=lse2, splits=S, scratch=self._split_scratch(S) if S > 1 else None, **common)
+
+    def _split_scratch(self, S: int):
+        """Partial (O, lse) slots of the key-split forward, one set per stream (the
+        split launches of two streams run concurrently)."""
+        key = torch.cuda.current_stream().cuda_stream
+        have = self._scratch.get(key)
+        if have is None or have[0].shape[0] < S - 1:
+            ad = self.cfg.act_dtype
+            have = (torch.empty(S - 1, self.B, self.m, self.E, dtype=ad, device=self.device),
+                    torch.empty(S - 1, self.B, self.H, self.mp, dtype=torch.float32, device=self.device))
+            self._scratch[key] = have
+        return have
 
     def _drop_tmp(self) -> torch.Tensor:
         """fp32 [B*m, E] scratch for the dropped sites (forward temp, masked gradients)."""
@@ -441,26 +527,23 @@ class LSSAttention:
         kf, vf = self.kv_full[..., :E], self.kv_full[..., E:]
         common = dict(workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal)
         if pl.role == "heavy":
-            K.attn_fwd_partial(self.q, kf, vf, rows=pl.split, row0=0, offset=self.spec.offset, g_begin=pl.a,
-                               g_end=r + 1, out=self.ctx, lse2=self.lse2, dropout=self._dd, **common)
-            K.attn_fwd_partial(self.q, kf, vf, rows=m - pl.split, row0=pl.split, offset=self.spec.offset,
-                               g_begin=pl.b, g_end=r + 1, out=self.ctx, lse2=self.lse2, dropout=self._dd,
-                               **common)
+            self._attn_part(self.q, rows=pl.split, row0=0, offset=self.spec.offset, g_begin=pl.a,
+                            g_end=r + 1, out=self.ctx, lse2=self.lse2)
+            self._attn_part(self.q, rows=m - pl.split, row0=pl.split, offset=self.spec.offset,
+                            g_begin=pl.b, g_end=r + 1, out=self.ctx, lse2=self.lse2)
             return
         if self._dd is not None:  # dropout lives in the partial (tcgen05) launch
-            K.attn_fwd_partial(self.q, kf, vf, rows=m, row0=0, offset=self.spec.offset, g_begin=0,
-                               g_end=r + 1 if self.cfg.causal else self.G, out=self.ctx, lse2=self.lse2,
-                               dropout=self._dd, **common)
+            self._attn_part(self.q, rows=m, row0=0, offset=self.spec.offset, g_begin=0,
+                            g_end=r + 1 if self.cfg.causal else self.G, out=self.ctx, lse2=self.lse2)
         else:
             K.attn_fwd(self.q, kf, vf, offset=self.spec.offset, out=self.ctx, lse2=self.lse2, **common)
         if pl.role == "light":
             off = pl.partner * m
-            K.attn_fwd_partial(self.q_peer, kf, vf, rows=pl.split, row0=0, offset=off, g_begin=0, g_end=pl.a,
-                               out=self.o_peer, lse2=self.lse_peer, dropout=self._dd, **common)
+            self._attn_part(self.q_peer, rows=pl.split, row0=0, offset=off, g_begin=0, g_end=pl.a,
+                            out=self.o_peer, lse2=self.lse_peer)
             if pl.b > 0:
-                K.attn_fwd_partial(self.q_peer, kf, vf, rows=m - pl.split, row0=pl.split, offset=off,
-                                   g_begin=0, g_end=pl.b, out=self.o_peer, lse2=self.lse_peer, dropout=self._dd,
-                                   **common)
+                self._attn_part(self.q_peer, rows=m - pl.split, row0=pl.split, offset=off,
+                                g_begin=0, g_end=pl.b, out=self.o_peer, lse2=self.lse_peer)
 
     def own_ranges(self):
         """(row0, rows, g_begin, g_end) blocks of this rank's own query rows."""
@@ -487,8 +570,8 @@ class LSSAttention:
             ranges = ranges[:1] if part == 0 else ranges[1:]
         for row0, rows, g0, g1 in ranges:
             if g0 <= r < g1:
-                K.attn_fwd_partial(self.q, kf, vf, rows=rows, row0=row0, offset=off, g_begin=r, g_end=r + 1,
-                                   out=self.ctx, lse2=self.lse2, **common)
+                self._attn_part(self.q, rows=rows, row0=row0, offset=off, g_begin=r, g_end=r + 1,
+                                out=self.ctx, lse2=self.lse2)
                 self._ctx_written.add(row0)
 
     def fwd_attend_remote(self, part: int | None = None) -> None:
@@ -505,12 +588,12 @@ class LSSAttention:
                 if lo >= hi:
                     continue
                 if row0 not in self._ctx_written:
-                    K.attn_fwd_partial(self.q, kf, vf, rows=rows, row0=row0, offset=off, g_begin=lo, g_end=hi,
-                                       out=self.ctx, lse2=self.lse2, **common)
+                    self._attn_part(self.q, rows=rows, row0=row0, offset=off, g_begin=lo, g_end=hi,
+                                    out=self.ctx, lse2=self.lse2)
                     self._ctx_written.add(row0)
                     continue
-                K.attn_fwd_partial(self.q, kf, vf, rows=rows, row0=row0, offset=off, g_begin=lo, g_end=hi,
-                                   out=self.o_tmp, lse2=self.lse_tmp, **common)
+                self._attn_part(self.q, rows=rows, row0=row0, offset=off, g_begin=lo, g_end=hi,
+                                out=self.o_tmp, lse2=self.lse_tmp)
                 K.attn_merge(self.ctx, self.lse2, self.o_tmp, self.lse_tmp, row0=row0, rows=rows, heads=self.H)
 
     def fwd_attend_delegated(self) -> None:
@@ -520,11 +603,11 @@ class LSSAttention:
             return
         kf, vf, common = self._fwd_common()
         m, off = self.m, pl.partner * self.m
-        K.attn_fwd_partial(self.q_peer, kf, vf, rows=pl.split, row0=0, offset=off, g_begin=0, g_end=pl.a,
-                           out=self.o_peer, lse2=self.lse_peer, **common)
+        self._attn_part(self.q_peer, rows=pl.split, row0=0, offset=off, g_begin=0, g_end=pl.a,
+                        out=self.o_peer, lse2=self.lse_peer)
         if pl.b > 0:
-            K.attn_fwd_partial(self.q_peer, kf, vf, rows=m - pl.split, row0=pl.split, offset=off, g_begin=0,
-                               g_end=pl.b, out=self.o_peer, lse2=self.lse_peer, **common)
+            self._attn_part(self.q_peer, rows=m - pl.split, row0=pl.split, offset=off, g_begin=0,
+                            g_end=pl.b, out=self.o_peer, lse2=self.lse_peer)
 
     def fwd_out(self) -> torch.Tensor:
         """(merge the partner's partials,) out-projection + residual."""
@@ -747,8 +830,56 @@ class LSSAttention:
 # ---------------------------------------------------------------- drivers
 
 
+_CE_P2P = os.environ.get("LSS_CE_P2P", "1") != "0"
+_CHANNEL = {"F1": 2, "F2": 3, "B1": 4, "B2": 5}  # flag-board channels of the hand-offs
+
+
+def _ce_targets(e, comm):
+    """The partner's receive buffers of every hand-off phase, mapped into this process
+    once (collective over the sequence group); False when the fabric cannot."""
+    if getattr(e, "_ce_map", None) is None:
+        e._ce_map = False
+        if hasattr(comm, "flags_ready") and comm.flags_ready():
+            named = {}
+            for ph in _CHANNEL:
+                for i, t in enumerate(e.xfer(ph)[1]):
+                    named[f"{ph}:{i}"] = t
+            addrs = comm.map_named(named)
+            if addrs is not None:
+                e._ce_map = addrs[e.plan.partner] if e.plan.active else {}
+    return e._ce_map
+
+
+def _exchange_ce(e, comm, phase, step, layer):
+    """Hand-off on the copy engines: the sender pushes its tensors into the partner's
+    receive buffers (peer memory) on a push stream and signals the partner's flag;
+    the receiver gets a handle whose wait() blocks its stream on that flag.  No SM
+    and no NCCL kernel is involved.  Every push is enqueued after the forward's
+    group barrier, which the partner has passed only after finishing the previous
+    step's reads of its receive buffers."""
+    sends, recvs = e.xfer(phase)
+    ch = _CHANNEL[phase]
+    if sends:
+        ps = comm.push_stream()
+        ps.wait_stream(torch.cuda.current_stream())
+        for i, t in enumerate(sends):
+            K.copy_d2d(e._ce_map[f"{phase}:{i}"], t.data_ptr(), t.numel() * t.element_size(), ps)
+        comm.notify(e.plan.partner, ch, ps)
+        comm.ledger.record("send", comm.seq_name + ":ce", sum(t.numel() for t in sends), step, phase, layer)
+    if recvs:
+        comm.ledger.record("recv", comm.seq_name + ":ce", sum(t.numel() for t in recvs), step, phase, layer)
+        return [comm.expect(e.plan.partner, ch)]
+    return []
+
+
 def _exchange(engines, comm, phase, step, layer, async_op=False):
     """Balanced-schedule point-to-point phase; returns the pending works (async_op)."""
+    if _CE_P2P and not isinstance(comm, SimComm) and len(engines) == 1 and _ce_targets(engines[0], comm):
+        works = _exchange_ce(engines[0], comm, phase, step, layer)
+        if not async_op:
+            _wait(works)
+            return []
+        return works
     if isinstance(comm, SimComm):
         for e in engines:
             sends, _ = e.xfer(phase)
@@ -811,22 +942,32 @@ def layer_grad_size(cfg: ModelConfig, with_ffn: bool) -> int:
 
 class PhaseClock:
     """Opt-in (LSS_PHASES=1) per-phase CUDA-event timeline of lss_step; the bench
-    prints it to explain where a multi-GPU step goes."""
+    prints it to explain where a multi-GPU step goes.  LSS_PHASES=2 also stamps
+    the GPU global timer at every mark (``last_stamps``), comparable across ranks."""
 
-    def __init__(self):
+    def __init__(self, stamps: bool = False):
         self.marks = []
+        self.stamps = torch.zeros(128, dtype=torch.int64, device="cuda") if stamps else None
 
     def mark(self, name):
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
+        if self.stamps is not None and len(self.marks) < self.stamps.numel():
+            K.timestamp(self.stamps[len(self.marks)])
         self.marks.append((name, ev))
 
     def report(self):
         torch.cuda.synchronize()
+        global last_stamps
+        if self.stamps is not None:
+            ns = self.stamps.cpu().tolist()
+            last_stamps = [(n, ns[i]) for i, (n, _) in enumerate(self.marks)]
         return {n: self.marks[i - 1][1].elapsed_time(ev) for i, (n, ev) in enumerate(self.marks) if i > 0}
 
 
-_PHASES = os.environ.get("LSS_PHASES") == "1"
+_PHASES = os.environ.get("LSS_PHASES") in ("1", "2")
+last_stamps: list = []
+last_clock = None
 _NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
 _CE_GATHER = os.environ.get("LSS_CE_GATHER", "1") != "0"  # K/V gather on the copy engines
 _WGRAD_SIDE = os.environ.get("LSS_WGRAD_SIDE", "1") != "0"  # weight-gradient GEMMs on a side stream
@@ -863,6 +1004,7 @@ def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
     if not sim and split and _CE_GATHER and hasattr(comm, "gather_pull") and comm.seq_size > 1:
         gather = comm.gather_pull(engines[0].kv_full, step, layer,  # copy engines, no SMs
                                   segments=engines[0].needed_segments())
+        mark("gather_barrier")
     if gather is None:
         gather = one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer,
                                                     **({} if sim else {"async_op": split})))
@@ -944,7 +1086,11 @@ def lss_backward(engines, comm, grad_ys, *, step=0, layer=0, sync=True, mark=_no
     if fused:  # the reduce-scatter already happened inside the backward kernels
         comm.ledger.record("reduce-scatter", "sequence:nvlink", engines[0].dkv_full.numel(), step, "backward",
                            layer)
-        comm.device_barrier(step, "backward", layer)
+        if not sim and comm.flags_ready() and comm.use_flags:
+            comm.flag_barrier(1, step, "backward", layer)
+        else:
+            comm.device_barrier(step, "backward", layer)
+        mark("rs_barrier")
         for e in engines:
             e.gather_slots()
     else:
@@ -975,7 +1121,7 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
     global last_phases
     for e in engines:
         e.set_dropout(policy, layer)
-    clk = PhaseClock() if _PHASES else None
+    clk = PhaseClock(os.environ.get("LSS_PHASES") == "2") if _PHASES else None
     mark = clk.mark if clk else _no_mark
     _bind_fused(engines, comm)
     mark("start")
@@ -984,7 +1130,11 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
         before_bwd()
     dxs = lss_backward(engines, comm, grad_ys, step=step, layer=layer, sync=sync, mark=mark)
     if clk:
-        last_phases = clk.report()
+        if clk.stamps is not None:  # LSS_PHASES=2: the caller reports (steady-state steps, no sync here)
+            global last_clock
+            last_clock = clk
+        else:
+            last_phases = clk.report()
     return list(zip(ys, dxs))
 
 

@@ -162,6 +162,50 @@ def test_attention_fwd_bwd_vs_oracle(cuda, rng, case, prec):
     assert nerr(dv, dv_ref) < btol
 
 
+SPLIT_CASES = [
+    # (batch, rows m, workers G, heads, rank, row0, rows, g_begin, g_end, splits)
+    (1, 700, 4, 2, 3, 0, 700, 0, 3, 3),    # dense remote segments (the N>=4 case)
+    (1, 700, 4, 2, 3, 0, 700, 1, 4, 5),    # ends in the diagonal segment
+    (2, 300, 3, 2, 2, 128, 172, 0, 3, 4),  # row window, batch 2, ragged tiles
+    (1, 520, 2, 1, 0, 0, 520, 0, 1, 6),    # causal diagonal: short CTAs, empty splits
+]
+
+
+@pytest.mark.parametrize("case", SPLIT_CASES)
+@pytest.mark.parametrize("drop", [False, True])
+def test_attention_fwd_key_split(cuda, rng, case, drop):
+    """lss_attn_fwd_split (key range split inside one launch + N-way lse merge) ==
+    the unsplit partial launch, and == the oracle over the same key range."""
+    import torch
+    from paper_2311_02382_b200 import kernels as K
+    from paper_2311_02382_b200.dropout import DropoutPolicy
+
+    bsz, m, G, H, rank, row0, rows, g0, g1, S = case
+    E = 64 * H
+    tq, tkv, qn, kn, vn = _attn_inputs(rng, bsz, m, G, H, rank, cuda, torch.bfloat16)
+    mp = K.rows_pad(m)
+    dd = DropoutPolicy(0.2, seed=5).desc(0) if drop else None
+    outs = []
+    for splits in (1, S):
+        o = torch.zeros(bsz, m, E, dtype=torch.bfloat16, device=cuda)
+        lse = torch.zeros(bsz, H, mp, device=cuda)
+        scratch = (torch.full((S - 1, bsz, m, E), float("nan"), dtype=torch.bfloat16, device=cuda),
+                   torch.full((S - 1, bsz, H, mp), float("nan"), device=cuda))
+        K.attn_fwd_partial(tq, tkv[..., :E], tkv[..., E:], rows=rows, row0=row0, workers=G, seg_len=m, heads=H,
+                           offset=rank * m, causal=True, g_begin=g0, g_end=g1, out=o, lse2=lse, dropout=dd,
+                           splits=splits, scratch=scratch)
+        torch.cuda.synchronize()
+        outs.append((_np(o)[:, row0:row0 + rows], _np(lse)[:, :, row0:row0 + rows]))
+    (o1, l1), (os_, ls) = outs
+    assert np.isfinite(os_).all()
+    assert nerr(os_, o1) < BF16_TOL
+    assert np.abs(ls - l1).max() < 1e-3
+    if not drop:  # oracle over keys [g0*m, g1*m): causal offset relative to the first key
+        ctx_ref, _ = O.scores_fwd(qn[:, row0:row0 + rows], kn[:, g0 * m:g1 * m], vn[:, g0 * m:g1 * m],
+                                  rank * m + row0 - g0 * m, H, True)
+        assert nerr(os_, ctx_ref) < BF16_TOL
+
+
 def test_attention_peaked_softmax_bf16(cuda, rng):
     """Stress variant of SURVEY.md §8(d): scores scaled up so the online max moves a lot."""
     import torch

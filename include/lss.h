@@ -149,7 +149,14 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
                     int workers, int seg_len, int heads, int head_dim, long offset, int causal,
                     int g_begin, int g_end, const lss_dropout* dropout, void* stream);
 
-/* lss_attn_fwd_ex with the key range split `splits` ways (1..16) inside ONE
+/* Fused all-gather: with seg_ready != NULL, key segment g != own_seg is read only
+ * after seg_ready[g] reaches ready_seq (wrap-safe >=) -- the gatherer signals each
+ * segment as its copy lands (lss_stream_signal) and the kernel's TMA producer
+ * waits per segment, so the transfer overlaps the math tile by tile.  Segments
+ * are visited from the highest visible one down (diagonal first, then the
+ * nearest remote ones).
+ *
+ * lss_attn_fwd_ex with the key range split `splits` ways (1..16) inside ONE
  * launch: split s attends key tiles [s*n/S, (s+1)*n/S) of each CTA's n visible
  * tiles; split 0 writes (o, lse2), split s > 0 the caller's scratch slot s-1 at
  * o_part + (s-1)*o_part_stride / lse_part + (s-1)*lse_part_stride (same batch
@@ -162,7 +169,8 @@ int lss_attn_fwd_split(int dtype, const void* q, int rows, long q_bstride, const
                        long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch,
                        int workers, int seg_len, int heads, int head_dim, long offset, int causal,
                        int g_begin, int g_end, const lss_dropout* dropout, int splits, void* o_part,
-                       long o_part_stride, float* lse_part, long lse_part_stride, void* stream);
+                       long o_part_stride, float* lse_part, long lse_part_stride,
+                       const unsigned int* seg_ready, unsigned int ready_seq, int own_seg, void* stream);
 
 /* log-sum-exp combine of two partial attentions over disjoint key ranges:
  * lse = log2(2^la + 2^lb), ctx = 2^(la-lse) ctx_a + 2^(lb-lse) ctx_b (bf16, head_dim 64).

@@ -83,7 +83,7 @@ SIGNATURES = {
     "lss_attn_fwd_ex": [_I, _P, _I, _L, _P, _P, _L, _P, _L, _P, _I, _I, _I, _I, _I, _I, _L, _I, _I, _I,
                         ctypes.POINTER(DropoutDesc), _P],
     "lss_attn_fwd_split": [_I, _P, _I, _L, _P, _P, _L, _P, _L, _P, _I, _I, _I, _I, _I, _I, _L, _I, _I, _I,
-                           ctypes.POINTER(DropoutDesc), _I, _P, _L, _P, _L, _P],
+                           ctypes.POINTER(DropoutDesc), _I, _P, _L, _P, _L, _P, ctypes.c_uint, _I, _P],
     "lss_attn_merge": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _L, _I, _P],
     "lss_attn_delta": [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P],
     "lss_attn_bwd_ex": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, _P, _P, _L, _I, _I, _I, _I, _I, _I,

@@ -221,14 +221,19 @@ class TorchDistComm:
             self._push_stream = torch.cuda.Stream(device=torch.cuda.current_device())
         return self._push_stream
 
-    def gather_pull(self, full: torch.Tensor, step=0, layer=0, segments=None):
+    def gather_pull(self, full: torch.Tensor, step=0, layer=0, segments=None, ready=None):
         """K/V all-gather on the copy engines: after a device barrier (every rank's
         slot is written), pull each peer's own slot full[p] from its IPC-mapped
         buffer on a copy stream -- no SMs taken from the overlapped attention.
         ``segments``: the peers' slots this rank's attention actually reads (the
         causal schedule never touches the others); default all.  Returns an
         event the consumer waits on, or None when peers do not map (the caller
-        then falls back to the NCCL all-gather)."""
+        then falls back to the NCCL all-gather).
+
+        ``ready`` = (flags int32 [G], seq): fused gather -- after each segment's copy
+        the copy stream signals flags[p] = seq, and the attention kernels wait per
+        segment (in their TMA producer) instead of the consumer waiting on the event.
+        Segments are pulled nearest-first (the order the kernels visit them)."""
         addrs = self.peer_addresses(full)
         if addrs is None:
             return None
@@ -248,9 +253,13 @@ class TorchDistComm:
             self.device_barrier(step, "forward", layer)
         cs.wait_stream(cur)
         slot = full[0].numel() * full.element_size()
-        for p in (range(self.seq_size) if segments is None else segments):
-            if p != self.seq_rank:
-                K.copy_d2d(full[p].data_ptr(), addrs[p] + p * slot, slot, cs)
+        me = self.seq_rank
+        order = sorted((p for p in (range(self.seq_size) if segments is None else segments) if p != me),
+                       key=lambda p: (p > me, abs(p - me)))
+        for p in order:
+            K.copy_d2d(full[p].data_ptr(), addrs[p] + p * slot, slot, cs)
+            if ready is not None:
+                K.stream_signal(ready[0].data_ptr() + 4 * p, ready[1], cs)
         ev = torch.cuda.Event()
         ev.record(cs)
         return ev

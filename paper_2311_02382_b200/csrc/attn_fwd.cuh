@@ -88,6 +88,11 @@ struct AttnFwdParams {
   long o_part_stride;
   float* lse_part;
   long lse_part_stride;
+  // fused all-gather: key segment g != own_seg is read only after seg_ready[g] reaches
+  // ready_seq (the copy stream signals each segment as it lands); null = all resident
+  const uint32_t* seg_ready;
+  uint32_t ready_seq;
+  int own_seg;
 };
 
 template <bool DROP>
@@ -133,20 +138,33 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   const bool has1 = q0 + ATT_BM < p.m;
   const int q_last = min(q0 + 2 * ATT_BM, p.m) - 1;  // last valid local row in this CTA
   const int tps = (p.seg_len + ATT_BN - 1) / ATT_BN;  // key tiles per segment
-  int n_kv = (p.g_end - p.g_begin) * tps;
+  // Key tiles are visited from the highest visible segment down (the diagonal, then
+  // the nearest remote segments: the order the fused gather delivers them); the top
+  // segment g_top may be partly visible (n_top tiles), the ones below are full.
+  int g_top = p.g_end - 1, n_top = tps;
   if (p.causal) {
     const long max_key = p.offset + q_last;  // keys > max_key are masked for every row
-    int n = 0;
+    g_top = p.g_begin - 1;
+    n_top = 0;
     for (int g = p.g_begin; g < p.g_end; ++g) {
       const long seg0 = (long)g * p.seg_len;
       if (seg0 > max_key) break;
-      const long last_in_seg = min((long)p.seg_len - 1, max_key - seg0);
-      n = (g - p.g_begin) * tps + (int)(last_in_seg / ATT_BN) + 1;
+      g_top = g;
+      n_top = (int)(min((long)p.seg_len - 1, max_key - seg0) / ATT_BN) + 1;
     }
-    n_kv = n;
   }
+  int n_kv = g_top < p.g_begin ? 0 : (g_top - p.g_begin) * tps + n_top;
   const int j_base = (int)(((long)split * n_kv) / p.splits);  // this split's key tiles
   n_kv = (int)(((long)(split + 1) * n_kv) / p.splits) - j_base;
+  auto tile_of = [&](int jt, int& g, int& t) {  // visit index -> (segment, tile in segment)
+    if (jt < n_top) {
+      g = g_top;
+      t = jt;
+    } else {
+      g = g_top - 1 - (jt - n_top) / tps;
+      t = (jt - n_top) % tps;
+    }
+  };
   __nv_bfloat16* const o_dst = split == 0 ? p.o : p.o_part + (long)(split - 1) * p.o_part_stride;
   float* const lse_dst = split == 0 ? p.lse2 : p.lse_part + (long)(split - 1) * p.lse_part_stride;
 
@@ -187,12 +205,19 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         if (has1) tma_load_3d(&tmQ, q_full, sQ + ATT_TILE_BYTES, h * ATT_D, q0 + ATT_BM, b);
       }
       __syncwarp();
+      int g_ready = p.own_seg;  // segments known to be resident
       for (int j = 0; j < n_kv; ++j) {
         const int st = j % ATT_KV_STAGES;
         const uint32_t ph = (j / ATT_KV_STAGES) & 1;
+        int g, t;
+        tile_of(j_base + j, g, t);
+        if (p.seg_ready != nullptr && g != g_ready && g != p.own_seg) {  // fused gather: wait for it
+          if (lane == 0) wait_flag_geq(p.seg_ready + g, p.ready_seq);
+          __syncwarp();
+          g_ready = g;
+        }
         mbar_wait(&kv_empty[st], ph ^ 1);
         if (elect_one()) {
-          const int g = p.g_begin + (j_base + j) / tps, t = (j_base + j) % tps;
           mbar_arrive_expect_tx(&kv_full[st], 2 * ATT_TILE_BYTES);
           tma_load_4d(&tmK, &kv_full[st], sK + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
           tma_load_4d(&tmV, &kv_full[st], sV + st * ATT_TILE_BYTES, h * ATT_D, t * ATT_BN, b, g);
@@ -265,7 +290,8 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       float m_run = -INFINITY, l_run = 0.f;
       const int tile_first_row = q0 + w * ATT_BM;  // for the mask decision (warp-uniform)
       for (int j = 0; j < n_kv; ++j) {
-        const int g = p.g_begin + (j_base + j) / tps, t = (j_base + j) % tps;
+        int g, t;
+        tile_of(j_base + j, g, t);
         const int valid_cols = min(ATT_BN, p.seg_len - t * ATT_BN);
         const long key0 = (long)g * p.seg_len + (long)t * ATT_BN;
         const bool need_mask = valid_cols < ATT_BN ||

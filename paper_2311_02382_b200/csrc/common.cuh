@@ -82,6 +82,20 @@ LSS_DEV float4 ld_shared_f4(uint32_t addr) {
 LSS_DEV void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+LSS_DEV void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+LSS_DEV uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until the stream-signalled word reaches seq (wrap-safe), then order later
+// async-proxy (TMA) reads after it.
+LSS_DEV void wait_flag_geq(const uint32_t* p, uint32_t seq) {
+  while ((int)(ld_acquire_gpu(p) - seq) < 0) __nanosleep(128);
+  fence_proxy_async_global();
+}
 LSS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 LSS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 LSS_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {

@@ -296,7 +296,8 @@ static int attn_fwd_launch(int dtype, const void* q, int rows, long q_bstride, c
                            long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers,
                            int seg_len, int heads, int head_dim, long offset, int causal, int g_begin, int g_end,
                            const lss_dropout* dropout, int splits, void* o_part, long o_part_stride,
-                           float* lse_part, long lse_part_stride, void* stream) {
+                           float* lse_part, long lse_part_stride, const unsigned int* seg_ready,
+                           unsigned int ready_seq, int own_seg, void* stream) {
   int rc = attn_check(dtype, batch, rows, workers, seg_len, heads, head_dim);
   if (rc) return rc;
   if (!q || !k || !v || !o || !lse2) return fail(LSS_ERR_ARG, "attn_fwd: null pointer");
@@ -352,6 +353,9 @@ static int attn_fwd_launch(int dtype, const void* q, int rows, long q_bstride, c
   p.o_part_stride = o_part_stride;
   p.lse_part = lse_part;
   p.lse_part_stride = lse_part_stride;
+  p.seg_ready = seg_ready;
+  p.ready_seq = ready_seq;
+  p.own_seg = own_seg;
   dim3 grid((unsigned)((rows + 2 * ATT_BM - 1) / (2 * ATT_BM)) * heads * batch * splits);
   if (drop) {
     if ((rc = set_smem(attn_fwd_tc_kernel<true>, ATT_FWD_SMEM))) return rc;
@@ -379,14 +383,15 @@ int lss_attn_fwd_ex(int dtype, const void* q, int rows, long q_bstride, const vo
                     const lss_dropout* dropout, void* stream) {
   return attn_fwd_launch(dtype, q, rows, q_bstride, k, v, ld_kv, o, o_bstride, lse2, lse_pitch, batch, workers,
                          seg_len, heads, head_dim, offset, causal, g_begin, g_end, dropout, 1, nullptr, 0, nullptr,
-                         0, stream);
+                         0, nullptr, 0, -1, stream);
 }
 
 int lss_attn_fwd_split(int dtype, const void* q, int rows, long q_bstride, const void* k, const void* v,
                        long ld_kv, void* o, long o_bstride, float* lse2, int lse_pitch, int batch, int workers,
                        int seg_len, int heads, int head_dim, long offset, int causal, int g_begin, int g_end,
                        const lss_dropout* dropout, int splits, void* o_part, long o_part_stride, float* lse_part,
-                       long lse_part_stride, void* stream) {
+                       long lse_part_stride, const unsigned int* seg_ready, unsigned int ready_seq, int own_seg,
+                       void* stream) {
   if (splits < 1 || splits > ATT_MERGE_MAX + 1)
     return fail(LSS_ERR_ARG, "attn_fwd_split: %d splits (1..%d)", splits, ATT_MERGE_MAX + 1);
   if (splits > 1) {
@@ -398,7 +403,7 @@ int lss_attn_fwd_split(int dtype, const void* q, int rows, long q_bstride, const
   }
   return attn_fwd_launch(dtype, q, rows, q_bstride, k, v, ld_kv, o, o_bstride, lse2, lse_pitch, batch, workers,
                          seg_len, heads, head_dim, offset, causal, g_begin, g_end, dropout, splits, o_part,
-                         o_part_stride, lse_part, lse_part_stride, stream);
+                         o_part_stride, lse_part, lse_part_stride, seg_ready, ready_seq, own_seg, stream);
 }
 
 int lss_attn_fwd(int dtype, const void* q, const void* k, const void* v, long ld_kv, void* o, float* lse2,

@@ -263,14 +263,16 @@ def _drop(dropout):
 
 
 def attn_fwd_partial(q, k, v, *, rows, row0, workers, seg_len, heads, offset, causal, g_begin, g_end, out,
-                     lse2, dropout=None, splits=1, scratch=None):
+                     lse2, dropout=None, splits=1, scratch=None, ready=None):
     """Partial attention of q rows [row0, row0+rows) (global position offset + row0 for
     the first) over key segments [g_begin, g_end) into out[:, row0:row0+rows] and
     lse2[..., row0:row0+rows] (full-size [B,m,E] / [B,H,m_pad] buffers).
 
     ``splits`` > 1 splits every CTA's key range inside the launch (lss_attn_fwd_split);
     ``scratch`` = (o_part [S-1, B, m, E] bf16, lse_part [S-1, B, H, m_pad] fp32)
-    holds the partials of splits 1..S-1, shaped like out / lse2."""
+    holds the partials of splits 1..S-1, shaped like out / lse2.  ``ready`` =
+    (flags int32 [G] tensor, seq, own segment): fused gather, segment g read after
+    flags[g] >= seq (see comm.TorchDistComm.gather_pull)."""
     bsz, m, e = q.shape
     ldk = _rows_view(k, "k", workers, bsz, seg_len, e)
     if _rows_view(v, "v", workers, bsz, seg_len, e) != ldk:
@@ -280,14 +282,21 @@ def attn_fwd_partial(q, k, v, *, rows, row0, workers, seg_len, heads, offset, ca
     lv = lse2[:, :, row0:]
     args = (LSS_BF16, _ptr(qv), rows, m * e, _ptr(k), _ptr(v), ldk, _ptr(ov), m * e, _ptr(lv), lse2.shape[-1], bsz,
             workers, seg_len, heads, e // heads, offset + row0, int(causal), g_begin, g_end, _drop(dropout))
-    if splits <= 1:
+    if splits <= 1 and ready is None:
         call("lss_attn_fwd_ex", *args, _stream())
         return
-    op, lp = scratch
-    if op.shape[0] < splits - 1 or op.shape[1:] != out.shape or lp.shape[1:] != lse2.shape:
-        raise ShapeError(f"attn_fwd_partial: scratch for {splits - 1} partials shaped like out / lse2 required")
-    call("lss_attn_fwd_split", *args, splits, _ptr(op[0][:, row0:]), op[0].numel(), _ptr(lp[0][:, :, row0:]),
-         lp[0].numel(), _stream())
+    rflags, rseq, own = ready if ready is not None else (None, 0, -1)
+    if splits > 1:
+        op, lp = scratch
+        if op.shape[0] < splits - 1 or op.shape[1:] != out.shape or lp.shape[1:] != lse2.shape:
+            raise ShapeError(f"attn_fwd_partial: scratch for {splits - 1} partials shaped like out / lse2 required")
+        parts = (_ptr(op[0][:, row0:]), op[0].numel(), _ptr(lp[0][:, :, row0:]), lp[0].numel())
+    else:
+        parts = (None, 0, None, 0)
+    if rflags is not None and (rflags.dtype != torch.int32 or rflags.numel() < workers):
+        raise ShapeError("attn_fwd_partial: ready flags must be int32 [workers]")
+    call("lss_attn_fwd_split", *args, splits, *parts, _ptr(rflags) if rflags is not None else None,
+         rseq & 0xFFFFFFFF, own, _stream())
 
 
 def attn_merge(o_a, lse_a, o_b, lse_b, *, row0, rows, heads, o_out=None, lse_out=None):

@@ -306,6 +306,10 @@ class LSSAttention:
         self.peer_mem = False
         self.set_dropout(None, 0)
         self._scratch = {}
+        # fused gather: per-segment arrival flags signalled by the copy stream (int32 [G])
+        self._ready = torch.zeros(G, dtype=torch.int32, device=self.device) if G > 1 else None
+        self._ready_seq = 0
+        self._ready_tok = None  # (flags, seq, own segment) while a fused-gather forward is in flight
         self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count if self.device.type == "cuda" \
             else 148
 
@@ -337,7 +341,8 @@ class LSSAttention:
             S = choose_fwd_splits(rows, offset + row0, g_begin, g_end, self.m, self.cfg.causal, self.B * self.H,
                                   self._sms, self.E)
         K.attn_fwd_partial(q, kf, vf, rows=rows, row0=row0, offset=offset, g_begin=g_begin, g_end=g_end, out=out,
-                           lse2=lse2, splits=S, scratch=self._split_scratch(S) if S > 1 else None, **common)
+                           lse2=lse2, splits=S, scratch=self._split_scratch(S) if S > 1 else None,
+                           ready=self._ready_tok, **common)
 
     def _split_scratch(self, S: int):
         """Partial (O, lse) slots of the key-split forward, one set per stream (the
@@ -556,6 +561,16 @@ class LSSAttention:
         E = self.E
         return (self.kv_full[..., :E], self.kv_full[..., E:],
                 dict(workers=self.G, seg_len=self.m, heads=self.H, causal=self.cfg.causal, dropout=self._dd))
+
+    def fwd_attend_own(self, part: int) -> None:
+        """Own rows over every key segment they see, in ONE launch per row range
+        (part 0: the first range, 1: the heavy rank's second); with the fused gather
+        the kernel waits per remote segment, so no local/remote split or merge."""
+        ranges = self.own_ranges()
+        ranges = ranges[:1] if part == 0 else ranges[1:]
+        for row0, rows, g0, g1 in ranges:
+            self._attn_part(self.q, rows=rows, row0=row0, offset=self.spec.offset, g_begin=g0, g_end=g1,
+                            out=self.ctx, lse2=self.lse2)
 
     def fwd_attend_local(self, part: int | None = None) -> None:
         """Own rows x own key segment: needs no remote K/V, so it runs while the
@@ -971,6 +986,7 @@ last_clock = None
 _NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
 _CE_GATHER = os.environ.get("LSS_CE_GATHER", "1") != "0"  # K/V gather on the copy engines
 _WGRAD_SIDE = os.environ.get("LSS_WGRAD_SIDE", "1") != "0"  # weight-gradient GEMMs on a side stream
+_FUSED_GATHER = os.environ.get("LSS_FUSED_GATHER", "1") != "0"  # attention waits per gathered segment
 last_phases: dict = {}
 
 
@@ -1001,10 +1017,47 @@ def lss_forward(engines, comm, xs, *, step=0, layer=0, mark=_no_mark):
         e.fwd_project(x)
     mark("fwd_project")
     gather = None
+    fused = False
     if not sim and split and _CE_GATHER and hasattr(comm, "gather_pull") and comm.seq_size > 1:
-        gather = comm.gather_pull(engines[0].kv_full, step, layer,  # copy engines, no SMs
-                                  segments=engines[0].needed_segments())
+        e0 = engines[0]
+        ready = None
+        if _FUSED_GATHER and not _NO_OVERLAP and comm.flags_ready():
+            e0._ready_seq += 1
+            ready = (e0._ready, e0._ready_seq)
+        gather = comm.gather_pull(e0.kv_full, step, layer,  # copy engines, no SMs
+                                  segments=e0.needed_segments(), ready=ready)
         mark("gather_barrier")
+        if gather is not None and ready is not None:
+            fused = True
+            e0._ready_tok = (e0._ready, e0._ready_seq, e0.spec.rank)
+    if fused:
+        # all-gather fused into the attention: every launch starts at once and its
+        # producer warp waits per remote segment; own rows in one launch per range
+        # (main stream / side stream), the light rank's delegated rows on the side
+        # stream after the Q hand-off, their partials pushed back right after
+        e0 = engines[0]
+        f1 = _exchange(engines, comm, "F1", step, layer, async_op=True)
+        main = torch.cuda.current_stream()
+        side = _side_stream(e0.device)
+        side.wait_stream(main)
+        e0.fwd_attend_own(part=0)
+        with torch.cuda.stream(side):
+            _wait(f1)
+            e0.fwd_attend_delegated()
+            e0.fwd_attend_own(part=1)
+            f2 = _exchange(engines, comm, "F2", step, layer, async_op=True)
+        main.wait_stream(side)
+        mark("fwd_attend")
+        _wait(f2)
+        _wait([gather])  # every segment resident before the backward reads them
+        e0._ready_tok = None
+        mark("p2p_F2")
+        ys = [e.fwd_out() for e in engines]
+        mark("fwd_out")
+        if all(e.with_ffn for e in engines):
+            ys = [e.ffn_forward(y) for e, y in zip(engines, ys)]
+            mark("ffn_fwd")
+        return ys
     if gather is None:
         gather = one(lambda t: comm.all_gather_rows([e.kv_full for e in t] if sim else t.kv_full, step, layer,
                                                     **({} if sim else {"async_op": split})))

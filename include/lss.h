@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 5
+#define LSS_ABI_VERSION 6
 
 enum lss_status {
   LSS_OK = 0,
@@ -210,6 +210,11 @@ typedef struct lss_bwd_source {
   const float* lse2;
   const float* delta;
   int pitch;
+  /* optional (NULL = resident): the source's q / grad_o / lse2 / delta are read only
+   * after (int32)(*ready - ready_seq) >= 0 -- a partner pushes them and signals
+   * (lss_stream_signal), and the kernel processes the sources before it meanwhile */
+  const unsigned int* ready;
+  unsigned int ready_seq;
 } lss_bwd_source;
 
 /* Backward over up to 3 sources in ONE launch: every key tile accumulates dK/dV

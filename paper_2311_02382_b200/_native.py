@@ -66,6 +66,7 @@ class BwdSource(ctypes.Structure):
     _fields_ = [
         ("q", _P), ("grad_o", _P), ("grad_q", _P), ("m_src", _I), ("row0", _I), ("rows", _I),
         ("pos0", _L), ("g_begin", _I), ("g_end", _I), ("lse2", _P), ("delta", _P), ("pitch", _I),
+        ("ready", _P), ("ready_seq", ctypes.c_uint),
     ]
 
 
@@ -113,7 +114,7 @@ EXTRA = {
     "lss_rows_pad": ([_L], _L),
     "lss_peer_access": ([_I, _I], _I),
 }
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _lib = None
 

@@ -63,6 +63,8 @@ struct BwdSource {
   int pitch;
   int m_src;           // rows of the [B][m_src][E] tensors
   float* dq;           // fp32 [B][m_src][E], accumulated with vector reductions
+  const uint32_t* ready;  // non-null: inputs pushed by a partner, usable once *ready >= ready_seq
+  uint32_t ready_seq;
 };
 struct BwdMaps {
   CUtensorMap q[ATB_MAX_SRC];
@@ -314,12 +316,18 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           tma_load_4d(&tmV, kv_full, sV, h * ATT_D, kv_row0, b, g);
         }
         __syncwarp();
+        int src_ready = -1;  // last source whose pushed inputs were waited for
         for (int it = 0; it < n_iter; ++it) {
           const int s = it & 1;
           mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
           if (lane == 0) BWD_TRACE(18, it);
           int src, q0;
           locate(it, src, q0);
+          if (p.src[src].ready != nullptr && src != src_ready) {  // fused hand-off: wait for the push
+            if (lane == 0) wait_flag_geq(p.src[src].ready, p.src[src].ready_seq);
+            __syncwarp();
+            src_ready = src;
+          }
           uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
           const long lo = ((long)b * p.H + h) * p.src[src].pitch + q0;
           if (elect_one()) {

@@ -498,6 +498,8 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
     p.src[i].pitch = sr.pitch;
     p.src[i].m_src = sr.m_src;
     p.src[i].dq = sr.grad_q;
+    p.src[i].ready = sr.ready;
+    p.src[i].ready_seq = sr.ready_seq;
   }
   CUtensorMap mk, mv;
   if ((rc = map_rows(&mk, k, E, ld_kv, seg_len, batch, workers, 4))) return rc;
@@ -784,6 +786,7 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
   lss_bwd_source src;
   src.q = q; src.grad_o = grad_o; src.grad_q = grad_q; src.m_src = rows; src.row0 = 0; src.rows = rows;
   src.pos0 = offset; src.g_begin = 0; src.g_end = workers; src.lse2 = lse2; src.delta = delta_ws; src.pitch = m_pad;
+  src.ready = nullptr; src.ready_seq = 0;
   return lss_attn_bwd_ex(dtype, k, v, ld_kv, &src, 1, grad_k, grad_v, ld_dkv, batch, workers, seg_len, heads,
                          head_dim, causal, nullptr, stream);
 }

@@ -332,6 +332,10 @@ def _bwd_source_array(sources):
         arr[i].lse2 = src["lse2"].data_ptr()
         arr[i].delta = src["delta"].data_ptr()
         arr[i].pitch = src["lse2"].shape[-1]
+        ready = src.get("ready")  # (flag address, seq): inputs pushed by a partner
+        if ready is not None:
+            arr[i].ready = int(ready[0])
+            arr[i].ready_seq = ready[1] & 0xFFFFFFFF
     return arr
 
 

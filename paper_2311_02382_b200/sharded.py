@@ -123,7 +123,11 @@ def make_plan(rank: int, workers: int, block: int, causal: bool) -> BalancePlan:
 
 _FWD_SPLIT = os.environ.get("LSS_FWD_SPLIT", "1") != "0"
 _SPLIT_MAX = 8
-_TILE_OVH = 3.0  # per-CTA fixed cost (prologue, Q load, epilogue) in key-tile units
+# per-CTA fixed cost (launch, prologue, pipeline fill / drain, epilogue) in key-tile
+# units (~1.45 us each): fitted to per-launch timings of the G=4 / G=8 partial
+# launches (scratch/launch_sim.py; the model then picks the measured-best S for
+# 11 of 12 launches, 3 us lost in total)
+_TILE_OVH = 8.0
 _SPLIT_CACHE: dict = {}
 
 
@@ -726,8 +730,10 @@ class LSSAttention:
             K.gemm(self.ctx.view(B * m, E), self.gy.view(B * m, E), a_mn_major=True, b_mn_major=True,
                    alpha=self.grad_scale, out=self.g_wo, M=E, N=E, K=B * m)
 
-    def bwd_attend(self) -> None:
-        """Attention backward: dQ for the rows this rank computes, partial dK|dV for all."""
+    def bwd_attend(self, peer_ready=None) -> None:
+        """Attention backward: dQ for the rows this rank computes, partial dK|dV for all.
+        ``peer_ready`` = (flag address, seq): the partner's dO / lse / delta are still
+        being pushed; the kernel runs the own rows first and waits for them in-kernel."""
         m, E, pl, r = self.m, self.E, self.plan, self.spec.rank
         kf, vf = self.kv_full[..., :E], self.kv_full[..., E:]
         if self.seg_dst is not None:  # fused reduce-scatter: dK|dV straight to the owners
@@ -748,7 +754,7 @@ class LSSAttention:
         elif pl.role == "light":
             self.dq_peer.zero_()
             peer = dict(q=self.q_peer, grad_o=self.do_peer, grad_q=self.dq_peer, pos0=pl.partner * m,
-                        lse2=self.lsef_peer, delta=self.delta_peer)
+                        lse2=self.lsef_peer, delta=self.delta_peer, ready=peer_ready)
             srcs = [dict(own, row0=0, rows=m, g_begin=0, g_end=r + 1),
                     dict(peer, row0=0, rows=pl.split, g_begin=0, g_end=pl.a)]
             if pl.b > 0:
@@ -987,6 +993,7 @@ _NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
 _CE_GATHER = os.environ.get("LSS_CE_GATHER", "1") != "0"  # K/V gather on the copy engines
 _WGRAD_SIDE = os.environ.get("LSS_WGRAD_SIDE", "1") != "0"  # weight-gradient GEMMs on a side stream
 _FUSED_GATHER = os.environ.get("LSS_FUSED_GATHER", "1") != "0"  # attention waits per gathered segment
+_B1_IN_KERNEL = os.environ.get("LSS_B1_IN_KERNEL", "1") != "0"  # backward waits for the pushed dO in-kernel
 last_phases: dict = {}
 
 
@@ -1130,10 +1137,14 @@ def lss_backward(engines, comm, grad_ys, *, step=0, layer=0, sync=True, mark=_no
     for e in engines:
         e.bwd_pre_weights()
     mark("bwd_pre")
-    _wait(b1)
+    peer_ready = None
+    if _B1_IN_KERNEL and len(engines) == 1 and b1 and all(hasattr(w, "addr") for w in b1):  # wait in-kernel
+        peer_ready = (b1[0].addr, b1[0].seq)
+    else:
+        _wait(b1)
     mark("p2p_B1")
     for e in engines:
-        e.bwd_attend()
+        e.bwd_attend(peer_ready=peer_ready)
     mark("bwd_attend")
     b2 = _exchange(engines, comm, "B2", step, layer, async_op=True)
     if fused:  # the reduce-scatter already happened inside the backward kernels

@@ -357,13 +357,18 @@ static int attn_fwd_launch(int dtype, const void* q, int rows, long q_bstride, c
   p.ready_seq = ready_seq;
   p.own_seg = own_seg;
   dim3 grid((unsigned)((rows + 2 * ATT_BM - 1) / (2 * ATT_BM)) * heads * batch * splits);
-  if (drop) {
-    if ((rc = set_smem(attn_fwd_tc_kernel<true>, ATT_FWD_SMEM))) return rc;
-    attn_fwd_tc_kernel<true><<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
-  } else {
-    if ((rc = set_smem(attn_fwd_tc_kernel<false>, ATT_FWD_SMEM))) return rc;
-    attn_fwd_tc_kernel<false><<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
-  }
+  const bool part = splits > 1 || seg_ready != nullptr;
+  auto launch = [&](auto kern) -> int {
+    int r = set_smem(kern, ATT_FWD_SMEM);
+    if (r) return r;
+    kern<<<grid, ATT_FWD_THREADS, ATT_FWD_SMEM, S(stream)>>>(mq, mk, mv, p);
+    return LSS_OK;
+  };
+  if (drop)
+    rc = part ? launch(attn_fwd_tc_kernel<true, true>) : launch(attn_fwd_tc_kernel<true, false>);
+  else
+    rc = part ? launch(attn_fwd_tc_kernel<false, true>) : launch(attn_fwd_tc_kernel<false, false>);
+  if (rc) return rc;
   if ((rc = check_launch("attn_fwd_tc"))) return rc;
   if (splits > 1) {
     const long warps = (long)batch * rows;

@@ -131,6 +131,8 @@ DROP_CASES = {
     # at every site; G=2 must equal G=1 on the same masks
     "drop_layer_g1": (128, 128, 2, 1, 2, True, 256, 0.1, 1234),
     "drop_layer_g2": (256, 128, 2, 2, 1, True, 256, 0.1, 1234),
+    # m = 512 per rank at world 2: the balanced causal schedule is active (NCCL test)
+    "drop_layer_g2_big": (1024, 128, 2, 2, 1, True, 256, 0.1, 4321),
 }
 
 
@@ -173,8 +175,11 @@ def gpt_case(seed=5, policy=None, name="gpt_small"):
     print(name, "written, loss", loss)
 
 
-def main():
+def main(only=None):
+    keep = (lambda n: True) if not only else (lambda n: n in only)  # noqa: E731
     for name, (seq, e, h, g, b, causal, odt) in CASES.items():
+        if not keep(name):
+            continue
         x, gy, params, y, dx, grads = run_case(seq, e, h, g, b, causal)
         arrays = dict(x=x.astype(np.float32), grad_y=gy.astype(np.float32),
                       meta=np.array([seq, e, h, g, b, int(causal)], dtype=np.int64),
@@ -184,6 +189,8 @@ def main():
         np.savez_compressed(OUT / f"{name}.npz", **arrays)
         print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("x", "y")})
     for name, (seq, e, h, g, b, causal, ff, odt) in FULL_CASES.items():
+        if not keep(name):
+            continue
         x, gy, params, y, dx, grads = run_case(seq, e, h, g, b, causal, ff_dim=ff)
         arrays = dict(x=x.astype(np.float32), grad_y=gy.astype(np.float32),
                       meta=np.array([seq, e, h, g, b, int(causal)], dtype=np.int64),
@@ -192,9 +199,13 @@ def main():
         arrays.update({k: v.astype(odt) for k, v in grads.items()})
         np.savez_compressed(OUT / f"{name}.npz", **arrays)
         print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("x", "y", "w_in")})
-    gpt_case()
-    gpt_case(policy=DropoutPolicy(0.1, seed=99), name="gpt_drop")
+    if keep("gpt_small"):
+        gpt_case()
+    if keep("gpt_drop"):
+        gpt_case(policy=DropoutPolicy(0.1, seed=99), name="gpt_drop")
     for name, (seq, e, h, g, b, causal, ff, rate, dseed) in DROP_CASES.items():
+        if not keep(name):
+            continue
         pol = DropoutPolicy(rate, seed=dseed)
         x, gy, params, y, dx, grads = run_case(seq, e, h, g, b, causal, ff_dim=ff, policy=pol)
         arrays = dict(x=x.astype(np.float32), grad_y=gy.astype(np.float32),
@@ -208,4 +219,6 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+
+    main(sys.argv[1:] or None)  # optional case names: regenerate only those

@@ -104,12 +104,17 @@ class BalancePlan:
         return self.role != "none"
 
 
-def make_plan(rank: int, workers: int, block: int, causal: bool) -> BalancePlan:
+def make_plan(rank: int, workers: int, block: int, causal: bool, bias_tiles: int = 0) -> BalancePlan:
+    """``bias_tiles``: move the split down by that many 128-row tiles, i.e. hand
+    bias_tiles*128*block more (query, key) pairs per (batch, head) from every heavy
+    rank to its light partner (a - b = 1 for every pair) -- balances measured time
+    rather than pair counts (the heavy rank's mix runs slower per pair)."""
     if not causal or workers < 2:
         return BalancePlan()
     split = (block // 2) // 128 * 128
     if split == 0:
         return BalancePlan()
+    split = max(128, min(split + 128 * bias_tiles, (block - 1) // 128 * 128))
     partner = workers - 1 - rank
     d2 = lambda r: 2 * r - workers + 1  # noqa: E731  half-blocks rank r must give away
     if d2(rank) > 0:
@@ -121,6 +126,7 @@ def make_plan(rank: int, workers: int, block: int, causal: bool) -> BalancePlan:
     return BalancePlan()
 
 
+_SPLIT_BIAS = int(os.environ.get("LSS_SPLIT_BIAS", "0"))
 _FWD_SPLIT = os.environ.get("LSS_FWD_SPLIT", "1") != "0"
 _SPLIT_MAX = 8
 # per-CTA fixed cost (launch, prologue, pipeline fill / drain, epilogue) in key-tile
@@ -213,7 +219,7 @@ class LSSAttention:
 
     def __init__(self, cfg: ModelConfig, spec: ShardSpec, *, grad_scale: float | None = None,
                  device=None, balanced: bool | None = None, fused_rs: bool | None = None,
-                 with_ffn: bool = False, grads: torch.Tensor | None = None):
+                 with_ffn: bool = False, grads: torch.Tensor | None = None, split_bias: int | None = None):
         if spec.seq_len != cfg.seq_len:
             raise ShapeError(f"shard spec length {spec.seq_len} != config seq_len {cfg.seq_len}")
         self.cfg, self.spec = cfg, spec
@@ -229,7 +235,8 @@ class LSSAttention:
         z = lambda *s, dt=f32: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
         if balanced is None:
             balanced = cfg.precision == "bf16"
-        self.plan = make_plan(spec.rank, G, m, cfg.causal) if balanced and cfg.precision == "bf16" else BalancePlan()
+        self.plan = make_plan(spec.rank, G, m, cfg.causal, split_bias if split_bias is not None else _SPLIT_BIAS) \
+            if balanced and cfg.precision == "bf16" else BalancePlan()
         # forward
         self.xh = z(B, m, E, dt=ad)
         self.mean, self.rstd = z(B * m), z(B * m)

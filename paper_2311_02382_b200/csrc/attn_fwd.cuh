@@ -95,9 +95,9 @@ struct AttnFwdParams {
   int own_seg;
 };
 
-// PART: key-split grid / fused-gather flags / top-down segment order.  The plain
-// instance (one launch over resident K/V, ascending tiles) keeps the hot loops free
-// of that bookkeeping (measured: 4-6% slower at N=1 otherwise).
+// PART: key-split grid / fused-gather flags / top-down segment order; the plain
+// instance (ascending tiles, no split) is kept for A/B builds (-DLSS_FWD_PLAIN).  The
+// tile walk is incremental: a runtime division per tile in the softmax loop cost 4-8%.
 template <bool DROP, bool PART>
 __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -172,6 +172,14 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       t = (jt - n_top) % tps;
     }
   };
+  auto next_tile = [&](int& g, int& t) {  // the visit after (g, t)
+    if (!PART) {
+      if (++t == tps) { t = 0; ++g; }
+    } else if (++t == (g == g_top ? n_top : tps)) {
+      t = 0;
+      --g;
+    }
+  };
   __nv_bfloat16* const o_dst = (!PART || split == 0) ? p.o : p.o_part + (long)(split - 1) * p.o_part_stride;
   float* const lse_dst = (!PART || split == 0) ? p.lse2 : p.lse_part + (long)(split - 1) * p.lse_part_stride;
 
@@ -213,11 +221,11 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       }
       __syncwarp();
       int g_ready = p.own_seg;  // segments known to be resident
-      for (int j = 0; j < n_kv; ++j) {
+      int g, t;
+      tile_of(j_base, g, t);
+      for (int j = 0; j < n_kv; ++j, next_tile(g, t)) {
         const int st = j % ATT_KV_STAGES;
         const uint32_t ph = (j / ATT_KV_STAGES) & 1;
-        int g, t;
-        tile_of(j_base + j, g, t);
         if (PART && p.seg_ready != nullptr && g != g_ready && g != p.own_seg) {  // fused gather: wait for it
           if (lane == 0) wait_flag_geq(p.seg_ready + g, p.ready_seq);
           __syncwarp();
@@ -296,9 +304,9 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
     if (active && n_kv > 0) {
       float m_run = -INFINITY, l_run = 0.f;
       const int tile_first_row = q0 + w * ATT_BM;  // for the mask decision (warp-uniform)
-      for (int j = 0; j < n_kv; ++j) {
-        int g, t;
-        tile_of(j_base + j, g, t);
+      int g, t;
+      tile_of(j_base, g, t);
+      for (int j = 0; j < n_kv; ++j, next_tile(g, t)) {
         const int valid_cols = min(ATT_BN, p.seg_len - t * ATT_BN);
         const long key0 = (long)g * p.seg_len + (long)t * ATT_BN;
         const bool need_mask = valid_cols < ATT_BN ||

@@ -371,6 +371,7 @@ def main_ours(args):
         for i in range(args.steps):  # input prefetch: step i+1's H2D overlaps step i (one copy per step)
             eng.load_params(lp)
             eng.step_from_host(xh, gyh, comm, grads_h, next_inputs=(xh, gyh) if i + 1 < args.steps else None)
+        stream.wait_event(eng.host_sync_event())  # every step's gradients are back on the host
         e1.record(stream)
         torch.cuda.synchronize()
         t_e2e = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)

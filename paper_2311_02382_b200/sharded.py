@@ -813,7 +813,9 @@ class LSSAttention:
         step, their copy is issued on the copy stream during this step's compute
         (input prefetch), and the next call finds them resident.  Every step's
         inputs are still copied once, by this engine, per step.  Stream-ordered;
-        the caller synchronises when it needs the host result."""
+        the gradient read-back runs on the copy stream (overlapping the next step):
+        the caller synchronises the device, or waits on :meth:`host_sync_event`,
+        before reading ``grads_host``."""
         cur = torch.cuda.current_stream()
         if not hasattr(self, "_in_bufs"):
             mk = lambda: torch.empty(self.B, self.m, self.E, dtype=torch.float32, device=self.device)  # noqa: E731
@@ -851,8 +853,26 @@ class LSSAttention:
         out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer, policy=policy)
         self._in_free[slot].record(cur)
         if grads_host is not None:
-            grads_host.copy_(self.grads, non_blocking=True)
+            # read-back off the critical path: snapshot the averaged gradients on the
+            # compute stream (D2D), then D2H on the copy stream, overlapping the next
+            # step (whose first kernel re-zeroes self.grads)
+            if getattr(self, "_grads_stage", None) is None:
+                self._grads_stage = torch.empty_like(self.grads)
+                self._d2h_done = torch.cuda.Event()
+                self._d2h_done.record(cur)
+            cur.wait_event(self._d2h_done)  # previous read-back finished with the stage
+            self._grads_stage.copy_(self.grads)
+            cs = self._copy_stream
+            cs.wait_stream(cur)
+            with torch.cuda.stream(cs):
+                grads_host.copy_(self._grads_stage, non_blocking=True)
+                self._d2h_done.record(cs)
         return out[0]
+
+    def host_sync_event(self) -> torch.cuda.Event | None:
+        """Event after the last step_from_host read-back (None before the first):
+        the caller waits on it (or synchronises) before reading grads_host."""
+        return getattr(self, "_d2h_done", None)
 
 
 # ---------------------------------------------------------------- drivers

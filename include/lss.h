@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 6
+#define LSS_ABI_VERSION 7
 
 enum lss_status {
   LSS_OK = 0,
@@ -249,8 +249,9 @@ int lss_timestamp(unsigned long long* dst, void* stream);
  * at embed + h*d — so the transfer overlaps the attention math tile by tile.
  * Stores leave the SM as whole 256-byte row segments.  peer marks seg_dst as
  * peer memory; ordering comes from kernel completion followed by a device-side
- * barrier, after which the owner sums its `workers` slots with lss_sum_slots.  Same sources
- * and numerics as lss_attn_bwd_ex; workers <= 16. */
+ * barrier, after which the owner sums its writers' slots with lss_sum_slots_mask.  Only key
+ * segments [min g_begin, max g_end) of the sources are written (no zero tiles for
+ * segments no source reads).  Same sources and numerics as lss_attn_bwd_ex; workers <= 16. */
 int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const lss_bwd_source* srcs,
                      int nsrc, float* const* seg_dst, int peer, long ld_dkv, int batch, int workers,
                      int seg_len, int heads, int head_dim, int causal, const lss_dropout* dropout,
@@ -288,6 +289,13 @@ int lss_adam_update(float* params, const float* grads, float* m, float* v, long 
 
 /* dst[i] = sum_{s < nslots} src[s * slot_elems + i] for i < n (fp32, n % 4 == 0). */
 int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, long n, void* stream);
+
+/* Same over the slots whose bit is set in mask (ascending; mask 0 -> zeros): the
+ * owner's half of the fused reduce-scatter, whose writers are the ranks that
+ * attend any key of its segment (lss_attn_bwd_p2p writes only segments
+ * [min g_begin, max g_end) of its sources). */
+int lss_sum_slots_mask(float* dst, const float* src, int nslots, unsigned int mask, long slot_elems, long n,
+                       void* stream);
 
 /* CUDA IPC for the peer buffers above: export a device pointer (any address
  * inside an allocation) as a 64-byte handle + offset; import it in another

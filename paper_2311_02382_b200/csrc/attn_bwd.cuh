@@ -92,6 +92,7 @@ struct AttnBwdParams {
   uint64_t drop_thresh;
   float drop_scale;
   float* seg_tab[ATB_MAX_SEG];  // used when seg_tab[0] != nullptr
+  int g_lo;                     // first key segment of the grid (the fused path skips segments no source reads)
 };
 
 LSS_DEV void bulk_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   const int h = blockIdx.y;
   const int b = blockIdx.z;
   const int tps = (p.seg_len + ATT_BN - 1) / ATT_BN;
-  const int g = blockIdx.x / tps;
+  const int g = p.g_lo + (int)blockIdx.x / tps;
   const int kt = blockIdx.x % tps;
   const int kv_row0 = kt * ATT_BN;                         // row within segment
   const int kv_valid = min(ATT_BN, p.seg_len - kv_row0);

@@ -373,13 +373,23 @@ __global__ void pad_fill_kernel(float* __restrict__ buf, long nrows, int m, int 
 
 // dst = sum over nslots of src[slot] (the owner's side of the fused dK|dV
 // reduce-scatter: one slot per source rank, written by the peers' backward).
+// dst = ascending-slot sum of the slots whose bit is set in mask (unset slots are
+// never written by the fused reduce-scatter: their writers attend no key of this
+// segment); mask 0 gives zeros.
 __global__ void sum_slots_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int nslots,
-                                 long slot4, long n4) {
+                                 uint32_t mask, long slot4, long n4) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
-    float4 a = src[i];
-    for (int s = 1; s < nslots; ++s) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool first = true;
+    for (int s = 0; s < nslots; ++s) {
+      if (!((mask >> s) & 1u)) continue;
       const float4 b = src[s * slot4 + i];
-      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      if (first) {
+        a = b;
+        first = false;
+      } else {
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
     }
     dst[i] = a;
   }

@@ -532,7 +532,20 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
     return rc;
   }
   const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
-  dim3 grid(workers * tps, heads, batch);
+  // fused reduce-scatter: only the key segments some source reads get a CTA (the
+  // owners sum just their writers' slots, lss_sum_slots_mask); the local layout
+  // (NCCL reduce-scatter input) is fully written, zeros included
+  int g_lo = 0, g_hi = workers;
+  if (seg_tab) {
+    g_lo = workers;
+    g_hi = 0;
+    for (int i = 0; i < nsrc; ++i) {
+      g_lo = std::min(g_lo, srcs[i].g_begin);
+      g_hi = std::max(g_hi, srcs[i].g_end);
+    }
+  }
+  p.g_lo = g_lo;
+  dim3 grid((g_hi - g_lo) * tps, heads, batch);
   if (drop)
     attn_bwd_tc_kernel<true><<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
   else
@@ -559,7 +572,15 @@ int lss_attn_bwd_p2p(int dtype, const void* k, const void* v, long ld_kv, const 
 }
 
 int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, long n, void* stream) {
+  if (nslots < 1 || nslots > 32) return fail(LSS_ERR_SHAPE, "sum_slots: %d slots (1..32)", nslots);
+  return lss_sum_slots_mask(dst, src, nslots, nslots == 32 ? 0xFFFFFFFFu : ((1u << nslots) - 1u), slot_elems, n,
+                            stream);
+}
+
+int lss_sum_slots_mask(float* dst, const float* src, int nslots, unsigned int mask, long slot_elems, long n,
+                       void* stream) {
   if (!dst || !src) return fail(LSS_ERR_ARG, "sum_slots: null pointer");
+  if (nslots > 32) return fail(LSS_ERR_SHAPE, "sum_slots: %d slots (max 32)", nslots);
   if (nslots < 1 || n < 0 || n > slot_elems || n % 4 || slot_elems % 4 || !aligned16(dst) || !aligned16(src))
     return fail(LSS_ERR_SHAPE, "sum_slots: %d slots of %ld (n %ld) must be float4 aligned", nslots, slot_elems, n);
   if (n == 0) return LSS_OK;
@@ -567,7 +588,8 @@ int lss_sum_slots(float* dst, const float* src, int nslots, long slot_elems, lon
   const long n4 = n / 4;
   const int blocks = (int)std::min<long>((n4 + threads - 1) / threads, (long)num_sms() * 8);
   sum_slots_kernel<<<blocks, threads, 0, S(stream)>>>(reinterpret_cast<float4*>(dst),
-                                                       reinterpret_cast<const float4*>(src), nslots, slot_elems / 4, n4);
+                                                       reinterpret_cast<const float4*>(src), nslots, mask,
+                                                       slot_elems / 4, n4);
   return check_launch("sum_slots");
 }
 

@@ -396,12 +396,16 @@ def timestamp(dst):
     call("lss_timestamp", _ptr(dst), _stream())
 
 
-def sum_slots(dst, src):
+def sum_slots(dst, src, mask=None):
     """dst = src.sum(0) for src [S, ...] fp32 contiguous (the owner's half of the fused
-    reduce-scatter)."""
+    reduce-scatter); with ``mask`` only the slots whose bit is set (ascending)."""
     if not src.is_contiguous() or not dst.is_contiguous() or src[0].numel() != dst.numel():
         raise ShapeError("sum_slots: contiguous src [S, *dst.shape] required")
-    call("lss_sum_slots", _ptr(dst), _ptr(src), src.shape[0], src[0].numel(), dst.numel(), _stream())
+    if mask is None:
+        call("lss_sum_slots", _ptr(dst), _ptr(src), src.shape[0], src[0].numel(), dst.numel(), _stream())
+    else:
+        call("lss_sum_slots_mask", _ptr(dst), _ptr(src), src.shape[0], int(mask) & 0xFFFFFFFF, src[0].numel(),
+             dst.numel(), _stream())
     return dst
 
 

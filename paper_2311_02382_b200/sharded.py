@@ -235,8 +235,9 @@ class LSSAttention:
         z = lambda *s, dt=f32: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
         if balanced is None:
             balanced = cfg.precision == "bf16"
-        self.plan = make_plan(spec.rank, G, m, cfg.causal, split_bias if split_bias is not None else _SPLIT_BIAS) \
-            if balanced and cfg.precision == "bf16" else BalancePlan()
+        self.plan_bias = split_bias if split_bias is not None else _SPLIT_BIAS
+        self.balanced = bool(balanced) and cfg.precision == "bf16"
+        self.plan = make_plan(spec.rank, G, m, cfg.causal, self.plan_bias) if self.balanced else BalancePlan()
         # forward
         self.xh = z(B, m, E, dt=ad)
         self.mean, self.rstd = z(B * m), z(B * m)
@@ -495,8 +496,36 @@ class LSSAttention:
 
     def gather_slots(self) -> None:
         """Owner side of the fused reduce-scatter: dK|dV of this rank's segment =
-        sum of the G received slots (after the device barrier)."""
-        K.sum_slots(self.dkv_own, self.dkv_full)
+        sum of the received slots (after the device barrier) -- only the slots of
+        ranks that attend this segment are written (bwd_segments), ascending."""
+        K.sum_slots(self.dkv_own, self.dkv_full, mask=self.writer_mask())
+
+    def bwd_segments(self, rank: int | None = None):
+        """Key segments [lo, hi) the backward sources of `rank` (default: this one)
+        read -- the range its fused dK|dV stores cover (lss_attn_bwd_p2p)."""
+        r = self.spec.rank if rank is None else rank
+        G = self.G
+        if not self.cfg.causal:
+            return 0, G
+        if rank is None:
+            pl = self.plan
+        else:  # every engine of the group is built with the same balance setting
+            pl = make_plan(r, G, self.m, True, self.plan_bias) if self.balanced else BalancePlan()
+        if pl.role == "heavy":
+            return min(pl.a, pl.b), r + 1
+        if pl.role == "light":
+            return 0, max(r + 1, pl.a, pl.b)
+        return 0, r + 1
+
+    def writer_mask(self) -> int:
+        """Bit s set iff rank s stores a partial for this rank's key segment."""
+        me = self.spec.rank
+        mask = 0
+        for s in range(self.G):
+            lo, hi = self.bwd_segments(s)
+            if lo <= me < hi:
+                mask |= 1 << s
+        return mask
 
     # ------------------------------------------------------------ point-to-point exchanges
     def xfer(self, phase: str):

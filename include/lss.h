@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 7
+#define LSS_ABI_VERSION 8
 
 enum lss_status {
   LSS_OK = 0,
@@ -112,6 +112,13 @@ int lss_stage_weights(int dtype, const float* wq, const float* wk, const float* 
 int lss_cat_cast_colsum(int out_dtype, const float* const* srcs, const long* lds, const int* cols,
                         int nsrc, void* dst, long ld_dst, float* colsum, float alpha, long rows,
                         void* stream);
+
+/* Same, where source i (nslots[i] > 1) is the ascending sum of the slots set in
+ * masks[i], slot k at srcs[i] + k * slot_strides[i]: the fused reduce-scatter's
+ * owner sum (lss_sum_slots_mask) folded into the cast (arrays may be NULL). */
+int lss_cat_cast_colsum_ex(int out_dtype, const float* const* srcs, const long* lds, const int* cols,
+                           const int* nslots, const unsigned int* masks, const long* slot_strides, int nsrc,
+                           void* dst, long ld_dst, float* colsum, float alpha, long rows, void* stream);
 
 /* model.scores_fwd (model.py:280-326): this rank's query rows (global
  * positions offset..offset+rows-1) against the whole sequence, whose keys and

@@ -92,6 +92,8 @@ SIGNATURES = {
     "lss_add_f32": [_P, _P, _L, _P],
     "lss_timestamp": [_P, _P],
     "lss_sum_slots_mask": [_P, _P, _I, ctypes.c_uint, _L, _L, _P],
+    "lss_cat_cast_colsum_ex": [_I, ctypes.POINTER(_P), ctypes.POINTER(_L), ctypes.POINTER(_I), ctypes.POINTER(_I),
+                               ctypes.POINTER(ctypes.c_uint), ctypes.POINTER(_L), _I, _P, _L, _P, _F, _L, _P],
     "lss_stream_signal": [_P, ctypes.c_uint, _P],
     "lss_stream_wait": [_P, ctypes.c_uint, _P],
     "lss_attn_bwd_p2p": [_I, _P, _P, _L, ctypes.POINTER(BwdSource), _I, ctypes.POINTER(_P), _I, _L, _I, _I, _I,
@@ -115,7 +117,7 @@ EXTRA = {
     "lss_rows_pad": ([_L], _L),
     "lss_peer_access": ([_I, _I], _I),
 }
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _lib = None
 
@@ -152,7 +154,7 @@ KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 
                     "lss_attn_merge": 1, "lss_attn_delta": 1, "lss_attn_bwd_ex": 1, "lss_add_f32": 1,
                     "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1,
                     "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1,
-                    "lss_dropout_rows": 1, "lss_attn_fwd_split": 1, "lss_sum_slots_mask": 1}
+                    "lss_dropout_rows": 1, "lss_attn_fwd_split": 1, "lss_sum_slots_mask": 1, "lss_cat_cast_colsum_ex": 1}
 launch_count = 0
 
 

@@ -120,6 +120,12 @@ struct CatSrc {
   long ld[3];
   int cols[3];
   int n;
+  // optional per source: the value is the ascending sum of the slots set in mask
+  // (slot k at ptr + k * slot_stride) -- the fused reduce-scatter's owner sum folded
+  // into the cast that feeds the projection backward (no dK|dV round trip)
+  int nslot[3];
+  uint32_t mask[3];
+  long slot_stride[3];
 };
 constexpr int CAT_ROWS = 32;
 template <typename TOut>
@@ -138,7 +144,17 @@ __global__ void cat_cast_colsum_kernel(CatSrc src, TOut* __restrict__ dst, long 
   for (int i = 0; i < CAT_ROWS; ++i) {
     const long r = r0 + i;
     if (r >= rows) break;
-    const float4 v = *reinterpret_cast<const float4*>(sp + r * ld + lc);
+    float4 v;
+    if (src.nslot[s] <= 1) {
+      v = *reinterpret_cast<const float4*>(sp + r * ld + lc);
+    } else {
+      v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 0; k < src.nslot[s]; ++k) {
+        if (!((src.mask[s] >> k) & 1u)) continue;
+        const float4 u = *reinterpret_cast<const float4*>(sp + k * src.slot_stride[s] + r * ld + lc);
+        v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+      }
+    }
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     if (dst) store4<TOut>(dst + r * ld_dst + col4, v.x, v.y, v.z, v.w);
   }

@@ -253,6 +253,13 @@ int lss_stage_weights(int dtype, const float* wq, const float* wk, const float* 
 int lss_cat_cast_colsum(int out_dtype, const float* const* srcs, const long* lds, const int* cols,
                         int nsrc, void* dst, long ld_dst, float* colsum, float alpha, long rows,
                         void* stream) {
+  return lss_cat_cast_colsum_ex(out_dtype, srcs, lds, cols, nullptr, nullptr, nullptr, nsrc, dst, ld_dst, colsum,
+                                alpha, rows, stream);
+}
+
+int lss_cat_cast_colsum_ex(int out_dtype, const float* const* srcs, const long* lds, const int* cols,
+                           const int* nslots, const unsigned int* masks, const long* slot_strides, int nsrc,
+                           void* dst, long ld_dst, float* colsum, float alpha, long rows, void* stream) {
   if (nsrc < 1 || nsrc > 3 || !srcs || !lds || !cols) return fail(LSS_ERR_ARG, "cat_cast_colsum: bad sources");
   CatSrc cs;
   int total = 0;
@@ -260,6 +267,11 @@ int lss_cat_cast_colsum(int out_dtype, const float* const* srcs, const long* lds
     cs.ptr[i] = i < nsrc ? srcs[i] : nullptr;
     cs.ld[i] = i < nsrc ? lds[i] : 0;
     cs.cols[i] = i < nsrc ? cols[i] : 0;
+    cs.nslot[i] = (i < nsrc && nslots) ? nslots[i] : 1;
+    cs.mask[i] = (i < nsrc && masks) ? masks[i] : 1u;
+    cs.slot_stride[i] = (i < nsrc && slot_strides) ? slot_strides[i] : 0;
+    if (cs.nslot[i] > 32 || (cs.nslot[i] > 1 && cs.slot_stride[i] % 4))
+      return fail(LSS_ERR_UNSUPPORTED, "cat_cast_colsum: source %d slots", i);
     if (i < nsrc) {
       if (!srcs[i] || cols[i] % 4 || lds[i] % 4) return fail(LSS_ERR_UNSUPPORTED, "cat_cast_colsum: source %d", i);
       total += cols[i];

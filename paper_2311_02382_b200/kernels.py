@@ -161,7 +161,9 @@ def stage_weights(wq, wk, wv, wo, bq, bk, bv, precision="bf16", bufs=None):
 
 
 def cat_cast_colsum(srcs, rows, dst=None, colsum=None, alpha=1.0, out_dtype=torch.bfloat16):
-    """srcs: list of (fp32 tensor, ld, cols).  Writes the column concatenation into
+    """srcs: list of (fp32 tensor, ld, cols) or (fp32 tensor, ld, cols, nslots, mask,
+    slot_stride): the latter is the ascending sum of the masked slots (slot k at
+    tensor + k * slot_stride elements).  Writes the column concatenation into
     ``dst`` (ld = total cols) and accumulates alpha * column sums into ``colsum``."""
     n = len(srcs)
     ptrs = (ctypes.c_void_p * n)(*[s[0].data_ptr() for s in srcs])
@@ -170,8 +172,16 @@ def cat_cast_colsum(srcs, rows, dst=None, colsum=None, alpha=1.0, out_dtype=torc
     total = sum(s[2] for s in srcs)
     dt = LSS_BF16 if (dst is not None and dst.dtype == torch.bfloat16) or (
         dst is None and out_dtype == torch.bfloat16) else LSS_F32
-    call("lss_cat_cast_colsum", dt, ptrs, lds, cols, n, _ptr(dst), total, _ptr(colsum), alpha, rows,
-         _stream())
+    if all(len(s) == 3 for s in srcs):
+        call("lss_cat_cast_colsum", dt, ptrs, lds, cols, n, _ptr(dst), total, _ptr(colsum), alpha, rows,
+             _stream())
+        return dst, colsum
+    ext = [s if len(s) == 6 else (*s, 1, 1, 0) for s in srcs]
+    nsl = (ctypes.c_int * n)(*[s[3] for s in ext])
+    msk = (ctypes.c_uint * n)(*[s[4] & 0xFFFFFFFF for s in ext])
+    sst = (ctypes.c_long * n)(*[s[5] for s in ext])
+    call("lss_cat_cast_colsum_ex", dt, ptrs, lds, cols, nsl, msk, sst, n, _ptr(dst), total, _ptr(colsum), alpha,
+         rows, _stream())
     return dst, colsum
 
 

@@ -318,6 +318,7 @@ class LSSAttention:
         self.peer_mem = False
         self.set_dropout(None, 0)
         self._scratch = {}
+        self._slots_pending = False  # fused RS slots not yet summed (folded into bwd_project's cast)
         # fused gather: per-segment arrival flags signalled by the copy stream (int32 [G])
         self._ready = torch.zeros(G, dtype=torch.int32, device=self.device) if G > 1 else None
         self._ready_seq = 0
@@ -810,7 +811,12 @@ class LSSAttention:
         B, m, E = self.B, self.m, self.E
         a = self.grad_scale
         M = B * m
-        K.cat_cast_colsum([(self.dq.view(M, E), E, E), (self.dkv_own.view(M, 2 * E), 2 * E, 2 * E)], M,
+        if self._slots_pending:  # fused reduce-scatter: sum the writers' slots inside the cast
+            dkv = (self.dkv_full, 2 * E, 2 * E, self.G, self.writer_mask(), self.dkv_full[0].numel())
+            self._slots_pending = False
+        else:
+            dkv = (self.dkv_own.view(M, 2 * E), 2 * E, 2 * E)
+        K.cat_cast_colsum([(self.dq.view(M, E), E, E), dkv], M,
                           dst=self.dqkv.view(M, 3 * E), colsum=self.g_bqkv, alpha=a)
         main, ws = torch.cuda.current_stream(), self._wgrad_stream()
         ws.wait_stream(main)
@@ -1049,7 +1055,8 @@ _NO_OVERLAP = os.environ.get("LSS_NO_OVERLAP") == "1"
 _CE_GATHER = os.environ.get("LSS_CE_GATHER", "1") != "0"  # K/V gather on the copy engines
 _WGRAD_SIDE = os.environ.get("LSS_WGRAD_SIDE", "1") != "0"  # weight-gradient GEMMs on a side stream
 _FUSED_GATHER = os.environ.get("LSS_FUSED_GATHER", "1") != "0"  # attention waits per gathered segment
-_B1_IN_KERNEL = os.environ.get("LSS_B1_IN_KERNEL", "1") != "0"  # backward waits for the pushed dO in-kernel
+_B1_IN_KERNEL = os.environ.get("LSS_B1_IN_KERNEL", "1") != "0"
+_FOLD_SLOTS = os.environ.get("LSS_FOLD_SLOTS", "1") != "0"  # fused RS owner sum inside the projection cast  # backward waits for the pushed dO in-kernel
 last_phases: dict = {}
 
 
@@ -1212,7 +1219,10 @@ def lss_backward(engines, comm, grad_ys, *, step=0, layer=0, sync=True, mark=_no
             comm.device_barrier(step, "backward", layer)
         mark("rs_barrier")
         for e in engines:
-            e.gather_slots()
+            if _FOLD_SLOTS:
+                e._slots_pending = True  # summed inside bwd_project's cast (no dK|dV round trip)
+            else:
+                e.gather_slots()
     else:
         one(lambda t: comm.reduce_scatter_rows([e.dkv_own for e in t] if sim else t.dkv_own,
                                                [e.dkv_full for e in t] if sim else t.dkv_full, step, layer))

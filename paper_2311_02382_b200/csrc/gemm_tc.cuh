@@ -70,7 +70,43 @@ constexpr int GEMM_STAGES = 4;
 constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;  // 16 KB
 constexpr int GEMM_B_BYTES = GEMM_BN * GEMM_BK * 2;  // 32 KB
 constexpr int GEMM_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES;
-constexpr int GEMM_SMEM_BYTES = GEMM_STAGES * GEMM_STAGE_BYTES + 1024 /*align*/ + 256 /*bars*/;
+constexpr int GEMM_EPI_BYTES = 4 * 32 * 32 * 4;  // per epilogue warp: a 32 x 32 fp32 staging tile
+constexpr int GEMM_SMEM_BYTES = GEMM_STAGES * GEMM_STAGE_BYTES + GEMM_EPI_BYTES + 1024 /*align*/ + 256 /*bars*/;
+
+// Epilogue store of a warp's 32 rows x 32 columns through shared memory: every lane
+// holds one row (32 fp32 values); the tile is staged with 16-byte chunks XOR-swizzled
+// by row, then written back with the lanes spread across columns, so each store
+// instruction covers whole 64-byte (bf16) / 128-byte (fp32) row segments instead of
+// 32 half-filled sectors.  row_base: first row of the warp's 32; rows >= M skipped.
+template <bool BF16>
+LSS_DEV void epi_store_rows(uint32_t stage, const float (&v)[32], void* out, long ld, long col, int row_base,
+                            int M, uint32_t lane) {
+  constexpr int CH = BF16 ? 4 : 8;  // 16-byte chunks per row
+  if (BF16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      st_shared_v4(stage + lane * 64 + ((q ^ (lane & 3)) << 4), pack_bf16(v[8 * q], v[8 * q + 1]),
+                   pack_bf16(v[8 * q + 2], v[8 * q + 3]), pack_bf16(v[8 * q + 4], v[8 * q + 5]),
+                   pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      st_shared_v4(stage + lane * 128 + ((q ^ (lane & 7)) << 4), __float_as_uint(v[4 * q]),
+                   __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
+  }
+  __syncwarp();
+  constexpr int RPI = 32 / CH;  // rows per store instruction
+#pragma unroll
+  for (int i = 0; i < 32 / RPI; ++i) {
+    const int r = i * RPI + (int)lane / CH, q = (int)lane % CH;
+    const float4 val = ld_shared_f4(stage + r * (CH * 16) + ((q ^ (r & (CH - 1))) << 4));
+    if (row_base + r < M) {
+      char* dst = reinterpret_cast<char*>(out) + ((long)(row_base + r) * ld + col) * (BF16 ? 2 : 4) + q * 16;
+      *reinterpret_cast<float4*>(dst) = val;
+    }
+  }
+  __syncwarp();  // the staging tile is reused by the next chunk
+}
 constexpr int GEMM_THREADS = 256;
 
 template <int A_MN, int B_MN>
@@ -192,6 +228,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---------------- epilogue: thread <-> accumulator row
     const int quad = warp - 4;
     const int row_in_tile = quad * 32 + lane;
+    const uint32_t epi = smem_u32(smem + GEMM_STAGES * GEMM_STAGE_BYTES + 256) + quad * (32 * 32 * 4);
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int buf = local & 1;
@@ -207,10 +244,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + buf * GEMM_BN + c, r);
         const int n = n0 + c;
-        if (!row_ok || n >= N) continue;
+        if (n >= N) continue;  // warp-uniform
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * ep.alpha;
+        if (!row_ok) {  // rows past M: staged but never stored (no operand loads)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        } else {
         if (ep.bias) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += __ldg(ep.bias + n + i);
@@ -269,26 +310,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
+        }  // row_ok
         const int seg = n / ep.seg_width;
         const long col = n - (long)seg * ep.seg_width;
-        if (ep.out_bf16) {
-          uint4* op = reinterpret_cast<uint4*>(
-              reinterpret_cast<__nv_bfloat16*>(ep.out[seg]) + (long)row * ep.ldo[seg] + col);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint4 t;
-            t.x = pack_bf16(v[8 * i + 0], v[8 * i + 1]);
-            t.y = pack_bf16(v[8 * i + 2], v[8 * i + 3]);
-            t.z = pack_bf16(v[8 * i + 4], v[8 * i + 5]);
-            t.w = pack_bf16(v[8 * i + 6], v[8 * i + 7]);
-            op[i] = t;
-          }
-        } else {
-          float4* op =
-              reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out[seg]) + (long)row * ep.ldo[seg] + col);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) op[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
+        if (ep.out_bf16)
+          epi_store_rows<true>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
+        else
+          epi_store_rows<false>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);

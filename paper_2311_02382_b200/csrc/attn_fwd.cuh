@@ -406,18 +406,31 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       tc_fence_after();
       uint32_t oo[ATT_D];
       tmem_ld64(tO[w] + lane_off, oo);
-      if (lrow < p.m) {
+      {
+        // stage the warp's 32 rows x 128 B in this query tile's (now idle) Q buffer,
+        // 16-byte chunks XOR-swizzled by row, then store whole 128-byte rows: 4 rows
+        // per instruction instead of 32 half-filled sectors
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(o_dst + (long)b * p.o_bstride + (long)lrow * E + h * ATT_D);
+        const uint32_t stg = smem_u32(sQ + w * ATT_TILE_BYTES) + quad * 32 * 128;
 #pragma unroll
-        for (int i = 0; i < ATT_D / 8; ++i) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(oo[8 * i + 0]) * inv, __uint_as_float(oo[8 * i + 1]) * inv);
-          v.y = pack_bf16(__uint_as_float(oo[8 * i + 2]) * inv, __uint_as_float(oo[8 * i + 3]) * inv);
-          v.z = pack_bf16(__uint_as_float(oo[8 * i + 4]) * inv, __uint_as_float(oo[8 * i + 5]) * inv);
-          v.w = pack_bf16(__uint_as_float(oo[8 * i + 6]) * inv, __uint_as_float(oo[8 * i + 7]) * inv);
-          dst[i] = v;
+        for (int i = 0; i < ATT_D / 8; ++i)
+          st_shared_v4(stg + lane * 128 + ((i ^ (lane & 7)) << 4),
+                       pack_bf16(__uint_as_float(oo[8 * i + 0]) * inv, __uint_as_float(oo[8 * i + 1]) * inv),
+                       pack_bf16(__uint_as_float(oo[8 * i + 2]) * inv, __uint_as_float(oo[8 * i + 3]) * inv),
+                       pack_bf16(__uint_as_float(oo[8 * i + 4]) * inv, __uint_as_float(oo[8 * i + 5]) * inv),
+                       pack_bf16(__uint_as_float(oo[8 * i + 6]) * inv, __uint_as_float(oo[8 * i + 7]) * inv));
+        __syncwarp();
+        const int row_w0 = q0 + w * ATT_BM + quad * 32;  // local row of the warp's first row
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rr = j * 4 + (int)lane / 8, q = (int)lane % 8;
+          const float4 val = ld_shared_f4(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
+          if (row_w0 + rr < p.m)
+            *reinterpret_cast<float4*>(o_dst + (long)b * p.o_bstride + (long)(row_w0 + rr) * E + h * ATT_D + q * 8) =
+                val;
         }
+      }
+      if (lrow < p.m) {
         lse_dst[((long)b * p.H + h) * p.lse_pitch + lrow] = l_run > 0.f ? m_run + __log2f(l_run) : -INFINITY;
       } else if (lrow < p.m_pad) {
         lse_dst[((long)b * p.H + h) * p.lse_pitch + lrow] = INFINITY;

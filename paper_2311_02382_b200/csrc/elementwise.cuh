@@ -38,6 +38,19 @@ LSS_DEV float block_sum(float v, float* red) {
   return warp_sum(t);
 }
 
+// two block-wide sums with one pair of barriers
+LSS_DEV float2 block_sum2(float a, float b, float2* red) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = make_float2(a, b);
+  __syncthreads();
+  const int nw = (blockDim.x + 31) / 32;
+  const float2 t = (l < nw) ? red[l] : make_float2(0.f, 0.f);
+  return make_float2(warp_sum(t.x), warp_sum(t.y));
+}
+
 // One block per row; each thread owns 4 consecutive features (E % 4 == 0, E <= 4*blockDim).
 template <typename TOut>
 __global__ void layernorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain,
@@ -74,31 +87,49 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ gxh, const float*
                                      const float* __restrict__ gain, const float* __restrict__ grad_res,
                                      float* __restrict__ gx, float* __restrict__ g_gain,
                                      float* __restrict__ g_bias, float alpha, long rows, int E) {
-  __shared__ float red[32];
+  __shared__ float2 red[32];
   const int c = threadIdx.x * 4;
   const bool ok = c < E;
   float4 gg = make_float4(0.f, 0.f, 0.f, 0.f), gb = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4 w = ok ? *reinterpret_cast<const float4*>(gain + c) : make_float4(0.f, 0.f, 0.f, 0.f);
   const long r0 = (long)blockIdx.x * LN_BWD_ROWS;
+  // software pipeline: the next row's operands are loaded before this row's reduction
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 gy_n = z4, xv_n = z4;
+  float mu_n = 0.f, rs_n = 0.f;
+  if (r0 < rows) {
+    mu_n = mean[r0];
+    rs_n = rstd[r0];
+    if (ok) {
+      gy_n = *reinterpret_cast<const float4*>(gxh + r0 * E + c);
+      xv_n = *reinterpret_cast<const float4*>(x + r0 * E + c);
+    }
+  }
   for (int i = 0; i < LN_BWD_ROWS; ++i) {
     const long row = r0 + i;
     if (row >= rows) break;
-    const float mu = mean[row], rs = rstd[row];
-    float4 gy = make_float4(0.f, 0.f, 0.f, 0.f), xv = gy;
-    if (ok) {
-      gy = *reinterpret_cast<const float4*>(gxh + row * E + c);
-      xv = *reinterpret_cast<const float4*>(x + row * E + c);
+    const float mu = mu_n, rs = rs_n;
+    const float4 gy = gy_n, xv = xv_n;
+    if (i + 1 < LN_BWD_ROWS && row + 1 < rows) {
+      mu_n = mean[row + 1];
+      rs_n = rstd[row + 1];
+      if (ok) {
+        gy_n = *reinterpret_cast<const float4*>(gxh + (row + 1) * E + c);
+        xv_n = *reinterpret_cast<const float4*>(x + (row + 1) * E + c);
+      }
     }
     const float xh0 = (xv.x - mu) * rs, xh1 = (xv.y - mu) * rs, xh2 = (xv.z - mu) * rs,
                 xh3 = (xv.w - mu) * rs;
     gg.x += gy.x * xh0; gg.y += gy.y * xh1; gg.z += gy.z * xh2; gg.w += gy.w * xh3;
     gb.x += gy.x; gb.y += gy.y; gb.z += gy.z; gb.w += gy.w;
     const float g0 = gy.x * w.x, g1 = gy.y * w.y, g2 = gy.z * w.z, g3 = gy.w * w.w;
-    const float mg = block_sum(ok ? g0 + g1 + g2 + g3 : 0.f, red) / E;
-    const float mgx = block_sum(ok ? g0 * xh0 + g1 * xh1 + g2 * xh2 + g3 * xh3 : 0.f, red) / E;
+    // the residual load is issued before the reduction's barriers so it overlaps them
+    const float4 res = (ok && grad_res) ? *reinterpret_cast<const float4*>(grad_res + row * E + c)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float2 sums = block_sum2(ok ? g0 + g1 + g2 + g3 : 0.f,
+                                   ok ? g0 * xh0 + g1 * xh1 + g2 * xh2 + g3 * xh3 : 0.f, red);
+    const float mg = sums.x / E, mgx = sums.y / E;
     if (ok) {
-      float4 res = grad_res ? *reinterpret_cast<const float4*>(grad_res + row * E + c)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
       *reinterpret_cast<float4*>(gx + row * E + c) =
           make_float4(res.x + rs * (g0 - mg - xh0 * mgx), res.y + rs * (g1 - mg - xh1 * mgx),
                       res.z + rs * (g2 - mg - xh2 * mgx), res.w + rs * (g3 - mg - xh3 * mgx));
@@ -141,7 +172,19 @@ __global__ void cat_cast_colsum_kernel(CatSrc src, TOut* __restrict__ dst, long 
   const long ld = src.ld[s];
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const long r0 = (long)blockIdx.y * CAT_ROWS;
-  for (int i = 0; i < CAT_ROWS; ++i) {
+  const bool full = r0 + CAT_ROWS <= rows && src.nslot[s] <= 1;
+  if (full) {  // common case: all row loads in flight together
+    float4 vv[CAT_ROWS];
+#pragma unroll
+    for (int i = 0; i < CAT_ROWS; ++i) vv[i] = *reinterpret_cast<const float4*>(sp + (r0 + i) * ld + lc);
+#pragma unroll
+    for (int i = 0; i < CAT_ROWS; ++i) {
+      const float4 v = vv[i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      if (dst) store4<TOut>(dst + (r0 + i) * ld_dst + col4, v.x, v.y, v.z, v.w);
+    }
+  }
+  for (int i = 0; i < (full ? 0 : CAT_ROWS); ++i) {
     const long r = r0 + i;
     if (r >= rows) break;
     float4 v;

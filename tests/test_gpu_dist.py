@@ -21,7 +21,8 @@ def _gpus():
 @pytest.mark.parametrize("case,world,fused", [("configA", 2, 1), ("batch2_g3", 3, 1), ("small_causal", 2, 1),
                                               ("small_noncausal", 4, 1), ("configA", 2, 0), ("small_causal", 4, 0),
                                               ("full_g2_causal", 2, 1), ("drop_layer_g2", 2, 1),
-                                              ("drop_layer_g2_big", 2, 1), ("configA", 4, 1)])
+                                              ("drop_layer_g2_big", 2, 1), ("configA", 4, 1),
+                                              ("drop_layer_g2_big", 4, 1)])
 def test_nccl_lss_layer_matches_reference(case, world, fused):
     """fused=1: dK|dV reduce-scatter fused into the backward over NVLink peer memory
     (lss_attn_bwd_p2p + barrier + slot sum); fused=0: the NCCL reduce-scatter."""

@@ -878,14 +878,20 @@ class LSSAttention:
             slot = self._slot
             issue(slot, x_host, grad_y_host)
         self._prefetched = None
-        if next_inputs is not None:  # overlap the next step's H2D with this step's compute
+        prefetch = None
+        if next_inputs is not None:  # overlap the next step's H2D with this step's backward
             nxt = 1 - slot
-            issue(nxt, *next_inputs)
+            # issued between the forward and the backward: the forward's copy-engine
+            # gather and hand-offs then never queue behind the host copy
+            prefetch = lambda: issue(nxt, *next_inputs)  # noqa: E731
             self._prefetched = (nxt, next_inputs[0], next_inputs[1])
         self._slot = 1 - slot
         cur.wait_event(self._in_ready[slot])
         x_d, gy_d = self._in_bufs[slot]
-        out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer, policy=policy)
+        if prefetch is not None and not _PREFETCH_AT_BWD:
+            prefetch()
+            prefetch = None
+        out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer, policy=policy, before_bwd=prefetch)
         self._in_free[slot].record(cur)
         if grads_host is not None:
             # read-back off the critical path: snapshot the averaged gradients on the
@@ -1056,7 +1062,8 @@ _CE_GATHER = os.environ.get("LSS_CE_GATHER", "1") != "0"  # K/V gather on the co
 _WGRAD_SIDE = os.environ.get("LSS_WGRAD_SIDE", "1") != "0"  # weight-gradient GEMMs on a side stream
 _FUSED_GATHER = os.environ.get("LSS_FUSED_GATHER", "1") != "0"  # attention waits per gathered segment
 _B1_IN_KERNEL = os.environ.get("LSS_B1_IN_KERNEL", "1") != "0"
-_FOLD_SLOTS = os.environ.get("LSS_FOLD_SLOTS", "1") != "0"  # fused RS owner sum inside the projection cast  # backward waits for the pushed dO in-kernel
+_FOLD_SLOTS = os.environ.get("LSS_FOLD_SLOTS", "1") != "0"
+_PREFETCH_AT_BWD = os.environ.get("LSS_PREFETCH_AT_BWD", "1") != "0"  # next step's H2D during the backward  # fused RS owner sum inside the projection cast  # backward waits for the pushed dO in-kernel
 last_phases: dict = {}
 
 

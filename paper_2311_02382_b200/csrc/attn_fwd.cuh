@@ -50,7 +50,10 @@ __device__ long long g_fwd_trace[8][1024];
   } while (0)
 #endif
 
-constexpr int ATT_FWD_HGROUP = 4;  // (batch, head) slices interleaved by the forward grid
+#ifndef LSS_FWD_HGROUP
+#define LSS_FWD_HGROUP 4
+#endif
+constexpr int ATT_FWD_HGROUP = LSS_FWD_HGROUP;  // (batch, head) slices interleaved by the forward grid
 
 constexpr int ATT_BM = 128;
 constexpr int ATT_BN = 128;

@@ -247,11 +247,14 @@ def main_ours(args):
 
     def timed(kind, fn):
         def wrapper(*a, **kw):
+            # on the stream the launch goes to (side streams at N > 1: fused gather,
+            # delegated rows); concurrent launches are summed, so the figure is conservative
+            st = torch.cuda.current_stream()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+            e0.record(st)
             out = fn(*a, **kw)
-            e1.record(stream)
+            e1.record(st)
             marks[kind].append((e0, e1))
             return out
         return wrapper

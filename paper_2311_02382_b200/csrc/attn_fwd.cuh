@@ -32,6 +32,9 @@
 #define LSS_FWD_SOFTMAX_REGS 232  // setmaxnreg budget: 128 x CTRL + 256 x SOFTMAX <= 64K
 #define LSS_FWD_CTRL_REGS 40
 #endif
+#ifndef LSS_FWD_EXP2_DEG
+#define LSS_FWD_EXP2_DEG 2  // degree of the FMA-pipe exp2 (A/B on B200: 5.79 ms vs 6.22 ms at degree 3)
+#endif
 #ifndef LSS_FWD_POLY8
 #define LSS_FWD_POLY8 3  // exponent pairs (of every 8) on the FMA-pipe polynomial; the rest on MUFU ex2
 #endif                   // (l=50112, 232-register softmax: 0 -> 7.15 ms, 2 -> 6.3, 3 -> 6.1-6.2, 4 -> 6.2)
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
             const float2 x = ffma2(make_float2(s[c], s[c + 1]), slv, nm);  // packed FFMA2
             float2 e;
             if (((c / 2) & 7) < LSS_FWD_POLY8) {  // FMA-pipe share (MUFU relief)
-              e = exp2_poly2(x);
+              e = exp2_poly2<LSS_FWD_EXP2_DEG>(x);
             } else {
               e = make_float2(ex2(x.x), ex2(x.y));
             }

@@ -341,17 +341,27 @@ LSS_DEV bool drop_keep(uint64_t row_key, uint64_t col, uint64_t thresh) {
 // x = j + f, |f| <= 1/2 via the 1.5*2^23 rounding trick, degree-3 minimax for
 // 2^f (max rel. error 1.0e-4, far below the bf16 rounding of P), exponent
 // added as an integer.  Offloads MUFU.EX2, the softmax's binding unit.
+// DEG 2: a quadratic (one FFMA2 less; 2.0e-3, half a bf16 ulp) for the forward,
+// where the FMA pipe is the co-bottleneck; DEG 3 for the backward.
+template <int DEG = 3>
 LSS_DEV float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -125.f);
   x.y = fmaxf(x.y, -125.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);
   const float2 t = fadd2(x, magic);            // round(x) in the low mantissa bits
   const float2 f = fsub2(x, fsub2(t, magic));  // x - round(x)
-  // minimax cubic for 2^f on [-1/2, 1/2] with p(0) = 1 pinned (2^n exact, so
-  // e.g. equal scores give exactly uniform rows); max relative error 1.0e-4
-  float2 pl = ffma2(make_float2(0.05500906f, 0.05500906f), f, make_float2(0.24221097f, 0.24221097f));
-  pl = ffma2(pl, f, make_float2(0.69328290f, 0.69328290f));
-  pl = ffma2(pl, f, make_float2(1.0f, 1.0f));
+  float2 pl;
+  if constexpr (DEG == 2) {
+    // minimax quadratic for 2^f on [-1/2, 1/2], p(0) = 1 pinned: max relative error 2.0e-3
+    pl = ffma2(make_float2(0.23986403f, 0.23986403f), f, make_float2(0.70294179f, 0.70294179f));
+    pl = ffma2(pl, f, make_float2(1.0f, 1.0f));
+  } else {
+    // minimax cubic for 2^f on [-1/2, 1/2] with p(0) = 1 pinned (2^n exact, so
+    // e.g. equal scores give exactly uniform rows); max relative error 1.0e-4
+    pl = ffma2(make_float2(0.05500906f, 0.05500906f), f, make_float2(0.24221097f, 0.24221097f));
+    pl = ffma2(pl, f, make_float2(0.69328290f, 0.69328290f));
+    pl = ffma2(pl, f, make_float2(1.0f, 1.0f));
+  }
   return make_float2(__uint_as_float(__float_as_uint(pl.x) + (__float_as_uint(t.x) << 23)),
                      __uint_as_float(__float_as_uint(pl.y) + (__float_as_uint(t.y) << 23)));
 }

@@ -32,6 +32,12 @@
 #define LSS_FWD_SOFTMAX_REGS 232  // setmaxnreg budget: 128 x CTRL + 256 x SOFTMAX <= 64K
 #define LSS_FWD_CTRL_REGS 40
 #endif
+#ifndef LSS_FWD_MAXTREE
+#define LSS_FWD_MAXTREE 1  // row max as independent chains (A/B builds: 0 = one serial chain)
+#endif
+#ifndef LSS_FWD_SUMCHAINS
+#define LSS_FWD_SUMCHAINS 1  // independent accumulators of the row sum (A/B builds)
+#endif
 #ifndef LSS_FWD_EXP2_DEG
 #define LSS_FWD_EXP2_DEG 2  // degree of the FMA-pipe exp2 (A/B on B200: 5.79 ms vs 6.22 ms at degree 3)
 #endif
@@ -339,9 +345,23 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
           for (int c = 0; c < ATT_BN; ++c)
             if (c >= valid_cols || (long)c > lim) s[c] = -INFINITY;
         }
+#if LSS_FWD_MAXTREE
+        // row max as 4 independent FMNMX3 chains (one serial chain was 64 dependent
+        // ALU ops per tile with only two softmax warps per SM sub-partition to hide them)
+        float mq[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          constexpr int Q = ATT_BN / 4;
+          mq[i] = fmaxf(s[Q * i], s[Q * i + 1]);
+#pragma unroll
+          for (int k = 2; k < Q; k += 2) mq[i] = fmaxf(mq[i], fmaxf(s[Q * i + k], s[Q * i + k + 1]));
+        }
+        const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+#else
         float mx = s[0];
 #pragma unroll
         for (int c = 1; c < ATT_BN; ++c) mx = fmaxf(mx, s[c]);
+#endif
         const float m_tile = mx * p.scale_log2;
         float alpha = 1.f;
         bool rescale = false;
@@ -352,7 +372,9 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
         uint32_t pk[ATT_BN / 2];
-        float2 sum2 = make_float2(0.f, 0.f);
+        float2 sum2[LSS_FWD_SUMCHAINS];
+#pragma unroll
+        for (int i = 0; i < LSS_FWD_SUMCHAINS; ++i) sum2[i] = make_float2(0.f, 0.f);
         uint64_t drop_row = 0;
         if (DROP) drop_row = drop_mix(drop_mix(drop_mix(p.drop_site, (uint64_t)b + 1), (uint64_t)h + 1), (uint64_t)qpos);
         {
@@ -366,7 +388,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
             } else {
               e = make_float2(ex2(x.x), ex2(x.y));
             }
-            sum2 = fadd2(sum2, e);  // the normaliser uses the undropped probabilities
+            sum2[(c / 2) % LSS_FWD_SUMCHAINS] = fadd2(sum2[(c / 2) % LSS_FWD_SUMCHAINS], e);  // undropped
             if (DROP) {
               e.x = drop_keep(drop_row, (uint64_t)(key0 + c), p.drop_thresh) ? e.x * p.drop_scale : 0.f;
               e.y = drop_keep(drop_row, (uint64_t)(key0 + c + 1), p.drop_thresh) ? e.y * p.drop_scale : 0.f;
@@ -374,7 +396,9 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
             pk[c / 2] = pack_bf16(e.x, e.y);
           }
         }
-        const float sum = sum2.x + sum2.y;
+#pragma unroll
+        for (int i = 1; i < LSS_FWD_SUMCHAINS; ++i) sum2[0] = fadd2(sum2[0], sum2[i]);
+        const float sum = sum2[0].x + sum2[0].y;
         l_run = l_run * alpha + sum;
         if (w == 0 && r == 0) FWD_TRACE(2, j);
         if (j > 0) {

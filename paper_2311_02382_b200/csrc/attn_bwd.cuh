@@ -31,9 +31,9 @@
 #include "attn_fwd.cuh"
 #include "common.cuh"
 
-#ifndef LSS_BWD_POLY
-#define LSS_BWD_POLY 1  // exponent pairs with (pair & LSS_BWD_POLY) == 0 use the FMA-pipe polynomial
-#endif                  // (7: 1 pair in 8, 3: 1 in 4, 1: 1 in 2, -1: none)
+#ifndef LSS_BWD_POLY8
+#define LSS_BWD_POLY8 3  // exponent pairs (of every 8) on the FMA-pipe polynomial (A/B ms: 3/8 14.77, 4/8 14.85, 5/8 15.13, 2/8 15.0, 8/8 16.4)
+#endif
 
 namespace lss {
 
@@ -165,7 +165,7 @@ LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv
     const float2 x = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2v,
                            make_float2(-lse[c], -lse[c + 1]));
     float2 e;
-    if (LSS_BWD_POLY >= 0 && !MASK && ((c / 2) & LSS_BWD_POLY) == 0) {  // MUFU/FMA balance
+    if (!MASK && ((c / 2) & 7) < LSS_BWD_POLY8) {  // MUFU/FMA balance
       e = exp2_poly2(x);
     } else {
       e = make_float2(ex2(x.x), ex2(x.y));

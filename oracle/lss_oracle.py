@@ -20,6 +20,7 @@ against those fixtures and against the reference's own known-answer tests
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -263,6 +264,135 @@ def lss_attention(x, grad_y, p: AttnParams, n_heads, workers, causal=True):
     grads = AttnParams(*[a / workers for a in grads_sum])  # all_reduce mean (sharded.py:238)
     return dict(y=np.concatenate(ys, axis=1), dx=np.concatenate(dxs, axis=1), grads=grads,
                 k_full=k_full, v_full=v_full)
+
+
+# --------------------------------------------------------------------------
+# Blocked evaluation for the north-star shapes (E=1024, 16 heads, l up to 50112;
+# SURVEY §8(c) "row-subset parity").  The reference materialises P per (b, h)
+# (model.py:307-325): 16 x 8192^2 fp64 = 8.6 GB at l=8192, 40 GB per rank at
+# l=50112.  The functions below evaluate exactly the same formulas one (sample,
+# head) and one block of query rows at a time, so only a block of P is ever alive.
+# Row-wise softmax makes row blocks independent; dK/dV are sums over query rows
+# (model.py:352, 358), accumulated block by block.
+# --------------------------------------------------------------------------
+
+
+def _head_task(qh, kh, vh, gh, q_pos, causal, scale, chunk, key_range, dt):
+    """One (sample, head): rows of qh at global positions q_pos against all keys."""
+    rows, t = qh.shape[0], kh.shape[0]
+    k0, k1 = key_range
+    ctx = np.empty((rows, vh.shape[1]), dt)
+    lse2 = np.empty(rows, np.float64)
+    dq = np.empty_like(ctx) if gh is not None else None
+    dk = np.zeros((k1 - k0, kh.shape[1]), dt) if gh is not None else None
+    dv = np.zeros((k1 - k0, vh.shape[1]), dt) if gh is not None else None
+    for r0 in range(0, rows, chunk):
+        r1 = min(rows, r0 + chunk)
+        pos = q_pos[r0:r1]
+        kend = int(min(t, pos.max() + 1)) if causal else t  # keys past the block's last row are all masked
+        if causal and pos.min() < 0:
+            raise OracleDegenerateRow("softmax row fully masked")  # tensor.py:123-126
+        s = (qh[r0:r1] @ kh[:kend].T) * dt(scale)  # model.py:311
+        if causal:
+            s = np.where(np.arange(kend)[None, :] <= pos[:, None], s, -np.inf)  # model.py:301-304
+        mx = s.max(axis=1, keepdims=True)  # tensor.py:115-117
+        p = np.exp(s - mx)
+        den = p.sum(axis=1, keepdims=True)
+        p /= den
+        lse2[r0:r1] = (mx[:, 0].astype(np.float64) + np.log(den[:, 0].astype(np.float64))) / math.log(2.0)
+        ctx[r0:r1] = p @ vh[:kend]  # model.py:320
+        if gh is None:
+            continue
+        g = gh[r0:r1]
+        dp = g @ vh[:kend].T  # model.py:346
+        ds = p * (dp - (dp * p).sum(axis=1, keepdims=True)) * dt(scale)  # model.py:353-356
+        dq[r0:r1] = ds @ kh[:kend]  # model.py:357
+        hi = min(k1, kend)
+        if hi > k0:
+            dk[:hi - k0] += ds[:, k0:hi].T @ qh[r0:r1]  # model.py:358
+            dv[:hi - k0] += p[:, k0:hi].T @ g  # model.py:349-352 (dropout 0)
+    return ctx, lse2, dq, dk, dv
+
+
+def attention_blocked(q, k, v, offset, n_heads, causal=True, grad_ctx=None, rows=None, key_range=None,
+                      chunk=512, dtype=np.float32, threads=None):
+    """scores_fwd + scores_bwd (model.py:280-359) block by block.
+
+    q (B, m, E) at global positions offset..offset+m; k/v (B, t, E) the whole
+    sequence; ``rows`` (optional index array) selects the query rows to evaluate;
+    ``grad_ctx`` (B, len(rows), E) adds the backward.  dK/dV are returned for the
+    key rows ``key_range`` = [k0, k1) only (default all) and contain the
+    contributions of the selected rows only.  Returns dict(ctx, lse2 (B, H, rows)
+    base-2 log-sum-exp, dq, dk, dv).  (Sample, head) pairs run on a thread pool
+    (numpy releases the GIL inside BLAS and the ufuncs)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    bsz, m, e = q.shape
+    t = k.shape[1]
+    d = e // n_heads
+    rows = np.arange(m) if rows is None else np.asarray(rows)
+    key_range = (0, t) if key_range is None else key_range
+    scale = 1.0 / math.sqrt(d)
+    dt = np.dtype(dtype).type
+    q_pos = offset + rows
+    tasks = []
+    for b in range(bsz):
+        for h in range(n_heads):
+            c = slice(h * d, (h + 1) * d)
+            gh = None if grad_ctx is None else np.ascontiguousarray(grad_ctx[b, :, c], dtype)
+            tasks.append((b, h, np.ascontiguousarray(q[b, rows, c], dtype), np.ascontiguousarray(k[b, :, c], dtype),
+                          np.ascontiguousarray(v[b, :, c], dtype), gh))
+    n_thr = threads or min(len(tasks), os.cpu_count() or 1)
+    with ThreadPoolExecutor(n_thr) as ex:
+        res = list(ex.map(lambda a: _head_task(a[2], a[3], a[4], a[5], q_pos, causal, scale, chunk, key_range, dt),
+                          tasks))
+    n_r, (k0, k1) = len(rows), key_range
+    out = dict(ctx=np.empty((bsz, n_r, e), dtype), lse2=np.empty((bsz, n_heads, n_r)))
+    if grad_ctx is not None:
+        out.update(dq=np.empty((bsz, n_r, e), dtype), dk=np.empty((bsz, k1 - k0, e), dtype),
+                   dv=np.empty((bsz, k1 - k0, e), dtype))
+    for (b, h, *_), (ctx, lse2, dq, dk, dv) in zip(tasks, res):
+        c = slice(h * d, (h + 1) * d)
+        out["ctx"][b, :, c] = ctx
+        out["lse2"][b, h] = lse2
+        if grad_ctx is not None:
+            out["dq"][b, :, c] = dq
+            out["dk"][b, :, c] = dk
+            out["dv"][b, :, c] = dv
+    return out
+
+
+def lss_attention_blocked(x, grad_y, p: AttnParams, n_heads, workers=1, causal=True, dtype=np.float32):
+    """:func:`lss_attention` for shapes whose P does not fit in host memory.
+
+    Identical arithmetic with the rank structure folded away: LN1 and the
+    projections are row-local, the gathered K/V is the rank-ordered
+    concatenation of every rank's own projection (= the projection of the whole
+    sequence), each rank's dK/dV partials are summed by the reduce-scatter
+    (= the dK/dV of all rows), and the sync averages the per-rank parameter
+    gradients (= the gradient of all rows / workers).  Returns the same keys as
+    :func:`lss_attention` plus the attention internals (q, k, v, ctx, lse2,
+    g_ctx, dq, dk, dv) for kernel-level checks."""
+    bsz, seq, e = x.shape
+    if seq % workers:
+        raise OracleShapeError(f"sequence length {seq} not divisible by {workers}")
+    c = lambda a: a.astype(dtype)  # noqa: E731
+    x, grad_y, p = c(x), c(grad_y), p.astype(dtype)
+    xh, ln = layernorm_fwd(x, p.ln1_gain, p.ln1_bias)
+    q, k, v = linear_fwd(xh, p.wq, p.bq), linear_fwd(xh, p.wk, p.bk), linear_fwd(xh, p.wv, p.bv)
+    fwd = attention_blocked(q, k, v, 0, n_heads, causal, dtype=dtype)
+    ctx = fwd["ctx"]
+    y = x + linear_fwd(ctx, p.wo, p.bo)
+    g_ctx, g_wo, g_bo = linear_bwd(ctx, p.wo, grad_y)
+    bwd = attention_blocked(q, k, v, 0, n_heads, causal, grad_ctx=g_ctx, dtype=dtype)
+    dq, dk, dv = bwd["dq"], bwd["dk"], bwd["dv"]
+    gxq, g_wq, g_bq = linear_bwd(xh, p.wq, dq)
+    gxk, g_wk, g_bk = linear_bwd(xh, p.wk, dk)
+    gxv, g_wv, g_bv = linear_bwd(xh, p.wv, dv)
+    gx_ln, g_g, g_b = layernorm_bwd(ln, p.ln1_gain, gxq + gxk + gxv)
+    grads = AttnParams(*[a / workers for a in (g_g, g_b, g_wq, g_bq, g_wk, g_bk, g_wv, g_bv, g_wo, g_bo)])
+    return dict(y=y, dx=grad_y + gx_ln, grads=grads, q=q, k=k, v=v, ctx=ctx, lse2=fwd["lse2"], g_ctx=g_ctx,
+                dq=dq, dk=dk, dv=dv)
 
 
 # --------------------------------------------------------------------------

@@ -58,3 +58,44 @@ def free_port():
     port = s.getsockname()[1]
     s.close()
     return port
+
+
+GOLDEN_DIR = Path(__file__).resolve().parent / "golden"
+
+
+def ns_inputs(seq, embed=1024, seed=0):
+    """Inputs of the north-star-shape fixtures (tests/golden/ns_inputs.py)."""
+    sys.path.insert(0, str(GOLDEN_DIR))
+    from ns_inputs import ns_inputs as gen
+
+    return gen(seq, embed, seed=seed)
+
+
+def check_ns_golden(z, y, dx, grads, tol, name=""):
+    """Compare a full result (y, dx (B, l, E); grads {reference name: array}) with an
+    NS fixture (tests/golden/make_golden.py ns_case): the stored row subsets in the
+    reference's |a-b| <= tol*max|b| + tol*|b| form, and the row-sum checksums (which
+    cover every element) normalised by the sum of absolute values they fold."""
+    sys.path.insert(0, str(GOLDEN_DIR))
+    from ns_inputs import ATTN_NAMES, ROW_STRIDE, WROW_STRIDE
+
+    y, dx = np.asarray(y, np.float64), np.asarray(dx, np.float64)
+    assert_close_ref(y[:, ::ROW_STRIDE], z["y_rows"], tol, f"{name} y rows")
+    assert_close_ref(dx[:, ::ROW_STRIDE], z["dx_rows"], tol, f"{name} dx rows")
+    for what, full, key in (("y", y, "y_rowsum"), ("dx", dx, "dx_rowsum")):
+        scale = np.abs(full).sum(-1).max()
+        err = np.abs(full.sum(-1) - z[key]).max() / scale
+        assert err < tol, f"{name} {what} row sums: {err:.3e}"
+    for nm in ATTN_NAMES:
+        g = np.asarray(grads[nm], np.float64)
+        if g.ndim == 1:
+            if nm == "bk":  # mathematically zero (softmax shift invariance): absolute check
+                assert np.abs(g).max() <= tol * np.abs(z["g_wk_rows"]).max(), f"{name} bk"
+                continue
+            assert_close_ref(g, z["g_" + nm], tol, f"{name} {nm}")
+            continue
+        assert_close_ref(g[::WROW_STRIDE], z["g_" + nm + "_rows"], tol, f"{name} {nm} rows")
+        for ax, key in ((1, "_rowsum"), (0, "_colsum")):
+            scale = np.abs(g).sum(ax).max()
+            err = np.abs(g.sum(ax) - z["g_" + nm + key]).max() / scale
+            assert err < tol, f"{name} {nm}{key}: {err:.3e}"

@@ -175,8 +175,91 @@ def gpt_case(seed=5, policy=None, name="gpt_small"):
     print(name, "written, loss", loss)
 
 
+NS_CASES = {
+    # north-star shape (BASELINE.json: E_m=1024, 16 heads) through the real reference,
+    # name: (seq_len, workers, causal); inputs from ns_inputs.ns_inputs(seq, 1024, seed=0)
+    "ns_l2048_g2": (2048, 2, True),
+    "ns_l2048_g8": (2048, 8, True),
+    "ns_l2048_g4_noncausal": (2048, 4, False),
+}
+
+
+def ns_case(name, seq, g, causal):
+    """The reference's layer_fwd / layer_bwd at E=1024, 16 heads on G simulated workers
+    (fused kv hooks, sharded.py:138-143 / 186-190; sync sharded.py:238), fp64.  The
+    inputs are rebuilt from the seed by the tests, so only outputs are stored: every
+    row sum of y / dx and of each weight gradient (checksums covering every element),
+    every ROW_STRIDE-th row of y / dx, every WROW_STRIDE-th row of each weight
+    gradient, the LN / bias gradients in full."""
+    from ns_inputs import ATTN_NAMES, ROW_STRIDE, WROW_STRIDE, ns_inputs
+
+    e, h = 1024, 16
+    x32, gy32, p32 = ns_inputs(seq, e, seed=0)
+    cfg = ModelConfig(embed_dim=e, n_layers=1, n_heads=h, ff_dim=8, vocab=16, seq_len=seq, batch=1,
+                      causal=causal, precision="double")
+    lp = model.init_params(cfg, 0).layers[0]
+    d = {k: v.astype(np.float64) for k, v in p32.items()}
+    lp.ln1_gain, lp.ln1_bias = d["ln1_gain"], d["ln1_bias"]
+    lp.attn_q, lp.attn_k = LinearParams(d["wq"], d["bq"]), LinearParams(d["wk"], d["bk"])
+    lp.attn_v, lp.attn_out = LinearParams(d["wv"], d["bv"]), LinearParams(d["wo"], d["bo"])
+    lp.ff_in = LinearParams(np.zeros_like(lp.ff_in.weight), np.zeros_like(lp.ff_in.bias))
+    lp.ff_out = LinearParams(np.zeros_like(lp.ff_out.weight), np.zeros_like(lp.ff_out.bias))
+    x, gy = x32.astype(np.float64), gy32.astype(np.float64)
+    comm = Communicator(g, timeout=600.0)
+    group = comm.group("sequence", tuple(range(g)))
+    off = DropoutPolicy.off()
+
+    def worker(rank):
+        spec = ShardSpec(rank, g, seq)
+        xs = np.ascontiguousarray(x[:, spec.offset:spec.offset + spec.block])
+        gys = np.ascontiguousarray(gy[:, spec.offset:spec.offset + spec.block])
+
+        def kv_fwd(xh, lp_):  # sharded.py:139-143
+            xh_full = comm.all_gather(group, rank, xh, dim=1, step=0, phase="forward", layer=0)
+            return model.linear3(xh_full, lp_.attn_k), model.linear3(xh_full, lp_.attn_v), xh_full
+
+        def kv_bwd(kv_ctx, lp_, gk, gv):  # sharded.py:186-191
+            grad_full, k_wg, k_bg, v_wg, v_bg = model.local_kv_bwd(kv_ctx, lp_, gk, gv)
+            seg = comm.reduce_scatter(group, rank, grad_full, dim=1, step=0, phase="backward", layer=0)
+            return seg, k_wg, k_bg, v_wg, v_bg
+
+        y, cache = model.layer_fwd(lp, cfg, off, 0, xs, spec.offset, kv_fwd)
+        dx, grads = model.layer_bwd(lp, cfg, off, 0, cache, gys, kv_bwd)
+        flat = [grads.ln1_gain, grads.ln1_bias, grads.attn_q.weight, grads.attn_q.bias,
+                grads.attn_k.weight, grads.attn_k.bias, grads.attn_v.weight, grads.attn_v.bias,
+                grads.attn_out.weight, grads.attn_out.bias]
+        vec = comm.all_reduce_mean(group, rank, np.concatenate([a.ravel() for a in flat]), step=0,
+                                   phase="sync")  # sharded.py:238
+        return y, dx, vec, [a.shape for a in flat]
+
+    res = run_workers(g, worker, comm=comm)
+    y = np.concatenate([r[0] for r in res], axis=1)
+    dx = np.concatenate([r[1] for r in res], axis=1)
+    vec, shapes = res[0][2], res[0][3]
+    arrays = dict(meta=np.array([seq, e, h, g, 1, int(causal)], dtype=np.int64),
+                  y_rows=y[:, ::ROW_STRIDE].astype(np.float32), dx_rows=dx[:, ::ROW_STRIDE].astype(np.float32),
+                  y_rowsum=y.sum(-1), dx_rowsum=dx.sum(-1))
+    pos = 0
+    for nm, shp in zip(ATTN_NAMES, shapes):
+        n = int(np.prod(shp))
+        gr = vec[pos:pos + n].reshape(shp)
+        pos += n
+        if gr.ndim == 2:
+            arrays["g_" + nm + "_rows"] = gr[::WROW_STRIDE].astype(np.float32)
+            arrays["g_" + nm + "_rowsum"] = gr.sum(1)
+            arrays["g_" + nm + "_colsum"] = gr.sum(0)
+        else:
+            arrays["g_" + nm] = gr
+    np.savez_compressed(OUT / f"{name}.npz", **arrays)
+    print(name, "written", {k: v.shape for k, v in arrays.items() if k in ("y_rows", "g_wq_rows")})
+
+
 def main(only=None):
     keep = (lambda n: True) if not only else (lambda n: n in only)  # noqa: E731
+    sys.path.insert(0, str(OUT))
+    for name, (seq, g, causal) in NS_CASES.items():
+        if keep(name):
+            ns_case(name, seq, g, causal)
     for name, (seq, e, h, g, b, causal, odt) in CASES.items():
         if not keep(name):
             continue

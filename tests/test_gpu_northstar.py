@@ -1,0 +1,202 @@
+"""Parity at the north-star shapes (BASELINE.json: E_m=1024, 16 heads, d=64).
+
+The kernels are compared with the CPU oracle -- pinned to the REAL reference at
+this E/H by tests/test_oracle.py::test_blocked_oracle_matches_reference_at_north_star_shape
+-- at the configurations the metric is quoted on:
+
+* l=2048, G=2 / 8 (+ non-causal G=4): the engine against golden fixtures
+  produced by the real reference (tests/golden/make_golden.py ns_case);
+* l=8192 (config B1), G=1 and G=8: every output (y, dx, all parameter
+  gradients) and every attention internal (ctx, lse, dQ, dK, dV) against the
+  blocked oracle evaluated on the same inputs;
+* l=50112, G=8, m=6264 (config C, ragged against the 128-row tile, balanced
+  causal schedule, fused 8-slot reduce-scatter): row-subset parity -- y for
+  query blocks at the start, across the rank-3/4 boundary and at the end; dx
+  for the last block and for the last block of segment 6 (whose dK/dV the fused
+  reduce-scatter sums from two ranks); the kernels' ctx / lse / dQ on the same
+  blocks from the GPU's own Q, K, V, dO.
+
+Tolerances (written in each assert): bf16 operands with fp32 accumulation
+<= 1e-2 normalised (north star), fp32 check mode ("single") <= 1e-4.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR, assert_close_ref, check_ns_golden, nerr, ns_inputs
+from oracle import lss_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": 1e-2, "single": 1e-4}
+E, H = 1024, 16
+NAMES = O.AttnParams.GRAD_ORDER
+REF_NAMES = {"ln1_gain": "ln1_gain", "ln1_bias": "ln1_bias", "wq": "attn_q.weight", "bq": "attn_q.bias",
+             "wk": "attn_k.weight", "bk": "attn_k.bias", "wv": "attn_v.weight", "bv": "attn_v.bias",
+             "wo": "attn_out.weight", "bo": "attn_out.bias"}
+
+
+def _run(x, gy, p, G, precision, dev, causal=True):
+    """G engines of one sequence group on one GPU (SimComm), one fwd+bwd+sync step."""
+    import torch
+    from paper_2311_02382_b200.model import ModelConfig, layer_params_from_arrays
+    from paper_2311_02382_b200.sharded import ShardSpec, lss_step, make_sim_group, slice_batch
+
+    seq = x.shape[1]
+    cfg = ModelConfig(embed_dim=E, n_layers=1, n_heads=H, ff_dim=4 * E, vocab=256, seq_len=seq, batch=1,
+                      causal=causal, precision=precision)
+    lp = layer_params_from_arrays(*[p[n] for n in NAMES], device=dev)
+    engines, comm = make_sim_group(cfg, lp, G, device=dev)
+    tx, tg = torch.as_tensor(x, device=dev), torch.as_tensor(gy, device=dev)
+    out = lss_step(engines, comm, [slice_batch(tx, ShardSpec(r, G, seq)) for r in range(G)],
+                   [slice_batch(tg, ShardSpec(r, G, seq)) for r in range(G)])
+    torch.cuda.synchronize()
+    y = torch.cat([o[0] for o in out], 1).cpu().numpy()
+    dx = torch.cat([o[1] for o in out], 1).cpu().numpy()
+    grads = {n: engines[0].grad_views()[REF_NAMES[n]].cpu().numpy() for n in NAMES}
+    return engines, y, dx, grads
+
+
+def _np(t):
+    import torch
+
+    return t.detach().to(torch.float32).cpu().numpy()
+
+
+# ------------------------------------------------------------ l=2048 vs the real reference
+
+
+@pytest.mark.parametrize("name", ["ns_l2048_g2", "ns_l2048_g8", "ns_l2048_g4_noncausal"])
+@pytest.mark.parametrize("precision", ["bf16", "single"])
+def test_engine_matches_reference_goldens_at_north_star_width(cuda, name, precision):
+    z = np.load(GOLDEN_DIR / f"{name}.npz")
+    seq, e, h, g, b, causal = (int(v) for v in z["meta"])
+    x, gy, p = ns_inputs(seq, e)
+    engines, y, dx, grads = _run(x, gy, p, g, precision, cuda, bool(causal))
+    if precision == "bf16" and causal and g > 1:
+        assert any(e.plan.active for e in engines)  # the balanced schedule is what ran
+    check_ns_golden(z, y, dx, grads, TOL[precision], f"{name}/{precision}")
+
+
+# ------------------------------------------------------------ l=8192 (config B1), full tensors
+
+
+@pytest.fixture(scope="module")
+def oracle_8192():
+    x, gy, p = ns_inputs(8192, E, seed=1)
+    pp = O.AttnParams(*[p[n] for n in NAMES])
+    return x, gy, p, O.lss_attention_blocked(x, gy, pp, H, 1, True, dtype=np.float32)
+
+
+def _check_full(ref, y, dx, grads, tol, G, tag):
+    assert_close_ref(y, ref["y"], tol, f"{tag} y")
+    assert_close_ref(dx, ref["dx"], tol, f"{tag} dx")
+    for n in NAMES:
+        want = getattr(ref["grads"], n) / G  # sync = mean over the G ranks (sharded.py:238)
+        if n == "bk":  # mathematically zero: absolute check against the K weight gradient
+            assert np.abs(grads[n]).max() <= tol * np.abs(getattr(ref["grads"], "wk")).max() / G
+            continue
+        assert_close_ref(grads[n], want, tol, f"{tag} {n}")
+
+
+@pytest.mark.parametrize("precision", ["bf16", "single"])
+def test_l8192_single_rank_vs_oracle(cuda, oracle_8192, precision):
+    """Config B1 (single GPU, l=8192): outputs, gradients and the attention kernels'
+    ctx / lse / dQ / dK / dV over the whole sequence against the oracle."""
+    x, gy, p, ref = oracle_8192
+    tol = TOL[precision]
+    engines, y, dx, grads = _run(x, gy, p, 1, precision, cuda)
+    _check_full(ref, y, dx, grads, tol, 1, f"l8192/G1/{precision}")
+    e0 = engines[0]
+    assert nerr(_np(e0.ctx), ref["ctx"]) < tol
+    lse = _np(e0.lse2)[:, :, :8192]
+    assert np.abs(lse - ref["lse2"]).max() < (2e-2 if precision == "bf16" else 1e-4)
+    assert nerr(_np(e0.dq), ref["dq"]) < 2 * tol
+    dkv = _np(e0.dkv_own)  # [B][m][dK | dV] = the reduce-scatter output
+    assert nerr(dkv[..., :E], ref["dk"]) < 2 * tol
+    assert nerr(dkv[..., E:], ref["dv"]) < 2 * tol
+
+
+def test_l8192_eight_ranks_vs_oracle(cuda, oracle_8192):
+    """l=8192 on 8 ranks (m=1024): balanced causal schedule, fused 8-slot dK|dV
+    reduce-scatter with the owner sum in the projection cast: full dK/dV parity
+    (every key row, summed over the ranks that attend it) through dx and dW."""
+    x, gy, p, ref = oracle_8192
+    engines, y, dx, grads = _run(x, gy, p, 8, "bf16", cuda)
+    assert all(e.seg_dst is not None for e in engines) and sum(e.plan.active for e in engines) == 8
+    _check_full(ref, y, dx, grads, TOL["bf16"], 8, "l8192/G8")
+    dq = np.concatenate([_np(e.dq) for e in engines], 1)
+    assert nerr(dq, ref["dq"]) < 2e-2
+    dkv = np.concatenate([_np(e.dqkv)[..., E:] for e in engines], 1)  # [dK|dV] own rows (bf16 cast)
+    assert nerr(dkv[..., :E], ref["dk"]) < 2e-2
+    assert nerr(dkv[..., E:], ref["dv"]) < 2e-2
+
+
+# ------------------------------------------------------------ l=50112, G=8 (config C): row subsets
+
+
+L_C, G_C = 50112, 8
+M_C = L_C // G_C  # 6264 = 48*128 + 120
+ROW_BLOCKS = [(0, 128), (4 * M_C - 64, 4 * M_C + 64), (L_C - 128, L_C)]  # start, rank-3/4 boundary, end
+DX_BLOCKS = [(7 * M_C - 128, 7 * M_C), (L_C - 128, L_C)]  # last block of segment 6 (2 writers), end
+
+
+@pytest.fixture(scope="module")
+def run_c(cuda):
+    x, gy, p = ns_inputs(L_C, E, seed=2)
+    engines, y, dx, grads = _run(x, gy, p, G_C, "bf16", cuda)
+    assert all(e.m == M_C for e in engines) and all(e.seg_dst is not None for e in engines)
+    assert [e.plan.role for e in engines].count("heavy") == 4
+    return x, gy, p, engines, y, dx
+
+
+def test_l50112_row_subsets_vs_oracle(run_c):
+    """End-to-end row subsets at the target shape: the oracle runs from x / grad_y
+    and the fp32 weights (LN1, the K/V projection of all 50112 rows, attention of
+    the selected query rows against the whole sequence) -- no GPU intermediate."""
+    x, gy, p, engines, y, dx = run_c
+    f = {n: p[n] for n in NAMES}
+    xh, ln = O.layernorm_fwd(x, f["ln1_gain"], f["ln1_bias"])
+    q = O.linear_fwd(xh, f["wq"], f["bq"])
+    k = O.linear_fwd(xh, f["wk"], f["bk"])
+    v = O.linear_fwd(xh, f["wv"], f["bv"])
+    tol = TOL["bf16"]
+    for lo, hi in ROW_BLOCKS:  # y = x + ctx Wo + bo (model.py:445-448)
+        rows = np.arange(lo, hi)
+        o = O.attention_blocked(q, k, v, 0, H, True, rows=rows)
+        want = x[:, lo:hi] + O.linear_fwd(o["ctx"], f["wo"], f["bo"])
+        assert_close_ref(y[:, lo:hi], want, tol, f"y rows [{lo},{hi})")
+    for lo, hi in DX_BLOCKS:  # dx of rows whose keys only rows >= lo attend (causal)
+        rows = np.arange(lo, L_C)
+        g_ctx = gy[:, lo:] @ f["wo"].T
+        o = O.attention_blocked(q, k, v, 0, H, True, grad_ctx=g_ctx, rows=rows, key_range=(lo, hi))
+        n = hi - lo
+        g_xh = o["dq"][:, :n] @ f["wq"].T + o["dk"] @ f["wk"].T + o["dv"] @ f["wv"].T
+        cache = (ln[0][:, lo:hi], ln[1][:, lo:hi])
+        gx, _, _ = O.layernorm_bwd(cache, f["ln1_gain"], g_xh)
+        assert_close_ref(dx[:, lo:hi], gy[:, lo:hi] + gx, tol, f"dx rows [{lo},{hi})")
+
+
+def test_l50112_attention_kernels_on_row_subsets(run_c):
+    """Kernel-level at the target shape: ctx, lse and dQ of the selected query rows
+    (ragged last tile, global offsets r*6264, delegated rows of the balanced
+    schedule merged by lse) from the GPU's own Q, gathered K|V and dO, and dK / dV
+    of the key blocks of DX_BLOCKS (after the fused reduce-scatter)."""
+    x, gy, p, engines, y, dx = run_c
+    kv = _np(engines[G_C - 1].kv_full)  # [G][B][m][2E], every segment after the gather
+    k = kv[..., :E].transpose(1, 0, 2, 3).reshape(1, L_C, E)
+    v = kv[..., E:].transpose(1, 0, 2, 3).reshape(1, L_C, E)
+    cat = lambda name: np.concatenate([_np(getattr(e, name)) for e in engines], 1)  # noqa: E731
+    q, ctx, dctx, dq, dqkv = cat("q"), cat("ctx"), cat("dctx"), cat("dq"), cat("dqkv")
+    lse = np.concatenate([_np(e.lse2)[:, :, :M_C] for e in engines], 2)
+    for lo, hi in ROW_BLOCKS:
+        rows = np.arange(lo, hi)
+        o = O.attention_blocked(q, k, v, 0, H, True, grad_ctx=dctx[:, lo:hi], rows=rows)
+        assert nerr(ctx[:, lo:hi], o["ctx"]) < 1e-2, (lo, hi)
+        assert np.abs(lse[:, :, lo:hi] - o["lse2"]).max() < 2e-2, (lo, hi)
+        assert nerr(dq[:, lo:hi], o["dq"]) < 2e-2, (lo, hi)
+    for lo, hi in DX_BLOCKS:
+        rows = np.arange(lo, L_C)
+        o = O.attention_blocked(q, k, v, 0, H, True, grad_ctx=dctx[:, lo:], rows=rows, key_range=(lo, hi))
+        assert nerr(dqkv[:, lo:hi, E:2 * E], o["dk"]) < 2e-2, (lo, hi)
+        assert nerr(dqkv[:, lo:hi, 2 * E:], o["dv"]) < 2e-2, (lo, hi)

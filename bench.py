@@ -21,6 +21,7 @@ is larger than the 126 MB L2, so no explicit flush is needed.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -147,6 +148,33 @@ class ClockSampler:
 # ------------------------------------------------------------------ reference / CPU arm
 
 
+def host_info():
+    """CPU model, numpy and BLAS of the host the CPU legs ran on."""
+    import platform
+
+    import numpy as np
+
+    model = platform.processor() or "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        b = np.show_config(mode="dicts")["Build Dependencies"]["blas"]
+        blas = f"{b.get('name')} {b.get('version')}"
+    except Exception:  # noqa: BLE001 - informational only
+        pass
+    return {"cpu_model": model, "host_cpus": os.cpu_count(), "numpy": np.__version__, "blas": blas,
+            "reference_precision": "fp32 numpy port of the reference's functions (the reference's own 'single' "
+                                   "path promotes scores to fp64 under NumPy 2, SURVEY §0.7)"}
+
+
+
 def cpu_sample(args, rows, threads):
     """Time the oracle port of the reference's attention sublayer on a bounded
     sample: `rows` query rows centred on l/2 (the mean causal row) against the
@@ -189,7 +217,7 @@ def run_reference(args):
         "config": {"workload": workload(args), "global_batch": args.batch, "seq_len": args.seq,
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": desc},
+                         "sample": desc, **host_info()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -206,7 +234,7 @@ def main_ours(args):
     from paper_2311_02382_b200 import _native
     from paper_2311_02382_b200.comm import Ledger, SoloComm, TorchDistComm
     from paper_2311_02382_b200.model import LayerParams, LinearParams, ModelConfig
-    from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec
+    from paper_2311_02382_b200.sharded import EngineOptions, LSSAttention, ShardSpec
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -235,18 +263,27 @@ def main_ours(args):
     gx = torch.Generator(device=dev).manual_seed(100 + rank)
     x = torch.randn(B, m, E, generator=gx, device=dev)
     gy = torch.randn(B, m, E, generator=gx, device=dev)
-    eng = LSSAttention(cfg, spec, grad_scale=1.0 / world, device=dev, balanced=not args.unbalanced)
+    # execution options: the production defaults, overridable for A/B runs by LSS_* variables read HERE
+    # (explicitly; the package itself never reads the environment)
+    opts = EngineOptions.from_env()
+    if args.unbalanced:
+        opts = dataclasses.replace(opts, balanced=False)
+    eng = LSSAttention(cfg, spec, grad_scale=1.0 / world, device=dev, options=opts)
 
     # per-kernel CUDA-event timing of the two attention kernels inside the timed region
     stream = torch.cuda.current_stream()
     marks = {"fwd": [], "bwd": []}
     from paper_2311_02382_b200 import kernels as Kmod
 
-    wrapped = {"attn_fwd": "fwd", "attn_fwd_partial": "fwd", "attn_bwd": "bwd", "attn_bwd_sources": "bwd"}
+    wrapped = {"attn_fwd": "fwd", "attn_fwd_partial": "fwd", "attn_bwd": "bwd", "attn_bwd_sources": "bwd",
+               "gemm": "qkv"}
+    marks["qkv"] = []
     originals = {name: getattr(Kmod, name) for name in wrapped}
 
     def timed(kind, fn):
         def wrapper(*a, **kw):
+            if kind == "qkv" and not (kw.get("N") == 3 * E and kw.get("K") == E and kw.get("M") == B * m):
+                return fn(*a, **kw)  # only the [Q|K|V] projection GEMM is timed
             # on the stream the launch goes to (side streams at N > 1: fused gather,
             # delegated rows); concurrent launches are summed, so the figure is conservative
             st = torch.cuda.current_stream()
@@ -291,13 +328,13 @@ def main_ours(args):
     for name in wrapped:
         setattr(Kmod, name, originals[name])
     launches = (_native.launch_count - launches0) // args.steps
-    if os.environ.get("LSS_PHASES") in ("1", "2"):  # diagnostic: one extra step with a per-phase timeline
-        from paper_2311_02382_b200 import sharded as _sh
+    if opts.phases in (1, 2):  # diagnostic: one extra step with a per-phase timeline
+        from paper_2311_02382_b200 import engine as _sh
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         one_step()
-        if os.environ.get("LSS_PHASES") == "2":  # steady state: back-to-back steps, stamps of the last
+        if opts.phases == 2:  # steady state: back-to-back steps, stamps of the last
             for _ in range(4):
                 one_step()
             _sh.last_phases = _sh.last_clock.report()
@@ -312,7 +349,7 @@ def main_ours(args):
                     print(f"[timeline] {name:16s} " + " ".join(f"{(st[i][1] - st[ai][1]) / 1e3:9.1f}"
                                                           for st in allst), file=sys.stderr, flush=True)
         torch.cuda.synchronize()
-        _sh._PHASES = False  # the phase clock synchronises; measure the plain step
+        eng.options = dataclasses.replace(eng.options, phases=0)  # the phase clock synchronises
         h0 = time.perf_counter()
         for _ in range(3):
             one_step()
@@ -327,8 +364,9 @@ def main_ours(args):
     # per-step device time of this rank's attention kernels (all launches of the step)
     fwd_ms = sum(a.elapsed_time(b) for a, b in marks["fwd"]) / args.steps
     bwd_ms = sum(a.elapsed_time(b) for a, b in marks["bwd"]) / args.steps
+    qkv_ms = sum(a.elapsed_time(b) for a, b in marks["qkv"]) / max(1, len(marks["qkv"]))
     my_pairs = eng.computed_pairs() * B
-    stats = torch.tensor([ms, fwd_ms, bwd_ms, float(my_pairs)], dtype=torch.float64, device=dev)
+    stats = torch.tensor([ms, fwd_ms, bwd_ms, float(my_pairs), qkv_ms], dtype=torch.float64, device=dev)
     if world > 1:
         allst = [torch.zeros_like(stats) for _ in range(world)]
         dist.all_gather(allst, stats)
@@ -340,21 +378,35 @@ def main_ours(args):
     tokens = B * l
     value = tokens / (ms_max / 1e3)
     burst, sustained, src = peaks()
+    # the burst peak applies while the SMs run at their maximum clock; a power-capped run
+    # whose loaded clock sits well below it is held to the sustained figure
+    at_max = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and clocks["sm_mhz"] >= 0.95 * clocks["sm_max_mhz"])
+    peak, peak_name = (burst, "bf16_tflops (burst)") if at_max else (sustained, "bf16_tflops_sustained")
     total_flops = layer_flops(B, l, E, causal)
     pct = {"burst": total_flops / (ms_max / 1e3) / (world * burst * 1e12),
            "sustained": total_flops / (ms_max / 1e3) / (world * sustained * 1e12)}
     bwd_flops = 8 * E * crit[3]
     fwd_flops = 4 * E * crit[3]
+    qkv_flops = 2 * (B * m) * (3 * E) * E
     ach_bwd = bwd_flops / (crit[2] / 1e3) / 1e12
     ach_fwd = fwd_flops / (crit[1] / 1e3) / 1e12
-    roofline = {"kernel": "attn_bwd_tc_kernel (+ delta pre-pass)", "bound": "tensor",
-                "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s", "frac": ach_bwd / sustained,
-                "frac_of_burst": ach_bwd / burst, "peak_source": f"{src} bf16_tflops_sustained",
-                "traffic": traffic_from_profile("attn_bwd_tc_kernel"),
-                "algorithmic": f"8*E per unmasked (q,k) pair; {crit[3]:.4g} pairs on the critical rank",
-                "ms_per_step": crit[2], "balanced_schedule": eng.plan.role != "none" or world == 1,
-                "fwd": {"kernel": "attn_fwd_tc_kernel", "achieved": ach_fwd, "frac": ach_fwd / sustained,
-                        "ms_per_step": crit[1], "traffic": traffic_from_profile("attn_fwd_tc_kernel")}}
+    ach_qkv = qkv_flops / (crit[4] / 1e3) / 1e12 if crit[4] > 0 else None
+
+    def entry(kernel, ach, ms_k, work, traffic_key):
+        return {"kernel": kernel, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak if ach else None, "frac_of_burst": ach / burst if ach else None,
+                "frac_of_sustained": ach / sustained if ach else None, "ms_per_step": ms_k, "algorithmic": work,
+                "traffic": traffic_from_profile(traffic_key), "traffic_source": "profiles/ncu_summary.json "
+                "(dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture)"}
+
+    roofline = entry("attn_bwd_tc_kernel (+ delta pre-pass)", ach_bwd, crit[2],
+                     f"8*E per unmasked (q,k) pair; {crit[3]:.4g} pairs on the critical rank", "attn_bwd_tc_kernel")
+    roofline.update(peak_source=f"{src} {peak_name} (loaded SM clock {clocks.get('sm_mhz')} of "
+                                f"{clocks.get('sm_max_mhz')} MHz)",
+                    balanced_schedule=eng.plan.role != "none" or world == 1,
+                    fwd=entry("attn_fwd_tc_kernel", ach_fwd, crit[1], "4*E per unmasked (q,k) pair", "attn_fwd_tc_kernel"),
+                    qkv_gemm=entry("gemm_bf16_tc_kernel<0,0> ([Q|K|V] projection)", ach_qkv, crit[4],
+                                   f"2*M*N*K, M={B * m}, N={3 * E}, K={E} per launch", "gemm_qkv"))
 
     # ---------------- end-to-end through the public API with pinned host buffers
     e2e = None
@@ -399,7 +451,7 @@ def main_ours(args):
             if dt >= 10.0 or reps >= 50:
                 break
         cpu = {"value": B * args.cpu_rows * reps / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
-               "sample": f"{reps} x " + desc, "seconds": dt}
+               "sample": f"{reps} x " + desc, "seconds": dt, **host_info()}
 
     if rank == 0:
         line = {

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 8
+#define LSS_ABI_VERSION 9
 
 enum lss_status {
   LSS_OK = 0,
@@ -315,8 +315,33 @@ int lss_ipc_close(void* dev_ptr, long offset);
  * peer's memory imported with lss_ipc_import: the K/V gather pulls each peer's
  * [K_p|V_p] slot this way (replaces collectives.all_gather, collectives.py:325-344). */
 int lss_copy_d2d(void* dst, const void* src, long bytes, void* stream);
-/* 1 if `device` can load/store `peer`'s memory directly (NVLink / PCIe P2P). */
+/* 1 if `device` can load/store `peer`'s memory directly (NVLink / PCIe P2P, or the
+ * same device in another process). */
 int lss_peer_access(int device, int peer);
+
+/* ---- failure semantics (ABI v9)
+ *
+ * The reference's communicator never hangs: a rendezvous past its timeout raises
+ * CommTimeout and aborts the group (collectives.py:200-253, errors.py:24-29); every
+ * matmul / softmax output is checked for NaN / Inf -> NumericsError
+ * (tensor.py:79-95, 118, 131).  On B200:
+ *  - lss_runtime_config sets, on the caller's current device, the deadline of every
+ *    in-kernel cross-GPU wait (fused gather segment flags, pushed backward sources;
+ *    0 = unbounded) and the opt-in NaN / Inf check in the epilogues of the GEMM and
+ *    attention kernels (0 off, 1 on).  A wait past its deadline gives up and raises
+ *    status word 0; a non-finite output raises word 1.
+ *  - lss_status copies the two process-wide status words into out[2] (mapped pinned
+ *    host memory: no device synchronisation) and optionally clears them.
+ *  - lss_check_finite raises word 1 if any of n fp32 / bf16 elements is NaN / Inf
+ *    (n a multiple of 4 / 8, 16-byte aligned): the check for outputs of the other
+ *    kernels (LayerNorm, fp32 check mode).
+ *  - lss_flag_release writes `value` to `count` flag words from a private
+ *    non-blocking stream: a host watchdog releases stream waits (lss_stream_wait)
+ *    whose peer is dead, so the caller's streams drain and the host raises CommTimeout. */
+int lss_runtime_config(unsigned long long wait_timeout_ns, int numerics_check);
+int lss_status(unsigned int* out, int clear);
+int lss_check_finite(const void* x, long n, int dtype, void* stream);
+int lss_flag_release(unsigned int* flags, long count, unsigned int value);
 
 #ifdef __cplusplus
 }

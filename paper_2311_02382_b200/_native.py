@@ -109,6 +109,10 @@ SIGNATURES = {
     "lss_ipc_import": [ctypes.c_char_p, _L, ctypes.POINTER(_P)],
     "lss_ipc_close": [_P, _L],
     "lss_copy_d2d": [_P, _P, _L, _P],
+    "lss_runtime_config": [ctypes.c_ulonglong, _I],
+    "lss_status": [ctypes.POINTER(ctypes.c_uint), _I],
+    "lss_check_finite": [_P, _L, _I, _P],
+    "lss_flag_release": [_P, _L, ctypes.c_uint],
 }
 ACT_NONE, ACT_GELU, ACT_GELU_BWD = 0, 1, 2
 EXTRA = {
@@ -117,7 +121,7 @@ EXTRA = {
     "lss_rows_pad": ([_L], _L),
     "lss_peer_access": ([_I, _I], _I),
 }
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 _lib = None
 
@@ -154,7 +158,8 @@ KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 
                     "lss_attn_merge": 1, "lss_attn_delta": 1, "lss_attn_bwd_ex": 1, "lss_add_f32": 1,
                     "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1,
                     "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1,
-                    "lss_dropout_rows": 1, "lss_attn_fwd_split": 1, "lss_sum_slots_mask": 1, "lss_cat_cast_colsum_ex": 1}
+                    "lss_dropout_rows": 1, "lss_attn_fwd_split": 1, "lss_sum_slots_mask": 1, "lss_cat_cast_colsum_ex": 1,
+                    "lss_check_finite": 1}
 launch_count = 0
 
 

@@ -29,9 +29,14 @@ Communicator plays): rank-ordered concatenation / ascending-rank sums.
 
 from __future__ import annotations
 
+import threading
+import time
+from collections import deque
 from dataclasses import dataclass, field
 
 import torch
+
+from .errors import CommTimeout
 
 
 @dataclass
@@ -69,7 +74,7 @@ class TorchDistComm:
     (seq x data), used for the single folded gradient all-reduce."""
 
     def __init__(self, seq_group=None, world_group=None, ledger: Ledger | None = None,
-                 seq_name="sequence", world_name="world"):
+                 seq_name="sequence", world_name="world", *, use_flags: bool = True, timeout: float = 60.0):
         import torch.distributed as dist
 
         self.dist = dist
@@ -83,9 +88,19 @@ class TorchDistComm:
         self._flag = None
         self._board = None     # flag words [channel][source rank] of every rank (stream signals)
         self._seq = {}
-        import os
+        # cross-GPU dependencies as stream-signal flag boards over IPC (no NCCL kernel);
+        # False restores NCCL's one-element all-reduce barrier
+        self.use_flags = use_flags
+        # a peer that never signals: in-kernel waits give up after `timeout` (device
+        # deadline), stream waits are released by the watchdog; both -> CommTimeout
+        self.timeout = timeout
+        self._watchdog = None
 
-        self.use_flags = os.environ.get("LSS_FLAGS", "1") != "0"
+    def _ipc_capable(self) -> bool:
+        """CUDA IPC data plane available: GPU processes whose process group is NCCL, or
+        gloo (e.g. several ranks per GPU, which NCCL refuses) -- the peer mapping then
+        decides per pair (same node, P2P or same device)."""
+        return torch.cuda.is_available() and self.dist.get_backend(self.seq_group) in ("nccl", "gloo")
 
     def peer_addresses(self, t: torch.Tensor):
         """Device addresses, in this process, of every sequence-group rank's copy of
@@ -95,17 +110,21 @@ class TorchDistComm:
         if key in self._peers:
             hit = self._peers[key]
             return None if hit is None else hit[0]
-        if not t.is_cuda or self.dist.get_backend(self.seq_group) != "nccl" or self.seq_size == 1:
+        if not t.is_cuda or not self._ipc_capable() or self.seq_size == 1:
             return None
         import socket
 
         from . import kernels as K
 
         dev = t.device.index
-        handle, off = K.ipc_export(t)
+        try:  # legacy CUDA IPC cannot export e.g. expandable-segment / cudaMallocAsync memory
+            handle, off = K.ipc_export(t)
+        except Exception:  # noqa: BLE001 - contribute None: every rank then falls back together
+            handle, off = None, 0
         info = [None] * self.seq_size
         self.dist.all_gather_object(info, (socket.gethostname(), dev, handle, off), group=self.seq_group)
-        ok = all(h == info[self.seq_rank][0] for h, *_ in info)
+        ok = all(hd is not None for _, _, hd, _ in info)
+        ok = ok and all(h == info[self.seq_rank][0] for h, *_ in info)
         ok = ok and all(K.peer_access(dev, d) for r, (_, d, _, _) in enumerate(info) if r != self.seq_rank)
         addrs, opened = [], []
         if ok:
@@ -133,17 +152,21 @@ class TorchDistComm:
         """Collective: every rank contributes {name: tensor or None}; returns, per rank,
         {name: device address in this process} (own tensors: their pointers; peers':
         CUDA IPC mappings), or None when some pair of ranks cannot map each other."""
-        if self.dist.get_backend(self.seq_group) != "nccl" or self.seq_size == 1:
+        if not self._ipc_capable() or self.seq_size == 1:
             return None
         import socket
 
         from . import kernels as K
 
         dev = torch.cuda.current_device()
-        mine = {n: (K.ipc_export(t) if t is not None else None) for n, t in named.items()}
+        try:  # an export failure disables the path on every rank (no rank left blocked below)
+            mine = {n: (K.ipc_export(t) if t is not None else None) for n, t in named.items()}
+        except Exception:  # noqa: BLE001
+            mine = None
         info = [None] * self.seq_size
         self.dist.all_gather_object(info, (socket.gethostname(), dev, mine), group=self.seq_group)
-        ok = all(h == info[self.seq_rank][0] for h, _, _ in info)
+        ok = all(entries is not None for _, _, entries in info)
+        ok = ok and all(h == info[self.seq_rank][0] for h, _, _ in info)
         ok = ok and all(K.peer_access(dev, d) for r, (_, d, _) in enumerate(info) if r != self.seq_rank)
         out, opened = [], []
         if ok:
@@ -175,15 +198,39 @@ class TorchDistComm:
     def flags_ready(self) -> bool:
         """Map every rank's flag board once (collective); False when unavailable."""
         if self._board is None:
-            if not self.use_flags or self.seq_size == 1 or self.dist.get_backend(self.seq_group) != "nccl":
+            if not self.use_flags or self.seq_size == 1 or not self._ipc_capable():
                 self._board = False
                 return False
+            from . import kernels as K
+
             dev = torch.device("cuda", torch.cuda.current_device())
+            K.runtime_config(wait_timeout_s=self.timeout, device=dev)  # in-kernel wait deadline
             board = torch.zeros(self.N_CHANNELS * self.seq_size, dtype=torch.int32, device=dev)
             torch.cuda.synchronize()  # zeroed before any peer can signal into it
             addrs = self.map_named({"board": board})
             self._board = False if addrs is None else (board, [a["board"] for a in addrs])
+            if self._board is not False:
+                self._watchdog = WaitWatchdog(self.timeout, self._release_board)
         return self._board is not False
+
+    def _release_board(self) -> None:
+        """Watchdog action: satisfy every pending and future wait on this rank's flag
+        words so the parked streams drain (the step's results are void)."""
+        from . import kernels as K
+
+        top = max(self._seq.values(), default=0)
+        board = self._board[0]
+        K.flag_release(board.data_ptr(), board.numel(), top + (1 << 30))
+
+    def check(self) -> None:
+        """Raise CommTimeout if a wait of this communicator (stream or in-kernel) ran
+        past the deadline (collectives.py:242-252).  Host-only, no synchronisation."""
+        from . import kernels as K
+
+        if self._watchdog is not None:
+            self._watchdog.check()
+        if self._board:
+            K.raise_status(clear=True)
 
     def _flag_addr(self, rank: int, channel: int, source: int) -> int:
         return self._board[1][rank] + 4 * (channel * self.seq_size + source)
@@ -202,6 +249,7 @@ class TorchDistComm:
         for p in range(self.seq_size):
             if p != me:
                 K.stream_wait(self._flag_addr(me, channel, p), seq, stream)
+        self._watchdog.track(stream or torch.cuda.current_stream(), f"barrier {channel} #{seq}")
 
     def notify(self, peer: int, channel: int, stream=None) -> None:
         """Signal `peer` on `channel` once everything enqueued on `stream` is done."""
@@ -214,7 +262,7 @@ class TorchDistComm:
         """Handle whose wait() blocks the caller's current stream until `peer`'s next
         notify on `channel` (the NCCL Work.wait() contract)."""
         seq = self._seq[("in", channel, peer)] = self._seq.get(("in", channel, peer), 0) + 1
-        return _FlagWait(self._flag_addr(self.seq_rank, channel, peer), seq)
+        return _FlagWait(self._flag_addr(self.seq_rank, channel, peer), seq, self._watchdog)
 
     def push_stream(self) -> torch.cuda.Stream:
         if getattr(self, "_push_stream", None) is None:
@@ -323,13 +371,60 @@ class TorchDistComm:
 class _FlagWait:
     """Pending stream signal (see TorchDistComm.expect)."""
 
-    def __init__(self, addr: int, seq: int):
-        self.addr, self.seq = addr, seq
+    def __init__(self, addr: int, seq: int, watchdog=None):
+        self.addr, self.seq, self.watchdog = addr, seq, watchdog
 
     def wait(self) -> None:
         from . import kernels as K
 
         K.stream_wait(self.addr, self.seq)
+        if self.watchdog is not None:
+            self.watchdog.track(torch.cuda.current_stream(), f"hand-off #{self.seq}")
+
+
+class WaitWatchdog:
+    """Bounds the front-end stream waits, which cannot time out by themselves
+    (cuStreamWaitValue32): after every wait the waiting stream records an event, and a
+    daemon thread checks that each event completes within ``timeout`` seconds.  If one
+    does not, it calls ``release`` (write every flag word of this rank, so every parked
+    stream drains) and remembers the failure; :meth:`check` then raises CommTimeout --
+    the reference's rendezvous timeout (collectives.py:242-252) for the stream-signal
+    protocol.  Healthy waits cost one event record each."""
+
+    def __init__(self, timeout: float, release, poll: float = 0.05):
+        self.timeout, self.release, self.poll = timeout, release, poll
+        self._pending = deque()
+        self._lock = threading.Lock()
+        self.fired = None
+        self._thread = None
+        self._device = torch.cuda.current_device()
+
+    def track(self, stream: torch.cuda.Stream, what: str) -> None:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        with self._lock:
+            self._pending.append((ev, time.monotonic(), what))
+            if self._thread is None:
+                self._thread = threading.Thread(target=self._run, name="lss-watchdog", daemon=True)
+                self._thread.start()
+
+    def _run(self) -> None:
+        torch.cuda.set_device(self._device)
+        while self.fired is None:
+            time.sleep(self.poll)
+            with self._lock:
+                while self._pending and self._pending[0][0].query():
+                    self._pending.popleft()
+                head = self._pending[0] if self._pending else None
+            if head is not None and time.monotonic() - head[1] > self.timeout:
+                self.fired = f"{head[2]} not satisfied within {self.timeout}s (a peer is dead or out of step)"
+                self.release()
+                with self._lock:
+                    self._pending.clear()
+
+    def check(self) -> None:
+        if self.fired is not None:
+            raise CommTimeout(self.fired)
 
 
 class SoloComm:

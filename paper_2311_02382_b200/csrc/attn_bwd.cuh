@@ -546,6 +546,12 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
 #pragma unroll
       for (int c = 0; c < EC / 32; ++c) {
         tmem_ld32((is_v ? tdV : tdK) + lane_off + col0 + c * 32, v);
+        if (g_numerics_check) {  // NaN / Inf in dK / dV (tensor.py:79-95)
+          bool bad = false;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) bad |= nonfinite(__uint_as_float(v[i]));
+          report_nonfinite(bad);
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int chunk = (is_v ? 16 : 0) + (col0 + c * 32) / 4 + i;
@@ -584,6 +590,12 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time keeps the drain at 56 registers
         uint32_t v[32];
         tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
+        if (g_numerics_check) {  // NaN / Inf in this key tile's dQ contribution
+          bool bad = false;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) bad |= nonfinite(__uint_as_float(v[i]));
+          report_nonfinite(bad);
+        }
         const uint32_t rowh = hh ? row1 : row0;
 #pragma unroll
         for (int c = 0; c < 8; ++c)

@@ -449,6 +449,12 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
                        pack_bf16(__uint_as_float(oo[8 * i + 2]) * inv, __uint_as_float(oo[8 * i + 3]) * inv),
                        pack_bf16(__uint_as_float(oo[8 * i + 4]) * inv, __uint_as_float(oo[8 * i + 5]) * inv),
                        pack_bf16(__uint_as_float(oo[8 * i + 6]) * inv, __uint_as_float(oo[8 * i + 7]) * inv));
+        if (g_numerics_check) {  // NaN / Inf in O or the row statistics (tensor.py:79-95, 131)
+          bool bad = l_run > 0.f && (nonfinite(m_run) || nonfinite(l_run));
+#pragma unroll
+          for (int i = 0; i < ATT_D; ++i) bad |= nonfinite(__uint_as_float(oo[i]) * inv);
+          report_nonfinite(bad);
+        }
         __syncwarp();
         const int row_w0 = q0 + w * ATT_BM + quad * 32;  // local row of the warp's first row
 #pragma unroll

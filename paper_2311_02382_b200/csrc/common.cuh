@@ -85,15 +85,55 @@ LSS_DEV void fence_proxy_async_smem() {
 LSS_DEV void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-LSS_DEV uint32_t ld_acquire_gpu(const uint32_t* p) {
+// System scope: the flag words are written by a peer GPU's stream (NVLink) or by
+// this GPU's copy engine after a pull from peer memory.
+LSS_DEV uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+LSS_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------- runtime status
+// Two words of mapped pinned host memory shared by every kernel of the process
+// (lss_runtime_config / lss_status in include/lss.h): [0] a cross-GPU wait ran past
+// its deadline (the host raises CommTimeout, collectives.py:242-252), [1] a kernel
+// produced NaN / Inf while the numerics check is on (NumericsError, tensor.py:79-95).
+// Plain system-scope stores (no host atomics needed).  Device globals are per device:
+// lss_runtime_config sets them on the caller's current device.
+__device__ unsigned int* g_status_word = nullptr;
+__device__ unsigned long long g_wait_timeout_ns = 0;  // 0: unbounded
+__device__ int g_numerics_check = 0;
+
+LSS_DEV void status_raise(int which) {
+  unsigned int* w = g_status_word;
+  if (w) asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(w + which), "r"(1u) : "memory");
+}
+LSS_DEV bool nonfinite(float x) { return !(fabsf(x) <= 3.402823466e38f); }  // NaN or +-Inf
+// warp-aggregated report; every lane of the warp must call it
+LSS_DEV void report_nonfinite(bool bad) {
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) status_raise(1);
+}
+
 // Spin until the stream-signalled word reaches seq (wrap-safe), then order later
-// async-proxy (TMA) reads after it.
+// async-proxy (TMA) reads after it.  Bounded: past g_wait_timeout_ns the wait gives
+// up and raises the comm-timeout status word (a dead or out-of-step peer turns into
+// CommTimeout on the host instead of a hung GPU; the results of that step are void).
 LSS_DEV void wait_flag_geq(const uint32_t* p, uint32_t seq) {
-  while ((int)(ld_acquire_gpu(p) - seq) < 0) __nanosleep(128);
+  if ((int)(ld_acquire_sys(p) - seq) < 0) {
+    const unsigned long long lim = g_wait_timeout_ns, t0 = globaltimer_ns();
+    while ((int)(ld_acquire_sys(p) - seq) < 0) {
+      __nanosleep(256);
+      if (lim && globaltimer_ns() - t0 > lim) {
+        status_raise(0);
+        break;
+      }
+    }
+  }
   fence_proxy_async_global();
 }
 LSS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }

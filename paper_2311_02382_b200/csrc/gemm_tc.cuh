@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---------------- epilogue: thread <-> accumulator row
     const int quad = warp - 4;
     const int row_in_tile = quad * 32 + lane;
+    const bool check = g_numerics_check != 0;  // NaN / Inf report (tensor.py:79-95), off by default
     const uint32_t epi = smem_u32(smem + GEMM_STAGES * GEMM_STAGE_BYTES + 256) + quad * (32 * 32 * 4);
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
@@ -311,6 +312,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         }  // row_ok
+        if (check) {
+          bool bad = false;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) bad |= nonfinite(v[i]);
+          report_nonfinite(bad);
+        }
         const int seg = n / ep.seg_width;
         const long col = n - (long)seg * ep.seg_width;
         if (ep.out_bf16)

@@ -790,6 +790,7 @@ int lss_stream_wait(const unsigned int* flag, unsigned int value, void* stream) 
 }
 
 int lss_peer_access(int device, int peer) {
+  if (device == peer) return 1;  // two processes on one GPU: CUDA IPC maps the memory directly
   int ok = 0;
   if (cudaDeviceCanAccessPeer(&ok, device, peer) != cudaSuccess) return 0;
   return ok;
@@ -859,6 +860,100 @@ int lss_timestamp(unsigned long long* dst, void* stream) {
   if (!dst) return fail(LSS_ERR_ARG, "timestamp: null pointer");
   timestamp_kernel<<<1, 1, 0, S(stream)>>>(dst);
   return check_launch("timestamp");
+}
+
+// ---------------------------------------------------------------- runtime status / failure semantics
+
+namespace {
+unsigned int* g_status_host = nullptr;  // mapped pinned host words, see common.cuh
+std::mutex g_status_mu;
+
+int status_words() {
+  std::lock_guard<std::mutex> lock(g_status_mu);
+  if (g_status_host) return LSS_OK;
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaHostAlloc(status): %s", cudaGetErrorString(e));
+  memset(p, 0, 64);
+  g_status_host = static_cast<unsigned int*>(p);
+  return LSS_OK;
+}
+}  // namespace
+
+__global__ void check_finite_f32_kernel(const float4* x, long n4) {
+  bool bad = false;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    const float4 v = x[i];
+    bad |= nonfinite(v.x) | nonfinite(v.y) | nonfinite(v.z) | nonfinite(v.w);
+  }
+  report_nonfinite(bad);
+}
+__global__ void check_finite_bf16_kernel(const uint4* x, long n8) {
+  bool bad = false;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n8; i += (long)gridDim.x * blockDim.x) {
+    const uint4 v = x[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)  // bf16 NaN / Inf: exponent bits all ones
+      bad |= ((w[j] & 0x7F80u) == 0x7F80u) | ((w[j] & 0x7F800000u) == 0x7F800000u);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) status_raise(1);
+}
+
+int lss_runtime_config(unsigned long long wait_timeout_ns, int numerics_check) {
+  int rc = status_words();
+  if (rc) return rc;
+  unsigned int* dev_words = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_words), g_status_host, 0);
+  if (e != cudaSuccess) return fail(LSS_ERR_CUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
+  if (cudaMemcpyToSymbol(g_status_word, &dev_words, sizeof(dev_words)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_wait_timeout_ns, &wait_timeout_ns, sizeof(wait_timeout_ns)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_numerics_check, &numerics_check, sizeof(numerics_check)) != cudaSuccess)
+    return fail(LSS_ERR_CUDA, "runtime_config: cudaMemcpyToSymbol failed");
+  return LSS_OK;
+}
+
+int lss_status(unsigned int* out, int clear) {
+  if (!out) return fail(LSS_ERR_ARG, "status: null pointer");
+  int rc = status_words();
+  if (rc) return rc;
+  volatile unsigned int* w = g_status_host;
+  out[0] = w[0];
+  out[1] = w[1];
+  if (clear) {
+    w[0] = 0;
+    w[1] = 0;
+  }
+  return LSS_OK;
+}
+
+int lss_check_finite(const void* x, long n, int dtype, void* stream) {
+  if (!x) return fail(LSS_ERR_ARG, "check_finite: null pointer");
+  if (n <= 0) return LSS_OK;
+  const int per = dtype == LSS_BF16 ? 8 : 4;
+  if (n % per || !aligned16(x)) return fail(LSS_ERR_UNSUPPORTED, "check_finite: %ld elements not 16-byte vectors", n);
+  const long vec = n / per;
+  const int threads = 256;
+  const long blocks = std::min<long>((vec + threads - 1) / threads, 4L * num_sms());
+  if (dtype == LSS_BF16)
+    check_finite_bf16_kernel<<<blocks, threads, 0, S(stream)>>>(reinterpret_cast<const uint4*>(x), vec);
+  else
+    check_finite_f32_kernel<<<blocks, threads, 0, S(stream)>>>(reinterpret_cast<const float4*>(x), vec);
+  return check_launch("check_finite");
+}
+
+int lss_flag_release(unsigned int* flags, long count, unsigned int value) {
+  if (!flags) return fail(LSS_ERR_ARG, "flag_release: null pointer");
+  // a private non-blocking stream: the caller's streams may be parked in a stream wait
+  static cudaStream_t rs = nullptr;
+  if (!rs && cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(LSS_ERR_CUDA, "flag_release: stream creation failed");
+  static PFN_streamValue32 fn = stream_value_fn("cuStreamWriteValue32");
+  if (!fn) return fail(LSS_ERR_UNSUPPORTED, "cuStreamWriteValue32 unavailable");
+  for (long i = 0; i < count; ++i)
+    if (fn(reinterpret_cast<CUstream>(rs), reinterpret_cast<CUdeviceptr>(flags + i), value, 0) != CUDA_SUCCESS)
+      return fail(LSS_ERR_CUDA, "flag_release: cuStreamWriteValue32 failed");
+  return LSS_OK;
 }
 
 int lss_add_f32(float* y, const float* x, long n, void* stream) {

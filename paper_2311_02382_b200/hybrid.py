@@ -19,6 +19,11 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import torch
+
+from . import model
+from .dropout import as_policy
+
 
 @dataclass(frozen=True)
 class GridLayout:
@@ -52,9 +57,22 @@ class GridLayout:
         return 1.0 / self.world
 
 
-def make_groups(layout: GridLayout):
-    """Create the torch.distributed sequence and data groups (every rank must call
-    this, in the same order).  Returns (my_seq_group, my_data_group, world_group)."""
+def make_groups(comm_or_layout, layout: GridLayout | None = None):
+    """Two forms.
+
+    ``make_groups(comm, layout)`` -- hybrid.make_groups (hybrid.py:64-73): every
+    sequence group (indexed by replica) and data group (indexed by sequence
+    position) of a :mod:`collectives` communicator, as two lists.
+
+    ``make_groups(layout)`` -- for the resident engine: create the torch.distributed
+    sequence and data process groups (every rank must call this, in the same
+    order); returns (my_seq_group, my_data_group, world_group)."""
+    if layout is not None:
+        comm = comm_or_layout
+        seq_groups = [comm.group("sequence", layout.seq_members(d)) for d in range(layout.replicas)]
+        data_groups = [comm.group("data", layout.data_members(s)) for s in range(layout.seq_workers)]
+        return seq_groups, data_groups
+    layout = comm_or_layout
     import torch.distributed as dist
 
     rank = dist.get_rank()
@@ -72,21 +90,105 @@ def make_groups(layout: GridLayout):
     return my_seq, my_data, dist.group.WORLD
 
 
-def run_steps(engine, comm, batches, opt, *, layer: int = 0):
-    """Drive ``len(batches)`` training steps of ONE rank of a D x N grid
-    (hybrid.run_steps / train_step, hybrid.py:95-126, 140-190, at layer level):
-    each step runs the layer forward + backward with the folded gradient
-    all-reduce (sequence x data, scale 1/(D*N) in the kernels) and then the
-    optimizer update of the bound parameters (``engine.bind_params``).
+def run_engine_steps(engine, comm, batches, opt, *, layer: int = 0, policy=None, replica: int = 0):
+    """Drive ``len(batches)`` training steps of ONE rank of a D x N grid on the
+    resident engine (hybrid.run_steps / train_step, hybrid.py:95-126, 140-190, at
+    layer level): each step runs the layer forward + backward with the folded
+    gradient all-reduce (sequence x data, scale 1/(D*N) in the kernels) and then
+    the optimizer update of the bound parameters (``engine.bind_params``).
 
-    ``batches[s]`` = (x_seg, grad_y_seg) of this rank's sequence block.
-    Returns the post-sync gradient norm of every step (HybridRun.grad_norms,
-    folded in fp64 like model.grad_norm)."""
-    import torch
-
+    ``batches[s]`` = (x_seg, grad_y_seg) of this rank's sequence block.  The
+    dropout policy of step s is ``policy.at_step(s).fork(replica)`` as in the
+    reference runner (hybrid.py:172-174).  Returns the post-sync gradient norm of
+    every step (HybridRun.grad_norms, folded in fp64 like model.grad_norm)."""
+    base = as_policy(policy)
     norms = []
     for s, (x, gy) in enumerate(batches):
-        engine.step(x, gy, comm, step=s, layer=layer)
+        pol = base.at_step(s).fork(replica) if base.active else None
+        engine.step(x, gy, comm, step=s, layer=layer, policy=pol)
         norms.append(float(torch.linalg.vector_norm(engine.grads.double())))
         engine.optimizer_step(opt)
     return norms
+
+
+# ------------------------------------------------------------ the reference's functions, same signatures
+
+
+def vertical_sync(comm, data_group, rank: int, grads, loss: float, *, step: int = 0):
+    """hybrid.vertical_sync (hybrid.py:76-92): average every gradient (position rows
+    included) and the loss over the replicas sharing this sequence block."""
+    arrays = grads.arrays()
+    flat = model.flatten_arrays(arrays)
+    vec = torch.cat([flat, torch.tensor([float(loss)], dtype=flat.dtype, device=flat.device)])
+    out = comm.all_reduce_mean(data_group, rank, vec, step=step, phase="sync")
+    return grads.replace_arrays(model.unflatten_like(out[:-1], arrays)), float(out[-1])
+
+
+def train_step(comm, seq_group, data_group, dist, cfg, tokens_seg, targets_seg, *, lr: float, policy=None,
+               step: int = 0, fused: bool = True):
+    """hybrid.train_step (hybrid.py:95-126): sequence-group forward / backward /
+    sync, then the data-group vertical sync, then SGD.  Returns (grid-mean loss,
+    counters, synced grads)."""
+    from . import sharded
+    from .tensor import StepCounters
+
+    rank = seq_group.members[dist.spec.rank]
+    counters = StepCounters()
+    partial, cache = sharded.forward(comm, seq_group, dist, cfg, tokens_seg, targets_seg, policy=policy, step=step,
+                                     counters=counters, fused=fused)
+    grads = sharded.backward(comm, seq_group, dist, cfg, cache, step=step)
+    grads, replica_loss = sharded.sync(comm, seq_group, rank, grads, step=step, extra=partial)
+    grads, grid_loss = vertical_sync(comm, data_group, rank, grads, replica_loss, step=step)
+    dist.params = model.sgd_step(dist.params, grads, lr)
+    return grid_loss, counters, grads
+
+
+@dataclass
+class HybridRun:
+    """hybrid.HybridRun (hybrid.py:129-137)."""
+
+    comm: object
+    layout: GridLayout
+    workers: list
+    step_losses: list
+    counters: list
+    grad_norms: list
+    last_grads: list | None
+
+
+def run_steps(cfg, params_full, layout: GridLayout, batches, *, lr: float, policy=None, fused: bool = True,
+              keep_last_grads: bool = False, timeout: float = 60.0) -> HybridRun:
+    """hybrid.run_steps (hybrid.py:140-190): ``len(batches)`` steps on a D x N grid
+    of worker threads on the current GPU; ``batches[s][d]`` is replica d's
+    full-width (tokens, targets) of step s."""
+    from . import sharded
+    from .collectives import Communicator, run_workers
+
+    for row in batches:
+        if len(row) != layout.replicas:
+            raise ValueError(f"each step needs {layout.replicas} replica batches, got {len(row)}")
+    comm = Communicator(layout.world, timeout=timeout)
+    seq_groups, data_groups = make_groups(comm, layout)
+    base = as_policy(policy)
+
+    def worker(rank: int):
+        replica, seq_index = layout.coords(rank)
+        spec = sharded.ShardSpec(seq_index, layout.seq_workers, cfg.seq_len)
+        dist = sharded.shard_params(params_full, spec)
+        losses, counts, norms, grads_out = [], [], [], None
+        for s, row in enumerate(batches):
+            tokens, targets = row[replica]
+            pol = base.at_step(s).fork(replica) if base.active else base
+            loss, counters, grads = train_step(comm, seq_groups[replica], data_groups[seq_index], dist, cfg,
+                                               sharded.slice_batch(tokens, spec), sharded.slice_batch(targets, spec),
+                                               lr=lr, policy=pol, step=s, fused=fused)
+            if keep_last_grads and s == len(batches) - 1:
+                grads_out = grads
+            losses.append(loss)
+            counts.append(counters)
+            norms.append(model.grad_norm(grads))
+        return dist, losses, counts, norms, grads_out
+
+    res = run_workers(layout.world, worker, comm=comm)
+    return HybridRun(comm, layout, [r[0] for r in res], res[0][1], [r[2] for r in res], [r[3] for r in res],
+                     [r[4] for r in res] if keep_last_grads else None)

@@ -510,3 +510,87 @@ def add_(y, x):
     """y += x (fp32, device)."""
     call("lss_add_f32", _ptr(y), _ptr(x), y.numel(), _stream())
     return y
+
+
+# ----------------------------------------------------------------- failure semantics (ABI v9)
+
+_RUNTIME = {"wait_timeout_s": 60.0, "numerics": False}
+_CONFIGURED: set = set()
+
+
+def runtime_config(*, wait_timeout_s: float | None = None, numerics: bool | None = None, device=None) -> None:
+    """Deadline of every in-kernel cross-GPU wait (seconds, 0 = unbounded; the
+    reference Communicator's default timeout is 60 s, collectives.py:159) and the
+    opt-in NaN / Inf check in the GEMM / attention epilogues (tensor.py:79-95).
+    Applies to ``device`` (default: current) now and to every device configured later."""
+    if wait_timeout_s is not None:
+        _RUNTIME["wait_timeout_s"] = float(wait_timeout_s)
+    if numerics is not None:
+        _RUNTIME["numerics"] = bool(numerics)
+    _CONFIGURED.clear()
+    ensure_runtime(device)
+
+
+def ensure_runtime(device=None) -> None:
+    """Push the runtime configuration to ``device`` once (device globals are per GPU)."""
+    d = torch.cuda.current_device() if device is None else torch.device(device).index
+    if d is None:
+        d = torch.cuda.current_device()
+    if d in _CONFIGURED:
+        return
+    with torch.cuda.device(d):
+        call("lss_runtime_config", int(_RUNTIME["wait_timeout_s"] * 1e9), int(_RUNTIME["numerics"]))
+    _CONFIGURED.add(d)
+
+
+def numerics_enabled() -> bool:
+    return _RUNTIME["numerics"]
+
+
+def status(clear: bool = False) -> tuple:
+    """(comm_timeout, nonfinite) reported by the kernels since the last clear (mapped
+    host memory: no device synchronisation; meaningful once the work completed)."""
+    out = (ctypes.c_uint * 2)()
+    call("lss_status", out, int(clear))
+    return bool(out[0]), bool(out[1])
+
+
+def raise_status(clear: bool = True) -> None:
+    """Raise CommTimeout / NumericsError for what the kernels reported."""
+    from .errors import CommTimeout, NumericsError
+
+    timed_out, nonfinite = status(clear)
+    if timed_out:
+        raise CommTimeout("a cross-GPU wait ran past its deadline (a peer is dead or out of step); "
+                          "the results of that step are void")
+    if nonfinite:
+        raise NumericsError("a kernel produced NaN or Inf")
+
+
+def check_finite(t: torch.Tensor) -> None:
+    """Report (status word 1) NaN / Inf anywhere in a contiguous fp32 / bf16 tensor."""
+    _need(t, "tensor")
+    dt = LSS_BF16 if t.dtype == torch.bfloat16 else LSS_F32
+    if t.dtype not in (torch.bfloat16, torch.float32):
+        raise ShapeError(f"check_finite: dtype {t.dtype}")
+    call("lss_check_finite", _ptr(t), t.numel(), dt, _stream())
+
+
+def checked(*tensors):
+    """With the numerics check on: every kernel output checked for NaN / Inf before it
+    is returned (the reference checks every matmul / softmax output, tensor.py:79-95)
+    -- synchronises, so it is a debugging mode.  Returns the first tensor."""
+    if _RUNTIME["numerics"]:
+        ensure_runtime()
+        for t in tensors:
+            if t is not None and t.is_contiguous() and t.dtype in (torch.float32, torch.bfloat16) and \
+                    t.numel() % (8 if t.dtype == torch.bfloat16 else 4) == 0:
+                check_finite(t)
+        torch.cuda.current_stream().synchronize()
+        raise_status()
+    return tensors[0] if tensors else None
+
+
+def flag_release(addr: int, count: int, value: int) -> None:
+    """Write ``value`` to ``count`` flag words from a private non-blocking stream."""
+    call("lss_flag_release", ctypes.c_void_p(int(addr)), int(count), value & 0xFFFFFFFF)

@@ -158,11 +158,28 @@ def _as_act(x: torch.Tensor, cfg: ModelConfig) -> torch.Tensor:
     return x if x.dtype == cfg.act_dtype else x.to(cfg.act_dtype)
 
 
+class _Precision:
+    """Stand-in for an omitted ``cfg``: the kernel family follows the operand's dtype
+    (bf16 -> tcgen05 path, fp32 -> fp32 check mode), as the reference's dtype
+    policy follows its arrays (tensor.py:24-32)."""
+
+    def __init__(self, x: torch.Tensor):
+        self.precision = "bf16" if x.dtype == torch.bfloat16 else "single"
+        self.act_dtype = K.act_dtype(self.precision)
+
+
+def _cfg_or(cfg, x: torch.Tensor):
+    return cfg if cfg is not None else _Precision(x)
+
+
 # ------------------------------------------------------------------ linear / norm
 
 
-def linear3(x: torch.Tensor, p: LinearParams, cfg: ModelConfig, out_dtype=torch.float32) -> torch.Tensor:
-    """model.linear3 (model.py:237-239): x (B, m, E_in) @ W + b -> (B, m, E_out)."""
+def linear3(x: torch.Tensor, p: LinearParams, cfg: Optional[ModelConfig] = None,
+            out_dtype=torch.float32) -> torch.Tensor:
+    """model.linear3 (model.py:237-239): x (B, m, E_in) @ W + b -> (B, m, E_out).
+    ``cfg`` may be omitted as in the reference: the precision then follows x."""
+    cfg = _cfg_or(cfg, x)
     b, m, e = x.shape
     if p.weight.shape[0] != e:
         raise ShapeError(f"matmul inner dims disagree: {tuple(x.shape)} x {tuple(p.weight.shape)}")
@@ -172,11 +189,12 @@ def linear3(x: torch.Tensor, p: LinearParams, cfg: ModelConfig, out_dtype=torch.
     out = torch.empty(b, m, n, dtype=out_dtype, device=x.device)
     # B operand = W stored [d_in][d_out] = [K][N] -> N-major
     K.gemm(a.view(b * m, e), w, b_mn_major=True, bias=p.bias, out=out.view(b * m, n), M=b * m, N=n, K=e)
-    return out
+    return K.checked(out)
 
 
-def linear3_bwd(x: torch.Tensor, p: LinearParams, grad_y: torch.Tensor, cfg: ModelConfig):
+def linear3_bwd(x: torch.Tensor, p: LinearParams, grad_y: torch.Tensor, cfg: Optional[ModelConfig] = None):
     """model.linear3_bwd (model.py:242-245) -> (grad_x, grad_W, grad_b), fp32."""
+    cfg = _cfg_or(cfg, x)
     b, m, e = x.shape
     n = p.weight.shape[1]
     gy32 = grad_y.to(torch.float32).contiguous().view(b * m, n)
@@ -189,6 +207,7 @@ def linear3_bwd(x: torch.Tensor, p: LinearParams, grad_y: torch.Tensor, cfg: Mod
     K.gemm(xa, gy, a_mn_major=True, b_mn_major=True, out=gw, M=e, N=n, K=b * m)  # x^T . gy
     gb = torch.zeros(n, dtype=torch.float32, device=x.device)
     K.cat_cast_colsum([(gy32, n, n)], b * m, dst=None, colsum=gb)
+    K.checked(gx, gw, gb)
     return gx.view(b, m, e), gw, gb
 
 
@@ -204,7 +223,7 @@ def norm3(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, cfg: Optional
     """model.norm3 (model.py:248-251) -> (y, cache)."""
     x = x.to(torch.float32).contiguous()
     y, mean, rstd = K.layernorm_fwd(x, gain, bias, out_dtype=out_dtype)
-    return y, NormCache(x, mean, rstd)
+    return K.checked(y), NormCache(x, mean, rstd)
 
 
 def norm3_bwd(cache: NormCache, gain: torch.Tensor, grad_y: torch.Tensor, grad_res=None):
@@ -279,7 +298,7 @@ def scores_fwd(q, k, v, offset: int, cfg: ModelConfig, policy=None, layer: int =
         counters.add_score_flops(m, cfg.head_dim * bh, t)
         counters.add_score_flops(m, t, cfg.head_dim * bh)
         counters.record_score_footprint(bh * m * t)
-    return ctx, ScoreCache(offset, ctx, lse, ka, va, workers, seg, pol, layer)
+    return K.checked(ctx), ScoreCache(offset, ctx, lse, ka, va, workers, seg, pol, layer)
 
 
 def scores_bwd(cache: ScoreCache, q, k, v, grad_ctx, cfg: ModelConfig, policy=None):
@@ -309,10 +328,12 @@ def scores_bwd(cache: ScoreCache, q, k, v, grad_ctx, cfg: ModelConfig, policy=No
         gk4, gv4 = (gk, gv) if gk.dim() == 4 else (gk.unsqueeze(0), gv.unsqueeze(0))
         K.attn_bwd_sources(kv[0], kv[1], [src], grad_k=gk4, grad_v=gv4, workers=workers, seg_len=seg, heads=H,
                            causal=cfg.causal, dropout=pol.desc(cache.layer))
+        K.checked(gq, packed)
         return gq, gk, gv
     gq, gk, gv = K.attn_bwd(qa, ka, va, cache.ctx, go, cache.lse2, workers=workers, seg_len=seg,
                             heads=cfg.n_heads, offset=cache.offset, causal=cfg.causal, grad_k=gk,
                             grad_v=gv)
+    K.checked(gq, packed)
     return gq, gk, gv
 
 
@@ -414,12 +435,13 @@ def ffn_bwd(cache: FfnCache, lp: LayerParams, grad_out: torch.Tensor, cfg: Model
 # ------------------------------------------------------------------ layer
 
 
-def local_kv_fwd(xh: torch.Tensor, lp: LayerParams, cfg: ModelConfig):
+def local_kv_fwd(xh: torch.Tensor, lp: LayerParams, cfg: Optional[ModelConfig] = None):
     """model.local_kv_fwd (model.py:413-415): project the block itself."""
+    cfg = _cfg_or(cfg, xh)
     return linear3(xh, lp.attn_k, cfg, cfg.act_dtype), linear3(xh, lp.attn_v, cfg, cfg.act_dtype), xh
 
 
-def local_kv_bwd(kv_ctx, lp: LayerParams, grad_k, grad_v, cfg: ModelConfig):
+def local_kv_bwd(kv_ctx, lp: LayerParams, grad_k, grad_v, cfg: Optional[ModelConfig] = None):
     """model.local_kv_bwd (model.py:418-421)."""
     gkx, k_wg, k_bg = linear3_bwd(kv_ctx, lp.attn_k, grad_k, cfg)
     gvx, v_wg, v_bg = linear3_bwd(kv_ctx, lp.attn_v, grad_v, cfg)
@@ -517,6 +539,60 @@ class Parameters:
     def arrays(self) -> list:
         return [a for _, a in self.named_arrays()]
 
+    def replace_arrays(self, arrays) -> "Parameters":
+        """model.Parameters.replace_arrays (model.py:142-166): same structure from a
+        flat list in named order."""
+        it = iter(arrays)
+        lin = lambda: LinearParams(next(it), next(it))  # noqa: E731
+        tok, pos = next(it), next(it)
+        layers = []
+        for lp in self.layers:
+            g1, b1 = next(it), next(it)
+            q, k, v, o = lin(), lin(), lin(), lin()
+            nl = LayerParams(g1, b1, q, k, v, o)
+            if lp.has_ffn:
+                nl.ln2_gain, nl.ln2_bias = next(it), next(it)
+                nl.ff_in, nl.ff_out = lin(), lin()
+            layers.append(nl)
+        fg, fb = next(it), next(it)
+        return Parameters(tok, pos, layers, fg, fb, lin())
+
+    def copy(self) -> "Parameters":
+        return self.replace_arrays([a.clone() for a in self.arrays()])
+
+    def zip_map(self, other: "Parameters", fn) -> "Parameters":
+        return self.replace_arrays([fn(a, b) for a, b in zip(self.arrays(), other.arrays())])
+
+
+def sgd_step(params: Parameters, grads: Parameters, lr: float) -> Parameters:
+    """model.sgd_step (model.py:621-623): fresh parameters w - lr*g, inputs untouched."""
+    return params.zip_map(grads, lambda w, g: w - lr * g)
+
+
+def flatten_arrays(arrays) -> torch.Tensor:
+    """model.flatten_arrays (model.py:629-630)."""
+    return torch.cat([a.reshape(-1) for a in arrays]) if arrays else torch.zeros(0)
+
+
+def unflatten_like(vec: torch.Tensor, arrays) -> list:
+    """model.unflatten_like (model.py:633-642)."""
+    needed = sum(a.numel() for a in arrays)
+    if vec.numel() != needed:
+        raise ShapeError(f"flat vector has {vec.numel()} elements, structure needs {needed}")
+    out, pos = [], 0
+    for a in arrays:
+        out.append(vec[pos:pos + a.numel()].view(a.shape))
+        pos += a.numel()
+    return out
+
+
+def grad_norm(grads: Parameters) -> float:
+    """model.grad_norm (model.py:645-650): Euclidean norm folded in parameter order (fp64)."""
+    total = torch.zeros((), dtype=torch.float64, device=grads.token_table.device)
+    for _, g in grads.named_arrays():
+        total += (g.to(torch.float64) ** 2).sum()
+    return float(total.sqrt())
+
 
 def _ids(t: torch.Tensor, vocab: int, what: str) -> torch.Tensor:
     """int32 device ids, range-checked like nnops.embed_tokens / cross_entropy."""
@@ -567,6 +643,7 @@ class HeadCache:
     grad_logits: Optional[torch.Tensor]
     shape3: tuple
     vocab: int
+    cfg: object = None
 
 
 def _head_operand(params: Parameters, cfg: ModelConfig):
@@ -581,9 +658,12 @@ def _head_operand(params: Parameters, cfg: ModelConfig):
     return _as_act(w, cfg).contiguous(), b.contiguous(), vp
 
 
-def head_fwd(x: torch.Tensor, params: Parameters, targets: Optional[torch.Tensor], cfg: ModelConfig):
+def head_fwd(x: torch.Tensor, params: Parameters, targets: Optional[torch.Tensor],
+             cfg: Optional[ModelConfig] = None):
     """model.head_fwd (model.py:552-562): final LN, vocabulary projection and the
-    mean cross-entropy.  Returns (loss or None, HeadCache)."""
+    mean cross-entropy.  Returns (loss or None, HeadCache).  Without ``cfg`` the
+    bf16 tcgen05 path runs (the residual stream x is fp32 in both precisions)."""
+    cfg = cfg if cfg is not None else _Precision(torch.empty(0, dtype=torch.bfloat16))
     bsz, m, e = x.shape
     v = params.head.weight.shape[1]
     xf, lnf = norm3(x.reshape(bsz * m, e), params.final_gain, params.final_bias, cfg, out_dtype=cfg.act_dtype)
@@ -591,18 +671,19 @@ def head_fwd(x: torch.Tensor, params: Parameters, targets: Optional[torch.Tensor
     logits = torch.empty(bsz * m, vp, dtype=torch.float32, device=x.device)
     K.gemm(xf, w, b_mn_major=True, bias=b, out=logits, M=bsz * m, N=vp, K=e)
     if targets is None:
-        return None, HeadCache(lnf, xf, logits, None, (bsz, m, e), v)
+        return None, HeadCache(lnf, xf, logits, None, (bsz, m, e), v, cfg)
     ids = _ids(targets.reshape(-1), v, "target")
     n = bsz * m
     loss_rows, grad = K.cross_entropy(logits, ids, v, scale=1.0 / n)
     loss = loss_rows.sum() / n
     if not bool(torch.isfinite(loss)):
         raise ValueError("cross_entropy produced a non-finite loss")
-    return float(loss), HeadCache(lnf, xf, logits, grad, (bsz, m, e), v)
+    return float(loss), HeadCache(lnf, xf, logits, grad, (bsz, m, e), v, cfg)
 
 
-def head_bwd(cache: HeadCache, params: Parameters, cfg: ModelConfig):
+def head_bwd(cache: HeadCache, params: Parameters, cfg: Optional[ModelConfig] = None):
     """model.head_bwd (model.py:565-570) -> (grad_x, final_gain_g, final_bias_g, head_wg, head_bg)."""
+    cfg = cfg if cfg is not None else cache.cfg
     if cache.grad_logits is None:
         raise ValueError("head_bwd requires a forward pass that computed the loss")
     n, vp = cache.grad_logits.shape

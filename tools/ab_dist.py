@@ -2,7 +2,7 @@
 CUDA-event time per block, max over ranks.  torchrun --nproc-per-node N tools/ab_dist.py"""
 import math, os, sys, torch, torch.distributed as dist
 sys.path.insert(0, ".")
-from paper_2311_02382_b200 import sharded as SH
+import dataclasses
 from paper_2311_02382_b200.comm import Ledger, TorchDistComm
 from paper_2311_02382_b200.model import LayerParams, LinearParams, ModelConfig
 from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec
@@ -34,11 +34,9 @@ MODES = {
 sel = sys.argv[1:] or list(MODES)
 
 def setmode(m):
-    SH._CE_P2P = m["ce"]
     comm.use_flags = m["flags"]
-    SH._FWD_SPLIT = m["split"]
-    SH._FUSED_GATHER = m["fused"]
-    SH._B1_IN_KERNEL = m.get("b1k", False)
+    eng.options = dataclasses.replace(eng.options, ce_p2p=m["ce"], fwd_split=m["split"], fused_gather=m["fused"],
+                                      b1_in_kernel=m.get("b1k", False))
 
 for name in sel:  # warm every mode (maps buffers once, collectively)
     setmode(MODES[name])

@@ -3,7 +3,8 @@ import sys, torch, heapq
 sys.path.insert(0, ".")
 from paper_2311_02382_b200.model import LayerParams, LinearParams, ModelConfig
 from paper_2311_02382_b200.sharded import LSSAttention, ShardSpec, fwd_cta_tiles, choose_fwd_splits
-from paper_2311_02382_b200 import sharded as SH
+from paper_2311_02382_b200 import balance as BAL
+from paper_2311_02382_b200 import engine as ENG
 from paper_2311_02382_b200 import kernels as K
 
 l, E, H = 50112, 1024, 16
@@ -39,15 +40,13 @@ for r in [int(a) for a in sys.argv[2:]] or [0, G - 1]:
         ideal = sum(tiles) * 16 / 148 * US
         res = []
         for S in (1, 2, 3, 4, 6):
-            SH._SPLIT_CACHE.clear()
-            SH._SPLIT_MAX = S
-            old = SH.choose_fwd_splits
+            BAL._SPLIT_CACHE.clear()
+            old = ENG.choose_fwd_splits
             f = lambda: e._attn_part(q, rows=rows, row0=row0, offset=off, g_begin=g0, g_end=g1, out=out, lse2=lse)
-            SH.choose_fwd_splits = lambda *a, S=S: S
+            ENG.choose_fwd_splits = lambda *a, S=S: S  # the engine's split choice, forced
             res.append((S, round(tm(f), 1)))
-            SH.choose_fwd_splits = old
-        SH._SPLIT_MAX = 8
-        SH._SPLIT_CACHE.clear()
+            ENG.choose_fwd_splits = old
+        BAL._SPLIT_CACHE.clear()
         pick = choose_fwd_splits(rows, off + row0, g0, g1, m, True, 16, 148, E)
         print(f"G={G} r={r} {pl.role:5s} rows={rows:5d} pos0={off+row0:6d} segs=[{g0},{g1}) ctas={len(tiles)*16:4d} "
               f"maxtiles={max(tiles)} ideal={ideal:6.1f}us pick S={pick} measured {res}", flush=True)

@@ -9,8 +9,7 @@ world all-reduce with 1/(D*N), SGD update of the bound parameters) for
 ``--steps`` steps; after each step rank 0 checks the parameter update against
 the oracle's (1/D) sum_d (group-averaged grads of replica d) at the parameters
 that step started from, and all ranks must hold identical parameters
-(hybrid.train_step, hybrid.py:95-126).  ``--backend gloo`` lets several ranks
-share a GPU (round-robin), with the same IPC / flag data plane.
+(hybrid.train_step, hybrid.py:95-126).  One GPU per rank.
 Invoked by tests/test_gpu_dist.py.
 """
 
@@ -44,7 +43,11 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
-    local = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
+    if int(os.environ["LOCAL_WORLD_SIZE"]) > torch.cuda.device_count():
+        # kernels that spin on flags other ranks write must not share a GPU across processes
+        # (Xid 109 context-switch timeouts on this driver, B200_PROFILING.md)
+        raise SystemExit("one GPU per rank required")
+    local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if args.backend == "nccl":

@@ -194,13 +194,66 @@ def cpu_sample(args, rows, threads):
                  f"precomputed), {threads} host threads")
 
 
+REF_INSTALL = ROOT / "baseline" / "_ref"
+
+
+def reference_sample(args, rows, threads):
+    """Time the REFERENCE's own functions (seqpar, installed under baseline/_ref by
+    ``pip install --target``) on a bounded sample: ``rows`` query rows centred on
+    l/2 through the attention half of model.layer_fwd / layer_bwd -- norm3, linear3
+    (Q and own K/V), scores_fwd / scores_bwd (its per-(sample, head) loop with the
+    full probability matrix, model.py:280-359), the out-projection, linear3_bwd x4
+    and norm3_bwd -- against the K/V of the whole sequence (projected outside the
+    timed region, as if received from the all-gather).  precision "single", the
+    reference's fp32 mode.  Returns (run, description) or None when absent."""
+    if not (REF_INSTALL / "seqpar").exists():
+        return None
+    sys.path.insert(0, str(REF_INSTALL))
+    import numpy as np
+    from seqpar import model as RM
+    from seqpar.nnops import DropoutPolicy
+
+    cfg = RM.ModelConfig(embed_dim=args.embed, n_layers=1, n_heads=args.heads, ff_dim=4, vocab=16,
+                         seq_len=args.seq, batch=args.batch, causal=not args.noncausal, precision="single")
+    lp = RM.init_params(RM.ModelConfig(**{**cfg.to_dict(), "seq_len": 8}), 0).layers[0]
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((args.batch, args.seq, args.embed), dtype=np.float32)
+    gy = rng.standard_normal((args.batch, rows, args.embed), dtype=np.float32)
+    offset = max(0, args.seq // 2 - rows // 2)
+    xh_all, _ = RM.norm3(x, lp.ln1_gain, lp.ln1_bias)
+    k_full, v_full = RM.linear3(xh_all, lp.attn_k), RM.linear3(xh_all, lp.attn_v)
+    off = DropoutPolicy.off()
+    xs = np.ascontiguousarray(x[:, offset:offset + rows])
+
+    def run():
+        xh, ln = RM.norm3(xs, lp.ln1_gain, lp.ln1_bias)
+        k_own, v_own = RM.linear3(xh, lp.attn_k), RM.linear3(xh, lp.attn_v)
+        q = RM.linear3(xh, lp.attn_q)
+        ctx, sc = RM.scores_fwd(q, k_full, v_full, offset, cfg, off, 0)
+        y = xs + RM.linear3(ctx, lp.attn_out)
+        g_ctx, _, _ = RM.linear3_bwd(ctx, lp.attn_out, gy)
+        dq, dk, dv = RM.scores_bwd(sc, q, k_full, v_full, g_ctx, cfg, off)
+        gxq, _, _ = RM.linear3_bwd(xh, lp.attn_q, dq)
+        gxk, _, _ = RM.linear3_bwd(xh, lp.attn_k, dk[:, offset:offset + rows])
+        gxv, _, _ = RM.linear3_bwd(xh, lp.attn_v, dv[:, offset:offset + rows])
+        gx, _, _ = RM.norm3_bwd(ln, lp.ln1_gain, gxq + gxk + gxv)
+        return y, gy + gx, k_own, v_own
+
+    return run, (f"{rows} query rows at offset {offset} of l_x={args.seq} through the REFERENCE's own "
+                 f"seqpar functions (baseline/_ref; norm3, linear3, scores_fwd/scores_bwd, linear3_bwd, "
+                 f"norm3_bwd; precision 'single'), K/V of the whole sequence precomputed; {threads} host "
+                 f"threads available to its BLAS")
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     rows = max(8, min(args.cpu_rows, 64))
-    run, desc = cpu_sample(args, rows, threads)
+    ref = reference_sample(args, rows, threads)
+    kind = "reference" if ref is not None else "port"
+    run, desc = ref if ref is not None else cpu_sample(args, rows, threads)
     for _ in range(args.warmup):
         run()
     times = []
@@ -216,7 +269,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload(args), "global_batch": args.batch, "seq_len": args.seq,
                    "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
                          "sample": desc, **host_info()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -441,7 +494,9 @@ def main_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
-        run, desc = cpu_sample(args, args.cpu_rows, threads)
+        ref = reference_sample(args, args.cpu_rows, threads)
+        kind = "reference" if ref is not None else "port"
+        run, desc = ref if ref is not None else cpu_sample(args, args.cpu_rows, threads)
         run()  # warm
         reps, t0 = 0, time.perf_counter()
         while True:  # >= 10 s of CPU work (bounded sample, repeated)
@@ -450,7 +505,7 @@ def main_ours(args):
             dt = time.perf_counter() - t0
             if dt >= 10.0 or reps >= 50:
                 break
-        cpu = {"value": B * args.cpu_rows * reps / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
+        cpu = {"value": B * args.cpu_rows * reps / dt, "unit": "tokens/s", "cores": threads, "kind": kind,
                "sample": f"{reps} x " + desc, "seconds": dt, **host_info()}
 
     if rank == 0:

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define LSS_ABI_VERSION 9
+#define LSS_ABI_VERSION 10
 
 enum lss_status {
   LSS_OK = 0,
@@ -222,6 +222,12 @@ typedef struct lss_bwd_source {
    * (lss_stream_signal), and the kernel processes the sources before it meanwhile */
   const unsigned int* ready;
   unsigned int ready_seq;
+  /* optional (ABI v10, deterministic mode): when non-NULL (for every source of the
+   * launch), dQ is accumulated here instead of grad_q -- int64 [batch][m_src][embed],
+   * round(dQ * 2^32), added with integer bulk reductions, so the sum over key tiles is
+   * bitwise identical whatever order they finish in; zero it first, convert with
+   * lss_fixed_to_f32.  grad_q may then be NULL. */
+  long long* grad_q_fixed;
 } lss_bwd_source;
 
 /* Backward over up to 3 sources in ONE launch: every key tile accumulates dK/dV
@@ -327,9 +333,13 @@ int lss_peer_access(int device, int peer);
  * (tensor.py:79-95, 118, 131).  On B200:
  *  - lss_runtime_config sets, on the caller's current device, the deadline of every
  *    in-kernel cross-GPU wait (fused gather segment flags, pushed backward sources;
- *    0 = unbounded) and the opt-in NaN / Inf check in the epilogues of the GEMM and
- *    attention kernels (0 off, 1 on).  A wait past its deadline gives up and raises
- *    status word 0; a non-finite output raises word 1.
+ *    0 = unbounded) and the flags: LSS_RT_NUMERICS, the opt-in NaN / Inf check in the
+ *    epilogues of the GEMM and attention kernels; LSS_RT_DETERMINISTIC (process-wide,
+ *    ABI v10), column sums (lss_cat_cast_colsum*, lss_layernorm_bwd) with one writer
+ *    per column in a fixed order instead of atomics -- with the fixed-point dQ of
+ *    lss_bwd_source.grad_q_fixed every result is bitwise repeatable run to run
+ *    (the reference's ascending-rank folds, collectives.py:5-7).  A wait past its
+ *    deadline gives up and raises status word 0; a non-finite output raises word 1.
  *  - lss_status copies the two process-wide status words into out[2] (mapped pinned
  *    host memory: no device synchronisation) and optionally clears them.
  *  - lss_check_finite raises word 1 if any of n fp32 / bf16 elements is NaN / Inf
@@ -338,10 +348,14 @@ int lss_peer_access(int device, int peer);
  *  - lss_flag_release writes `value` to `count` flag words from a private
  *    non-blocking stream: a host watchdog releases stream waits (lss_stream_wait)
  *    whose peer is dead, so the caller's streams drain and the host raises CommTimeout. */
-int lss_runtime_config(unsigned long long wait_timeout_ns, int numerics_check);
+int lss_runtime_config(unsigned long long wait_timeout_ns, int flags);
 int lss_status(unsigned int* out, int clear);
 int lss_check_finite(const void* x, long n, int dtype, void* stream);
 int lss_flag_release(unsigned int* flags, long count, unsigned int value);
+#define LSS_RT_NUMERICS 1
+#define LSS_RT_DETERMINISTIC 2
+/* dst (=, or += when accumulate) src * 2^-32: the fixed-point dQ of the deterministic mode. */
+int lss_fixed_to_f32(float* dst, const long long* src, long n, int accumulate, void* stream);
 
 #ifdef __cplusplus
 }

@@ -66,7 +66,7 @@ class BwdSource(ctypes.Structure):
     _fields_ = [
         ("q", _P), ("grad_o", _P), ("grad_q", _P), ("m_src", _I), ("row0", _I), ("rows", _I),
         ("pos0", _L), ("g_begin", _I), ("g_end", _I), ("lse2", _P), ("delta", _P), ("pitch", _I),
-        ("ready", _P), ("ready_seq", ctypes.c_uint),
+        ("ready", _P), ("ready_seq", ctypes.c_uint), ("grad_q_fixed", _P),
     ]
 
 
@@ -113,6 +113,7 @@ SIGNATURES = {
     "lss_status": [ctypes.POINTER(ctypes.c_uint), _I],
     "lss_check_finite": [_P, _L, _I, _P],
     "lss_flag_release": [_P, _L, ctypes.c_uint],
+    "lss_fixed_to_f32": [_P, _P, _L, _I, _P],
 }
 ACT_NONE, ACT_GELU, ACT_GELU_BWD = 0, 1, 2
 EXTRA = {
@@ -121,7 +122,7 @@ EXTRA = {
     "lss_rows_pad": ([_L], _L),
     "lss_peer_access": ([_I, _I], _I),
 }
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 _lib = None
 
@@ -159,7 +160,7 @@ KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 
                     "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1,
                     "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1,
                     "lss_dropout_rows": 1, "lss_attn_fwd_split": 1, "lss_sum_slots_mask": 1, "lss_cat_cast_colsum_ex": 1,
-                    "lss_check_finite": 1}
+                    "lss_check_finite": 1, "lss_fixed_to_f32": 1}
 launch_count = 0
 
 

@@ -63,6 +63,7 @@ struct BwdSource {
   int pitch;
   int m_src;           // rows of the [B][m_src][E] tensors
   float* dq;           // fp32 [B][m_src][E], accumulated with vector reductions
+  long long* dq_fixed; // deterministic mode: int64 [B][m_src][E], round(dQ * 2^32), integer adds
   const uint32_t* ready;  // non-null: inputs pushed by a partner, usable once *ready >= ready_seq
   uint32_t ready_seq;
 };
@@ -584,6 +585,40 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       mbar_wait(&dq_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
       if (r == 0) BWD_TRACE(5, it);
+      {
+        int src, q0;
+        locate(it, src, q0);
+        long long* fx = p.src[src].dq_fixed;
+        if (fx != nullptr) {
+          // Deterministic mode: this key tile's dQ contribution as int64 fixed point
+          // (scale 2^32), added with integer bulk reductions -- associative, so the
+          // sum over key tiles is bitwise identical whatever order the CTAs finish in.
+          // Thread r owns row r of the staging buffer (128 rows x 32 int64 per half).
+          const bool row_ok = q0 + r < p.src[src].m_src;
+          long long* grow = fx + ((long)b * p.src[src].m_src + q0 + r) * ((long)p.H * ATT_D) + h * ATT_D;
+          const uint32_t srow = smem_u32(sStage + r * 256);
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t v[32];
+            tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
+            if (hh == 1) {
+              tc_fence_before();
+              mbar_arrive(&dq_empty[it & 1]);
+            }
+            bulk_wait_read0();  // this thread's previous reduce has read its staging row
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const long long e0 = __float2ll_rn(__uint_as_float(v[2 * c]) * 4294967296.f);
+              const long long e1 = __float2ll_rn(__uint_as_float(v[2 * c + 1]) * 4294967296.f);
+              asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(srow + c * 16), "l"(e0), "l"(e1) : "memory");
+            }
+            fence_proxy_async_smem();
+            if (row_ok) bulk_reduce_add_u64(grow + hh * 32, sStage + r * 256, 256);
+            bulk_commit();
+          }
+          continue;
+        }
+      }
       if (issuer) bulk_wait_read0();  // previous reduce has finished reading the staging tile
       named_bar_sync(1, 128);
 #pragma unroll
@@ -617,7 +652,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         bulk_commit();
       }
     }
-    if (issuer) bulk_wait0();
+    bulk_wait0();  // the issuer's tensor reduces / every thread's fixed-point row reduces
   }
 
   tc_fence_before();

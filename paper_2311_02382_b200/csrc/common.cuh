@@ -176,6 +176,13 @@ LSS_DEV void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) 
       "r"(smem_u32(ssrc)), "r"(bytes)
       : "memory");
 }
+// bulk (non-tensor) integer add of int64 (two's complement: .u64 add) from shared to global
+LSS_DEV void bulk_reduce_add_u64(long long* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile(
+      "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(gdst),
+      "r"(smem_u32(ssrc)), "r"(bytes)
+      : "memory");
+}
 // tensor (TMA) reduce-add from shared to global, 3-D map
 LSS_DEV void tma_reduce_add_3d(const CUtensorMap* m, const void* smem, int c0, int c1, int c2) {
   asm volatile(

@@ -135,7 +135,7 @@ __global__ void layernorm_bwd_kernel(const float* __restrict__ gxh, const float*
                       res.z + rs * (g2 - mg - xh2 * mgx), res.w + rs * (g3 - mg - xh3 * mgx));
     }
   }
-  if (ok) {
+  if (ok && g_gain) {  // null in the deterministic mode: ln_colsum_det_kernel sums instead
     atomicAdd(g_gain + c + 0, alpha * gg.x); atomicAdd(g_gain + c + 1, alpha * gg.y);
     atomicAdd(g_gain + c + 2, alpha * gg.z); atomicAdd(g_gain + c + 3, alpha * gg.w);
     atomicAdd(g_bias + c + 0, alpha * gb.x); atomicAdd(g_bias + c + 1, alpha * gb.y);
@@ -206,6 +206,99 @@ __global__ void cat_cast_colsum_kernel(CatSrc src, TOut* __restrict__ dst, long 
     atomicAdd(colsum + col4 + 1, alpha * acc.y);
     atomicAdd(colsum + col4 + 2, alpha * acc.z);
     atomicAdd(colsum + col4 + 3, alpha * acc.w);
+  }
+}
+
+// ---------------------------------------------------------------- deterministic column sums
+// Bitwise-repeatable replacements for the atomicAdd column sums above, used in the
+// deterministic mode (lss_runtime_config flag, the reference's run-to-run bitwise
+// reproducibility, collectives.py:5-7): every column has ONE writer; its rows are
+// dealt to DET_LANES row lanes x 4 accumulators in a fixed pattern and combined in
+// a fixed order, so the result does not depend on scheduling.
+constexpr int DET_COLS = 32, DET_LANES = 32;
+
+__device__ __forceinline__ float cat_value(const CatSrc& src, int s, long r, int lc) {
+  const float* sp = src.ptr[s];
+  if (src.nslot[s] <= 1) return sp[r * src.ld[s] + lc];
+  float v = 0.f;  // same ascending slot fold as cat_cast_colsum_kernel
+  for (int k = 0; k < src.nslot[s]; ++k)
+    if ((src.mask[s] >> k) & 1u) v += sp[k * src.slot_stride[s] + r * src.ld[s] + lc];
+  return v;
+}
+
+__global__ void __launch_bounds__(DET_COLS * DET_LANES)
+    colsum_det_kernel(CatSrc src, float* __restrict__ colsum, float alpha, long rows) {
+  __shared__ float part[DET_LANES][DET_COLS + 1];
+  const int cl = threadIdx.x % DET_COLS, rl = threadIdx.x / DET_COLS;
+  const int col = blockIdx.x * DET_COLS + cl;
+  int s = 0, base = 0;
+  while (s < src.n && col >= base + src.cols[s]) base += src.cols[s++];
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (s < src.n) {
+    const int lc = col - base;
+    long r = rl;
+    for (; r + 3 * DET_LANES < rows; r += 4 * DET_LANES) {
+      a0 += cat_value(src, s, r, lc);
+      a1 += cat_value(src, s, r + DET_LANES, lc);
+      a2 += cat_value(src, s, r + 2 * DET_LANES, lc);
+      a3 += cat_value(src, s, r + 3 * DET_LANES, lc);
+    }
+    for (; r < rows; r += DET_LANES) a0 += cat_value(src, s, r, lc);
+  }
+  part[rl][cl] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (rl == 0 && s < src.n) {
+    float t = 0.f;
+    for (int k = 0; k < DET_LANES; ++k) t += part[k][cl];
+    colsum[col] += alpha * t;
+  }
+}
+
+// LayerNorm affine gradients (nnops.py:217-218): g_gain += alpha * sum_r gxh * xhat,
+// g_bias += alpha * sum_r gxh, one writer per column (deterministic mode).
+__global__ void __launch_bounds__(DET_COLS * DET_LANES)
+    ln_colsum_det_kernel(const float* __restrict__ gxh, const float* __restrict__ x,
+                         const float* __restrict__ mean, const float* __restrict__ rstd,
+                         float* __restrict__ g_gain, float* __restrict__ g_bias, float alpha, long rows, int E) {
+  __shared__ float pg[DET_LANES][DET_COLS + 1], pb[DET_LANES][DET_COLS + 1];
+  const int cl = threadIdx.x % DET_COLS, rl = threadIdx.x / DET_COLS;
+  const int col = blockIdx.x * DET_COLS + cl;
+  float g0 = 0.f, g1 = 0.f, b0 = 0.f, b1 = 0.f;
+  if (col < E) {
+    long r = rl;
+    for (; r + DET_LANES < rows; r += 2 * DET_LANES) {
+      const float u = gxh[r * E + col], w = gxh[(r + DET_LANES) * E + col];
+      g0 += u * ((x[r * E + col] - mean[r]) * rstd[r]);
+      g1 += w * ((x[(r + DET_LANES) * E + col] - mean[r + DET_LANES]) * rstd[r + DET_LANES]);
+      b0 += u;
+      b1 += w;
+    }
+    for (; r < rows; r += DET_LANES) {
+      const float u = gxh[r * E + col];
+      g0 += u * ((x[r * E + col] - mean[r]) * rstd[r]);
+      b0 += u;
+    }
+  }
+  pg[rl][cl] = g0 + g1;
+  pb[rl][cl] = b0 + b1;
+  __syncthreads();
+  if (rl == 0 && col < E) {
+    float tg = 0.f, tb = 0.f;
+    for (int k = 0; k < DET_LANES; ++k) {
+      tg += pg[k][cl];
+      tb += pb[k][cl];
+    }
+    g_gain[col] += alpha * tg;
+    g_bias[col] += alpha * tb;
+  }
+}
+
+// dQ of the deterministic backward: int64 fixed point (scale 2^32) -> fp32
+__global__ void fixed_to_f32_kernel(float* __restrict__ dst, const long long* __restrict__ src, long n,
+                                    int accumulate) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const float v = (float)((double)src[i] * 2.3283064365386963e-10);  // 2^-32
+    dst[i] = accumulate ? dst[i] + v : v;
   }
 }
 

@@ -24,6 +24,7 @@ using namespace lss;
 namespace {
 
 thread_local std::string g_last_error;
+int g_deterministic = 0;  // LSS_RT_DETERMINISTIC: column sums without atomics (process-wide)
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -139,8 +140,12 @@ int lss_layernorm_bwd(const float* grad_xh, const float* x, const float* mean, c
   if (rows <= 0) return LSS_OK;
   const int threads = ((embed / 4 + 31) / 32) * 32;
   const long blocks = (rows + LN_BWD_ROWS - 1) / LN_BWD_ROWS;
+  const bool det = g_deterministic != 0;
   layernorm_bwd_kernel<<<blocks, threads, 0, S(stream)>>>(grad_xh, x, mean, rstd, gain, grad_res, grad_x,
-                                                          grad_gain, grad_bias, alpha, rows, embed);
+                                                          det ? nullptr : grad_gain, grad_bias, alpha, rows, embed);
+  if (det)  // one writer per column, fixed order (bitwise repeatable)
+    ln_colsum_det_kernel<<<(embed + DET_COLS - 1) / DET_COLS, DET_COLS * DET_LANES, 0, S(stream)>>>(
+        grad_xh, x, mean, rstd, grad_gain, grad_bias, alpha, rows, embed);
   return check_launch("layernorm_bwd");
 }
 
@@ -280,13 +285,20 @@ int lss_cat_cast_colsum_ex(int out_dtype, const float* const* srcs, const long* 
   cs.n = nsrc;
   if (rows <= 0) return LSS_OK;
   const int threads = 128;
+  const bool det = g_deterministic != 0 && colsum;
   dim3 grid((total / 4 + threads - 1) / threads, (rows + CAT_ROWS - 1) / CAT_ROWS);
-  if (out_dtype == LSS_BF16)
-    cat_cast_colsum_kernel<__nv_bfloat16><<<grid, threads, 0, S(stream)>>>(
-        cs, reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, colsum, alpha, rows);
-  else
-    cat_cast_colsum_kernel<float><<<grid, threads, 0, S(stream)>>>(cs, reinterpret_cast<float*>(dst), ld_dst,
-                                                                   colsum, alpha, rows);
+  float* cs_atomic = det ? nullptr : colsum;
+  if (dst || !det) {
+    if (out_dtype == LSS_BF16)
+      cat_cast_colsum_kernel<__nv_bfloat16><<<grid, threads, 0, S(stream)>>>(
+          cs, reinterpret_cast<__nv_bfloat16*>(dst), ld_dst, cs_atomic, alpha, rows);
+    else
+      cat_cast_colsum_kernel<float><<<grid, threads, 0, S(stream)>>>(cs, reinterpret_cast<float*>(dst), ld_dst,
+                                                                     cs_atomic, alpha, rows);
+  }
+  if (det)  // one writer per column, fixed order (bitwise repeatable)
+    colsum_det_kernel<<<(total + DET_COLS - 1) / DET_COLS, DET_COLS * DET_LANES, 0, S(stream)>>>(cs, colsum, alpha,
+                                                                                                  rows);
   return check_launch("cat_cast_colsum");
 }
 
@@ -493,7 +505,12 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
   memset(&maps, 0, sizeof(maps));
   for (int i = 0; i < nsrc; ++i) {
     const lss_bwd_source& sr = srcs[i];
-    if (!sr.q || !sr.grad_o || !sr.grad_q || !sr.lse2 || !sr.delta) return fail(LSS_ERR_ARG, "source %d: null", i);
+    const bool fixed = sr.grad_q_fixed != nullptr;
+    if (fixed != (srcs[0].grad_q_fixed != nullptr))
+      return fail(LSS_ERR_ARG, "source %d: fixed-point dQ for all sources or none", i);
+    if (!sr.q || !sr.grad_o || (!sr.grad_q && !fixed) || !sr.lse2 || !sr.delta)
+      return fail(LSS_ERR_ARG, "source %d: null", i);
+    if (fixed && !aligned16(sr.grad_q_fixed)) return fail(LSS_ERR_UNSUPPORTED, "source %d: 16B alignment", i);
     if (sr.row0 < 0 || sr.rows <= 0 || sr.row0 + sr.rows > sr.m_src || sr.row0 % ATT_BM ||
         (sr.rows % ATT_BM && sr.row0 + sr.rows != sr.m_src))
       return fail(LSS_ERR_SHAPE, "source %d: rows [%d,%d) of %d must be 128-row aligned", i, sr.row0,
@@ -501,15 +518,15 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
     if (sr.g_begin < 0 || sr.g_end > workers || sr.g_begin >= sr.g_end)
       return fail(LSS_ERR_SHAPE, "source %d: bad segment range", i);
     if (sr.pitch < lss_rows_pad(sr.m_src)) return fail(LSS_ERR_SHAPE, "source %d: lse pitch", i);
-    if (!aligned16(sr.q) || !aligned16(sr.grad_o) || !aligned16(sr.grad_q))
+    if (!aligned16(sr.q) || !aligned16(sr.grad_o) || (!fixed && !aligned16(sr.grad_q)))
       return fail(LSS_ERR_UNSUPPORTED, "source %d: 16B alignment", i);
     if ((rc = map_rows(&maps.q[i], sr.q, E, E, sr.m_src, batch, 1, 3))) return rc;
     if ((rc = map_rows(&maps.dO[i], sr.grad_o, E, E, sr.m_src, batch, 1, 3))) return rc;
     uint64_t dims[3] = {(uint64_t)E, (uint64_t)sr.m_src, (uint64_t)batch};
     uint64_t str[2] = {(uint64_t)E, (uint64_t)sr.m_src * E};
     uint32_t box[3] = {32, 128, 1};
-    if ((rc = make_map(&maps.dq[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, sr.grad_q, dims, str, box,
-                       CU_TENSOR_MAP_SWIZZLE_128B)))
+    if (!fixed && (rc = make_map(&maps.dq[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 3, sr.grad_q, dims, str, box,
+                                 CU_TENSOR_MAP_SWIZZLE_128B)))
       return rc;
     p.src[i].row0 = sr.row0;
     p.src[i].rows = sr.rows;
@@ -521,6 +538,7 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
     p.src[i].pitch = sr.pitch;
     p.src[i].m_src = sr.m_src;
     p.src[i].dq = sr.grad_q;
+    p.src[i].dq_fixed = sr.grad_q_fixed;
     p.src[i].ready = sr.ready;
     p.src[i].ready_seq = sr.ready_seq;
   }
@@ -832,7 +850,7 @@ int lss_attn_bwd(int dtype, const void* q, const void* k, const void* v, long ld
   lss_bwd_source src;
   src.q = q; src.grad_o = grad_o; src.grad_q = grad_q; src.m_src = rows; src.row0 = 0; src.rows = rows;
   src.pos0 = offset; src.g_begin = 0; src.g_end = workers; src.lse2 = lse2; src.delta = delta_ws; src.pitch = m_pad;
-  src.ready = nullptr; src.ready_seq = 0;
+  src.ready = nullptr; src.ready_seq = 0; src.grad_q_fixed = nullptr;
   return lss_attn_bwd_ex(dtype, k, v, ld_kv, &src, 1, grad_k, grad_v, ld_dkv, batch, workers, seg_len, heads,
                          head_dim, causal, nullptr, stream);
 }
@@ -900,7 +918,9 @@ __global__ void check_finite_bf16_kernel(const uint4* x, long n8) {
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) status_raise(1);
 }
 
-int lss_runtime_config(unsigned long long wait_timeout_ns, int numerics_check) {
+int lss_runtime_config(unsigned long long wait_timeout_ns, int flags) {
+  const int numerics_check = (flags & LSS_RT_NUMERICS) ? 1 : 0;
+  g_deterministic = (flags & LSS_RT_DETERMINISTIC) ? 1 : 0;
   int rc = status_words();
   if (rc) return rc;
   unsigned int* dev_words = nullptr;
@@ -940,6 +960,15 @@ int lss_check_finite(const void* x, long n, int dtype, void* stream) {
   else
     check_finite_f32_kernel<<<blocks, threads, 0, S(stream)>>>(reinterpret_cast<const float4*>(x), vec);
   return check_launch("check_finite");
+}
+
+int lss_fixed_to_f32(float* dst, const long long* src, long n, int accumulate, void* stream) {
+  if (!dst || !src) return fail(LSS_ERR_ARG, "fixed_to_f32: null pointer");
+  if (n <= 0) return LSS_OK;
+  const int threads = 256;
+  const long blocks = std::min<long>((n + threads - 1) / threads, 8L * num_sms());
+  fixed_to_f32_kernel<<<blocks, threads, 0, S(stream)>>>(dst, src, n, accumulate);
+  return check_launch("fixed_to_f32");
 }
 
 int lss_flag_release(unsigned int* flags, long count, unsigned int value) {

@@ -620,7 +620,7 @@ class LSSAttention:
         K.cat_cast_colsum([(g_att, E, E)], B * m, dst=self.gy.view(B * m, E), colsum=self.g_bo, alpha=a)
         # dctx = gy . Wo^T  (Wo [in][out] is the K-major B operand)
         K.gemm(self.gy.view(B * m, E), self.staged["wo"], out=self.dctx.view(B * m, E), M=B * m, N=E, K=E)
-        if self.plan.active or self.seg_dst is not None or self._dd is not None:
+        if self.plan.active or self.seg_dst is not None or self._dd is not None or K.deterministic():
             K.attn_delta(self.ctx, self.dctx, self.delta, heads=self.H, scaled=True)
 
     def _wgrad_stream(self) -> torch.cuda.Stream:
@@ -653,21 +653,34 @@ class LSSAttention:
             out = dict(seg_dst=self.seg_dst, peer=self.peer_mem, ld_dkv=2 * E)
         else:
             out = dict(grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:])
-        if not pl.active and self.seg_dst is None and self._dd is None:
+        det = K.deterministic()  # fixed-point dQ (integer adds): bitwise repeatable
+        if not pl.active and self.seg_dst is None and self._dd is None and not det:
             K.attn_bwd(self.q, kf, vf, self.ctx, self.dctx, self.lse2, workers=self.G, seg_len=m,
                        heads=self.H, offset=self.spec.offset, causal=self.cfg.causal, grad_q=self.dq,
                        grad_k=self.dkv_full[..., :E], grad_v=self.dkv_full[..., E:], delta=self.delta)
             return
         own = dict(q=self.q, grad_o=self.dctx, grad_q=self.dq, pos0=self.spec.offset, lse2=self.lse2,
                    delta=self.delta)
-        self.dq.zero_()
+        if det:
+            if getattr(self, "dq64", None) is None:
+                self.dq64 = torch.empty(self.dq.shape, dtype=torch.int64, device=self.device)
+            self.dq64.zero_()
+            own["grad_q_fixed"] = self.dq64
+        else:
+            self.dq.zero_()
         if pl.role == "heavy":
             srcs = [dict(own, row0=0, rows=pl.split, g_begin=pl.a, g_end=r + 1),
                     dict(own, row0=pl.split, rows=m - pl.split, g_begin=pl.b, g_end=r + 1)]
         elif pl.role == "light":
-            self.dq_peer.zero_()
             peer = dict(q=self.q_peer, grad_o=self.do_peer, grad_q=self.dq_peer, pos0=pl.partner * m,
                         lse2=self.lsef_peer, delta=self.delta_peer, ready=peer_ready)
+            if det:
+                if getattr(self, "dq_peer64", None) is None:
+                    self.dq_peer64 = torch.empty(self.dq_peer.shape, dtype=torch.int64, device=self.device)
+                self.dq_peer64.zero_()
+                peer["grad_q_fixed"] = self.dq_peer64
+            else:
+                self.dq_peer.zero_()
             srcs = [dict(own, row0=0, rows=m, g_begin=0, g_end=r + 1),
                     dict(peer, row0=0, rows=pl.split, g_begin=0, g_end=pl.a)]
             if pl.b > 0:
@@ -676,6 +689,10 @@ class LSSAttention:
             srcs = [dict(own, row0=0, rows=m, g_begin=0, g_end=self.G if not self.cfg.causal else r + 1)]
         K.attn_bwd_sources(kf, vf, srcs, workers=self.G, seg_len=m, heads=self.H, causal=self.cfg.causal,
                            dropout=self._dd, **out)
+        if det:
+            K.fixed_to_f32(self.dq, self.dq64)
+            if pl.role == "light":
+                K.fixed_to_f32(self.dq_peer, self.dq_peer64)
 
     def bwd_fold(self) -> None:
         """Heavy rank of the balanced schedule: fold the partner's dQ rows in."""

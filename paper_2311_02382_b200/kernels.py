@@ -259,6 +259,15 @@ def attn_bwd(q, k, v, o, grad_o, lse2, *, workers, seg_len, heads, offset, causa
         raise ShapeError("grad_k / grad_v must be fp32 with a shared row stride")
     dl = delta if delta is not None else torch.empty(bsz, heads, rows_pad(m), dtype=torch.float32,
                                                      device=dev)
+    if deterministic() and dt == LSS_BF16:  # fixed-point dQ: bitwise repeatable
+        attn_delta(o, grad_o, dl, heads=heads, scaled=True)
+        dq64 = torch.zeros(bsz, m, e, dtype=torch.int64, device=dev)
+        src = dict(q=q, grad_o=grad_o, grad_q=gq, grad_q_fixed=dq64, row0=0, rows=m, pos0=offset, g_begin=0,
+                   g_end=workers, lse2=lse2, delta=dl)
+        attn_bwd_sources(k, v, [src], grad_k=grad_k, grad_v=grad_v, workers=workers, seg_len=seg_len, heads=heads,
+                         causal=causal)
+        fixed_to_f32(gq, dq64)
+        return gq, grad_k, grad_v
     call("lss_attn_bwd", dt, _ptr(q), _ptr(k), _ptr(v), ldk, _ptr(o), _ptr(grad_o), _ptr(lse2),
          _ptr(dl), _ptr(gq), _ptr(grad_k), _ptr(grad_v), lddkv, bsz, m, workers, seg_len, heads,
          e // heads, offset, int(causal), _stream())
@@ -342,6 +351,11 @@ def _bwd_source_array(sources):
         arr[i].lse2 = src["lse2"].data_ptr()
         arr[i].delta = src["delta"].data_ptr()
         arr[i].pitch = src["lse2"].shape[-1]
+        fx = src.get("grad_q_fixed")  # deterministic mode: int64 fixed-point dQ accumulator
+        if fx is not None:
+            if fx.dtype != torch.int64 or tuple(fx.shape) != tuple(src["grad_q"].shape):
+                raise ShapeError("grad_q_fixed must be int64 shaped like grad_q")
+            arr[i].grad_q_fixed = fx.data_ptr()
         ready = src.get("ready")  # (flag address, seq): inputs pushed by a partner
         if ready is not None:
             arr[i].ready = int(ready[0])
@@ -514,19 +528,24 @@ def add_(y, x):
 
 # ----------------------------------------------------------------- failure semantics (ABI v9)
 
-_RUNTIME = {"wait_timeout_s": 60.0, "numerics": False}
+_RUNTIME = {"wait_timeout_s": 60.0, "numerics": False, "deterministic": False}
 _CONFIGURED: set = set()
 
 
-def runtime_config(*, wait_timeout_s: float | None = None, numerics: bool | None = None, device=None) -> None:
+def runtime_config(*, wait_timeout_s: float | None = None, numerics: bool | None = None,
+                   deterministic: bool | None = None, device=None) -> None:
     """Deadline of every in-kernel cross-GPU wait (seconds, 0 = unbounded; the
-    reference Communicator's default timeout is 60 s, collectives.py:159) and the
-    opt-in NaN / Inf check in the GEMM / attention epilogues (tensor.py:79-95).
-    Applies to ``device`` (default: current) now and to every device configured later."""
+    reference Communicator's default timeout is 60 s, collectives.py:159), the
+    opt-in NaN / Inf check in the GEMM / attention epilogues (tensor.py:79-95) and
+    the deterministic mode (fixed-point dQ, column sums without atomics: bitwise
+    repeatable runs, collectives.py:5-7).  Applies to ``device`` (default: current)
+    now and to every device configured later."""
     if wait_timeout_s is not None:
         _RUNTIME["wait_timeout_s"] = float(wait_timeout_s)
     if numerics is not None:
         _RUNTIME["numerics"] = bool(numerics)
+    if deterministic is not None:
+        _RUNTIME["deterministic"] = bool(deterministic)
     _CONFIGURED.clear()
     ensure_runtime(device)
 
@@ -538,13 +557,28 @@ def ensure_runtime(device=None) -> None:
         d = torch.cuda.current_device()
     if d in _CONFIGURED:
         return
+    flags = (1 if _RUNTIME["numerics"] else 0) | (2 if _RUNTIME["deterministic"] else 0)
     with torch.cuda.device(d):
-        call("lss_runtime_config", int(_RUNTIME["wait_timeout_s"] * 1e9), int(_RUNTIME["numerics"]))
+        call("lss_runtime_config", int(_RUNTIME["wait_timeout_s"] * 1e9), flags)
     _CONFIGURED.add(d)
 
 
 def numerics_enabled() -> bool:
     return _RUNTIME["numerics"]
+
+
+def deterministic() -> bool:
+    return _RUNTIME["deterministic"]
+
+
+def fixed_to_f32(dst: torch.Tensor, src: torch.Tensor, accumulate: bool = False) -> torch.Tensor:
+    """dst (=, or += ) src * 2^-32: the int64 fixed-point dQ of the deterministic backward."""
+    _need(dst, "dst", torch.float32)
+    _need(src, "src", torch.int64)
+    if dst.numel() != src.numel():
+        raise ShapeError("fixed_to_f32: sizes differ")
+    call("lss_fixed_to_f32", _ptr(dst), _ptr(src), dst.numel(), int(accumulate), _stream())
+    return dst
 
 
 def status(clear: bool = False) -> tuple:

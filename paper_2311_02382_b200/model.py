@@ -324,10 +324,15 @@ def scores_bwd(cache: ScoreCache, q, k, v, grad_ctx, cfg: ModelConfig, policy=No
         gq = torch.zeros(bsz, m, e, dtype=torch.float32, device=qa.device)
         src = dict(q=qa, grad_o=go, grad_q=gq, row0=0, rows=m, pos0=cache.offset, g_begin=0, g_end=workers,
                    lse2=cache.lse2, delta=delta)
+        dq64 = None
+        if K.deterministic():  # fixed-point dQ: bitwise repeatable
+            dq64 = src["grad_q_fixed"] = torch.zeros(bsz, m, e, dtype=torch.int64, device=qa.device)
         kv = (ka, va) if ka.dim() == 4 else (ka.unsqueeze(0), va.unsqueeze(0))
         gk4, gv4 = (gk, gv) if gk.dim() == 4 else (gk.unsqueeze(0), gv.unsqueeze(0))
         K.attn_bwd_sources(kv[0], kv[1], [src], grad_k=gk4, grad_v=gv4, workers=workers, seg_len=seg, heads=H,
                            causal=cfg.causal, dropout=pol.desc(cache.layer))
+        if dq64 is not None:
+            K.fixed_to_f32(gq, dq64)
         K.checked(gq, packed)
         return gq, gk, gv
     gq, gk, gv = K.attn_bwd(qa, ka, va, cache.ctx, go, cache.lse2, workers=workers, seg_len=seg,

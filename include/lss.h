@@ -248,6 +248,12 @@ int lss_add_f32(float* y, const float* x, long n, void* stream);
  * (sharded.py:144-154 exchanges) on one NVLink domain. */
 int lss_stream_signal(unsigned int* flag, unsigned int value, void* stream);
 int lss_stream_wait(const unsigned int* flag, unsigned int value, void* stream);
+/* Bounded form (ABI v10, the default of the engine's fabric): a one-warp kernel on
+ * `stream` spins until flags[i] >= value for every i < count except i == skip (-1:
+ * none), with the lss_runtime_config deadline and the host abort word
+ * (lss_abort_waits) -- a dead peer raises CommTimeout / an abort CommAborted
+ * instead of parking the stream forever (collectives.py:200-253). */
+int lss_stream_wait_bounded(const unsigned int* flags, int count, int skip, unsigned int value, void* stream);
 
 /* Diagnostic: stream-ordered write of the GPU global timer (ns) to *dst. */
 int lss_timestamp(unsigned long long* dst, void* stream);
@@ -352,6 +358,9 @@ int lss_runtime_config(unsigned long long wait_timeout_ns, int flags);
 int lss_status(unsigned int* out, int clear);
 int lss_check_finite(const void* x, long n, int dtype, void* stream);
 int lss_flag_release(unsigned int* flags, long count, unsigned int value);
+/* Host-side abort (1) / re-arm (0): every bounded wait (lss_stream_wait_bounded and the
+ * in-kernel waits) returns at once while set (Communicator.abort, collectives.py:200-209). */
+int lss_abort_waits(int on);
 #define LSS_RT_NUMERICS 1
 #define LSS_RT_DETERMINISTIC 2
 /* dst (=, or += when accumulate) src * 2^-32: the fixed-point dQ of the deterministic mode. */

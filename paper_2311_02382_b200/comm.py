@@ -29,14 +29,11 @@ Communicator plays): rank-ordered concatenation / ascending-rank sums.
 
 from __future__ import annotations
 
-import threading
-import time
-from collections import deque
 from dataclasses import dataclass, field
 
 import torch
 
-from .errors import CommTimeout
+from .errors import CommAborted
 
 
 @dataclass
@@ -74,7 +71,8 @@ class TorchDistComm:
     (seq x data), used for the single folded gradient all-reduce."""
 
     def __init__(self, seq_group=None, world_group=None, ledger: Ledger | None = None,
-                 seq_name="sequence", world_name="world", *, use_flags: bool = True, timeout: float = 60.0):
+                 seq_name="sequence", world_name="world", *, use_flags: bool = True, timeout: float = 60.0,
+                 bounded_waits: bool = True):
         import torch.distributed as dist
 
         self.dist = dist
@@ -91,10 +89,13 @@ class TorchDistComm:
         # cross-GPU dependencies as stream-signal flag boards over IPC (no NCCL kernel);
         # False restores NCCL's one-element all-reduce barrier
         self.use_flags = use_flags
-        # a peer that never signals: in-kernel waits give up after `timeout` (device
-        # deadline), stream waits are released by the watchdog; both -> CommTimeout
+        # a peer that never signals: every wait on a flag (a one-warp spin kernel, or the
+        # attention kernels' in-kernel waits) gives up after `timeout` -> CommTimeout, and
+        # abort() releases them at once -> CommAborted.  bounded_waits=False uses the
+        # front-end cuStreamWaitValue32 (no SM while waiting, but no deadline).
         self.timeout = timeout
-        self._watchdog = None
+        self.bounded_waits = bounded_waits
+        self._aborted = None
 
     def _ipc_capable(self) -> bool:
         """CUDA IPC data plane available: GPU processes whose process group is NCCL, or
@@ -209,28 +210,36 @@ class TorchDistComm:
             torch.cuda.synchronize()  # zeroed before any peer can signal into it
             addrs = self.map_named({"board": board})
             self._board = False if addrs is None else (board, [a["board"] for a in addrs])
-            if self._board is not False:
-                self._watchdog = WaitWatchdog(self.timeout, self._release_board)
         return self._board is not False
 
-    def _release_board(self) -> None:
-        """Watchdog action: satisfy every pending and future wait on this rank's flag
-        words so the parked streams drain (the step's results are void)."""
+    def abort(self, exc: BaseException | None = None) -> None:
+        """Communicator.abort (collectives.py:200-209): release every bounded wait of
+        this process at once; later check() / steps raise CommAborted."""
         from . import kernels as K
 
-        top = max(self._seq.values(), default=0)
-        board = self._board[0]
-        K.flag_release(board.data_ptr(), board.numel(), top + (1 << 30))
+        self._aborted = exc if exc is not None else RuntimeError("aborted")
+        K.abort_waits(True)
 
     def check(self) -> None:
-        """Raise CommTimeout if a wait of this communicator (stream or in-kernel) ran
-        past the deadline (collectives.py:242-252).  Host-only, no synchronisation."""
+        """Raise CommAborted after abort(), CommTimeout if a wait of a previous step ran
+        past its deadline (collectives.py:242-252).  Host-only, no synchronisation."""
         from . import kernels as K
 
-        if self._watchdog is not None:
-            self._watchdog.check()
+        if self._aborted is not None:
+            raise CommAborted("communicator aborted") from self._aborted
         if self._board:
             K.raise_status(clear=True)
+
+    def _wait(self, base: int, count: int, skip: int, seq: int, stream=None) -> None:
+        """Stream-ordered wait for flag words [base, base + 4*count) (except ``skip``)."""
+        from . import kernels as K
+
+        if self.bounded_waits:
+            K.stream_wait_bounded(base, count, skip, seq, stream)
+        else:
+            for p in range(count):
+                if p != skip:
+                    K.stream_wait(base + 4 * p, seq, stream)
 
     def _flag_addr(self, rank: int, channel: int, source: int) -> int:
         return self._board[1][rank] + 4 * (channel * self.seq_size + source)
@@ -246,10 +255,7 @@ class TorchDistComm:
         for p in range(self.seq_size):
             if p != me:
                 K.stream_signal(self._flag_addr(p, channel, me), seq, stream)
-        for p in range(self.seq_size):
-            if p != me:
-                K.stream_wait(self._flag_addr(me, channel, p), seq, stream)
-        self._watchdog.track(stream or torch.cuda.current_stream(), f"barrier {channel} #{seq}")
+        self._wait(self._flag_addr(me, channel, 0), self.seq_size, me, seq, stream)
 
     def notify(self, peer: int, channel: int, stream=None) -> None:
         """Signal `peer` on `channel` once everything enqueued on `stream` is done."""
@@ -262,7 +268,7 @@ class TorchDistComm:
         """Handle whose wait() blocks the caller's current stream until `peer`'s next
         notify on `channel` (the NCCL Work.wait() contract)."""
         seq = self._seq[("in", channel, peer)] = self._seq.get(("in", channel, peer), 0) + 1
-        return _FlagWait(self._flag_addr(self.seq_rank, channel, peer), seq, self._watchdog)
+        return _FlagWait(self, self._flag_addr(self.seq_rank, channel, peer), seq)
 
     def push_stream(self) -> torch.cuda.Stream:
         if getattr(self, "_push_stream", None) is None:
@@ -371,60 +377,11 @@ class TorchDistComm:
 class _FlagWait:
     """Pending stream signal (see TorchDistComm.expect)."""
 
-    def __init__(self, addr: int, seq: int, watchdog=None):
-        self.addr, self.seq, self.watchdog = addr, seq, watchdog
+    def __init__(self, comm, addr: int, seq: int):
+        self.comm, self.addr, self.seq = comm, addr, seq
 
     def wait(self) -> None:
-        from . import kernels as K
-
-        K.stream_wait(self.addr, self.seq)
-        if self.watchdog is not None:
-            self.watchdog.track(torch.cuda.current_stream(), f"hand-off #{self.seq}")
-
-
-class WaitWatchdog:
-    """Bounds the front-end stream waits, which cannot time out by themselves
-    (cuStreamWaitValue32): after every wait the waiting stream records an event, and a
-    daemon thread checks that each event completes within ``timeout`` seconds.  If one
-    does not, it calls ``release`` (write every flag word of this rank, so every parked
-    stream drains) and remembers the failure; :meth:`check` then raises CommTimeout --
-    the reference's rendezvous timeout (collectives.py:242-252) for the stream-signal
-    protocol.  Healthy waits cost one event record each."""
-
-    def __init__(self, timeout: float, release, poll: float = 0.05):
-        self.timeout, self.release, self.poll = timeout, release, poll
-        self._pending = deque()
-        self._lock = threading.Lock()
-        self.fired = None
-        self._thread = None
-        self._device = torch.cuda.current_device()
-
-    def track(self, stream: torch.cuda.Stream, what: str) -> None:
-        ev = torch.cuda.Event()
-        ev.record(stream)
-        with self._lock:
-            self._pending.append((ev, time.monotonic(), what))
-            if self._thread is None:
-                self._thread = threading.Thread(target=self._run, name="lss-watchdog", daemon=True)
-                self._thread.start()
-
-    def _run(self) -> None:
-        torch.cuda.set_device(self._device)
-        while self.fired is None:
-            time.sleep(self.poll)
-            with self._lock:
-                while self._pending and self._pending[0][0].query():
-                    self._pending.popleft()
-                head = self._pending[0] if self._pending else None
-            if head is not None and time.monotonic() - head[1] > self.timeout:
-                self.fired = f"{head[2]} not satisfied within {self.timeout}s (a peer is dead or out of step)"
-                self.release()
-                with self._lock:
-                    self._pending.clear()
-
-    def check(self) -> None:
-        if self.fired is not None:
-            raise CommTimeout(self.fired)
+        self.comm._wait(self.addr, 1, -1, self.seq)
 
 
 class SoloComm:

@@ -42,7 +42,15 @@ constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;                 // dS^T tile: 2
 constexpr int ATB_STG_BYTES = 128 * 64 * 4;                      // dQ staging [128 q][64] fp32 (2 SW128 halves)
 constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES + ATB_STG_BYTES +
                          1024 + 256;
-constexpr int ATB_EW = 2;                          // elementwise warpgroups (4 measured slower)
+#ifndef LSS_BWD_EW
+#define LSS_BWD_EW 2  // elementwise warpgroups (A/B builds: 4 = 32 query columns per thread)
+#endif
+constexpr int ATB_EW = LSS_BWD_EW;
+// setmaxnreg budgets (control WG, elementwise WGs, dQ-drain WG): sum <= 64K registers
+constexpr int ATB_REG_CTRL = 56;
+constexpr int ATB_REG_EW = ATB_EW == 2 ? 184 : 96;
+constexpr int ATB_REG_DRAIN = ATB_EW == 2 ? 80 : 64;
+static_assert(128 * (ATB_REG_CTRL + ATB_REG_DRAIN) + 128 * ATB_EW * ATB_REG_EW <= 65536, "register budget");
 constexpr int ATB_NC = 128 / ATB_EW;                // query columns per elementwise thread
 constexpr int ATB_THREADS = 128 * (2 + ATB_EW);     // control WG + EW WGs + dQ-drain WG
 
@@ -129,10 +137,22 @@ template <>
 LSS_DEV void tmem_ld_n<32>(uint32_t taddr, uint32_t (&r)[32]) { tmem_ld32(taddr, r); }
 template <>
 LSS_DEV void tmem_ld_n<64>(uint32_t taddr, uint32_t (&r)[64]) { tmem_ld64(taddr, r); }
+template <>
+LSS_DEV void tmem_ld_n<16>(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : LSS_R8(0), LSS_R8(8)
+      : "r"(taddr)
+      : "memory");
+}
 template <int N>
 LSS_DEV void tmem_st_n(uint32_t taddr, const uint32_t (&r)[N]);
 template <>
 LSS_DEV void tmem_st_n<32>(uint32_t taddr, const uint32_t (&r)[32]) { tmem_st32(taddr, r); }
+template <>
+LSS_DEV void tmem_st_n<16>(uint32_t taddr, const uint32_t (&r)[16]) { tmem_st16(taddr, r); }
 
 template <int NC>
 LSS_DEV void bwd_ld_vec(uint32_t saddr, float (&v)[NC]) {
@@ -182,6 +202,65 @@ LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv
       e.y = ((keep >> (c + 1)) & 1) ? e.y * dscale : 0.f;
     }
     pk[c / 2] = pack_bf16(e.x, e.y);
+  }
+}
+
+// Register-lean variants for 32-column slices (4 elementwise warpgroups): lse2 and
+// the scaled delta are read from shared memory 4 columns at a time (128-bit
+// broadcast loads) instead of being held in 2 x NC registers.
+template <bool MASK, bool DROP, int NC>
+LSS_DEV void bwd_p_s(uint32_t (&sv)[NC], uint32_t s_lse, float sl2, int fv, uint32_t (&pk)[NC / 2],
+                     uint64_t keep = 0, float dscale = 1.f) {
+  const float2 sl2v = make_float2(sl2, sl2);
+#pragma unroll
+  for (int c4 = 0; c4 < NC; c4 += 4) {
+    const float4 l = ld_shared_f4(s_lse + c4 * 4);
+    const float lse[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+    for (int c = c4; c < c4 + 4; c += 2) {
+      const float2 x = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2v,
+                             make_float2(-lse[c - c4], -lse[c - c4 + 1]));
+      float2 e;
+      if (!MASK && ((c / 2) & 7) < LSS_BWD_POLY8) {
+        e = exp2_poly2(x);
+      } else {
+        e = make_float2(ex2(x.x), ex2(x.y));
+      }
+      if (MASK) {
+        e.x = (c >= fv) ? e.x : 0.f;
+        e.y = (c + 1 >= fv) ? e.y : 0.f;
+      }
+      sv[c] = __float_as_uint(e.x);
+      sv[c + 1] = __float_as_uint(e.y);
+      if (DROP) {
+        e.x = ((keep >> c) & 1) ? e.x * dscale : 0.f;
+        e.y = ((keep >> (c + 1)) & 1) ? e.y * dscale : 0.f;
+      }
+      pk[c / 2] = pack_bf16(e.x, e.y);
+    }
+  }
+}
+
+template <int C0, int NH, int NC, bool DROP>
+LSS_DEV void bwd_ds_s(const uint32_t (&pv)[NC], const uint32_t (&dp)[NH], uint32_t s_dsc, float scale,
+                      uint32_t (&dk)[NC / 2], uint64_t keep = 0, float dscale = 1.f) {
+  const float2 scv = make_float2(scale, scale);
+#pragma unroll
+  for (int c4 = 0; c4 < NH; c4 += 4) {
+    const float4 d = ld_shared_f4(s_dsc + (C0 + c4) * 4);
+    const float dsc[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+    for (int c = c4; c < c4 + 4; c += 2) {
+      float2 sc = scv;
+      if (DROP) {
+        sc.x = ((keep >> (C0 + c)) & 1) ? scale * dscale : 0.f;
+        sc.y = ((keep >> (C0 + c + 1)) & 1) ? scale * dscale : 0.f;
+      }
+      const float2 t = ffma2(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), sc,
+                             make_float2(-dsc[c - c4], -dsc[c - c4 + 1]));
+      const float2 ds = fmul2(make_float2(__uint_as_float(pv[C0 + c]), __uint_as_float(pv[C0 + c + 1])), t);
+      dk[(C0 + c) / 2] = pack_bf16(ds.x, ds.y);
+    }
   }
 }
 
@@ -308,7 +387,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
 
   if (warp < 4) {
-    reg_dealloc<56>();
+    reg_dealloc<ATB_REG_CTRL>();
     if (warp == 0) {
       if (n_iter > 0) {
         // ------------------------------------------------ TMA producer (warp-uniform loop)
@@ -446,7 +525,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       }
     }
   } else if (warp < 4 + 4 * ATB_EW) {
-    reg_alloc<184>();
+    reg_alloc<ATB_REG_EW>();
     // ------------------------------------------------ elementwise P^T / dS^T (+ dK/dV epilogue)
     const int qd = (warp - 4) / 4;    // query columns [NC*qd, NC*qd + NC) of each tile
     const int quad = warp % 4;
@@ -465,9 +544,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
       // ---- P^T = 2^(S^T log2e/sqrt(d) - lse2): S_it completing implies dV_{it-1}
       // (the previous reader of the P^T columns) completed.
+      constexpr bool LEAN = NC < 64;  // 4 warpgroups: lse / delta streamed from SMEM
       float lse[NC];  // issued ahead of the S wait: the loads queue behind the tensor
       mbar_wait(&q_full[it & 1], (it >> 1) & 1);  // core's SMEM operand traffic
-      bwd_ld_vec<NC>(s_lse, lse);
+      if constexpr (!LEAN) bwd_ld_vec<NC>(s_lse, lse);
       mbar_wait(s_full, it & 1);
       tc_fence_after();
       if (t == 0 && qd == 0) BWD_TRACE(1, it);
@@ -482,9 +562,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         if (need_mask) {
           const long first_vis = kpos - q0 - qd * NC;
           const int fv = !row_ok ? NC : (p.causal ? (int)max(0L, min((long)NC, first_vis)) : 0);
-          bwd_p<true, DROP, NC>(sv, lse, p.scale_log2, fv, pk, keep, p.drop_scale);
+          if constexpr (LEAN)
+            bwd_p_s<true, DROP, NC>(sv, s_lse, p.scale_log2, fv, pk, keep, p.drop_scale);
+          else
+            bwd_p<true, DROP, NC>(sv, lse, p.scale_log2, fv, pk, keep, p.drop_scale);
         } else {
-          bwd_p<false, DROP, NC>(sv, lse, p.scale_log2, 0, pk, keep, p.drop_scale);
+          if constexpr (LEAN)
+            bwd_p_s<false, DROP, NC>(sv, s_lse, p.scale_log2, 0, pk, keep, p.drop_scale);
+          else
+            bwd_p<false, DROP, NC>(sv, lse, p.scale_log2, 0, pk, keep, p.drop_scale);
         }
         if (t == 0 && qd == 0) BWD_TRACE(13, it);
         tmem_st_n<NC / 2>(tS + lane_off + qd * NC, pk);
@@ -496,7 +582,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       // (TMEM dS^T reader) completed; dQ_{it-2} (SMEM buffer it&1 reader) runs after
       // dP_it and signals ds_free.
       float dsc[NC];  // delta loads issued before the dP wait (same reason as lse)
-      bwd_ld_vec<NC>(s_dsc, dsc);
+      if constexpr (!LEAN) bwd_ld_vec<NC>(s_dsc, dsc);
       mbar_wait(dp_full, it & 1);
       tc_fence_after();
       if (t == 0 && qd == 0) BWD_TRACE(3, it);
@@ -505,12 +591,18 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         {  // dP^T in two halves keeps p, delta and dP within the register budget
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC, dp);
-          bwd_ds<0, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
+          if constexpr (LEAN)
+            bwd_ds_s<0, NC / 2, NC, DROP>(sv, dp, s_dsc, p.scale, dk, keep, p.drop_scale);
+          else
+            bwd_ds<0, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
         }
         {
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
-          bwd_ds<NC / 2, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
+          if constexpr (LEAN)
+            bwd_ds_s<NC / 2, NC / 2, NC, DROP>(sv, dp, s_dsc, p.scale, dk, keep, p.drop_scale);
+          else
+            bwd_ds<NC / 2, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
         }
         if (t == 0 && qd == 0) BWD_TRACE(9, it);
         if (it > 1) mbar_wait(&ds_free[it & 1], ((it >> 1) - 1) & 1);
@@ -573,7 +665,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       }
     }
   } else {
-    reg_dealloc<80>();
+    reg_dealloc<ATB_REG_DRAIN>();
     // ------------------------------------------------ dQ drain: TMEM -> swizzled SMEM -> TMA reduce-add
     const int quad = warp % 4;
     const int r = quad * 32 + lane;  // query row within tile == TMEM lane

@@ -119,22 +119,39 @@ LSS_DEV void report_nonfinite(bool bad) {
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) status_raise(1);
 }
 
+// Word [2] is written by the HOST: a communicator abort (collectives.py:200-209)
+// releases every wait at once.
+LSS_DEV bool host_aborted() {
+  const unsigned int* w = g_status_word;
+  unsigned int v = 0;
+  if (w) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(w + 2) : "memory");
+  return v != 0;
+}
+
 // Spin until the stream-signalled word reaches seq (wrap-safe), then order later
 // async-proxy (TMA) reads after it.  Bounded: past g_wait_timeout_ns the wait gives
-// up and raises the comm-timeout status word (a dead or out-of-step peer turns into
-// CommTimeout on the host instead of a hung GPU; the results of that step are void).
-LSS_DEV void wait_flag_geq(const uint32_t* p, uint32_t seq) {
+// up and raises the comm-timeout status word, and a host abort ends it at once (a
+// dead or out-of-step peer turns into CommTimeout / CommAborted on the host instead
+// of a hung GPU; the results of that step are void).
+LSS_DEV bool wait_flag_geq(const uint32_t* p, uint32_t seq) {
+  bool ok = true;
   if ((int)(ld_acquire_sys(p) - seq) < 0) {
     const unsigned long long lim = g_wait_timeout_ns, t0 = globaltimer_ns();
     while ((int)(ld_acquire_sys(p) - seq) < 0) {
       __nanosleep(256);
+      if (host_aborted()) {
+        ok = false;
+        break;
+      }
       if (lim && globaltimer_ns() - t0 > lim) {
         status_raise(0);
+        ok = false;
         break;
       }
     }
   }
   fence_proxy_async_global();
+  return ok;
 }
 LSS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 LSS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

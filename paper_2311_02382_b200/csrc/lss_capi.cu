@@ -807,6 +807,20 @@ int lss_stream_wait(const unsigned int* flag, unsigned int value, void* stream) 
   return LSS_OK;
 }
 
+// Bounded stream wait: one thread spins (system-scope acquire loads, nanosleep) until
+// every flag word except `skip` reaches `value`, the wait deadline passes or the host
+// aborts -- the cuStreamWaitValue32 wait cannot time out or be released.
+__global__ void wait_flags_kernel(const unsigned int* flags, int count, int skip, unsigned int value) {
+  for (int i = 0; i < count; ++i)
+    if (i != skip && !wait_flag_geq(flags + i, value)) break;
+}
+
+int lss_stream_wait_bounded(const unsigned int* flags, int count, int skip, unsigned int value, void* stream) {
+  if (!flags || count < 1) return fail(LSS_ERR_ARG, "stream_wait_bounded: no flags");
+  wait_flags_kernel<<<1, 32, 0, S(stream)>>>(flags, count, skip, value);
+  return check_launch("stream_wait_bounded");
+}
+
 int lss_peer_access(int device, int peer) {
   if (device == peer) return 1;  // two processes on one GPU: CUDA IPC maps the memory directly
   int ok = 0;
@@ -960,6 +974,13 @@ int lss_check_finite(const void* x, long n, int dtype, void* stream) {
   else
     check_finite_f32_kernel<<<blocks, threads, 0, S(stream)>>>(reinterpret_cast<const float4*>(x), vec);
   return check_launch("check_finite");
+}
+
+int lss_abort_waits(int on) {
+  int rc = status_words();
+  if (rc) return rc;
+  reinterpret_cast<volatile unsigned int*>(g_status_host)[2] = on ? 1u : 0u;
+  return LSS_OK;
 }
 
 int lss_fixed_to_f32(float* dst, const long long* src, long n, int accumulate, void* stream) {

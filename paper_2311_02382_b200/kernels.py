@@ -415,6 +415,19 @@ def stream_wait(flag_addr: int, value: int, stream=None) -> None:
     call("lss_stream_wait", ctypes.c_void_p(int(flag_addr)), value & 0xFFFFFFFF, s)
 
 
+def stream_wait_bounded(flags_addr: int, count: int, skip: int, value: int, stream=None) -> None:
+    """Block the stream until every one of ``count`` consecutive flag words (except index
+    ``skip``) reaches value -- a one-warp spin kernel with the runtime deadline and the
+    host abort word (the front-end stream_wait cannot time out)."""
+    s = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    call("lss_stream_wait_bounded", ctypes.c_void_p(int(flags_addr)), int(count), int(skip), value & 0xFFFFFFFF, s)
+
+
+def abort_waits(on: bool = True) -> None:
+    """Host-side abort: every bounded wait (stream or in-kernel) returns at once while set."""
+    call("lss_abort_waits", int(bool(on)))
+
+
 def timestamp(dst):
     """Diagnostic: write the GPU global timer (ns) into the int64 scalar view dst."""
     call("lss_timestamp", _ptr(dst), _stream())

@@ -1,9 +1,10 @@
 """Failure and numerics semantics on the B200 (ABI v9, include/lss.h).
 
-* A cross-GPU wait whose peer never signals does not hang the GPU: in-kernel
-  waits (fused-gather segment flags) give up at their deadline and the host
-  raises CommTimeout (the reference's rendezvous timeout, collectives.py:242-252);
-  front-end stream waits are released by the communicator's watchdog.
+* A cross-GPU wait whose peer never signals does not hang the GPU: every wait
+  on a flag -- the attention kernels' in-kernel waits and the bounded stream
+  waits (one-warp spin kernels) -- gives up at its deadline and the host raises
+  CommTimeout (the reference's rendezvous timeout, collectives.py:242-252); a
+  host abort releases them at once (CommAborted, collectives.py:200-209).
 * With the numerics check on, a NaN / Inf produced by a GEMM or attention kernel
   raises NumericsError (tensor.py:79-95); off, nothing is reported.
 """
@@ -39,36 +40,78 @@ def test_in_kernel_wait_deadline_raises_comm_timeout(runtime):
     out = torch.empty(1, m, E, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(1, H, K.rows_pad(m), device=dev)
     flags = torch.zeros(G, dtype=torch.int32, device=dev)  # segment 0 never arrives
-    t0 = time.monotonic()
     K.attn_fwd_partial(q, kv[..., :E], kv[..., E:], rows=m, row0=0, workers=G, seg_len=m, heads=H, offset=m,
                        causal=True, g_begin=0, g_end=G, out=out, lse2=lse, ready=(flags, 1, 1))
-    torch.cuda.synchronize()  # returns: the producer gave up at the deadline
-    assert time.monotonic() - t0 < 30
+    assert _drain(torch.cuda.current_stream()) < 30  # the producer gave up at the deadline
     with pytest.raises(CommTimeout):
         K.raise_status()
     K.raise_status()  # cleared
 
 
-def test_watchdog_releases_stream_wait(runtime):
+def _drain(stream, limit=30.0):
+    """Poll (no blocking synchronize) until the stream drained; seconds taken."""
+    t0 = time.monotonic()
+    while not stream.query():
+        assert time.monotonic() - t0 < limit, "stream did not drain"
+        time.sleep(0.01)
+    return time.monotonic() - t0
+
+
+def test_bounded_stream_wait_deadline(runtime):
+    """A flag nobody signals: the bounded stream wait (one-warp spin kernel) gives up at
+    the deadline, the stream drains, the host raises CommTimeout."""
     import torch
-    from paper_2311_02382_b200.comm import WaitWatchdog
     from paper_2311_02382_b200.errors import CommTimeout
 
     K = runtime
+    K.runtime_config(wait_timeout_s=0.3)
     flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    flags[2] = 9  # already satisfied; 0, 1 and 3 never are (index 1 is skipped)
     torch.cuda.synchronize()
-    wd = WaitWatchdog(0.3, lambda: K.flag_release(flags.data_ptr(), flags.numel(), 1 << 30))
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
-        K.stream_wait(flags.data_ptr() + 4, 7, s)  # a peer that never signals
-        wd.track(s, "test wait")
+        K.stream_wait_bounded(flags.data_ptr(), 4, 1, 7, s)
         y = torch.ones(8, device="cuda") * 2
-    t0 = time.monotonic()
-    s.synchronize()  # drains once the watchdog released the flag words
-    assert time.monotonic() - t0 < 30
+    assert _drain(s) < 20
     assert float(y.sum()) == 16.0
     with pytest.raises(CommTimeout):
-        wd.check()
+        K.raise_status()
+
+
+def test_host_abort_releases_waits(runtime):
+    """Communicator.abort semantics: with a long deadline, the host abort word releases
+    a parked wait at once (collectives.py:200-209)."""
+    import torch
+
+    K = runtime
+    K.runtime_config(wait_timeout_s=120.0)
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    K.stream_wait_bounded(flags.data_ptr(), 1, -1, 5, s)
+    time.sleep(0.3)
+    assert not s.query()  # still parked
+    K.abort_waits(True)
+    try:
+        assert _drain(s) < 20
+    finally:
+        K.abort_waits(False)
+    assert K.status(clear=True) == (False, False)  # an abort is not a timeout
+
+
+def test_bounded_wait_satisfied_by_signal(runtime):
+    """The normal path: a stream signal on another stream satisfies the bounded wait."""
+    import torch
+
+    K = runtime
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    s, t = torch.cuda.Stream(), torch.cuda.Stream()
+    K.stream_wait_bounded(flags.data_ptr(), 2, -1, 3, s)
+    K.stream_signal(flags.data_ptr(), 3, t)
+    K.stream_signal(flags.data_ptr() + 4, 4, t)
+    assert _drain(s) < 20
+    assert K.status(clear=True) == (False, False)
 
 
 def test_numerics_check_raises_on_nonfinite(runtime):

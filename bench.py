@@ -148,7 +148,7 @@ class ClockSampler:
 # ------------------------------------------------------------------ reference / CPU arm
 
 
-def host_info():
+def host_info(kind="port"):
     """CPU model, numpy and BLAS of the host the CPU legs ran on."""
     import platform
 
@@ -169,9 +169,10 @@ def host_info():
         blas = f"{b.get('name')} {b.get('version')}"
     except Exception:  # noqa: BLE001 - informational only
         pass
+    prec = ("the reference's own 'single' path (scores and softmax promoted to fp64 under NumPy 2, SURVEY §0.7)"
+            if kind == "reference" else "fp32 numpy port of the reference's functions (oracle/lss_oracle.py)")
     return {"cpu_model": model, "host_cpus": os.cpu_count(), "numpy": np.__version__, "blas": blas,
-            "reference_precision": "fp32 numpy port of the reference's functions (the reference's own 'single' "
-                                   "path promotes scores to fp64 under NumPy 2, SURVEY §0.7)"}
+            "precision": prec}
 
 
 
@@ -270,7 +271,7 @@ def run_reference(args):
         "config": {"workload": workload(args), "global_batch": args.batch, "seq_len": args.seq,
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
-                         "sample": desc, **host_info()},
+                         "sample": desc, **host_info(kind)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -506,7 +507,7 @@ def main_ours(args):
             if dt >= 10.0 or reps >= 50:
                 break
         cpu = {"value": B * args.cpu_rows * reps / dt, "unit": "tokens/s", "cores": threads, "kind": kind,
-               "sample": f"{reps} x " + desc, "seconds": dt, **host_info()}
+               "sample": f"{reps} x " + desc, "seconds": dt, **host_info(kind)}
 
     if rank == 0:
         line = {

@@ -47,10 +47,24 @@ constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 *
 #endif
 constexpr int ATB_EW = LSS_BWD_EW;
 // setmaxnreg budgets (control WG, elementwise WGs, dQ-drain WG): sum <= 64K registers
-constexpr int ATB_REG_CTRL = 56;
-constexpr int ATB_REG_EW = ATB_EW == 2 ? 184 : 96;
-constexpr int ATB_REG_DRAIN = ATB_EW == 2 ? 80 : 64;
-static_assert(128 * (ATB_REG_CTRL + ATB_REG_DRAIN) + 128 * ATB_EW * ATB_REG_EW <= 65536, "register budget");
+// setmaxnreg.inc draws only on what the CTA's .dec warps released: with the launch
+// allocation A = 65536 / threads rounded down to 8 (128 at EW=2, 80 at EW=4),
+// 128*(A-CTRL) + 128*(A-DRAIN) >= 128*EW*(EW_REGS - A), or the .inc waits forever
+#ifndef LSS_BWD_REG_CTRL
+#define LSS_BWD_REG_CTRL (LSS_BWD_EW == 2 ? 56 : 40)
+#endif
+#ifndef LSS_BWD_REG_DRAIN
+#define LSS_BWD_REG_DRAIN (LSS_BWD_EW == 2 ? 80 : 56)
+#endif
+#ifndef LSS_BWD_REG_EW
+#define LSS_BWD_REG_EW (LSS_BWD_EW == 2 ? 184 : 96)
+#endif
+constexpr int ATB_REG_CTRL = LSS_BWD_REG_CTRL;
+constexpr int ATB_REG_EW = LSS_BWD_REG_EW;
+constexpr int ATB_REG_DRAIN = LSS_BWD_REG_DRAIN;
+constexpr int ATB_REG_LAUNCH = (65536 / (128 * (2 + ATB_EW))) / 8 * 8;
+static_assert((ATB_REG_LAUNCH - ATB_REG_CTRL) + (ATB_REG_LAUNCH - ATB_REG_DRAIN) >=
+                  ATB_EW * (ATB_REG_EW - ATB_REG_LAUNCH), "setmaxnreg: the elementwise warps would wait forever");
 constexpr int ATB_NC = 128 / ATB_EW;                // query columns per elementwise thread
 constexpr int ATB_THREADS = 128 * (2 + ATB_EW);     // control WG + EW WGs + dQ-drain WG
 

@@ -150,10 +150,15 @@ def test_reference_layer_with_b200_attention_core(cuda, seqpar, precision):
     tol = 1e-2 if precision == "bf16" else 1e-4
     assert_close_ref(y1, y0, tol, "y")
     assert_close_ref(dx1, dx0, tol, "dx")
-    for (n, a), (_, b) in zip(g1.named_arrays(), g0.named_arrays()):
-        if n == "attn_k.bias":
-            continue
-        assert_close_ref(a, b, tol, n)
+    for n in ("ln1_gain", "ln1_bias", "attn_q", "attn_k", "attn_v", "attn_out", "ln2_gain", "ln2_bias", "ff_in",
+              "ff_out"):
+        a, b = getattr(g1, n), getattr(g0, n)
+        pairs = [(n, a, b)] if isinstance(a, np.ndarray) else [(n + ".weight", a.weight, b.weight),
+                                                                 (n + ".bias", a.bias, b.bias)]
+        for name, ga, gb in pairs:
+            if name == "attn_k.bias":  # mathematically zero (softmax shift invariance)
+                continue
+            assert_close_ref(ga, gb, tol, name)
 
 
 def test_reference_sharded_engine_with_b200_attention_core(cuda, seqpar):
@@ -175,4 +180,7 @@ def test_reference_sharded_engine_with_b200_attention_core(cuda, seqpar):
         restore()
     assert np.allclose(got.step_losses, ref.step_losses, rtol=1e-4)
     for (n, a), (_, b) in zip(got.workers[0].params.named_arrays(), ref.workers[0].params.named_arrays()):
+        if n.endswith("attn_k.bias"):  # its gradient is mathematically zero: both sides are rounding noise
+            assert np.abs(a - b).max() < 1e-6
+            continue
         assert_close_ref(a, b, 1e-4, n)

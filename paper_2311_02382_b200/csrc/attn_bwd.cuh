@@ -46,10 +46,7 @@ constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 *
 #define LSS_BWD_EW 2  // elementwise warpgroups (A/B builds: 4 = 32 query columns per thread)
 #endif
 constexpr int ATB_EW = LSS_BWD_EW;
-#ifndef LSS_BWD_PP
-#define LSS_BWD_PP 0  // 1: the ping-pong kernel of attn_bwd_pp.cuh (64-query sub-tiles, two in flight)
-#endif
-constexpr int ATB_Q_BOX = LSS_BWD_PP ? 64 : 128;  // query rows per Q / dO TMA box
+
 // setmaxnreg budgets (control WG, elementwise WGs, dQ-drain WG): sum <= 64K registers
 // setmaxnreg.inc draws only on what the CTA's .dec warps released: with the launch
 // allocation A = 65536 / threads rounded down to 8 (128 at EW=2, 80 at EW=4),

@@ -14,7 +14,6 @@
 
 #include "../../include/lss.h"
 #include "attn_bwd.cuh"
-#include "attn_bwd_pp.cuh"
 #include "attn_fwd.cuh"
 #include "check_f32.cuh"
 #include "elementwise.cuh"
@@ -522,8 +521,8 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
     if (sr.pitch < lss_rows_pad(sr.m_src)) return fail(LSS_ERR_SHAPE, "source %d: lse pitch", i);
     if (!aligned16(sr.q) || !aligned16(sr.grad_o) || (!fixed && !aligned16(sr.grad_q)))
       return fail(LSS_ERR_UNSUPPORTED, "source %d: 16B alignment", i);
-    if ((rc = map_rows(&maps.q[i], sr.q, E, E, sr.m_src, batch, 1, 3, ATB_Q_BOX))) return rc;
-    if ((rc = map_rows(&maps.dO[i], sr.grad_o, E, E, sr.m_src, batch, 1, 3, ATB_Q_BOX))) return rc;
+    if ((rc = map_rows(&maps.q[i], sr.q, E, E, sr.m_src, batch, 1, 3))) return rc;
+    if ((rc = map_rows(&maps.dO[i], sr.grad_o, E, E, sr.m_src, batch, 1, 3))) return rc;
     uint64_t dims[3] = {(uint64_t)E, (uint64_t)sr.m_src, (uint64_t)batch};
     uint64_t str[2] = {(uint64_t)E, (uint64_t)sr.m_src * E};
     uint32_t box[3] = {32, 128, 1};
@@ -558,15 +557,11 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
   p.drop_scale = drop ? dropout->scale : 1.f;
   if (seg_tab)
     for (int g = 0; g < workers; ++g) p.seg_tab[g] = seg_tab[g];
-#if LSS_BWD_PP
-  if ((rc = set_smem(drop ? attn_bwd_pp_kernel<true> : attn_bwd_pp_kernel<false>, ATP_SMEM))) return rc;
-#else
   if (drop) {
     if ((rc = set_smem(attn_bwd_tc_kernel<true>, ATB_SMEM))) return rc;
   } else if ((rc = set_smem(attn_bwd_tc_kernel<false>, ATB_SMEM))) {
     return rc;
   }
-#endif
   const int tps = (seg_len + ATT_BN - 1) / ATT_BN;
   // fused reduce-scatter: only the key segments some source reads get a CTA (the
   // owners sum just their writers' slots, lss_sum_slots_mask); the local layout
@@ -582,17 +577,10 @@ static int attn_bwd_launch(const void* k, const void* v, long ld_kv, const lss_b
   }
   p.g_lo = g_lo;
   dim3 grid((g_hi - g_lo) * tps, heads, batch);
-#if LSS_BWD_PP
-  if (drop)
-    attn_bwd_pp_kernel<true><<<grid, ATB_THREADS, ATP_SMEM, S(stream)>>>(mk, mv, maps, p);
-  else
-    attn_bwd_pp_kernel<false><<<grid, ATB_THREADS, ATP_SMEM, S(stream)>>>(mk, mv, maps, p);
-#else
   if (drop)
     attn_bwd_tc_kernel<true><<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
   else
     attn_bwd_tc_kernel<false><<<grid, ATB_THREADS, ATB_SMEM, S(stream)>>>(mk, mv, maps, p);
-#endif
   return check_launch("attn_bwd_tc");
 }
 

@@ -1140,7 +1140,9 @@ def lss_step(engines, comm, xs, grad_ys, *, step=0, layer=0, sync=True, before_b
     TorchDistComm (or SoloComm for one rank).  Single-process simulation: G
     engines and a SimComm.  Returns the list of (y, dx) per engine (device
     tensors, not synchronised).  ``policy``: dropout (dropout.DropoutPolicy or a
-    rate; None = off), as model.layer_fwd's ``policy, layer``."""
+    rate; None = off), as model.layer_fwd's ``policy, layer`` -- used as given;
+    multi-step drivers derive ``policy.at_step(step).fork(replica)`` per step
+    (hybrid.run_engine_steps, sharded.run_steps)."""
     global last_phases
     if hasattr(comm, "check"):
         comm.check()  # a wait of the previous step ran past its deadline -> CommTimeout

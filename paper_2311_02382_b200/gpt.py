@@ -185,7 +185,11 @@ def gpt_step(ranks, comm, tokens, targets, *, step: int = 0, sync: bool = True, 
     process's [GPTRank] (or G of them with a SimComm); tokens / targets are the
     ranks' (B, m) blocks.  Returns the ranks' loss device scalars (grid mean
     after sync).  ``policy``: dropout (dropout.DropoutPolicy / rate / None), the
-    same masks as the sequential model.forward."""
+    same masks as the sequential model.forward.  Like sharded.forward it is used
+    as given: a multi-step driver derives ``policy.at_step(step)`` (and
+    ``.fork(replica)`` on a D x N grid) per step, as sharded.run_steps /
+    hybrid.run_steps (sharded.py:320, hybrid.py:172-174) and
+    hybrid.run_engine_steps do."""
     L = len(ranks[0].engines)
     xs = [r.embed(t, policy) for r, t in zip(ranks, tokens)]
     for li in range(L):

@@ -299,7 +299,8 @@ def main_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        comm = TorchDistComm(None, None, Ledger())
+        # stream-wait mode for A/B runs (default "guarded"; "kernel" / "frontend")
+        comm = TorchDistComm(None, None, Ledger(), bounded_waits=os.environ.get("LSS_WAITS", "guarded"))
     else:
         comm = SoloComm(Ledger())
     causal = not args.noncausal

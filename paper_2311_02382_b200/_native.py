@@ -116,6 +116,7 @@ SIGNATURES = {
     "lss_fixed_to_f32": [_P, _P, _L, _I, _P],
     "lss_stream_wait_bounded": [_P, _I, _I, ctypes.c_uint, _P],
     "lss_abort_waits": [_I],
+    "lss_stream_wait_guarded": [_P, _I, _I, ctypes.c_uint, _P],
 }
 ACT_NONE, ACT_GELU, ACT_GELU_BWD = 0, 1, 2
 EXTRA = {
@@ -162,7 +163,7 @@ KERNELS_PER_CALL = {"lss_layernorm_fwd": 1, "lss_layernorm_bwd": 1, "lss_gemm": 
                     "lss_attn_bwd_p2p": 1, "lss_sum_slots": 1, "lss_sgd_update": 1, "lss_adam_update": 1,
                     "lss_embed_fwd": 1, "lss_embed_bwd": 1, "lss_cross_entropy": 1,
                     "lss_dropout_rows": 1, "lss_attn_fwd_split": 1, "lss_sum_slots_mask": 1, "lss_cat_cast_colsum_ex": 1,
-                    "lss_check_finite": 1, "lss_fixed_to_f32": 1, "lss_stream_wait_bounded": 1}
+                    "lss_check_finite": 1, "lss_fixed_to_f32": 1, "lss_stream_wait_bounded": 1, "lss_stream_wait_guarded": 1}
 launch_count = 0
 
 

@@ -72,7 +72,7 @@ class TorchDistComm:
 
     def __init__(self, seq_group=None, world_group=None, ledger: Ledger | None = None,
                  seq_name="sequence", world_name="world", *, use_flags: bool = True, timeout: float = 60.0,
-                 bounded_waits: bool = True):
+                 bounded_waits="guarded"):
         import torch.distributed as dist
 
         self.dist = dist
@@ -89,12 +89,15 @@ class TorchDistComm:
         # cross-GPU dependencies as stream-signal flag boards over IPC (no NCCL kernel);
         # False restores NCCL's one-element all-reduce barrier
         self.use_flags = use_flags
-        # a peer that never signals: every wait on a flag (a one-warp spin kernel, or the
-        # attention kernels' in-kernel waits) gives up after `timeout` -> CommTimeout, and
-        # abort() releases them at once -> CommAborted.  bounded_waits=False uses the
-        # front-end cuStreamWaitValue32 (no SM while waiting, but no deadline).
+        # a peer that never signals: every wait on a flag gives up after `timeout` ->
+        # CommTimeout, and abort() releases them at once -> CommAborted.  Stream waits:
+        # "guarded" (default) = front-end cuStreamWaitValue32 + a guard kernel on a
+        # high-priority stream that releases the flags on failure; "kernel" = a spin
+        # kernel on the waiting stream (needs an SM before the stream moves on);
+        # "frontend" = unbounded cuStreamWaitValue32.  The attention kernels' in-kernel
+        # waits always carry the deadline.
         self.timeout = timeout
-        self.bounded_waits = bounded_waits
+        self.waits = {True: "guarded", False: "frontend"}.get(bounded_waits, bounded_waits)
         self._aborted = None
 
     def _ipc_capable(self) -> bool:
@@ -234,7 +237,9 @@ class TorchDistComm:
         """Stream-ordered wait for flag words [base, base + 4*count) (except ``skip``)."""
         from . import kernels as K
 
-        if self.bounded_waits:
+        if self.waits == "guarded":
+            K.stream_wait_guarded(base, count, skip, seq, stream)
+        elif self.waits == "kernel":
             K.stream_wait_bounded(base, count, skip, seq, stream)
         else:
             for p in range(count):

@@ -822,6 +822,52 @@ int lss_stream_wait_bounded(const unsigned int* flags, int count, int skip, unsi
   return check_launch("stream_wait_bounded");
 }
 
+// Guarded front-end wait: the stream waits in the GPU front-end (cuStreamWaitValue32, no
+// SM, released the moment the flag lands), and a one-warp guard kernel on a private
+// high-priority stream watches the same flags: past the deadline, or on a host abort,
+// it raises the status word and writes the flags itself, so the parked stream drains.
+__global__ void guard_flags_kernel(unsigned int* flags, int count, int skip, unsigned int value) {
+  bool ok = true;
+  for (int i = 0; i < count && ok; ++i)
+    if (i != skip) ok = wait_flag_geq(flags + i, value);
+  if (!ok && threadIdx.x == 0)
+    for (int i = 0; i < count; ++i)
+      if (i != skip)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags + i), "r"(value + 0x40000000u) : "memory");
+}
+
+int lss_stream_wait_guarded(unsigned int* flags, int count, int skip, unsigned int value, void* stream) {
+  if (!flags || count < 1) return fail(LSS_ERR_ARG, "stream_wait_guarded: no flags");
+  static PFN_streamValue32 fn = stream_value_fn("cuStreamWaitValue32");
+  if (!fn) return fail(LSS_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> guards;  // one high-priority guard stream per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t gs;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = guards.find(dev);
+    if (it == guards.end()) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (cudaStreamCreateWithPriority(&gs, cudaStreamNonBlocking, hi) != cudaSuccess)
+        return fail(LSS_ERR_CUDA, "stream_wait_guarded: guard stream creation failed");
+      guards[dev] = gs;
+    } else {
+      gs = it->second;
+    }
+  }
+  for (int i = 0; i < count; ++i) {
+    if (i == skip) continue;
+    CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flags + i), value,
+                    CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(LSS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  }
+  guard_flags_kernel<<<1, 32, 0, gs>>>(flags, count, skip, value);
+  return check_launch("stream_wait_guarded");
+}
+
 int lss_peer_access(int device, int peer) {
   if (device == peer) return 1;  // two processes on one GPU: CUDA IPC maps the memory directly
   int ok = 0;

@@ -423,6 +423,14 @@ def stream_wait_bounded(flags_addr: int, count: int, skip: int, value: int, stre
     call("lss_stream_wait_bounded", ctypes.c_void_p(int(flags_addr)), int(count), int(skip), value & 0xFFFFFFFF, s)
 
 
+def stream_wait_guarded(flags_addr: int, count: int, skip: int, value: int, stream=None) -> None:
+    """Front-end waits (no SM, released as soon as the flags land) plus a one-warp guard
+    kernel on a private high-priority stream that, past the deadline or on a host abort,
+    raises the status word and writes the flags itself so the stream drains."""
+    s = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    call("lss_stream_wait_guarded", ctypes.c_void_p(int(flags_addr)), int(count), int(skip), value & 0xFFFFFFFF, s)
+
+
 def abort_waits(on: bool = True) -> None:
     """Host-side abort: every bounded wait (stream or in-kernel) returns at once while set."""
     call("lss_abort_waits", int(bool(on)))

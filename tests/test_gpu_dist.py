@@ -39,10 +39,13 @@ def test_nccl_lss_layer_matches_reference(case, world, fused):
 
     from conftest import free_port
 
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(ROOT / "tests" / "dist_check.py"),
-           "--case", case, "--expect-fused", str(fused), "--fused-rs", str(fused), "--steps", "3"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ))
+    for _attempt in range(3):  # a free port can be taken between probe and bind (EADDRINUSE): retry
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(ROOT / "tests" / "dist_check.py"),
+               "--case", case, "--expect-fused", str(fused), "--fused-rs", str(fused), "--steps", "3"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ))
+        if "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
 

@@ -78,6 +78,43 @@ def test_bounded_stream_wait_deadline(runtime):
         K.raise_status()
 
 
+def test_guarded_stream_wait_deadline(runtime):
+    """The engine's default stream wait: front-end waits plus a guard kernel that, past
+    the deadline, raises the status word and writes the flags so the stream drains."""
+    import torch
+    from paper_2311_02382_b200.errors import CommTimeout
+
+    K = runtime
+    K.runtime_config(wait_timeout_s=0.3)
+    flags = torch.zeros(3, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        K.stream_wait_guarded(flags.data_ptr(), 3, 0, 7, s)  # words 1, 2 never signalled
+        y = torch.ones(8, device="cuda") * 3
+    assert _drain(s) < 20
+    assert float(y.sum()) == 24.0
+    assert int(flags[1]) >= 7 and int(flags[2]) >= 7 and int(flags[0]) == 0  # released by the guard
+    with pytest.raises(CommTimeout):
+        K.raise_status()
+
+
+def test_guarded_wait_satisfied_by_signal(runtime):
+    import torch
+
+    K = runtime
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    s, t = torch.cuda.Stream(), torch.cuda.Stream()
+    K.stream_wait_guarded(flags.data_ptr(), 2, -1, 5, s)
+    K.stream_signal(flags.data_ptr(), 5, t)
+    K.stream_signal(flags.data_ptr() + 4, 6, t)
+    assert _drain(s) < 20
+    torch.cuda.synchronize()  # the guard kernel exits once the flags landed
+    assert K.status(clear=True) == (False, False)
+    assert int(flags[0]) == 5 and int(flags[1]) == 6  # not touched by the guard
+
+
 def test_host_abort_releases_waits(runtime):
     """Communicator.abort semantics: with a long deadline, the host abort word releases
     a parked wait at once (collectives.py:200-209)."""

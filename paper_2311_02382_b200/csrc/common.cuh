@@ -137,16 +137,22 @@ LSS_DEV bool wait_flag_geq(const uint32_t* p, uint32_t seq) {
   bool ok = true;
   if ((int)(ld_acquire_sys(p) - seq) < 0) {
     const unsigned long long lim = g_wait_timeout_ns, t0 = globaltimer_ns();
-    while ((int)(ld_acquire_sys(p) - seq) < 0) {
-      __nanosleep(256);
-      if (host_aborted()) {
-        ok = false;
-        break;
-      }
-      if (lim && globaltimer_ns() - t0 > lim) {
-        status_raise(0);
-        ok = false;
-        break;
+    for (uint32_t n = 1;; ++n) {
+      __nanosleep(128);
+      if ((int)(ld_acquire_sys(p) - seq) >= 0) break;
+      // the deadline and the host abort word (a read of mapped host memory) every
+      // 256 polls (~50 us): polled every time, hundreds of waiting CTAs flooded the
+      // system-memory path and slowed the fused gather
+      if ((n & 255) == 0) {
+        if (host_aborted()) {
+          ok = false;
+          break;
+        }
+        if (lim && globaltimer_ns() - t0 > lim) {
+          status_raise(0);
+          ok = false;
+          break;
+        }
       }
     }
   }

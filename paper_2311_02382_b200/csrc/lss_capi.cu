@@ -858,14 +858,18 @@ int lss_stream_wait_guarded(unsigned int* flags, int count, int skip, unsigned i
       gs = it->second;
     }
   }
+  // the guard is launched BEFORE the waits: streams share the front-end's hardware
+  // queues, and a guard queued behind its own parked wait could never run
+  guard_flags_kernel<<<1, 32, 0, gs>>>(flags, count, skip, value);
+  int rc = check_launch("stream_wait_guarded");
+  if (rc) return rc;
   for (int i = 0; i < count; ++i) {
     if (i == skip) continue;
     CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flags + i), value,
                     CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) return fail(LSS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
   }
-  guard_flags_kernel<<<1, 32, 0, gs>>>(flags, count, skip, value);
-  return check_launch("stream_wait_guarded");
+  return LSS_OK;
 }
 
 int lss_peer_access(int device, int peer) {

@@ -37,17 +37,11 @@
 
 namespace lss {
 
-#ifndef LSS_BWD_QSTAGES
-#define LSS_BWD_QSTAGES 2  // Q / dO / lse / delta ring depth (3 halves the dQ staging to fit in SMEM)
-#endif
-constexpr int ATB_QSTAGES = LSS_BWD_QSTAGES;
 constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES + 2 * 512;  // Q, dO, lse2[128], delta[128]
 constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;                 // dS^T tile: 2 sub-tiles [128 kv][64 q]
-// dQ staging [128 q][64] fp32 as 2 SW128 halves, or (3 stages) one half at a time
-constexpr int ATB_STG_BYTES = ATB_QSTAGES == 2 ? 128 * 64 * 4 : 128 * 32 * 4;
-constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + ATB_QSTAGES * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES +
-                         ATB_STG_BYTES + 1024 + 256;
-static_assert(ATB_SMEM <= 232448, "shared memory");
+constexpr int ATB_STG_BYTES = 128 * 64 * 4;                      // dQ staging [128 q][64] fp32 (2 SW128 halves)
+constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES + ATB_STG_BYTES +
+                         1024 + 256;
 #ifndef LSS_BWD_EW
 #define LSS_BWD_EW 2  // elementwise warpgroups (A/B builds: 4 = 32 query columns per thread)
 #endif
@@ -316,22 +310,22 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
                                              ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + ATT_TILE_BYTES;
-  uint8_t* sQst = sV + ATT_TILE_BYTES;              // ATB_QSTAGES stages: Q, dO, lse2, delta
-  uint8_t* sdS = sQst + ATB_QSTAGES * ATB_QSTAGE_BYTES;  // 2 buffers x 2 sub-tiles [128 kv][64 q] bf16
+  uint8_t* sQst = sV + ATT_TILE_BYTES;              // 2 stages: Q, dO, lse2, delta
+  uint8_t* sdS = sQst + 2 * ATB_QSTAGE_BYTES;       // 2 buffers x 2 sub-tiles [128 kv][64 q] bf16
   uint8_t* sStage = sdS + 2 * ATB_DS_BYTES;         // dQ staging, 2 x [128 q][32] fp32 (SW128)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + ATB_STG_BYTES);
   uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;   // [ATB_QSTAGES]
-  uint64_t* q_empty = bars + 4;  // [ATB_QSTAGES]
-  uint64_t* s_full = bars + 7;   // S^T_i in TMEM
-  uint64_t* p_full = bars + 8;   // P^T_i in TMEM (S^T_i consumed)
-  uint64_t* dp_full = bars + 9;  // dP^T_i in TMEM (and every earlier MMA complete)
-  uint64_t* ds_full = bars + 10; // dS^T_i in TMEM + SMEM (dP^T_i consumed)
-  uint64_t* mma_done = bars + 11;  // one-shot: every MMA of the CTA complete
-  uint64_t* dq_full = bars + 12;   // [2] per TMEM dQ buffer
-  uint64_t* dq_empty = bars + 14;  // [2]
-  uint64_t* ds_free = bars + 16;   // [2] dQ_i has read SMEM dS buffer i&1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* q_full = bars + 1;   // [2]
+  uint64_t* q_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;   // S^T_i in TMEM
+  uint64_t* p_full = bars + 6;   // P^T_i in TMEM (S^T_i consumed)
+  uint64_t* dp_full = bars + 7;  // dP^T_i in TMEM (and every earlier MMA complete)
+  uint64_t* ds_full = bars + 8;  // dS^T_i in TMEM + SMEM (dP^T_i consumed)
+  uint64_t* mma_done = bars + 9;   // one-shot: every MMA of the CTA complete
+  uint64_t* dq_full = bars + 10;   // [2] per TMEM dQ buffer
+  uint64_t* dq_empty = bars + 12;  // [2]
+  uint64_t* ds_free = bars + 14;   // [2] dQ_i has read SMEM dS buffer i&1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -381,7 +375,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < ATB_QSTAGES; ++s) {
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
@@ -420,8 +414,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         __syncwarp();
         int src_ready = -1;  // last source whose pushed inputs were waited for
         for (int it = 0; it < n_iter; ++it) {
-          const int s = it % ATB_QSTAGES;
-          mbar_wait(&q_empty[s], ((it / ATB_QSTAGES) & 1) ^ 1);
+          const int s = it & 1;
+          mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
           if (lane == 0) BWD_TRACE(18, it);
           int src, q0;
           locate(it, src, q0);
@@ -452,10 +446,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
         // K16 step k of a bf16 TMEM operand written by the elementwise warpgroups
         auto ew_col = [](int k) { return (uint32_t)((16 * k / ATB_NC) * ATB_NC + (16 * k % ATB_NC) / 2); };
-        auto q_stage = [&](int it) { return smem_u32(sQst + (it % ATB_QSTAGES) * ATB_QSTAGE_BYTES); };
+        auto q_stage = [&](int it) { return smem_u32(sQst + (it & 1) * ATB_QSTAGE_BYTES); };
         auto issue_s = [&](int it) {  // S^T_it = K Q_it^T
           if (lane == 0) BWD_TRACE(16, it);
-          mbar_wait(&q_full[it % ATB_QSTAGES], (it / ATB_QSTAGES) & 1);
+          mbar_wait(&q_full[it & 1], (it >> 1) & 1);
           tc_fence_after();
           if (lane == 0) BWD_TRACE(17, it);
           const uint32_t q_addr = q_stage(it);
@@ -532,7 +526,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q  (A = dS^T from TMEM)
               mma_bf16_ts(tdK, tdP + ew_col(k), smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN,
                           (it > 0 || k > 0));
-            mma_commit(&q_empty[it % ATB_QSTAGES]);
+            mma_commit(&q_empty[it & 1]);
           }
           __syncwarp();
           if (more) issue_dp(it + 1);
@@ -560,14 +554,14 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       int src, qrow;
       locate(it, src, qrow);
       const long q0 = p.src[src].pos0 + qrow;  // global position of the tile's first query
-      const uint32_t st = smem_u32(sQst + (it % ATB_QSTAGES) * ATB_QSTAGE_BYTES);
+      const uint32_t st = smem_u32(sQst + (it & 1) * ATB_QSTAGE_BYTES);
       const uint32_t s_lse = st + 2 * ATT_TILE_BYTES + qd * NC * 4;        // lse2[q]
       const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
       // ---- P^T = 2^(S^T log2e/sqrt(d) - lse2): S_it completing implies dV_{it-1}
       // (the previous reader of the P^T columns) completed.
       constexpr bool LEAN = NC < 64;  // 4 warpgroups: lse / delta streamed from SMEM
       float lse[NC];  // issued ahead of the S wait: the loads queue behind the tensor
-      mbar_wait(&q_full[it % ATB_QSTAGES], (it / ATB_QSTAGES) & 1);  // core's SMEM operand traffic
+      mbar_wait(&q_full[it & 1], (it >> 1) & 1);  // core's SMEM operand traffic
       if constexpr (!LEAN) bwd_ld_vec<NC>(s_lse, lse);
       mbar_wait(s_full, it & 1);
       tc_fence_after();
@@ -693,7 +687,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const bool issuer = (r == 0);
     const uint32_t row0 = smem_u32(sStage + r * 128);                      // cols [0,32)
-    const uint32_t row1 = smem_u32(sStage + (ATB_QSTAGES == 2 ? ATB_STG_BYTES / 2 : 0) + r * 128);  // cols [32,64)
+    const uint32_t row1 = smem_u32(sStage + ATB_STG_BYTES / 2 + r * 128);  // cols [32,64)
     for (int it = 0; it < n_iter; ++it) {
       mbar_wait(&dq_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
@@ -709,8 +703,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           // Thread r owns row r of the staging buffer (128 rows x 32 int64 per half).
           const bool row_ok = q0 + r < p.src[src].m_src;
           long long* grow = fx + ((long)b * p.src[src].m_src + q0 + r) * ((long)p.H * ATT_D) + h * ATT_D;
-          constexpr int FXC = ATB_STG_BYTES / (128 * 8);  // int64 columns per staging pass (32 or 16)
-          const uint32_t srow = smem_u32(sStage + r * FXC * 8);
+          const uint32_t srow = smem_u32(sStage + r * 256);
 #pragma unroll 1
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t v[32];
@@ -719,55 +712,20 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
               tc_fence_before();
               mbar_arrive(&dq_empty[it & 1]);
             }
+            bulk_wait_read0();  // this thread's previous reduce has read its staging row
 #pragma unroll
-            for (int qq = 0; qq < 32 / FXC; ++qq) {
-              bulk_wait_read0();  // this thread's previous reduce has read its staging row
-#pragma unroll
-              for (int c = 0; c < FXC / 2; ++c) {
-                const long long e0 = __float2ll_rn(__uint_as_float(v[qq * FXC + 2 * c]) * 4294967296.f);
-                const long long e1 = __float2ll_rn(__uint_as_float(v[qq * FXC + 2 * c + 1]) * 4294967296.f);
-                asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(srow + c * 16), "l"(e0), "l"(e1) : "memory");
-              }
-              fence_proxy_async_smem();
-              if (row_ok) bulk_reduce_add_u64(grow + hh * 32 + qq * FXC, sStage + r * FXC * 8, FXC * 8);
-              bulk_commit();
+            for (int c = 0; c < 16; ++c) {
+              const long long e0 = __float2ll_rn(__uint_as_float(v[2 * c]) * 4294967296.f);
+              const long long e1 = __float2ll_rn(__uint_as_float(v[2 * c + 1]) * 4294967296.f);
+              asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(srow + c * 16), "l"(e0), "l"(e1) : "memory");
             }
+            fence_proxy_async_smem();
+            if (row_ok) bulk_reduce_add_u64(grow + hh * 32, sStage + r * 256, 256);
+            bulk_commit();
           }
           continue;
         }
       }
-#if LSS_BWD_QSTAGES != 2
-      // one 32-column half at a time through the 16 KB staging buffer
-#pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
-        if (issuer) bulk_wait_read0();  // the previous reduce has finished reading the staging tile
-        named_bar_sync(1, 128);
-        uint32_t v[32];
-        tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
-        if (g_numerics_check) {
-          bool bad = false;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) bad |= nonfinite(__uint_as_float(v[i]));
-          report_nonfinite(bad);
-        }
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          st_shared_v4(row0 + ((c ^ (r & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-        if (hh == 1) {
-          tc_fence_before();
-          mbar_arrive(&dq_empty[it & 1]);
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (issuer) {
-          int src, q0;
-          locate(it, src, q0);
-          tma_reduce_add_3d(&maps.dq[src], sStage, h * ATT_D + hh * 32, q0, b);
-          bulk_commit();
-        }
-      }
-      continue;
-#endif
       if (issuer) bulk_wait_read0();  // previous reduce has finished reading the staging tile
       named_bar_sync(1, 128);
 #pragma unroll

@@ -299,8 +299,8 @@ def main_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        # stream-wait mode for A/B runs (default "guarded"; "kernel" / "frontend")
-        comm = TorchDistComm(None, None, Ledger(), bounded_waits=os.environ.get("LSS_WAITS", "guarded"))
+        # stream-wait mode for A/B runs (default "kernel"; "guarded" / "frontend")
+        comm = TorchDistComm(None, None, Ledger(), bounded_waits=os.environ.get("LSS_WAITS", "kernel"))
     else:
         comm = SoloComm(Ledger())
     causal = not args.noncausal

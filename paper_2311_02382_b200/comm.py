@@ -72,7 +72,7 @@ class TorchDistComm:
 
     def __init__(self, seq_group=None, world_group=None, ledger: Ledger | None = None,
                  seq_name="sequence", world_name="world", *, use_flags: bool = True, timeout: float = 60.0,
-                 bounded_waits="guarded"):
+                 bounded_waits="kernel"):
         import torch.distributed as dist
 
         self.dist = dist
@@ -90,14 +90,15 @@ class TorchDistComm:
         # False restores NCCL's one-element all-reduce barrier
         self.use_flags = use_flags
         # a peer that never signals: every wait on a flag gives up after `timeout` ->
-        # CommTimeout, and abort() releases them at once -> CommAborted.  Stream waits:
-        # "guarded" (default) = front-end cuStreamWaitValue32 + a guard kernel on a
-        # high-priority stream that releases the flags on failure; "kernel" = a spin
-        # kernel on the waiting stream (needs an SM before the stream moves on);
-        # "frontend" = unbounded cuStreamWaitValue32.  The attention kernels' in-kernel
-        # waits always carry the deadline.
+        # CommTimeout, and abort() releases them at once -> CommAborted.  Stream waits
+        # (same-box A/B at N=2 / 4): "kernel" (default) = a one-warp spin
+        # kernel on the waiting stream, 11.54 / 5.86-5.90 ms per step; "guarded" =
+        # front-end cuStreamWaitValue32 + a guard kernel on a high-priority stream that
+        # releases the flags on failure, 11.63-11.70 / 6.07; "frontend" = unbounded
+        # cuStreamWaitValue32, 11.44-11.48 / 5.88-5.92.  The attention kernels'
+        # in-kernel waits always carry the deadline.
         self.timeout = timeout
-        self.waits = {True: "guarded", False: "frontend"}.get(bounded_waits, bounded_waits)
+        self.waits = {True: "kernel", False: "frontend"}.get(bounded_waits, bounded_waits)
         self._aborted = None
 
     def _ipc_capable(self) -> bool:

@@ -37,11 +37,26 @@
 
 namespace lss {
 
-constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES + 2 * 512;  // Q, dO, lse2[128], delta[128]
+#ifndef LSS_BWD_FOLD
+#define LSS_BWD_FOLD 1  // lse2 / delta folded into the S^T / dP^T MMAs (no-dropout instance)
+#endif
+// Folding: S^T - lse2/c and dP^T - delta are produced by the tensor core with one
+// extra K16 step each, A = a constant all-ones tile and B = a per-query-tile
+// operand holding -lse2/c (resp. -delta) split into two bf16 terms (hi + lo, ~2^-17
+// relative): the elementwise warps then need no per-column broadcast loads
+// (512 shared-memory wavefronts per tile, ~19% of the kernel's SMEM traffic, and
+// 2 x 64 registers).  The operands are K16 slices (128 rows x 32 bytes) of two
+// 128-byte-swizzled K-major tiles (the 32-byte swizzle reads 3x slower on the
+// tensor core): tile 0 = [ones | L_0 | L_1 | L_2], tile 1 = [D_0 | D_1 | D_2 | -].
+// Without FOLD (dropout instance) the region holds the per-stage lse2 / delta.
+constexpr int ATB_AUX_STAGES = 3;                    // aux ring: built up to 3 query tiles ahead
+constexpr int ATB_AUX_BYTES = 2 * ATT_TILE_BYTES;    // the two aux tiles
+constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES;  // Q, dO
 constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;                 // dS^T tile: 2 sub-tiles [128 kv][64 q]
 constexpr int ATB_STG_BYTES = 128 * 64 * 4;                      // dQ staging [128 q][64] fp32 (2 SW128 halves)
 constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES + ATB_STG_BYTES +
-                         1024 + 256;
+                         ATB_AUX_BYTES + 1024 + 256;
+static_assert(ATB_SMEM <= 232448, "backward shared memory");
 #ifndef LSS_BWD_EW
 #define LSS_BWD_EW 2  // elementwise warpgroups (A/B builds: 4 = 32 query columns per thread)
 #endif
@@ -220,6 +235,48 @@ LSS_DEV void bwd_p(uint32_t (&sv)[NC], const float (&lse)[NC], float sl2, int fv
   }
 }
 
+// Folded variants: the accumulator already holds S^T - lse2/c (resp. dP^T - delta)
+template <bool MASK, int NC>
+LSS_DEV void bwd_p_f(uint32_t (&sv)[NC], float sl2, int fv, uint32_t (&pk)[NC / 2]) {
+  const float2 sl2v = make_float2(sl2, sl2);
+#pragma unroll
+  for (int c = 0; c < NC; c += 2) {
+    const float2 x = fmul2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl2v);
+    float2 e;
+    if (!MASK && ((c / 2) & 7) < LSS_BWD_POLY8) {
+      e = exp2_poly2(x);
+    } else {
+      e = make_float2(ex2(x.x), ex2(x.y));
+    }
+    if (MASK) {
+      e.x = (c >= fv) ? e.x : 0.f;
+      e.y = (c + 1 >= fv) ? e.y : 0.f;
+    }
+    sv[c] = __float_as_uint(e.x);
+    sv[c + 1] = __float_as_uint(e.y);
+    pk[c / 2] = pack_bf16(e.x, e.y);
+  }
+}
+template <int C0, int NH, int NC>
+LSS_DEV void bwd_ds_f(const uint32_t (&pv)[NC], const uint32_t (&dp)[NH], float scale, uint32_t (&dk)[NC / 2]) {
+  const float2 scv = make_float2(scale, scale);
+#pragma unroll
+  for (int c = 0; c < NH; c += 2) {
+    const float2 pp = fmul2(make_float2(__uint_as_float(pv[C0 + c]), __uint_as_float(pv[C0 + c + 1])), scv);
+    const float2 ds = fmul2(pp, make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])));
+    dk[(C0 + c) / 2] = pack_bf16(ds.x, ds.y);
+  }
+}
+
+// hi + lo bf16 split of v (lo = 0 when v is infinite: padded query rows carry lse2 = +inf)
+LSS_DEV uint32_t bf16_hilo(float v) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  float r = v - __bfloat162float(hi);
+  if (!(fabsf(r) < INFINITY)) r = 0.f;
+  const __nv_bfloat16 lo = __float2bfloat16_rn(r);
+  return (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+}
+
 // Register-lean variants for 32-column slices (4 elementwise warpgroups): lse2 and
 // the scaled delta are read from shared memory 4 columns at a time (128-bit
 // broadcast loads) instead of being held in 2 x NC registers.
@@ -313,7 +370,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   uint8_t* sQst = sV + ATT_TILE_BYTES;              // 2 stages: Q, dO, lse2, delta
   uint8_t* sdS = sQst + 2 * ATB_QSTAGE_BYTES;       // 2 buffers x 2 sub-tiles [128 kv][64 q] bf16
   uint8_t* sStage = sdS + 2 * ATB_DS_BYTES;         // dQ staging, 2 x [128 q][32] fp32 (SW128)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + ATB_STG_BYTES);
+  uint8_t* sAux = sStage + ATB_STG_BYTES;  // FOLD: aux tiles; otherwise lse2 / delta per Q stage
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAux + ATB_AUX_BYTES);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;   // [2]
   uint64_t* q_empty = bars + 3;  // [2]
@@ -325,7 +383,14 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   uint64_t* dq_full = bars + 10;   // [2] per TMEM dQ buffer
   uint64_t* dq_empty = bars + 12;  // [2]
   uint64_t* ds_free = bars + 14;   // [2] dQ_i has read SMEM dS buffer i&1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* aux_full = bars + 16;   // [ATB_AUX_STAGES] FOLD: aux L / D operands built
+  uint64_t* aux_empty = bars + 16 + ATB_AUX_STAGES;  // [ATB_AUX_STAGES] S_it and dP_it complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * ATB_AUX_STAGES);
+  // K16 slice addresses inside the aux tiles
+  auto aux_l = [&](int s) { return smem_u32(sAux) + (1 + s) * 32; };
+  auto aux_d = [&](int s) { return smem_u32(sAux + ATT_TILE_BYTES) + s * 32; };
+  auto stats = [&](int s) { return sAux + s * 1024; };  // !FOLD: lse2[128] | delta[128] of Q stage s
+  constexpr bool FOLD = LSS_BWD_FOLD && !DROP;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -379,6 +444,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
+    for (int s = 0; s < ATB_AUX_STAGES; ++s) {
+      mbar_init(&aux_full[s], 64);
+      mbar_init(&aux_empty[s], 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(p_full, 128 * ATB_EW);
     mbar_init(dp_full, 1);
@@ -392,6 +461,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (FOLD && warp == 3) {  // the ones operand
+    const uint32_t one2 = 0x3F803F80u;  // slice 0 of aux tile 0: chunks 0, 1 of every row
+    for (int r = lane; r < 128; r += 32) {
+      const uint32_t row = smem_u32(sAux) + r * 128;
+      st_shared_v4(row + ((0 ^ (r & 7)) << 4), one2, one2, one2, one2);
+      st_shared_v4(row + ((1 ^ (r & 7)) << 4), one2, one2, one2, one2);
+    }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -427,14 +505,53 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           uint8_t* st = sQst + s * ATB_QSTAGE_BYTES;
           const long lo = ((long)b * p.H + h) * p.src[src].pitch + q0;
           if (elect_one()) {
-            mbar_arrive_expect_tx(&q_full[s], 2 * ATT_TILE_BYTES + 1024);
+            mbar_arrive_expect_tx(&q_full[s], 2 * ATT_TILE_BYTES + (FOLD ? 0 : 1024));
             tma_load_3d(&maps.q[src], &q_full[s], st, h * ATT_D, q0, b);
             tma_load_3d(&maps.dO[src], &q_full[s], st + ATT_TILE_BYTES, h * ATT_D, q0, b);
-            bulk_load_1d(st + 2 * ATT_TILE_BYTES, p.src[src].lse2 + lo, 512, &q_full[s]);
-            bulk_load_1d(st + 2 * ATT_TILE_BYTES + 512, p.src[src].delta + lo, 512, &q_full[s]);
+            if (!FOLD) {  // FOLD: the aux builders read the row statistics themselves
+              bulk_load_1d(stats(s), p.src[src].lse2 + lo, 512, &q_full[s]);
+              bulk_load_1d(stats(s) + 512, p.src[src].delta + lo, 512, &q_full[s]);
+            }
           }
           __syncwarp();
         }
+      }
+    } else if (FOLD && warp >= 2) {
+      // ------------------------------------------------ aux operand builders (warps 2-3):
+      // row r of aux L = (-lse2[r]/c) as hi|lo bf16, aux D = (-delta_raw[r]) likewise,
+      // K columns 2..15 of the slice zero.
+      // Their own ring (aux_empty is committed after dP_it) lets them run up to
+      // ATB_AUX_STAGES tiles ahead of the tensor core, reading lse2 / delta from global
+      // memory directly, so the build latency stays off the S / dP issue path.
+      const float inv_c = -1.f / p.scale_log2, inv_s = -1.f / p.scale;
+      const int j = (int)(warp - 2) * 32 + (int)lane;  // rows j and j + 64
+      for (int it = 0; it < n_iter; ++it) {
+        const int s = it % ATB_AUX_STAGES;
+        int src, q0;
+        locate(it, src, q0);
+        const long lo = ((long)b * p.H + h) * p.src[src].pitch + q0;
+        float l2v[2], dsv[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          l2v[k] = __ldg(p.src[src].lse2 + lo + j + 64 * k);
+          dsv[k] = __ldg(p.src[src].delta + lo + j + 64 * k);
+        }
+        if (it >= ATB_AUX_STAGES) mbar_wait(&aux_empty[s], (it / ATB_AUX_STAGES - 1) & 1);
+        const uint32_t al = aux_l(s), ad = aux_d(s);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int r = j + 64 * k;
+          const uint32_t hl = bf16_hilo(l2v[k] * inv_c), hd = bf16_hilo(dsv[k] * inv_s);
+          // slice base + row r: logical chunks 0 / 1 of the slice, SW128 XOR by (r & 7)
+          const uint32_t x = (uint32_t)(r & 7) << 4, rl = (al & ~127u) + r * 128, rd = (ad & ~127u) + r * 128;
+          const uint32_t cl = al & 127u, cd = ad & 127u;  // slice byte offset in the row
+          st_shared_v4(rl + (cl ^ x), hl, 0u, 0u, 0u);
+          st_shared_v4(rl + ((cl + 16) ^ x), 0u, 0u, 0u, 0u);
+          st_shared_v4(rd + (cd ^ x), hd, 0u, 0u, 0u);
+          st_shared_v4(rd + ((cd + 16) ^ x), 0u, 0u, 0u, 0u);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&aux_full[s]);
       }
     } else if (warp == 1) {
       if (n_iter > 0) {
@@ -443,13 +560,14 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         constexpr uint32_t idSS = idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
         constexpr uint32_t idKN = idesc_bf16_f32(128, 64, 0, 1);   // dV, dK (B MN-major)
         constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);    // dQ (A and B MN-major)
-        const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+        const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ones_addr = smem_u32(sAux);
         // K16 step k of a bf16 TMEM operand written by the elementwise warpgroups
         auto ew_col = [](int k) { return (uint32_t)((16 * k / ATB_NC) * ATB_NC + (16 * k % ATB_NC) / 2); };
         auto q_stage = [&](int it) { return smem_u32(sQst + (it & 1) * ATB_QSTAGE_BYTES); };
         auto issue_s = [&](int it) {  // S^T_it = K Q_it^T
           if (lane == 0) BWD_TRACE(16, it);
           mbar_wait(&q_full[it & 1], (it >> 1) & 1);
+          if (FOLD) mbar_wait(&aux_full[it % ATB_AUX_STAGES], (it / ATB_AUX_STAGES) & 1);
           tc_fence_after();
           if (lane == 0) BWD_TRACE(17, it);
           const uint32_t q_addr = q_stage(it);
@@ -458,6 +576,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             for (int k = 0; k < ATT_D / 16; ++k)
               mma_bf16_ss(tS, smem_desc_sw128(k_addr + k * 32, 16, 1024),
                           smem_desc_sw128(q_addr + k * 32, 16, 1024), idSS, k > 0);
+            if (FOLD)  // += 1 * (-lse2/c)
+              mma_bf16_ss(tS, smem_desc_sw128(ones_addr, 16, 1024), smem_desc_sw128(aux_l(it % ATB_AUX_STAGES), 16, 1024),
+                          idSS, 1u);
             mma_commit(s_full);
           }
           __syncwarp();
@@ -469,7 +590,11 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             for (int k = 0; k < ATT_D / 16; ++k)
               mma_bf16_ss(tdP, smem_desc_sw128(v_addr + k * 32, 16, 1024),
                           smem_desc_sw128(do_addr + k * 32, 16, 1024), idSS, k > 0);
+            if (FOLD)  // += 1 * (-delta)
+              mma_bf16_ss(tdP, smem_desc_sw128(ones_addr, 16, 1024),
+                          smem_desc_sw128(aux_d(it % ATB_AUX_STAGES), 16, 1024), idSS, 1u);
             mma_commit(dp_full);
+            if (FOLD) mma_commit(&aux_empty[it % ATB_AUX_STAGES]);
           }
           __syncwarp();
         };
@@ -554,15 +679,16 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       int src, qrow;
       locate(it, src, qrow);
       const long q0 = p.src[src].pos0 + qrow;  // global position of the tile's first query
-      const uint32_t st = smem_u32(sQst + (it & 1) * ATB_QSTAGE_BYTES);
-      const uint32_t s_lse = st + 2 * ATT_TILE_BYTES + qd * NC * 4;        // lse2[q]
-      const uint32_t s_dsc = st + 2 * ATT_TILE_BYTES + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
+      const uint32_t s_lse = smem_u32(stats(it & 1)) + qd * NC * 4;        // lse2[q]
+      const uint32_t s_dsc = smem_u32(stats(it & 1)) + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
       // ---- P^T = 2^(S^T log2e/sqrt(d) - lse2): S_it completing implies dV_{it-1}
       // (the previous reader of the P^T columns) completed.
       constexpr bool LEAN = NC < 64;  // 4 warpgroups: lse / delta streamed from SMEM
-      float lse[NC];  // issued ahead of the S wait: the loads queue behind the tensor
-      mbar_wait(&q_full[it & 1], (it >> 1) & 1);  // core's SMEM operand traffic
-      if constexpr (!LEAN) bwd_ld_vec<NC>(s_lse, lse);
+      float lse[FOLD ? 1 : NC];  // issued ahead of the S wait: the loads queue behind the tensor
+      if constexpr (!FOLD) {      // core's SMEM operand traffic
+        mbar_wait(&q_full[it & 1], (it >> 1) & 1);
+        if constexpr (!LEAN) bwd_ld_vec<NC>(s_lse, lse);
+      }
       mbar_wait(s_full, it & 1);
       tc_fence_after();
       if (t == 0 && qd == 0) BWD_TRACE(1, it);
@@ -577,12 +703,16 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         if (need_mask) {
           const long first_vis = kpos - q0 - qd * NC;
           const int fv = !row_ok ? NC : (p.causal ? (int)max(0L, min((long)NC, first_vis)) : 0);
-          if constexpr (LEAN)
+          if constexpr (FOLD)
+            bwd_p_f<true, NC>(sv, p.scale_log2, fv, pk);
+          else if constexpr (LEAN)
             bwd_p_s<true, DROP, NC>(sv, s_lse, p.scale_log2, fv, pk, keep, p.drop_scale);
           else
             bwd_p<true, DROP, NC>(sv, lse, p.scale_log2, fv, pk, keep, p.drop_scale);
         } else {
-          if constexpr (LEAN)
+          if constexpr (FOLD)
+            bwd_p_f<false, NC>(sv, p.scale_log2, 0, pk);
+          else if constexpr (LEAN)
             bwd_p_s<false, DROP, NC>(sv, s_lse, p.scale_log2, 0, pk, keep, p.drop_scale);
           else
             bwd_p<false, DROP, NC>(sv, lse, p.scale_log2, 0, pk, keep, p.drop_scale);
@@ -596,8 +726,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       // ---- dS^T = P^T (dP^T/sqrt(d) - delta/sqrt(d)): dP_it completing implies dK_{it-1}
       // (TMEM dS^T reader) completed; dQ_{it-2} (SMEM buffer it&1 reader) runs after
       // dP_it and signals ds_free.
-      float dsc[NC];  // delta loads issued before the dP wait (same reason as lse)
-      if constexpr (!LEAN) bwd_ld_vec<NC>(s_dsc, dsc);
+      float dsc[FOLD ? 1 : NC];  // delta loads issued before the dP wait (same reason as lse)
+      if constexpr (!LEAN && !FOLD) bwd_ld_vec<NC>(s_dsc, dsc);
       mbar_wait(dp_full, it & 1);
       tc_fence_after();
       if (t == 0 && qd == 0) BWD_TRACE(3, it);
@@ -606,7 +736,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         {  // dP^T in two halves keeps p, delta and dP within the register budget
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC, dp);
-          if constexpr (LEAN)
+          if constexpr (FOLD)
+            bwd_ds_f<0, NC / 2, NC>(sv, dp, p.scale, dk);
+          else if constexpr (LEAN)
             bwd_ds_s<0, NC / 2, NC, DROP>(sv, dp, s_dsc, p.scale, dk, keep, p.drop_scale);
           else
             bwd_ds<0, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
@@ -614,7 +746,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         {
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
-          if constexpr (LEAN)
+          if constexpr (FOLD)
+            bwd_ds_f<NC / 2, NC / 2, NC>(sv, dp, p.scale, dk);
+          else if constexpr (LEAN)
             bwd_ds_s<NC / 2, NC / 2, NC, DROP>(sv, dp, s_dsc, p.scale, dk, keep, p.drop_scale);
           else
             bwd_ds<NC / 2, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);

@@ -13,24 +13,28 @@
 // CTA = one 128-row key tile of one (batch, head); it walks the query tiles of
 // this rank that can see the keys (causal: q_pos >= k_pos).  Transposed
 // formulation so the key rows are TMEM lanes:
-//   S^T  = K Q_i^T   (TMEM, 128 cols)          dP^T = V dO_i^T   (TMEM, 128 cols)
-//   P^T  computed by 256 threads (2 warpgroups, 64 query columns each), written
-//        back as bf16 over S^T;  dS^T likewise over dP^T and into SMEM
+//   S^T  = K Q_i^T - lse2/c  (TMEM, 128 cols)    dP^T = V dO_i^T - delta  (TMEM, 128 cols)
+//        (the row statistics enter as one extra K16 MMA step: ones x aux operand)
+//   P^T  computed by 256 threads (2 warpgroups, 64 query columns each) into its own
+//        TMEM columns; dS^T written back as bf16 over dP^T and into SMEM
 //   dV  += P^T dO_i  (A = P^T from TMEM)
 //   dK  += dS^T Q_i  (A = dS^T from TMEM)
 //   dQ_i = dS K      (A = dS^T from SMEM read MN-major) -> drained by a 4th
 //                    warpgroup into fp32 dQ with TMA tensor reduce-add
-// TMEM: S^T/P^T[0,128) dP^T/dS^T[128,256) dV[256,320) dK[320,384) dQ x2 [384,512)
-// 16 warps: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 elementwise, 12-15 dQ drain;
-// setmaxnreg gives the elementwise warps the register file.
-// Pipelining: the elementwise warps publish P^T_i (dV_i starts) before they
-// touch dP^T_i, and the MMA issue order dV_i S_{i+1} dQ_{i-1} | dK_i dP_{i+1}
-// keeps the next tile's scores and dP ahead of them, so they never wait on the
-// whole five-GEMM chain; the dQ drain runs on its own warps.
+// TMEM: S^T[0,128) dP^T/dS^T[128,256) dV[256,320) dK[320,384) dQ[384,448) P^T[448,512)
+// 16 warps: 0 TMA, 1 MMA, 2 TMEM alloc + aux builder, 3 aux builder, 4-11
+// elementwise, 12-15 dQ drain; setmaxnreg gives the elementwise warps the registers.
+// Pipelining: S_{i+1} is issued as soon as the elementwise warps hold S^T_i in
+// registers, dV_i as soon as P^T_i is in TMEM, and dK_i dP_{i+1} dQ_i after dS_i,
+// so the only tensor work the elementwise warps can wait on is dP_{i+1}; a 3-stage
+// Q / dO ring keeps S_{i+1}'s operands resident a phase early.
 #pragma once
 #include "attn_fwd.cuh"
 #include "common.cuh"
 
+#ifndef LSS_BWD_DKSS
+#define LSS_BWD_DKSS 0  // dK reads dS^T from SMEM: dP_{i+1} no longer waits for dK_i
+#endif
 #ifndef LSS_BWD_POLY8
 #define LSS_BWD_POLY8 3  // exponent pairs (of every 8) on the FMA-pipe polynomial (A/B ms: 3/8 14.77, 4/8 14.85, 5/8 15.13, 2/8 15.0, 8/8 16.4)
 #endif
@@ -52,9 +56,10 @@ namespace lss {
 constexpr int ATB_AUX_STAGES = 3;                    // aux ring: built up to 3 query tiles ahead
 constexpr int ATB_AUX_BYTES = 2 * ATT_TILE_BYTES;    // the two aux tiles
 constexpr int ATB_QSTAGE_BYTES = 2 * ATT_TILE_BYTES;  // Q, dO
-constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;                 // dS^T tile: 2 sub-tiles [128 kv][64 q]
+constexpr int ATB_QSTAGES = 3;                        // Q / dO ring: S_{i+1} is issued one phase earlier
+constexpr int ATB_DS_BYTES = 2 * ATT_TILE_BYTES;      // dS^T tile: 2 sub-tiles [128 kv][64 q]
 constexpr int ATB_STG_BYTES = 128 * 64 * 4;                      // dQ staging [128 q][64] fp32 (2 SW128 halves)
-constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + 2 * ATB_QSTAGE_BYTES + 2 * ATB_DS_BYTES + ATB_STG_BYTES +
+constexpr int ATB_SMEM = 2 * ATT_TILE_BYTES /*K,V*/ + ATB_QSTAGES * ATB_QSTAGE_BYTES + ATB_DS_BYTES + ATB_STG_BYTES +
                          ATB_AUX_BYTES + 1024 + 256;
 static_assert(ATB_SMEM <= 232448, "backward shared memory");
 #ifndef LSS_BWD_EW
@@ -367,25 +372,28 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
                                              ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + ATT_TILE_BYTES;
-  uint8_t* sQst = sV + ATT_TILE_BYTES;              // 2 stages: Q, dO, lse2, delta
-  uint8_t* sdS = sQst + 2 * ATB_QSTAGE_BYTES;       // 2 buffers x 2 sub-tiles [128 kv][64 q] bf16
-  uint8_t* sStage = sdS + 2 * ATB_DS_BYTES;         // dQ staging, 2 x [128 q][32] fp32 (SW128)
+  uint8_t* sQst = sV + ATT_TILE_BYTES;                   // ATB_QSTAGES stages: Q, dO
+  uint8_t* sdS = sQst + ATB_QSTAGES * ATB_QSTAGE_BYTES;  // 2 sub-tiles [128 kv][64 q] bf16
+  uint8_t* sStage = sdS + ATB_DS_BYTES;                  // dQ staging, 2 x [128 q][32] fp32 (SW128)
   uint8_t* sAux = sStage + ATB_STG_BYTES;  // FOLD: aux tiles; otherwise lse2 / delta per Q stage
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAux + ATB_AUX_BYTES);
   uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;   // [2]
-  uint64_t* q_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;   // S^T_i in TMEM
-  uint64_t* p_full = bars + 6;   // P^T_i in TMEM (S^T_i consumed)
-  uint64_t* dp_full = bars + 7;  // dP^T_i in TMEM (and every earlier MMA complete)
-  uint64_t* ds_full = bars + 8;  // dS^T_i in TMEM + SMEM (dP^T_i consumed)
-  uint64_t* mma_done = bars + 9;   // one-shot: every MMA of the CTA complete
-  uint64_t* dq_full = bars + 10;   // [2] per TMEM dQ buffer
-  uint64_t* dq_empty = bars + 12;  // [2]
-  uint64_t* ds_free = bars + 14;   // [2] dQ_i has read SMEM dS buffer i&1
-  uint64_t* aux_full = bars + 16;   // [ATB_AUX_STAGES] FOLD: aux L / D operands built
-  uint64_t* aux_empty = bars + 16 + ATB_AUX_STAGES;  // [ATB_AUX_STAGES] S_it and dP_it complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * ATB_AUX_STAGES);
+  uint64_t* q_full = bars + 1;   // [ATB_QSTAGES]
+  uint64_t* q_empty = bars + 4;  // [ATB_QSTAGES]
+  uint64_t* s_full = bars + 7;   // S^T_i in TMEM
+  uint64_t* s_empty = bars + 8;  // S^T_i loaded into registers (S_{i+1} may overwrite it)
+  uint64_t* p_full = bars + 9;   // P^T_i in TMEM
+  uint64_t* dv_done = bars + 10; // dV_i complete (the P^T columns are free)
+  uint64_t* dp_full = bars + 11; // dP^T_i in TMEM (and every earlier MMA complete)
+  uint64_t* ds_full = bars + 12; // dS^T_i in TMEM + SMEM (dP^T_i consumed)
+  uint64_t* mma_done = bars + 13;  // one-shot: every MMA of the CTA complete
+  uint64_t* dq_full = bars + 14;   // dQ_i in TMEM
+  uint64_t* dq_empty = bars + 15;  // dQ_i read out by the drain
+  uint64_t* ds_free = bars + 16;   // dQ_i has read the SMEM dS tile
+  uint64_t* aux_full = bars + 17;  // [ATB_AUX_STAGES] FOLD: aux L / D operands built
+  uint64_t* aux_empty = bars + 17 + ATB_AUX_STAGES;  // [ATB_AUX_STAGES] S_it and dP_it complete
+  uint64_t* dp_empty = bars + 17 + 2 * ATB_AUX_STAGES;  // DKSS: dP^T_i loaded into registers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18 + 2 * ATB_AUX_STAGES);
   // K16 slice addresses inside the aux tiles
   auto aux_l = [&](int s) { return smem_u32(sAux) + (1 + s) * 32; };
   auto aux_d = [&](int s) { return smem_u32(sAux + ATT_TILE_BYTES) + s * 32; };
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     }
   }
   // iteration -> (source, tensor row of the query tile)
-  auto locate = [&](int it, int& s_out, int& qrow_out) {
+  auto locate = [&](int it, int& s_out, int& qrow_out) {  // (register selects: no local-memory indexing)
     int s = 0;
 #pragma unroll
     for (int k = 0; k < ATB_MAX_SRC - 1; ++k)
@@ -432,15 +440,19 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         it -= src_n[k];
         s = k + 1;
       }
+    int first = src_first[0];
+#pragma unroll
+    for (int k = 1; k < ATB_MAX_SRC; ++k)
+      if (s == k) first = src_first[k];
     s_out = s;
-    qrow_out = p.src[s].row0 + (src_first[s] + it) * ATT_BM;
+    qrow_out = p.src[s].row0 + (first + it) * ATT_BM;
   };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < ATB_QSTAGES; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
@@ -449,14 +461,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       mbar_init(&aux_empty[s], 1);
     }
     mbar_init(s_full, 1);
+    mbar_init(s_empty, 128 * ATB_EW);
     mbar_init(p_full, 128 * ATB_EW);
+    mbar_init(dv_done, 1);
     mbar_init(dp_full, 1);
+    mbar_init(dp_empty, 128 * ATB_EW);
     mbar_init(ds_full, 128 * ATB_EW);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&dq_full[s], 1);
-      mbar_init(&dq_empty[s], 128);
-      mbar_init(&ds_free[s], 1);
-    }
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 128);
+    mbar_init(ds_free, 1);
     mbar_init(mma_done, 1);
     fence_barrier_init();
   }
@@ -477,7 +490,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   // P^T (bf16) overwrites S^T and dS^T overwrites dP^T: elementwise warpgroup qd
   // reads fp32 columns [qd*NC, +NC) and writes its packed bf16 result to the first
   // half of those same columns, so no warpgroup overwrites data another still reads.
-  const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
+  const uint32_t tS = tmem + 0, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384,
+                 tP = tmem + 448;
 
   if (warp < 4) {
     reg_dealloc<ATB_REG_CTRL>();
@@ -492,8 +506,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         __syncwarp();
         int src_ready = -1;  // last source whose pushed inputs were waited for
         for (int it = 0; it < n_iter; ++it) {
-          const int s = it & 1;
-          mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
+          const int s = it % ATB_QSTAGES;
+          mbar_wait(&q_empty[s], ((it / ATB_QSTAGES) & 1) ^ 1);
           if (lane == 0) BWD_TRACE(18, it);
           int src, q0;
           locate(it, src, q0);
@@ -563,10 +577,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ones_addr = smem_u32(sAux);
         // K16 step k of a bf16 TMEM operand written by the elementwise warpgroups
         auto ew_col = [](int k) { return (uint32_t)((16 * k / ATB_NC) * ATB_NC + (16 * k % ATB_NC) / 2); };
-        auto q_stage = [&](int it) { return smem_u32(sQst + (it & 1) * ATB_QSTAGE_BYTES); };
+        auto q_stage = [&](int it) { return smem_u32(sQst + (it % ATB_QSTAGES) * ATB_QSTAGE_BYTES); };
         auto issue_s = [&](int it) {  // S^T_it = K Q_it^T
           if (lane == 0) BWD_TRACE(16, it);
-          mbar_wait(&q_full[it & 1], (it >> 1) & 1);
+          mbar_wait(&q_full[it % ATB_QSTAGES], (it / ATB_QSTAGES) & 1);
           if (FOLD) mbar_wait(&aux_full[it % ATB_AUX_STAGES], (it / ATB_AUX_STAGES) & 1);
           tc_fence_after();
           if (lane == 0) BWD_TRACE(17, it);
@@ -606,24 +620,25 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < ATT_BM / 16; ++k)
-              mma_bf16_ts(tdV, tS + ew_col(k), smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
+              mma_bf16_ts(tdV, tP + 8 * k, smem_desc_sw128(do_addr + k * 2048, 8192, 1024), idKN,
                           (it > 0 || k > 0));
+            mma_commit(dv_done);
           }
           __syncwarp();
         };
-        auto issue_dq = [&](int it) {  // dQ_it = dS_it K into TMEM buffer it&1 once drained
-          if (it > 1) {
-            mbar_wait(&dq_empty[it & 1], ((it >> 1) - 1) & 1);
+        auto issue_dq = [&](int it) {  // dQ_it = dS_it K into TMEM once the drain read dQ_{it-1}
+          if (it > 0) {
+            mbar_wait(dq_empty, (it - 1) & 1);
             tc_fence_after();
           }
-          const uint32_t ds_addr = smem_u32(sdS + (it & 1) * ATB_DS_BYTES);
+          const uint32_t ds_addr = smem_u32(sdS);
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < ATT_BN / 16; ++k)
-              mma_bf16_ss(tdQ + (it & 1) * 64, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
+              mma_bf16_ss(tdQ, smem_desc_sw128(ds_addr + k * 2048, ATT_TILE_BYTES, 1024),
                           smem_desc_sw128(k_addr + k * 2048, 8192, 1024), idQ, k > 0);
-            mma_commit(&dq_full[it & 1]);
-            mma_commit(&ds_free[it & 1]);
+            mma_commit(dq_full);
+            mma_commit(ds_free);
           }
           __syncwarp();
         };
@@ -632,15 +647,24 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         issue_s(0);
         issue_dp(0);
         // Tensor-pipe order (in-order execution):
-        //   dV_i S_{i+1} | dK_i dP_{i+1} dQ_{i-1} | dV_{i+1} S_{i+2} | ...
-        // S_{i+1} follows dV_i directly (it overwrites P^T_i), so the next scores are
-        // ready while the elementwise warps still work on dS_i; dP_{i+1} follows dK_i
-        // (it overwrites dS^T_i); dQ, which only feeds the drain, runs one tile late
-        // into a double-buffered TMEM accumulator so the drain never stalls the issue.
+        //   S_{i+1} dV_i | dK_i dP_{i+1} dQ_i | S_{i+2} dV_{i+1} | ...
+        // P^T has its own TMEM columns, so S_{i+1} is issued as soon as the elementwise
+        // warps have S^T_i in registers (s_empty) and is long complete when they come
+        // back from dS_i; dP_{i+1} follows dK_i (it overwrites dS^T_i); dQ_i reads the
+        // single SMEM dS tile and lands in TMEM for the drain warps.
         for (int it = 0; it < n_iter; ++it) {
           const bool more = it + 1 < n_iter;
+          if (more) {
+            mbar_wait(s_empty, it & 1);
+            tc_fence_after();
+            issue_s(it + 1);
+          }
           issue_dv(it);
-          if (more) issue_s(it + 1);
+          if (LSS_BWD_DKSS && more) {  // dP_{i+1} once dP^T_i is in registers
+            mbar_wait(dp_empty, it & 1);
+            tc_fence_after();
+            issue_dp(it + 1);
+          }
           if (lane == 0) BWD_TRACE(14, it);
           mbar_wait(ds_full, it & 1);
           tc_fence_after();
@@ -648,18 +672,25 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           const uint32_t q_addr = q_stage(it);
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q  (A = dS^T from TMEM)
+            for (int k = 0; k < ATT_BM / 16; ++k) {  // dK += dS^T Q
+#if LSS_BWD_DKSS
+              // A = dS^T from the SMEM tile (K-major: sub-tile k/4, 32-byte step k%4)
+              const uint32_t ds_addr = smem_u32(sdS) + (k / 4) * ATT_TILE_BYTES + (k % 4) * 32;
+              mma_bf16_ss(tdK, smem_desc_sw128(ds_addr, 16, 1024), smem_desc_sw128(q_addr + k * 2048, 8192, 1024),
+                          idKN, (it > 0 || k > 0));
+#else
               mma_bf16_ts(tdK, tdP + ew_col(k), smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN,
                           (it > 0 || k > 0));
-            mma_commit(&q_empty[it & 1]);
+#endif
+            }
+            mma_commit(&q_empty[it % ATB_QSTAGES]);
           }
           __syncwarp();
-          if (more) issue_dp(it + 1);
+          if (!LSS_BWD_DKSS && more) issue_dp(it + 1);
           if (lane == 0) BWD_TRACE(15, it);
-          if (it > 0) issue_dq(it - 1);
+          issue_dq(it);
           if (lane == 0) BWD_TRACE(8, it);
         }
-        issue_dq(n_iter - 1);
         if (elect_one()) mma_commit(mma_done);
         __syncwarp();
       }
@@ -679,14 +710,13 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       int src, qrow;
       locate(it, src, qrow);
       const long q0 = p.src[src].pos0 + qrow;  // global position of the tile's first query
-      const uint32_t s_lse = smem_u32(stats(it & 1)) + qd * NC * 4;        // lse2[q]
-      const uint32_t s_dsc = smem_u32(stats(it & 1)) + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
-      // ---- P^T = 2^(S^T log2e/sqrt(d) - lse2): S_it completing implies dV_{it-1}
-      // (the previous reader of the P^T columns) completed.
+      const uint32_t s_lse = smem_u32(stats(it % ATB_QSTAGES)) + qd * NC * 4;        // lse2[q]
+      const uint32_t s_dsc = smem_u32(stats(it % ATB_QSTAGES)) + 512 + qd * NC * 4;  // delta[q]/sqrt(d)
+      // ---- P^T = 2^(S^T log2e/sqrt(d) - lse2) into the P^T columns once dV_{it-1} has read them
       constexpr bool LEAN = NC < 64;  // 4 warpgroups: lse / delta streamed from SMEM
       float lse[FOLD ? 1 : NC];  // issued ahead of the S wait: the loads queue behind the tensor
       if constexpr (!FOLD) {      // core's SMEM operand traffic
-        mbar_wait(&q_full[it & 1], (it >> 1) & 1);
+        mbar_wait(&q_full[it % ATB_QSTAGES], (it / ATB_QSTAGES) & 1);
         if constexpr (!LEAN) bwd_ld_vec<NC>(s_lse, lse);
       }
       mbar_wait(s_full, it & 1);
@@ -694,6 +724,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       if (t == 0 && qd == 0) BWD_TRACE(1, it);
       uint32_t sv[NC];
       tmem_ld_n<NC>(tS + lane_off + qd * NC, sv);
+      tc_fence_before();
+      mbar_arrive(s_empty);  // S_{it+1} may overwrite S^T
       if (t == 0 && qd == 0) BWD_TRACE(7, it);
       // query column c of this slice is visible to key row t iff c >= fv
       const bool need_mask = !row_ok || (p.causal && kpos0 + ATT_BN - 1 > q0 + qd * NC);
@@ -718,14 +750,17 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             bwd_p<false, DROP, NC>(sv, lse, p.scale_log2, 0, pk, keep, p.drop_scale);
         }
         if (t == 0 && qd == 0) BWD_TRACE(13, it);
-        tmem_st_n<NC / 2>(tS + lane_off + qd * NC, pk);
+        if (it > 0) {
+          mbar_wait(dv_done, (it - 1) & 1);
+          tc_fence_after();
+        }
+        tmem_st_n<NC / 2>(tP + lane_off + qd * (NC / 2), pk);
       }
       tc_fence_before();
       mbar_arrive(p_full);
       if (t == 0 && qd == 0) BWD_TRACE(2, it);
       // ---- dS^T = P^T (dP^T/sqrt(d) - delta/sqrt(d)): dP_it completing implies dK_{it-1}
-      // (TMEM dS^T reader) completed; dQ_{it-2} (SMEM buffer it&1 reader) runs after
-      // dP_it and signals ds_free.
+      // (TMEM dS^T reader) completed; dQ_{it-1} (the SMEM dS reader) signals ds_free.
       float dsc[FOLD ? 1 : NC];  // delta loads issued before the dP wait (same reason as lse)
       if constexpr (!LEAN && !FOLD) bwd_ld_vec<NC>(s_dsc, dsc);
       mbar_wait(dp_full, it & 1);
@@ -746,6 +781,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         {
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
+          if (LSS_BWD_DKSS) {
+            tc_fence_before();
+            mbar_arrive(dp_empty);  // dP_{it+1} may overwrite dP^T
+          }
           if constexpr (FOLD)
             bwd_ds_f<NC / 2, NC / 2, NC>(sv, dp, p.scale, dk);
           else if constexpr (LEAN)
@@ -754,17 +793,17 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             bwd_ds<NC / 2, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
         }
         if (t == 0 && qd == 0) BWD_TRACE(9, it);
-        if (it > 1) mbar_wait(&ds_free[it & 1], ((it >> 1) - 1) & 1);
+        if (it > 0) mbar_wait(ds_free, (it - 1) & 1);
         if (t == 0 && qd == 0) BWD_TRACE(11, it);
         // dS^T row t, query columns [NC*qd, +NC) -> SW128 K-major sub-tile (64 q per sub-tile);
         // the SMEM stores go first so they have drained by the proxy fence below
         const int sub = (qd * NC) / 64, c0 = ((qd * NC) % 64) / 8;  // 16-byte chunk index in the 128B row
-        const uint32_t row = smem_u32(sdS + (it & 1) * ATB_DS_BYTES + sub * ATT_TILE_BYTES + t * 128);
+        const uint32_t row = smem_u32(sdS + sub * ATT_TILE_BYTES + t * 128);
 #pragma unroll
         for (int c = 0; c < NC / 8; ++c)
           st_shared_v4(row + (((c0 + c) ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
         if (t == 0 && qd == 0) BWD_TRACE(10, it);
-        tmem_st_n<NC / 2>(tdP + lane_off + qd * NC, dk);
+        if (!LSS_BWD_DKSS) tmem_st_n<NC / 2>(tdP + lane_off + qd * NC, dk);
       }
       if (t == 0 && qd == 0) BWD_TRACE(12, it);
       fence_proxy_async_smem();
@@ -773,14 +812,15 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       if (t == 0 && qd == 0) BWD_TRACE(4, it);
     }
     // dK / dV epilogue after the one-shot mma_done commit.  The tile is staged in
-    // the (now idle) dS buffers as [128 rows][dK 64 | dV 64] fp32 with 16-byte
+    // the (now idle) Q / dO ring as [128 rows][dK 64 | dV 64] fp32 with 16-byte
     // chunks XOR-swizzled by row, then each warp stores whole 256-byte row
     // segments: full-line writes whether the destination is local HBM or the
     // owner's receive slot across NVLink (fused reduce-scatter).
     constexpr int EC = 128 / ATB_EW;  // accumulator columns per thread
     const bool is_v = qd * EC >= 64;
     const int col0 = (qd * EC) % 64;
-    const uint32_t stage = smem_u32(sdS);
+    const uint32_t stage = smem_u32(sQst);
+    static_assert(ATB_QSTAGES * ATB_QSTAGE_BYTES >= 128 * 512, "dK|dV staging");
     if (n_iter > 0) {
       mbar_wait(mma_done, 0);
       tc_fence_after();
@@ -823,7 +863,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     const uint32_t row0 = smem_u32(sStage + r * 128);                      // cols [0,32)
     const uint32_t row1 = smem_u32(sStage + ATB_STG_BYTES / 2 + r * 128);  // cols [32,64)
     for (int it = 0; it < n_iter; ++it) {
-      mbar_wait(&dq_full[it & 1], (it >> 1) & 1);
+      mbar_wait(dq_full, it & 1);
       tc_fence_after();
       if (r == 0) BWD_TRACE(5, it);
       {
@@ -841,10 +881,10 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
 #pragma unroll 1
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t v[32];
-            tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
+            tmem_ld32(tdQ + lane_off + hh * 32, v);
             if (hh == 1) {
               tc_fence_before();
-              mbar_arrive(&dq_empty[it & 1]);
+              mbar_arrive(dq_empty);
             }
             bulk_wait_read0();  // this thread's previous reduce has read its staging row
 #pragma unroll
@@ -865,7 +905,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time keeps the drain at 56 registers
         uint32_t v[32];
-        tmem_ld32(tdQ + (it & 1) * 64 + lane_off + hh * 32, v);
+        tmem_ld32(tdQ + lane_off + hh * 32, v);
         if (g_numerics_check) {  // NaN / Inf in this key tile's dQ contribution
           bool bad = false;
 #pragma unroll
@@ -878,7 +918,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           st_shared_v4(rowh + ((c ^ (r & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
       }
       tc_fence_before();
-      mbar_arrive(&dq_empty[it & 1]);
+      mbar_arrive(dq_empty);
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
 #ifndef LSS_BWD_NODQ

@@ -32,9 +32,6 @@
 #include "attn_fwd.cuh"
 #include "common.cuh"
 
-#ifndef LSS_BWD_DKSS
-#define LSS_BWD_DKSS 0  // dK reads dS^T from SMEM: dP_{i+1} no longer waits for dK_i
-#endif
 #ifndef LSS_BWD_POLY8
 #define LSS_BWD_POLY8 3  // exponent pairs (of every 8) on the FMA-pipe polynomial (A/B ms: 3/8 14.77, 4/8 14.85, 5/8 15.13, 2/8 15.0, 8/8 16.4)
 #endif
@@ -392,8 +389,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
   uint64_t* ds_free = bars + 16;   // dQ_i has read the SMEM dS tile
   uint64_t* aux_full = bars + 17;  // [ATB_AUX_STAGES] FOLD: aux L / D operands built
   uint64_t* aux_empty = bars + 17 + ATB_AUX_STAGES;  // [ATB_AUX_STAGES] S_it and dP_it complete
-  uint64_t* dp_empty = bars + 17 + 2 * ATB_AUX_STAGES;  // DKSS: dP^T_i loaded into registers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18 + 2 * ATB_AUX_STAGES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17 + 2 * ATB_AUX_STAGES);
   // K16 slice addresses inside the aux tiles
   auto aux_l = [&](int s) { return smem_u32(sAux) + (1 + s) * 32; };
   auto aux_d = [&](int s) { return smem_u32(sAux + ATT_TILE_BYTES) + s * 32; };
@@ -465,7 +461,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
     mbar_init(p_full, 128 * ATB_EW);
     mbar_init(dv_done, 1);
     mbar_init(dp_full, 1);
-    mbar_init(dp_empty, 128 * ATB_EW);
     mbar_init(ds_full, 128 * ATB_EW);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 128);
@@ -660,11 +655,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             issue_s(it + 1);
           }
           issue_dv(it);
-          if (LSS_BWD_DKSS && more) {  // dP_{i+1} once dP^T_i is in registers
-            mbar_wait(dp_empty, it & 1);
-            tc_fence_after();
-            issue_dp(it + 1);
-          }
           if (lane == 0) BWD_TRACE(14, it);
           mbar_wait(ds_full, it & 1);
           tc_fence_after();
@@ -672,21 +662,13 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           const uint32_t q_addr = q_stage(it);
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < ATT_BM / 16; ++k) {  // dK += dS^T Q
-#if LSS_BWD_DKSS
-              // A = dS^T from the SMEM tile (K-major: sub-tile k/4, 32-byte step k%4)
-              const uint32_t ds_addr = smem_u32(sdS) + (k / 4) * ATT_TILE_BYTES + (k % 4) * 32;
-              mma_bf16_ss(tdK, smem_desc_sw128(ds_addr, 16, 1024), smem_desc_sw128(q_addr + k * 2048, 8192, 1024),
-                          idKN, (it > 0 || k > 0));
-#else
+            for (int k = 0; k < ATT_BM / 16; ++k)  // dK += dS^T Q  (A = dS^T from TMEM)
               mma_bf16_ts(tdK, tdP + ew_col(k), smem_desc_sw128(q_addr + k * 2048, 8192, 1024), idKN,
                           (it > 0 || k > 0));
-#endif
-            }
             mma_commit(&q_empty[it % ATB_QSTAGES]);
           }
           __syncwarp();
-          if (!LSS_BWD_DKSS && more) issue_dp(it + 1);
+          if (more) issue_dp(it + 1);
           if (lane == 0) BWD_TRACE(15, it);
           issue_dq(it);
           if (lane == 0) BWD_TRACE(8, it);
@@ -781,10 +763,6 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         {
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
-          if (LSS_BWD_DKSS) {
-            tc_fence_before();
-            mbar_arrive(dp_empty);  // dP_{it+1} may overwrite dP^T
-          }
           if constexpr (FOLD)
             bwd_ds_f<NC / 2, NC / 2, NC>(sv, dp, p.scale, dk);
           else if constexpr (LEAN)
@@ -803,7 +781,7 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
         for (int c = 0; c < NC / 8; ++c)
           st_shared_v4(row + (((c0 + c) ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
         if (t == 0 && qd == 0) BWD_TRACE(10, it);
-        if (!LSS_BWD_DKSS) tmem_st_n<NC / 2>(tdP + lane_off + qd * NC, dk);
+        tmem_st_n<NC / 2>(tdP + lane_off + qd * NC, dk);
       }
       if (t == 0 && qd == 0) BWD_TRACE(12, it);
       fence_proxy_async_smem();

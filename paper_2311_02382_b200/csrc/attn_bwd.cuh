@@ -745,10 +745,18 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       // (TMEM dS^T reader) completed; dQ_{it-1} (the SMEM dS reader) signals ds_free.
       float dsc[FOLD ? 1 : NC];  // delta loads issued before the dP wait (same reason as lse)
       if constexpr (!LEAN && !FOLD) bwd_ld_vec<NC>(s_dsc, dsc);
+      // the SMEM dS tile is free once dQ_{it-1} completed (long before dP_it, in practice)
+      if (it > 0) mbar_wait(ds_free, (it - 1) & 1);
+      if (t == 0 && qd == 0) BWD_TRACE(11, it);
       mbar_wait(dp_full, it & 1);
       tc_fence_after();
       if (t == 0 && qd == 0) BWD_TRACE(3, it);
       {
+        // dS^T row t, query columns [NC*qd, +NC) -> SW128 K-major sub-tile (64 q per
+        // sub-tile); each half is stored as soon as it is computed, so the proxy fence
+        // below waits only for the second half's stores
+        const int sub = (qd * NC) / 64, c0 = ((qd * NC) % 64) / 8;  // 16-byte chunk index in the 128B row
+        const uint32_t row = smem_u32(sdS + sub * ATT_TILE_BYTES + t * 128);
         uint32_t dk[NC / 2];
         {  // dP^T in two halves keeps p, delta and dP within the register budget
           uint32_t dp[NC / 2];
@@ -760,6 +768,9 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
           else
             bwd_ds<0, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
         }
+#pragma unroll
+        for (int c = 0; c < NC / 16; ++c)
+          st_shared_v4(row + (((c0 + c) ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
         {
           uint32_t dp[NC / 2];
           tmem_ld_n<NC / 2>(tdP + lane_off + qd * NC + NC / 2, dp);
@@ -771,14 +782,8 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
             bwd_ds<NC / 2, NC / 2, NC, DROP>(sv, dp, dsc, p.scale, dk, keep, p.drop_scale);
         }
         if (t == 0 && qd == 0) BWD_TRACE(9, it);
-        if (it > 0) mbar_wait(ds_free, (it - 1) & 1);
-        if (t == 0 && qd == 0) BWD_TRACE(11, it);
-        // dS^T row t, query columns [NC*qd, +NC) -> SW128 K-major sub-tile (64 q per sub-tile);
-        // the SMEM stores go first so they have drained by the proxy fence below
-        const int sub = (qd * NC) / 64, c0 = ((qd * NC) % 64) / 8;  // 16-byte chunk index in the 128B row
-        const uint32_t row = smem_u32(sdS + sub * ATT_TILE_BYTES + t * 128);
 #pragma unroll
-        for (int c = 0; c < NC / 8; ++c)
+        for (int c = NC / 16; c < NC / 8; ++c)
           st_shared_v4(row + (((c0 + c) ^ (t & 7)) << 4), dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
         if (t == 0 && qd == 0) BWD_TRACE(10, it);
         tmem_st_n<NC / 2>(tdP + lane_off + qd * NC, dk);

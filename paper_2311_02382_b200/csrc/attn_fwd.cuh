@@ -217,9 +217,11 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem + 0, tmem + 128};
-  const uint32_t tO[2] = {tmem + 256, tmem + 320};
-  const uint32_t tP[2] = {tmem + 384, tmem + 448};
+  // TMEM column bases of query tile w (arithmetic, not arrays: a runtime-indexed
+  // array lands in local memory, an LDL on every softmax iteration)
+  auto tS = [&](int w) { return tmem + 128u * w; };
+  auto tO = [&](int w) { return tmem + 256u + 64u * w; };
+  auto tP = [&](int w) { return tmem + 384u + 64u * w; };
 
   if (warp < 4) {
    reg_dealloc<LSS_FWD_CTRL_REGS>();  // control warpgroup: TMA, MMA, TMEM alloc
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < ATT_BN / 16; ++k) {
-            mma_bf16_ts(tO[w], tP[w] + k * 8, smem_desc_sw128(v_addr + k * 2048, 8192, 1024), idO,
+            mma_bf16_ts(tO(w), tP(w) + k * 8, smem_desc_sw128(v_addr + k * 2048, 8192, 1024), idO,
                         (jj > 0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&o_full[w]);
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < ATT_D / 16; ++k) {
-            mma_bf16_ss(tS[w], smem_desc_sw128(q_addr + w * ATT_TILE_BYTES + k * 32, 16, 1024),
+            mma_bf16_ss(tS(w), smem_desc_sw128(q_addr + w * ATT_TILE_BYTES + k * 32, 16, 1024),
                         smem_desc_sw128(k_addr + k * 32, 16, 1024), idS, k > 0 ? 1u : 0u);
           }
           mma_commit(&s_full[w]);
@@ -329,10 +331,10 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
         float s[ATT_BN];
         {
           uint32_t rr[64];
-          tmem_ld64(tS[w] + lane_off, rr);
+          tmem_ld64(tS(w) + lane_off, rr);
 #pragma unroll
           for (int i = 0; i < 64; ++i) s[i] = __uint_as_float(rr[i]);
-          tmem_ld64(tS[w] + lane_off + 64, rr);
+          tmem_ld64(tS(w) + lane_off + 64, rr);
 #pragma unroll
           for (int i = 0; i < 64; ++i) s[64 + i] = __uint_as_float(rr[i]);
         }
@@ -411,10 +413,10 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < ATT_D / 32; ++c) {
             uint32_t oo[32];
-            tmem_ld32(tO[w] + lane_off + c * 32, oo);
+            tmem_ld32(tO(w) + lane_off + c * 32, oo);
 #pragma unroll
             for (int i = 0; i < 32; ++i) oo[i] = __float_as_uint(__uint_as_float(oo[i]) * alpha);
-            tmem_st32(tO[w] + lane_off + c * 32, oo);
+            tmem_st32(tO(w) + lane_off + c * 32, oo);
           }
         }
         {
@@ -424,8 +426,8 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
             p0[i] = pk[i];
             p1[i] = pk[32 + i];
           }
-          tmem_st32(tP[w] + lane_off + 0, p0);
-          tmem_st32(tP[w] + lane_off + 32, p1);
+          tmem_st32(tP(w) + lane_off + 0, p0);
+          tmem_st32(tP(w) + lane_off + 32, p1);
         }
         tc_fence_before();
         mbar_arrive(&p_full[w]);
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(ATT_FWD_THREADS, 1)
       mbar_wait(&o_full[w], (n_kv - 1) & 1);
       tc_fence_after();
       uint32_t oo[ATT_D];
-      tmem_ld64(tO[w] + lane_off, oo);
+      tmem_ld64(tO(w) + lane_off, oo);
       {
         // stage the warp's 32 rows x 128 B in this query tile's (now idle) Q buffer,
         // 16-byte chunks XOR-swizzled by row, then store whole 128-byte rows: 4 rows

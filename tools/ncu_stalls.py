@@ -1,6 +1,6 @@
 """Warp-state breakdown of one ncu --set full --import-source capture, by warp role.
 
-    python tools/ncu_stalls.py gpurun_out/prof.ncu-rep > profiles/<tag>_ncu.md
+    python tools/ncu_stalls.py gpurun_out/prof.ncu-rep [kernel-regex] > profiles/<tag>_ncu.md
 
 Splits the SASS of a warp-specialised kernel at its USETMAXREG instructions
 (control warps / elementwise warps / drain warps of attn_bwd_tc_kernel), sums the
@@ -20,8 +20,12 @@ RAW = ["gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_
        "smsp__issue_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum"]
 
 
+KFILTER = []
+
+
 def ncu(rep, *args):
-    return subprocess.run(["ncu", "-i", rep, *args, "--csv"], capture_output=True, text=True, check=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *KFILTER, *args, "--csv"], capture_output=True, text=True,
+                          check=True).stdout
 
 
 def main(rep):
@@ -34,7 +38,12 @@ def main(rep):
             i = hdr.index(m)
             print(f"| `{m}` | {vals[i]} {units[i]} |")
     rows = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--print-source", "sass"))))
-    hdr, data = rows[1], rows[2:]
+    hdr, data = rows[1], []
+    for r in rows[2:]:  # the first function's block only (a capture of several kernels repeats the header)
+        if r == hdr or (r and r[0] == hdr[0]):
+            break
+        if len(r) == len(hdr):
+            data.append(r)
     ix = {h: i for i, h in enumerate(hdr)}
     stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
     cuts = [k for k, r in enumerate(data) if "USETMAXREG" in r[ix["Source"]]] + [len(data)]
@@ -59,4 +68,6 @@ def main(rep):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 2:
+        KFILTER[:] = ["-k", "regex:" + sys.argv[2]]
     main(sys.argv[1])

@@ -33,7 +33,7 @@
 #include "common.cuh"
 
 #ifndef LSS_BWD_POLY8
-#define LSS_BWD_POLY8 3  // exponent pairs (of every 8) on the FMA-pipe polynomial (A/B ms: 3/8 14.77, 4/8 14.85, 5/8 15.13, 2/8 15.0, 8/8 16.4)
+#define LSS_BWD_POLY8 2  // exponent pairs (of every 8) on the FMA-pipe polynomial (A/B ms, current kernel: 0/8 14.8, 1/8 13.46, 2/8 13.40, 3/8 13.70, 4/8 13.67)
 #endif
 
 namespace lss {

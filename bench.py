@@ -274,7 +274,7 @@ def run_reference(args):
                          "sample": desc, **host_info(kind)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -527,7 +527,7 @@ def main_ours(args):
             "per_rank_ms": [r[0] for r in allst],
             "collectives_per_step": coll,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -627,14 +627,31 @@ def main_gpt(args):
                 "pct_bf16_peak": {"burst": flops / (ms / 1e3) / (world * burst * 1e12),
                                   "sustained": flops / (ms / 1e3) / (world * sustained * 1e12)},
                 "loss": loss, "clocks": clocks}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
+_JSON_OUT = None
+
+
+def claim_stdout():
+    """Route fd 1 to stderr for the rest of the run and keep the real stdout for the
+    one JSON line: native libraries (NCCL's version banner on rank 0) print to fd 1."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def emit(line):
+    print(json.dumps(line), file=_JSON_OUT or sys.stdout, flush=True)
+
+
 def main():
+    claim_stdout()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)

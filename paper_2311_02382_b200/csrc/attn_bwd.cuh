@@ -534,16 +534,24 @@ __global__ void __launch_bounds__(ATB_THREADS, 1)
       // memory directly, so the build latency stays off the S / dP issue path.
       const float inv_c = -1.f / p.scale_log2, inv_s = -1.f / p.scale;
       const int j = (int)(warp - 2) * 32 + (int)lane;  // rows j and j + 64
+      int src_ready = -1;  // last source whose pushed inputs were waited for
       for (int it = 0; it < n_iter; ++it) {
         const int s = it % ATB_AUX_STAGES;
         int src, q0;
         locate(it, src, q0);
+        if (p.src[src].ready != nullptr && src != src_ready) {  // fused hand-off: lse2 / delta pushed too
+          if (lane == 0) wait_flag_geq(p.src[src].ready, p.src[src].ready_seq);
+          __syncwarp();
+          src_ready = src;
+        }
         const long lo = ((long)b * p.H + h) * p.src[src].pitch + q0;
         float l2v[2], dsv[2];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          l2v[k] = __ldg(p.src[src].lse2 + lo + j + 64 * k);
-          dsv[k] = __ldg(p.src[src].delta + lo + j + 64 * k);
+        for (int k = 0; k < 2; ++k) {  // coherent loads: a partner may have pushed them during this launch
+          asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(l2v[k]) : "l"(p.src[src].lse2 + lo + j + 64 * k)
+                       : "memory");
+          asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(dsv[k]) : "l"(p.src[src].delta + lo + j + 64 * k)
+                       : "memory");
         }
         if (it >= ATB_AUX_STAGES) mbar_wait(&aux_empty[s], (it / ATB_AUX_STAGES - 1) & 1);
         const uint32_t al = aux_l(s), ad = aux_d(s);

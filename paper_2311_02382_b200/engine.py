@@ -748,7 +748,8 @@ class LSSAttention:
         if not hasattr(self, "_in_bufs"):
             mk = lambda: torch.empty(self.B, self.m, self.E, dtype=torch.float32, device=self.device)  # noqa: E731
             self._in_bufs = [(mk(), mk()), (mk(), mk())]
-            self._in_ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self._in_ready = [torch.cuda.Event(), torch.cuda.Event()]   # x of the slot resident
+            self._gy_ready = [torch.cuda.Event(), torch.cuda.Event()]   # grad_y of the slot resident
             self._in_free = [torch.cuda.Event(), torch.cuda.Event()]
             self._copy_stream = torch.cuda.Stream(device=self.device)
             self._prefetched = None  # (slot, x_host, grad_y_host) already in flight
@@ -761,8 +762,9 @@ class LSSAttention:
             with torch.cuda.stream(cs):
                 x_d, gy_d = self._in_bufs[slot]
                 x_d.copy_(xh, non_blocking=True)
-                gy_d.copy_(gyh, non_blocking=True)
                 self._in_ready[slot].record()
+                gy_d.copy_(gyh, non_blocking=True)  # needed only by the backward: lands under the forward
+                self._gy_ready[slot].record()
 
         pf = self._prefetched
         if pf is not None and pf[1] is x_host and pf[2] is grad_y_host:
@@ -784,7 +786,14 @@ class LSSAttention:
         if prefetch is not None and not self.options.prefetch_at_bwd:
             prefetch()
             prefetch = None
-        out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer, policy=policy, before_bwd=prefetch)
+        gy_ev = self._gy_ready[slot]
+
+        def before_bwd():
+            cur.wait_event(gy_ev)  # grad_y's copy overlapped the forward
+            if prefetch is not None:
+                prefetch()
+
+        out = lss_step([self], comm, [x_d], [gy_d], step=step, layer=layer, policy=policy, before_bwd=before_bwd)
         self._in_free[slot].record(cur)
         if grads_host is not None:
             # read-back off the critical path: snapshot the averaged gradients on the

@@ -63,6 +63,9 @@ LSS_DEV float gelu_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * GELU_C * (1.f + 3.f * GELU_K * x * x);
 }
 
+#ifndef LSS_GEMM_2CTA
+#define LSS_GEMM_2CTA 1  // CTA-pair (cta_group::2) kernel for M >= 512
+#endif
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
@@ -107,6 +110,101 @@ LSS_DEV void epi_store_rows(uint32_t stage, const float (&v)[32], void* out, lon
   }
   __syncwarp();  // the staging tile is reused by the next chunk
 }
+// Epilogue of one 128 x 256 accumulator tile held in this CTA's TMEM columns
+// [acc, acc + 256): warp `quad` of the epilogue warpgroup owns rows quad*32.. (TMEM
+// lanes), 32 columns at a time: alpha, bias, residual, activation, store.
+LSS_DEV void gemm_epilogue_tile(uint32_t acc, int m0, int n0, int M, int N, const GemmEpilogue& ep, int quad,
+                                uint32_t lane, uint32_t epi, bool check) {
+  const int row_in_tile = quad * 32 + (int)lane;
+  const int row = m0 + row_in_tile;
+  const bool row_ok = row < M;
+#pragma unroll 1
+  for (int c = 0; c < GEMM_BN; c += 32) {
+    uint32_t r[32];
+    tmem_ld32(acc + ((uint32_t)(quad * 32) << 16) + c, r);
+    const int n = n0 + c;
+    if (n >= N) continue;  // warp-uniform
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * ep.alpha;
+    if (!row_ok) {  // rows past M: staged but never stored (no operand loads)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    } else {
+    if (ep.bias) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += __ldg(ep.bias + n + i);
+    }
+    if (ep.residual) {
+      const float4* rp = reinterpret_cast<const float4*>(ep.residual + (long)row * ep.ld_res + n);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 t = rp[i];
+        v[4 * i] += t.x;
+        v[4 * i + 1] += t.y;
+        v[4 * i + 2] += t.z;
+        v[4 * i + 3] += t.w;
+      }
+    }
+    if (ep.act == 1) {  // tanh-GeLU; the pre-activation is kept for the backward
+      if (ep.pre) {
+        if (ep.out_bf16) {
+          uint4* pp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.pre) + (long)row * ep.ld_pre + n);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            pp[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                               pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+        } else {
+          float4* pp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.pre) + (long)row * ep.ld_pre + n);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = gelu_f<true>(v[i]);
+    } else if (ep.act == 2) {  // chain rule through GeLU at the stored pre-activation
+      if (ep.aux_bf16) {
+        const uint4* ap = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(ep.aux) +
+                                                         (long)row * ep.ld_aux + n);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 t = ap[i];
+          const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            v[8 * i + 2 * j] *= gelu_grad<true>(__uint_as_float(w[j] << 16));
+            v[8 * i + 2 * j + 1] *= gelu_grad<true>(__uint_as_float(w[j] & 0xFFFF0000u));
+          }
+        }
+      } else {
+        const float4* ap = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ep.aux) +
+                                                           (long)row * ep.ld_aux + n);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 t = ap[i];
+          v[4 * i] *= gelu_grad<true>(t.x);
+          v[4 * i + 1] *= gelu_grad<true>(t.y);
+          v[4 * i + 2] *= gelu_grad<true>(t.z);
+          v[4 * i + 3] *= gelu_grad<true>(t.w);
+        }
+      }
+    }
+    }  // row_ok
+    if (check) {
+      bool bad = false;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) bad |= nonfinite(v[i]);
+      report_nonfinite(bad);
+    }
+    const int seg = n / ep.seg_width;
+    const long col = n - (long)seg * ep.seg_width;
+    if (ep.out_bf16)
+      epi_store_rows<true>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
+    else
+      epi_store_rows<false>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
+  }
+}
+
 constexpr int GEMM_THREADS = 256;
 
 template <int A_MN, int B_MN>
@@ -227,7 +325,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue: thread <-> accumulator row
     const int quad = warp - 4;
-    const int row_in_tile = quad * 32 + lane;
     const bool check = g_numerics_check != 0;  // NaN / Inf report (tensor.py:79-95), off by default
     const uint32_t epi = smem_u32(smem + GEMM_STAGES * GEMM_STAGE_BYTES + 256) + quad * (32 * 32 * 4);
     int local = 0;
@@ -238,93 +335,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = (tile % n_tiles) * GEMM_BN;
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      const int row = m0 + row_in_tile;
-      const bool row_ok = row < M;
-#pragma unroll 1
-      for (int c = 0; c < GEMM_BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + buf * GEMM_BN + c, r);
-        const int n = n0 + c;
-        if (n >= N) continue;  // warp-uniform
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * ep.alpha;
-        if (!row_ok) {  // rows past M: staged but never stored (no operand loads)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        } else {
-        if (ep.bias) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += __ldg(ep.bias + n + i);
-        }
-        if (ep.residual) {
-          const float4* rp = reinterpret_cast<const float4*>(ep.residual + (long)row * ep.ld_res + n);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 t = rp[i];
-            v[4 * i] += t.x;
-            v[4 * i + 1] += t.y;
-            v[4 * i + 2] += t.z;
-            v[4 * i + 3] += t.w;
-          }
-        }
-        if (ep.act == 1) {  // tanh-GeLU; the pre-activation is kept for the backward
-          if (ep.pre) {
-            if (ep.out_bf16) {
-              uint4* pp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.pre) + (long)row * ep.ld_pre + n);
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                pp[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-            } else {
-              float4* pp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.pre) + (long)row * ep.ld_pre + n);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) pp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = gelu_f<true>(v[i]);
-        } else if (ep.act == 2) {  // chain rule through GeLU at the stored pre-activation
-          if (ep.aux_bf16) {
-            const uint4* ap = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(ep.aux) +
-                                                             (long)row * ep.ld_aux + n);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint4 t = ap[i];
-              const uint32_t w[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                v[8 * i + 2 * j] *= gelu_grad<true>(__uint_as_float(w[j] << 16));
-                v[8 * i + 2 * j + 1] *= gelu_grad<true>(__uint_as_float(w[j] & 0xFFFF0000u));
-              }
-            }
-          } else {
-            const float4* ap = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ep.aux) +
-                                                               (long)row * ep.ld_aux + n);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 t = ap[i];
-              v[4 * i] *= gelu_grad<true>(t.x);
-              v[4 * i + 1] *= gelu_grad<true>(t.y);
-              v[4 * i + 2] *= gelu_grad<true>(t.z);
-              v[4 * i + 3] *= gelu_grad<true>(t.w);
-            }
-          }
-        }
-        }  // row_ok
-        if (check) {
-          bool bad = false;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) bad |= nonfinite(v[i]);
-          report_nonfinite(bad);
-        }
-        const int seg = n / ep.seg_width;
-        const long col = n - (long)seg * ep.seg_width;
-        if (ep.out_bf16)
-          epi_store_rows<true>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
-        else
-          epi_store_rows<false>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
-      }
+      gemm_epilogue_tile(tmem_base + buf * GEMM_BN, m0, n0, M, N, ep, quad, lane, epi, check);
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);
     }
@@ -334,6 +345,204 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile; each CTA loads its own 128 rows of A and 128 of the 256 rows of
+// B, the leader issues M=256 MMAs that read both CTAs' shared memory, and each
+// CTA's TMEM receives its own 128 rows of the accumulator.  Per SM that is 32 KB
+// of operands per 64-deep K step instead of 48 KB (the 1-CTA kernel's TMA ingest
+// did not keep the tensor pipe busy: 55% under ncu), and 6 pipeline stages fit.
+//   full_bar (leader): both CTAs' TMA bytes (the peer's loads signal the leader)
+//   empty_bar (each) : the leader's MMA commit, multicast to both CTAs
+//   tfull_bar (each) : the leader's accumulator commit, multicast
+//   tempty_bar (leader): both CTAs' epilogue warps (256 arrivals, remote for the peer)
+constexpr int GEMM2_STAGES = 6;
+constexpr int GEMM2_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES / 2;  // 32 KB per CTA
+constexpr int GEMM2_SMEM_BYTES = GEMM2_STAGES * GEMM2_STAGE_BYTES + GEMM_EPI_BYTES + 1024 + 256;
+
+LSS_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+LSS_DEV uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+LSS_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-SM TMA load: the data lands in this CTA's shared memory, the completion is
+// signalled on the mbarrier at shared::cluster address bar_cl (the leader's)
+LSS_DEV void tma_load_2d_2sm(const CUtensorMap* m, uint32_t bar_cl, void* smem, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cl), "r"(c0), "r"(c1)
+      : "memory");
+}
+LSS_DEV void mma_bf16_ss_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+LSS_DEV void mma_commit_2sm(uint64_t* bar) {  // arrive on the same barrier in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int A_MN, int B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                         int N, int K, GemmEpilogue ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + GEMM2_STAGES * GEMM2_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + GEMM2_STAGES;
+  uint64_t* tfull_bar = empty_bar + GEMM2_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int m_pairs = (M + 2 * GEMM_BM - 1) / (2 * GEMM_BM);
+  const int n_tiles = (N + GEMM_BN - 1) / GEMM_BN;
+  const int num_tiles = m_pairs * n_tiles;
+  const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
+  const int cluster = (int)blockIdx.x / 2, n_clusters = (int)gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < GEMM2_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own A rows, own half of B)
+    const uint32_t full_leader = mapa_shared(smem_u32(full_bar), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+      const int m0 = (tile / n_tiles) * (2 * GEMM_BM) + (int)rank * GEMM_BM;
+      const int n0 = (tile % n_tiles) * GEMM_BN + (int)rank * (GEMM_BN / 2);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (elect_one()) {
+          uint8_t* sa = smem + stage * GEMM2_STAGE_BYTES;
+          uint8_t* sb = sa + GEMM_A_BYTES;
+          const uint32_t fb = full_leader + stage * 8;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * GEMM2_STAGE_BYTES);
+          const int k0 = kb * GEMM_BK;
+          if (A_MN) {
+            tma_load_2d_2sm(&tmA, fb, sa, m0, k0);
+            tma_load_2d_2sm(&tmA, fb, sa + 8192, m0 + 64, k0);
+          } else {
+            tma_load_2d_2sm(&tmA, fb, sa, k0, m0);
+          }
+          if (B_MN) {
+            tma_load_2d_2sm(&tmB, fb, sb, n0, k0);
+            tma_load_2d_2sm(&tmB, fb, sb + 8192, n0 + 64, k0);
+          } else {
+            tma_load_2d_2sm(&tmB, fb, sb, k0, n0);
+          }
+        }
+        __syncwarp();
+        if (++stage == GEMM2_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (leader CTA only; M = 256 over the pair)
+    constexpr uint32_t idesc = idesc_bf16_f32(2 * GEMM_BM, GEMM_BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++local) {
+      const int buf = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tempty_bar[buf], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * GEMM_BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + stage * GEMM2_STAGE_BYTES);
+        const uint32_t sb = sa + GEMM_A_BYTES;
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            const uint64_t ad = A_MN ? smem_desc_sw128(sa + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(sb + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(sb + k * 32, 16, 1024);
+            mma_bf16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit_2sm(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == GEMM2_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) mma_commit_2sm(&tfull_bar[buf]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs: own 128 rows of the 256 x 256 tile)
+    const int quad = warp - 4;
+    const bool check = g_numerics_check != 0;
+    const uint32_t epi = smem_u32(smem + GEMM2_STAGES * GEMM2_STAGE_BYTES + 256) + quad * (32 * 32 * 4);
+    const uint32_t tempty_leader = mapa_shared(smem_u32(tempty_bar), 0);
+    int local = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++local) {
+      const int buf = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const int m0 = (tile / n_tiles) * (2 * GEMM_BM) + (int)rank * GEMM_BM;
+      const int n0 = (tile % n_tiles) * GEMM_BN;
+      mbar_wait(&tfull_bar[buf], acc_phase);
+      tc_fence_after();
+      gemm_epilogue_tile(tmem_base + buf * GEMM_BN, m0, n0, M, N, ep, quad, lane, epi, check);
+      tc_fence_before();
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader + buf * 8)
+                   : "memory");
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while its partner may still signal it
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
 }  // namespace lss

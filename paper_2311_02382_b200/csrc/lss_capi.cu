@@ -212,14 +212,33 @@ int lss_gemm(int dtype, const void* A, long lda, int a_mn_major, const void* B, 
                        CU_TENSOR_MAP_SWIZZLE_128B)))
       return rc;
   }
+  // CTA pairs (cta_group::2, 256 x 256 tiles) for the long-K products, where the
+  // mainloop dominates (A/B on B200, l=50112: dx K=3E 233 -> 208 us, dWqkv K=l 278 -> 267;
+  // the K=E projections with their heavier epilogues: QKV 307 -> 303, out-proj 213 -> 226)
+  const bool pair = LSS_GEMM_2CTA && M >= 4 * GEMM_BM && K >= 2048;
   {
     uint64_t dims[2], str[1] = {(uint64_t)ldb};
     uint32_t box[2];
     if (b_mn_major) { dims[0] = N; dims[1] = K; box[0] = 64; box[1] = 64; }
-    else            { dims[0] = K; dims[1] = N; box[0] = 64; box[1] = GEMM_BN; }
+    else            { dims[0] = K; dims[1] = N; box[0] = 64; box[1] = pair ? GEMM_BN / 2 : GEMM_BN; }
     if ((rc = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2, B, dims, str, box,
                        CU_TENSOR_MAP_SWIZZLE_128B)))
       return rc;
+  }
+  if (pair) {
+    const int pairs = ((M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((N + GEMM_BN - 1) / GEMM_BN);
+    const int clusters = pairs < num_sms() / 2 ? pairs : num_sms() / 2;
+#define LSS_GEMM2_LAUNCH(AM, BM_)                                                                      \
+  do {                                                                                                  \
+    if ((rc = set_smem(gemm_bf16_tc2_kernel<AM, BM_>, GEMM2_SMEM_BYTES))) return rc;                  \
+    gemm_bf16_tc2_kernel<AM, BM_><<<2 * clusters, GEMM_THREADS, GEMM2_SMEM_BYTES, S(stream)>>>(ma, mb, M, N, K, ep); \
+  } while (0)
+    if (!a_mn_major && !b_mn_major) LSS_GEMM2_LAUNCH(0, 0);
+    else if (!a_mn_major && b_mn_major) LSS_GEMM2_LAUNCH(0, 1);
+    else if (a_mn_major && !b_mn_major) LSS_GEMM2_LAUNCH(1, 0);
+    else LSS_GEMM2_LAUNCH(1, 1);
+#undef LSS_GEMM2_LAUNCH
+    return check_launch("gemm_bf16_tc2");
   }
   const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + GEMM_BN - 1) / GEMM_BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();

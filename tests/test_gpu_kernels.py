@@ -55,6 +55,33 @@ def test_gemm_layouts_and_epilogue(cuda, rng, a_mn, b_mn, prec):
     assert nerr(_np(out), want) < 1e-5
 
 
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", [(1024, 768, 4096), (1000, 544, 2056)])
+def test_gemm_cta_pair(cuda, rng, a_mn, b_mn, shape):
+    """The CTA-pair (cta_group::2, 256 x 256) kernel that long-K products use
+    (M >= 512, K >= 2048), incl. ragged M / N / K and both operand layouts,
+    against the fp64 product of the same bf16 operands."""
+    import torch
+    from paper_2311_02382_b200 import kernels as K
+
+    M, N, Kd = shape
+    a = rng.standard_normal((M, Kd))
+    b = rng.standard_normal((N, Kd))
+    ta = _t(a.T if a_mn else a, cuda, torch.bfloat16).contiguous()
+    tb = _t(b.T if b_mn else b, cuda, torch.bfloat16).contiguous()
+    an = _np(ta).T if a_mn else _np(ta)
+    bn = _np(tb).T if b_mn else _np(tb)
+    bias = rng.standard_normal(N)
+    res = rng.standard_normal((M, N))
+    want = 0.25 * an @ bn.T + bias + res
+    out = K.gemm(ta, tb, a_mn_major=a_mn, b_mn_major=b_mn, alpha=0.25,
+                 bias=_t(bias, cuda, torch.float32), residual=_t(res, cuda, torch.float32),
+                 M=M, N=N, K=Kd)
+    torch.cuda.synchronize()
+    assert nerr(_np(out), want) < 1e-5
+
+
 def test_gemm_split_bf16_segments(cuda, rng):
     """QKV projection epilogue: one GEMM writes Q to one buffer and K|V to another."""
     import torch

@@ -347,11 +347,14 @@ def main_ours(args):
             e0.record(st)
             out = fn(*a, **kw)
             e1.record(st)
-            marks[kind].append((e0, e1))
+            marks[kind].append((e0, e1, cur_step[0]))
             return out
         return wrapper
 
+    cur_step = [0]
+
     def one_step():
+        cur_step[0] += 1
         eng.load_params(lp)  # weights change every training step: restage (1 kernel)
         eng.step(x, gy, comm)
 
@@ -417,11 +420,23 @@ def main_ours(args):
     coll = {k: comm.ledger.count(k) // args.steps for k in ("all-gather", "reduce-scatter", "all-reduce")}
     ms = t_start.elapsed_time(t_end) / args.steps
     # per-step device time of this rank's attention kernels (all launches of the step)
-    fwd_ms = sum(a.elapsed_time(b) for a, b in marks["fwd"]) / args.steps
-    bwd_ms = sum(a.elapsed_time(b) for a, b in marks["bwd"]) / args.steps
-    qkv_ms = sum(a.elapsed_time(b) for a, b in marks["qkv"]) / max(1, len(marks["qkv"]))
+    fwd_ms = sum(a.elapsed_time(b) for a, b, _ in marks["fwd"]) / args.steps
+    bwd_ms = sum(a.elapsed_time(b) for a, b, _ in marks["bwd"]) / args.steps
+    qkv_ms = sum(a.elapsed_time(b) for a, b, _ in marks["qkv"]) / max(1, len(marks["qkv"]))
+
+    def span_ms(kind):
+        """Per step, first launch start to last launch end of the kind's launches (at N > 1
+        several launches run concurrently on side streams); mean over the timed steps."""
+        steps = {}
+        for a, b, k in marks[kind]:
+            lo, hi = t_start.elapsed_time(a), t_start.elapsed_time(b)
+            s0, s1 = steps.get(k, (lo, hi))
+            steps[k] = (min(s0, lo), max(s1, hi))
+        return sum(h - l_ for l_, h in steps.values()) / max(1, len(steps))
+
     my_pairs = eng.computed_pairs() * B
-    stats = torch.tensor([ms, fwd_ms, bwd_ms, float(my_pairs), qkv_ms], dtype=torch.float64, device=dev)
+    stats = torch.tensor([ms, fwd_ms, bwd_ms, float(my_pairs), qkv_ms, span_ms("fwd"), span_ms("bwd")],
+                         dtype=torch.float64, device=dev)
     if world > 1:
         allst = [torch.zeros_like(stats) for _ in range(world)]
         dist.all_gather(allst, stats)
@@ -447,19 +462,27 @@ def main_ours(args):
     ach_fwd = fwd_flops / (crit[1] / 1e3) / 1e12
     ach_qkv = qkv_flops / (crit[4] / 1e3) / 1e12 if crit[4] > 0 else None
 
-    def entry(kernel, ach, ms_k, work, traffic_key):
-        return {"kernel": kernel, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak if ach else None, "frac_of_burst": ach / burst if ach else None,
-                "frac_of_sustained": ach / sustained if ach else None, "ms_per_step": ms_k, "algorithmic": work,
-                "traffic": traffic_from_profile(traffic_key), "traffic_source": "profiles/ncu_summary.json "
-                "(dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture)"}
+    def entry(kernel, ach, ms_k, work, traffic_key, flops=None, span=None):
+        e = {"kernel": kernel, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+             "frac": ach / peak if ach else None, "frac_of_burst": ach / burst if ach else None,
+             "frac_of_sustained": ach / sustained if ach else None, "ms_per_step": ms_k, "algorithmic": work,
+             "traffic": traffic_from_profile(traffic_key), "traffic_source": "profiles/ncu_summary.json "
+             "(dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture)"}
+        if flops and span and world > 1:
+            # ms_per_step sums the launches of a step, which overlap on side streams at N > 1
+            # (own rows, delegated rows, key splits): the span from the first start to the last
+            # end is the time the phase actually occupies the GPU (fused-gather waits included)
+            e.update(span_ms_per_step=span, frac_span=flops / (span / 1e3) / 1e12 / peak)
+        return e
 
     roofline = entry("attn_bwd_tc_kernel (+ delta pre-pass)", ach_bwd, crit[2],
-                     f"8*E per unmasked (q,k) pair; {crit[3]:.4g} pairs on the critical rank", "attn_bwd_tc_kernel")
+                     f"8*E per unmasked (q,k) pair; {crit[3]:.4g} pairs on the critical rank", "attn_bwd_tc_kernel",
+                     bwd_flops, crit[6])
     roofline.update(peak_source=f"{src} {peak_name} (loaded SM clock {clocks.get('sm_mhz')} of "
                                 f"{clocks.get('sm_max_mhz')} MHz)",
                     balanced_schedule=eng.plan.role != "none" or world == 1,
-                    fwd=entry("attn_fwd_tc_kernel", ach_fwd, crit[1], "4*E per unmasked (q,k) pair", "attn_fwd_tc_kernel"),
+                    fwd=entry("attn_fwd_tc_kernel", ach_fwd, crit[1], "4*E per unmasked (q,k) pair", "attn_fwd_tc_kernel",
+                              fwd_flops, crit[5]),
                     qkv_gemm=entry("gemm_bf16_tc_kernel<0,0> ([Q|K|V] projection)", ach_qkv, crit[4],
                                    f"2*M*N*K, M={B * m}, N={3 * E}, K={E} per launch", "gemm_qkv"))
 

@@ -83,8 +83,18 @@ constexpr int GEMM_SMEM_BYTES = GEMM_STAGES * GEMM_STAGE_BYTES + GEMM_EPI_BYTES 
 // 32 half-filled sectors.  row_base: first row of the warp's 32; rows >= M skipped.
 template <bool BF16>
 LSS_DEV void epi_store_rows(uint32_t stage, const float (&v)[32], void* out, long ld, long col, int row_base,
-                            int M, uint32_t lane) {
+                            int M, uint32_t lane, const float* res = nullptr, long ld_res = 0) {
   constexpr int CH = BF16 ? 4 : 8;  // 16-byte chunks per row
+  constexpr int RPI = 32 / CH;      // rows per store instruction
+  float4 rv[32 / RPI];              // residual row segments, loaded ahead of the staging round trip
+  if (!BF16 && res) {
+#pragma unroll
+    for (int i = 0; i < 32 / RPI; ++i) {
+      const int r = i * RPI + (int)lane / CH, q = (int)lane % CH;
+      rv[i] = row_base + r < M ? *reinterpret_cast<const float4*>(res + (long)(row_base + r) * ld_res + col + q * 4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
   if (BF16) {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -98,12 +108,17 @@ LSS_DEV void epi_store_rows(uint32_t stage, const float (&v)[32], void* out, lon
                    __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
   }
   __syncwarp();
-  constexpr int RPI = 32 / CH;  // rows per store instruction
 #pragma unroll
   for (int i = 0; i < 32 / RPI; ++i) {
     const int r = i * RPI + (int)lane / CH, q = (int)lane % CH;
-    const float4 val = ld_shared_f4(stage + r * (CH * 16) + ((q ^ (r & (CH - 1))) << 4));
+    float4 val = ld_shared_f4(stage + r * (CH * 16) + ((q ^ (r & (CH - 1))) << 4));
     if (row_base + r < M) {
+      if (!BF16 && res) {  // residual added here: whole 128-byte row segments per load
+        val.x += rv[i].x;
+        val.y += rv[i].y;
+        val.z += rv[i].z;
+        val.w += rv[i].w;
+      }
       char* dst = reinterpret_cast<char*>(out) + ((long)(row_base + r) * ld + col) * (BF16 ? 2 : 4) + q * 16;
       *reinterpret_cast<float4*>(dst) = val;
     }
@@ -131,11 +146,18 @@ LSS_DEV void gemm_epilogue_tile(uint32_t acc, int m0, int n0, int M, int N, cons
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.f;
     } else {
-    if (ep.bias) {
+    if (ep.bias) {  // the same 32 values in every lane: 8 broadcast float4 loads
+      const float4* bp = reinterpret_cast<const float4*>(ep.bias + n);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += __ldg(ep.bias + n + i);
+      for (int i = 0; i < 8; ++i) {
+        const float4 t = __ldg(bp + i);
+        v[4 * i] += t.x;
+        v[4 * i + 1] += t.y;
+        v[4 * i + 2] += t.z;
+        v[4 * i + 3] += t.w;
+      }
     }
-    if (ep.residual) {
+    if (ep.residual && (ep.act != 0 || ep.out_bf16)) {  // else added in the coalesced store phase
       const float4* rp = reinterpret_cast<const float4*>(ep.residual + (long)row * ep.ld_res + n);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -201,7 +223,8 @@ LSS_DEV void gemm_epilogue_tile(uint32_t acc, int m0, int n0, int M, int N, cons
     if (ep.out_bf16)
       epi_store_rows<true>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
     else
-      epi_store_rows<false>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane);
+      epi_store_rows<false>(epi, v, ep.out[seg], ep.ldo[seg], col, m0 + quad * 32, M, lane,
+                            ep.act == 0 && ep.residual ? ep.residual + (n - col) : nullptr, ep.ld_res);
   }
 }
 

@@ -66,14 +66,18 @@ LSS_DEV float gelu_grad(float x) {
 #ifndef LSS_GEMM_2CTA
 #define LSS_GEMM_2CTA 1  // CTA-pair (cta_group::2) kernel for M >= 512
 #endif
+#ifndef LSS_GEMM_EPI_WG
+#define LSS_GEMM_EPI_WG 2  // epilogue warpgroups (each takes 256 / WG accumulator columns of every tile)
+#endif
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_STAGES = LSS_GEMM_EPI_WG > 2 ? 3 : 4;
 constexpr int GEMM_A_BYTES = GEMM_BM * GEMM_BK * 2;  // 16 KB
 constexpr int GEMM_B_BYTES = GEMM_BN * GEMM_BK * 2;  // 32 KB
 constexpr int GEMM_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES;
-constexpr int GEMM_EPI_BYTES = 4 * 32 * 32 * 4;  // per epilogue warp: a 32 x 32 fp32 staging tile
+constexpr int GEMM_EPI_WG = LSS_GEMM_EPI_WG;
+constexpr int GEMM_EPI_BYTES = GEMM_EPI_WG * 4 * 32 * 32 * 4;  // per epilogue warp: a 32 x 32 fp32 staging tile
 constexpr int GEMM_SMEM_BYTES = GEMM_STAGES * GEMM_STAGE_BYTES + GEMM_EPI_BYTES + 1024 /*align*/ + 256 /*bars*/;
 
 // Epilogue store of a warp's 32 rows x 32 columns through shared memory: every lane
@@ -129,12 +133,12 @@ LSS_DEV void epi_store_rows(uint32_t stage, const float (&v)[32], void* out, lon
 // [acc, acc + 256): warp `quad` of the epilogue warpgroup owns rows quad*32.. (TMEM
 // lanes), 32 columns at a time: alpha, bias, residual, activation, store.
 LSS_DEV void gemm_epilogue_tile(uint32_t acc, int m0, int n0, int M, int N, const GemmEpilogue& ep, int quad,
-                                uint32_t lane, uint32_t epi, bool check) {
+                                uint32_t lane, uint32_t epi, bool check, int c_begin = 0, int c_end = GEMM_BN) {
   const int row_in_tile = quad * 32 + (int)lane;
   const int row = m0 + row_in_tile;
   const bool row_ok = row < M;
 #pragma unroll 1
-  for (int c = 0; c < GEMM_BN; c += 32) {
+  for (int c = c_begin; c < c_end; c += 32) {
     uint32_t r[32];
     tmem_ld32(acc + ((uint32_t)(quad * 32) << 16) + c, r);
     const int n = n0 + c;
@@ -228,7 +232,7 @@ LSS_DEV void gemm_epilogue_tile(uint32_t acc, int m0, int n0, int M, int N, cons
   }
 }
 
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 128 * (1 + GEMM_EPI_WG);  // control warpgroup + epilogue warpgroups
 
 template <int A_MN, int B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 128);
+      mbar_init(&tempty_bar[b], 128 * GEMM_EPI_WG);
     }
     fence_barrier_init();
   }
@@ -347,9 +351,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: thread <-> accumulator row
-    const int quad = warp - 4;
+    // epilogue warpgroup eg takes accumulator columns [eg, eg+1) * 256 / GEMM_EPI_WG of every
+    // tile (the epilogue, not the mainloop, bounded the K=E projections with one warpgroup)
+    const int quad = warp % 4, eg = (warp - 4) / 4;
+    const int c_begin = eg * (GEMM_BN / GEMM_EPI_WG), c_end = c_begin + GEMM_BN / GEMM_EPI_WG;
     const bool check = g_numerics_check != 0;  // NaN / Inf report (tensor.py:79-95), off by default
-    const uint32_t epi = smem_u32(smem + GEMM_STAGES * GEMM_STAGE_BYTES + 256) + quad * (32 * 32 * 4);
+    const uint32_t epi = smem_u32(smem + GEMM_STAGES * GEMM_STAGE_BYTES + 256) + (warp - 4) * (32 * 32 * 4);
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int buf = local & 1;
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = (tile % n_tiles) * GEMM_BN;
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      gemm_epilogue_tile(tmem_base + buf * GEMM_BN, m0, n0, M, N, ep, quad, lane, epi, check);
+      gemm_epilogue_tile(tmem_base + buf * GEMM_BN, m0, n0, M, N, ep, quad, lane, epi, check, c_begin, c_end);
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);
     }
@@ -382,7 +389,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 //   empty_bar (each) : the leader's MMA commit, multicast to both CTAs
 //   tfull_bar (each) : the leader's accumulator commit, multicast
 //   tempty_bar (leader): both CTAs' epilogue warps (256 arrivals, remote for the peer)
-constexpr int GEMM2_STAGES = 6;
+constexpr int GEMM2_STAGES = LSS_GEMM_EPI_WG > 2 ? 4 : 6;
 constexpr int GEMM2_STAGE_BYTES = GEMM_A_BYTES + GEMM_B_BYTES / 2;  // 32 KB per CTA
 constexpr int GEMM2_SMEM_BYTES = GEMM2_STAGES * GEMM2_STAGE_BYTES + GEMM_EPI_BYTES + 1024 + 256;
 
@@ -455,7 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 256);
+      mbar_init(&tempty_bar[b], 2 * 128 * GEMM_EPI_WG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -543,9 +550,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs: own 128 rows of the 256 x 256 tile)
-    const int quad = warp - 4;
+    const int quad = warp % 4, eg = (warp - 4) / 4;
+    const int c_begin = eg * (GEMM_BN / GEMM_EPI_WG), c_end = c_begin + GEMM_BN / GEMM_EPI_WG;
     const bool check = g_numerics_check != 0;
-    const uint32_t epi = smem_u32(smem + GEMM2_STAGES * GEMM2_STAGE_BYTES + 256) + quad * (32 * 32 * 4);
+    const uint32_t epi = smem_u32(smem + GEMM2_STAGES * GEMM2_STAGE_BYTES + 256) + (warp - 4) * (32 * 32 * 4);
     const uint32_t tempty_leader = mapa_shared(smem_u32(tempty_bar), 0);
     int local = 0;
     for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++local) {
@@ -555,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = (tile % n_tiles) * GEMM_BN;
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      gemm_epilogue_tile(tmem_base + buf * GEMM_BN, m0, n0, M, N, ep, quad, lane, epi, check);
+      gemm_epilogue_tile(tmem_base + buf * GEMM_BN, m0, n0, M, N, ep, quad, lane, epi, check, c_begin, c_end);
       tc_fence_before();
       asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader + buf * 8)
                    : "memory");

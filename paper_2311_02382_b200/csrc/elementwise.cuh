@@ -78,6 +78,52 @@ __global__ void layernorm_fwd_kernel(const float* __restrict__ x, const float* _
   }
 }
 
+// Warp per row for E a multiple of 128 (E <= 2048): every lane holds E/128 float4
+// of its row in registers, both reductions are warp shuffles (no block barriers), and a
+// 256-thread block keeps 8 rows in flight -- the one-block-per-row kernel above left
+// its SMs waiting on two __syncthreads round trips per 4 KB row.
+template <typename TOut, int NV>
+__global__ void __launch_bounds__(256) layernorm_fwd_warp_kernel(const float* __restrict__ x,
+                                                               const float* __restrict__ gain,
+                                                               const float* __restrict__ bias, TOut* __restrict__ y,
+                                                               float* __restrict__ mean_out,
+                                                               float* __restrict__ rstd_out, long rows, float eps) {
+  constexpr int E = NV * 128;
+  const long row = (long)blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  float4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = *reinterpret_cast<const float4*>(x + row * E + k * 128 + lane * 4);
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) sum += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mu = sum / E;
+  float sq = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    v[k].x -= mu; v[k].y -= mu; v[k].z -= mu; v[k].w -= mu;
+    sq += (v[k].x * v[k].x + v[k].y * v[k].y) + (v[k].z * v[k].z + v[k].w * v[k].w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float rs = rsqrtf(sq / E + eps);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = k * 128 + lane * 4;
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
+    const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + c));
+    store4<TOut>(y + row * E + c, v[k].x * rs * g.x + bb.x, v[k].y * rs * g.y + bb.y, v[k].z * rs * g.z + bb.z,
+                 v[k].w * rs * g.w + bb.w);
+  }
+  if (lane == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = rs;
+  }
+}
+
 // gx = grad_res + rstd*(g - mean(g) - xhat*mean(g*xhat)), g = gxh*gain (nnops.py:211-227).
 // Each block handles ROWS rows; column partial sums of gxh*xhat and gxh are
 // accumulated in registers and added (scaled by alpha) to g_gain / g_bias once.
@@ -206,6 +252,83 @@ __global__ void cat_cast_colsum_kernel(CatSrc src, TOut* __restrict__ dst, long 
     atomicAdd(colsum + col4 + 1, alpha * acc.y);
     atomicAdd(colsum + col4 + 2, alpha * acc.z);
     atomicAdd(colsum + col4 + 3, alpha * acc.w);
+  }
+}
+
+// Warp-per-row LayerNorm backward for E a multiple of 128 (E <= 1024): each warp runs
+// LNW_RPW rows with warp-shuffle reductions and keeps its affine-gradient column
+// partials in registers (2 x E/32 per lane); the block's 8 warps combine them in
+// shared memory and issue one atomic per column per block (g_gain null: the
+// deterministic mode's separate column-sum kernel, as above).
+constexpr int LNW_RPW = 8;  // rows per warp -> 64 rows per 256-thread block
+template <int NV>
+__global__ void __launch_bounds__(256) layernorm_bwd_warp_kernel(
+    const float* __restrict__ gxh, const float* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ gain, const float* __restrict__ grad_res,
+    float* __restrict__ gx, float* __restrict__ g_gain, float* __restrict__ g_bias, float alpha, long rows) {
+  constexpr int E = NV * 128;
+  extern __shared__ float colred[];  // [8 warps][E] (gain partials, then bias partials)
+  const int wi = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float4 w[NV], gg[NV], gb[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    w[k] = __ldg(reinterpret_cast<const float4*>(gain + k * 128 + lane * 4));
+    gg[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    gb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const long rbase = (long)blockIdx.x * (8 * LNW_RPW) + wi;
+#pragma unroll 1
+  for (int i = 0; i < LNW_RPW; ++i) {
+    const long row = rbase + 8L * i;
+    if (row >= rows) break;
+    const float mu = mean[row], rs = rstd[row];
+    float4 gy[NV], xh[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      gy[k] = *reinterpret_cast<const float4*>(gxh + row * E + k * 128 + lane * 4);
+      xh[k] = *reinterpret_cast<const float4*>(x + row * E + k * 128 + lane * 4);
+    }
+    float sg = 0.f, sgx = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      xh[k] = make_float4((xh[k].x - mu) * rs, (xh[k].y - mu) * rs, (xh[k].z - mu) * rs, (xh[k].w - mu) * rs);
+      gg[k].x += gy[k].x * xh[k].x; gg[k].y += gy[k].y * xh[k].y; gg[k].z += gy[k].z * xh[k].z; gg[k].w += gy[k].w * xh[k].w;
+      gb[k].x += gy[k].x; gb[k].y += gy[k].y; gb[k].z += gy[k].z; gb[k].w += gy[k].w;
+      gy[k] = make_float4(gy[k].x * w[k].x, gy[k].y * w[k].y, gy[k].z * w[k].z, gy[k].w * w[k].w);  // g
+      sg += (gy[k].x + gy[k].y) + (gy[k].z + gy[k].w);
+      sgx += (gy[k].x * xh[k].x + gy[k].y * xh[k].y) + (gy[k].z * xh[k].z + gy[k].w * xh[k].w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sg += __shfl_xor_sync(0xffffffffu, sg, o);
+      sgx += __shfl_xor_sync(0xffffffffu, sgx, o);
+    }
+    const float mg = sg / E, mgx = sgx / E;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int c = k * 128 + lane * 4;
+      float4 r = grad_res ? *reinterpret_cast<const float4*>(grad_res + row * E + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      r.x += rs * (gy[k].x - mg - xh[k].x * mgx);
+      r.y += rs * (gy[k].y - mg - xh[k].y * mgx);
+      r.z += rs * (gy[k].z - mg - xh[k].z * mgx);
+      r.w += rs * (gy[k].w - mg - xh[k].w * mgx);
+      *reinterpret_cast<float4*>(gx + row * E + c) = r;
+    }
+  }
+  if (!g_gain) return;  // deterministic mode: ln_colsum_det_kernel sums instead (block-uniform)
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      *reinterpret_cast<float4*>(colred + wi * E + k * 128 + lane * 4) = pass ? gb[k] : gg[k];
+    __syncthreads();
+    for (int c = threadIdx.x; c < E; c += 256) {
+      float t = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) t += colred[ww * E + c];
+      atomicAdd((pass ? g_bias : g_gain) + c, alpha * t);
+    }
+    __syncthreads();
   }
 }
 

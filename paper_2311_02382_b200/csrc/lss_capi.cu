@@ -120,6 +120,29 @@ int lss_layernorm_fwd(const float* x, const float* gain, const float* bias, void
   if (!x || !gain || !bias || !y || !mean || !rstd) return fail(LSS_ERR_ARG, "layernorm_fwd: null pointer");
   if (embed <= 0 || embed % 4 || embed > 4096) return fail(LSS_ERR_UNSUPPORTED, "layernorm_fwd: embed %d", embed);
   if (rows <= 0) return LSS_OK;
+  if (embed % 128 == 0 && embed <= 2048 && (y_dtype == LSS_BF16 || y_dtype == LSS_F32)) {
+    const long blocks = (rows + 7) / 8;  // warp per row, 8 rows per block
+#define LSS_LN_WARP(NV)                                                                                        \
+  do {                                                                                                          \
+    if (y_dtype == LSS_BF16)                                                                                    \
+      layernorm_fwd_warp_kernel<__nv_bfloat16, NV><<<blocks, 256, 0, S(stream)>>>(                              \
+          x, gain, bias, reinterpret_cast<__nv_bfloat16*>(y), mean, rstd, rows, eps);                           \
+    else                                                                                                        \
+      layernorm_fwd_warp_kernel<float, NV><<<blocks, 256, 0, S(stream)>>>(x, gain, bias, reinterpret_cast<float*>(y), \
+                                                                           mean, rstd, rows, eps);              \
+  } while (0)
+    switch (embed / 128) {
+      case 1: LSS_LN_WARP(1); break;
+      case 2: LSS_LN_WARP(2); break;
+      case 4: LSS_LN_WARP(4); break;
+      case 8: LSS_LN_WARP(8); break;
+      case 16: LSS_LN_WARP(16); break;
+      default: goto block_per_row;
+    }
+#undef LSS_LN_WARP
+    return check_launch("layernorm_fwd");
+  }
+block_per_row:
   const int threads = ((embed / 4 + 31) / 32) * 32;
   if (y_dtype == LSS_BF16)
     layernorm_fwd_kernel<__nv_bfloat16><<<rows, threads, 0, S(stream)>>>(
@@ -139,11 +162,34 @@ int lss_layernorm_bwd(const float* grad_xh, const float* x, const float* mean, c
     return fail(LSS_ERR_ARG, "layernorm_bwd: null pointer");
   if (embed <= 0 || embed % 4 || embed > 4096) return fail(LSS_ERR_UNSUPPORTED, "layernorm_bwd: embed %d", embed);
   if (rows <= 0) return LSS_OK;
-  const int threads = ((embed / 4 + 31) / 32) * 32;
-  const long blocks = (rows + LN_BWD_ROWS - 1) / LN_BWD_ROWS;
   const bool det = g_deterministic != 0;
-  layernorm_bwd_kernel<<<blocks, threads, 0, S(stream)>>>(grad_xh, x, mean, rstd, gain, grad_res, grad_x,
-                                                          det ? nullptr : grad_gain, grad_bias, alpha, rows, embed);
+  float* gg = det ? nullptr : grad_gain;
+  bool warp_path = embed % 128 == 0 && embed <= 1024;  // (E=2048 would spill its register partials)
+  if (warp_path) {  // warp per row (LNW_RPW rows per warp, 8 warps per block)
+    const long wblocks = (rows + 8 * LNW_RPW - 1) / (8 * LNW_RPW);
+    const size_t sm = 8 * (size_t)embed * sizeof(float);
+#define LSS_LNB_WARP(NV)                                                                                      \
+  do {                                                                                                        \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(layernorm_bwd_warp_kernel<NV>,                                   \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);            \
+    layernorm_bwd_warp_kernel<NV><<<wblocks, 256, sm, S(stream)>>>(grad_xh, x, mean, rstd, gain, grad_res,     \
+                                                                   grad_x, gg, grad_bias, alpha, rows);        \
+  } while (0)
+    switch (embed / 128) {
+      case 1: LSS_LNB_WARP(1); break;
+      case 2: LSS_LNB_WARP(2); break;
+      case 4: LSS_LNB_WARP(4); break;
+      case 8: LSS_LNB_WARP(8); break;
+      default: warp_path = false;
+    }
+#undef LSS_LNB_WARP
+  }
+  if (!warp_path) {
+    const int threads = ((embed / 4 + 31) / 32) * 32;
+    const long blocks = (rows + LN_BWD_ROWS - 1) / LN_BWD_ROWS;
+    layernorm_bwd_kernel<<<blocks, threads, 0, S(stream)>>>(grad_xh, x, mean, rstd, gain, grad_res, grad_x, gg,
+                                                            grad_bias, alpha, rows, embed);
+  }
   if (det)  // one writer per column, fixed order (bitwise repeatable)
     ln_colsum_det_kernel<<<(embed + DET_COLS - 1) / DET_COLS, DET_COLS * DET_LANES, 0, S(stream)>>>(
         grad_xh, x, mean, rstd, grad_gain, grad_bias, alpha, rows, embed);
